@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 (I - Lambda Sigma) matvec -- the hot path of rtkrylov.
+
+Workload (BASELINE.json configs[1], "cfg2"): 1D slab, N_z = 2000 log-spaced
+optical depths 1e-6..1e6 with a seeded log-normal perturbation (sigma 0.3),
+32+32 Gauss-Legendre mu, N_nu = 512 over +-8 Doppler widths, dipole x PRD
+(dense 512 x 512 R), eps = 1e-6, implicit-Euler formal solver, FP64:
+N = 65,536,000 DOF, 524 MB per vector.  A step is one matvec y = A x.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+N > 1 (torchrun): every rank runs an independent replica on its own GPU
+(weak scaling; the matvec shards by direction with one moment all-reduce,
+which this single-GPU tier does not implement -- DESIGN.md "Multi-GPU").
+Timing: CUDA events on the launching stream, barrier + synchronize on both
+sides, max over ranks.  The vector (524 MB) exceeds the 126 MB L2, so no
+explicit flush is needed between steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "(I-Lambda Sigma) matvecs/s"
+UNIT = "matvec/s"
+CFG = 2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--formal-solver", default="ie", choices=["ie", "exp_linear", "exp_parabolic"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gmres", action="store_true")
+    return ap.parse_args()
+
+
+def dist_setup(backend):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend=backend)
+    return world, rank, local
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def workload_config(extra=None):
+    from paper_2602_21958_b200 import configs
+
+    c = configs.SLAB_CONFIGS[CFG]
+    cfg = {"workload": "cfg2: 1D slab 2000 z x 64 mu x 512 nu, dipole x PRD (dense 512x512 R), eps 1e-6",
+           "n_dof": c["n_space"] * c["n_angles"] * c["n_freq"], "n_space": c["n_space"], "n_angles": c["n_angles"],
+           "n_freq": c["n_freq"], "l2_policy": "inputs larger than L2 (524 MB vector vs 126 MB L2); no flush"}
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.fh,
+                                         stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.fh.close()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax = float(parts[2])
+                except ValueError:
+                    continue
+                for nm, val in zip(names, parts[5:9]):
+                    if val.lower().startswith("active"):
+                        reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_port_timing(problem, target_s=12.0, max_steps=30):
+    """The oracle's C/OpenMP restatement (oracle/librto.so) on this host's cores."""
+    from oracle import cport
+    from tests._problems import oracle_desc
+
+    port = cport.SlabPort(oracle_desc(problem))
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal(problem.n_total)
+    y = np.empty_like(x)
+    threads = cport.max_threads()
+    port.apply_A(x, y)  # warm-up (page faults, thread pool)
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max_steps and (time.perf_counter() - t_start) < target_s:
+        t0 = time.perf_counter()
+        port.apply_A(x, y)
+        times.append(time.perf_counter() - t0)
+    return {"value": 1.0 / statistics.mean(times), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{len(times)} full cfg2 matvecs (N=65.5M) by oracle/rt_oracle_c.c, OpenMP over {threads} "
+                      f"threads, mean {statistics.mean(times) * 1e3:.1f} ms"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle port of the reference CPU path on the host cores (rank 0 only)."""
+    world, rank, _ = dist_setup("gloo")
+    if rank != 0:
+        return
+    from oracle import cport
+    from paper_2602_21958_b200 import configs
+    from tests._problems import oracle_desc
+
+    problem = configs.slab_problem(CFG, formal_solver=args.formal_solver)
+    port = cport.SlabPort(oracle_desc(problem))
+    x = np.random.default_rng(7).standard_normal(problem.n_total)
+    y = np.empty_like(x)
+    for _ in range(max(args.warmup, 0)):
+        port.apply_A(x, y)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        port.apply_A(x, y)
+    elapsed = time.perf_counter() - t0
+    value = args.steps / elapsed
+    threads = cport.max_threads()
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config({"formal_solver": args.formal_solver}),
+            "gdof_per_s": value * problem.n_total / 1e9,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"each step one full cfg2 matvec by oracle/rt_oracle_c.c (C restatement of "
+                                       f"R/operator.py:48-53 + R/_kernels.py:70-88), OpenMP {threads} threads"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args):
+    import torch
+
+    world, rank, local = dist_setup("nccl")
+    torch.cuda.set_device(local)
+    import paper_2602_21958_b200 as P
+    from paper_2602_21958_b200 import _device, _native, configs
+
+    lib = _native.lib()
+    problem = configs.slab_problem(CFG, formal_solver=args.formal_solver)
+    n = problem.n_total
+    h = problem.device()
+    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    x = torch.randn(n, dtype=torch.float64, device="cuda", generator=gen)
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+    sptr = ctypes.c_void_p(stream.cuda_stream)
+
+    def step():
+        _native.check(lib.rtk_apply_A(h.h, _device.ptr(x), _device.ptr(y), n, sptr))
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = _native.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = _native.launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_per_step = ms_max / args.steps
+    value = world * args.steps / (ms_max / 1e3)
+
+    # per-kernel durations inside the same matvec (events on the launching stream)
+    kms = np.zeros(3)
+    buf = (ctypes.c_float * 3)()
+    kreps = max(5, min(args.steps, 20))
+    for _ in range(kreps):
+        _native.check(lib.rtk_profile_apply_A(h.h, _device.ptr(x), _device.ptr(y), n, sptr, buf))
+        kms += np.array(list(buf), dtype=float)
+    kms /= kreps
+    g = problem.grid
+    n_mom = P.separable_form(problem.scattering.kernel, g)[0].shape[0]
+    mom_elems = n_mom * g.n_freq * g.n_space
+    peaks, peak_src = measured_peaks()
+    hbm = float(peaks["hbm_gbs"])
+    sweep_bytes = 16 * n + 8 * mom_elems + 8 * g.n_space
+    moments_bytes = 8 * n + 8 * mom_elems
+    r_flops = 2.0 * g.n_freq * g.n_freq * mom_elems
+    fp64_peak = 37.1  # DMMA TF/s measured by tools/peaks_fp64.cu (profiles/r01_peaks_fp64.json)
+    kernels = {
+        "sweep": {"ms": kms[2], "bytes": sweep_bytes, "achieved_gbs": sweep_bytes / kms[2] / 1e6,
+                  "frac_hbm": sweep_bytes / kms[2] / 1e6 / hbm},
+        "moments": {"ms": kms[0], "bytes": moments_bytes, "achieved_gbs": moments_bytes / kms[0] / 1e6,
+                    "frac_hbm": moments_bytes / kms[0] / 1e6 / hbm},
+        "redistribute": {"ms": kms[1], "flops": r_flops, "achieved_tflops": r_flops / kms[1] / 1e9,
+                         "frac_fp64": r_flops / kms[1] / 1e9 / fp64_peak},
+    }
+    matvec_bytes = 24 * n + 16 * mom_elems + 8 * g.n_freq ** 2 + 8 * g.n_space
+    roofline = {"bound": "hbm", "kernel": "sweep1d_kernel (K1: fused source expansion + IE sweep + y = x - acc)",
+                "achieved": sweep_bytes / kms[2] / 1e6, "peak": hbm, "unit": "GB/s",
+                "frac": sweep_bytes / kms[2] / 1e6 / hbm, "traffic": None, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": sweep_bytes,
+                "matvec_algorithmic_bytes": matvec_bytes,
+                "matvec_frac_hbm": matvec_bytes / (ms_per_step / 1e3) / 1e9 / hbm}
+
+    # e2e: reference-facing call with host buffers (pinned), H2D + matvec + D2H per step
+    e2e = None
+    if rank == 0 or world > 1:
+        hx = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        hy = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        hx.copy_(x.cpu())
+        hxp, hyp = ctypes.c_void_p(hx.data_ptr()), ctypes.c_void_p(hy.data_ptr())
+        for _ in range(2):
+            _native.check(lib.rtk_apply_A_host(h.h, hxp, hyp, n, sptr))
+        k_e2e = max(3, min(args.steps, 10))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            _native.check(lib.rtk_apply_A_host(h.h, hxp, hyp, n, sptr))
+        el = time.perf_counter() - t0
+        e2e = {"value": world * k_e2e / el, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+               "path": "rtk_apply_A_host (C ABI, pinned host buffers)"}
+        del hx, hy
+
+    extra = {}
+    if rank == 0 and not args.no_gmres:
+        extra["gmres"] = gmres_timings(torch)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_port_timing(problem)
+        except Exception as exc:  # pragma: no cover
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {exc}"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; BASELINE cfg2 shapes)",
+                "config": workload_config({"formal_solver": args.formal_solver,
+                                           "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}),
+                "gdof_per_s": value * n / 1e9, "gpu_launches": launches, "clocks": clk, "roofline": roofline,
+                "kernels": kernels, "e2e": e2e, "cpu_baseline": cpu}
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def gmres_timings(torch):
+    """Time-to-1e-8 of the device GMRES on cfg1 (restart 30 and unrestarted)."""
+    import paper_2602_21958_b200 as P
+    from paper_2602_21958_b200 import configs
+
+    p = configs.slab_problem(1)
+    b = P.build_rhs(p, device=True)
+    out = {}
+    for name, restart in (("cfg1_gmres30", 30), ("cfg1_gmres_full", None)):
+        cfg = P.SolveConfig(rel_tol=1e-8, max_iter=6000, restart=restart)
+        P.gmres(p, b, P.SolveConfig(rel_tol=1e-8, max_iter=5, restart=restart))   # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = P.gmres(p, b, cfg)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        out[name] = {"iterations": rep.iterations, "converged": rep.converged, "time_s": el,
+                     "true_residual": rep.true_residual, "matvecs": rep.matvecs}
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,159 @@
+/*
+ * rtk_b200.h -- C ABI of the B200-native (I - Lambda Sigma) operator and its GMRES driver.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * rtkrylov (arXiv 2602.21958).  R/ = /root/reference/pkg/src/rtkrylov/.
+ * Every entry point names the reference interface it replaces.  Plain C
+ * types only: host arrays are `const double*` + sizes, device vectors are raw
+ * device pointers (float64, the reference's space-major layout
+ * index = i_space * n_rays + a * n_freq + f, R/grid.py:83-88), streams are
+ * `void*` (a cudaStream_t, NULL = the legacy default stream).
+ *
+ * Status codes: 0 ok, 1 invalid argument (Python: ValueError), 2 resource or
+ * capacity (ResourceLimitError, R/errors.py:6-7), 3 CUDA error (RuntimeError).
+ * rtk_last_error_message() returns the thread's last message.
+ * Non-convergence of a solve is a report flag, never an error
+ * (R/krylov.py:154-158).
+ */
+#ifndef RTK_B200_H
+#define RTK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RTK_OK 0
+#define RTK_EINVAL 1
+#define RTK_ERESOURCE 2
+#define RTK_ECUDA 3
+
+/* formal solvers (R/_kernels.py:70-88 is IE; the exponential ones are new) */
+#define RTK_FS_IE 0
+#define RTK_FS_EXP_LINEAR 1
+#define RTK_FS_EXP_PARABOLIC 2
+
+#define RTK_MAX_MOMENTS 8
+
+typedef struct rtk_problem rtk_problem;
+
+/*
+ * 1D plane-parallel slab.  Replaces the state held by Grid (R/grid.py:63-112),
+ * TransferOperator (R/transfer.py:65-104) and ScatteringOperator
+ * (R/scattering.py:74-100).  Sigma is the separable kernel
+ *   Psi[(a,f),(a',f')] = sum_k coeffs[k] ybasis[k][a] ybasis[k][a'] * R[f][f']
+ * which expresses LegendreKernel (ybasis = P_l(mu), R = 1), CRDKernel
+ * (ybasis = 1, R = phi phi'), CoherentKernel (R = diag(phi / w_f)) and the
+ * dipole x PRD kernel (ybasis = P_0, P_2; coeffs = 1, 1/2).
+ */
+typedef struct rtk_slab_desc {
+    int64_t n_space;
+    int32_t n_angles;
+    int32_t n_freq;
+    int32_t n_moments;        /* rows of ybasis, 1..RTK_MAX_MOMENTS */
+    int32_t formal_solver;    /* RTK_FS_* */
+    int32_t gamma_per_ray;    /* 0: gamma[n_space][n_freq]; 1: gamma[n_space][n_angles*n_freq] (R/grid.py:107-112) */
+    int32_t reserved;
+    const double* t_nodes;        /* [n_space] strictly increasing optical-depth scale (R/grid.py:68) */
+    const double* mu;             /* [n_angles] direction cosines, none zero */
+    const double* ang_w;          /* [n_angles] angular weights */
+    const double* phi;            /* [n_freq] profile at the frequency nodes */
+    const double* freq_w;         /* [n_freq] frequency weights */
+    const double* ybasis;         /* [n_moments][n_angles] */
+    const double* coeffs;         /* [n_moments] */
+    const double* redistribution; /* [n_freq][n_freq] R(nu, nu') */
+    const double* gamma;          /* see gamma_per_ray */
+    const double* inflow;         /* [n_angles*n_freq] boundary intensity per ray, or NULL for 0 (R/transfer.py:101-103) */
+} rtk_slab_desc;
+
+const char* rtk_last_error_message(void);
+int rtk_version(void);
+/* Number of this library's kernels launched since load (bench / evidence counter). */
+int64_t rtk_kernel_launch_count(void);
+
+/* Build the device-resident operator: ONE host->device upload of the tables
+ * (dt, phi, 1/|mu|, w*Y, R*w, gamma, inflow) plus the matvec workspace.
+ * Replaces build_grid/build_transfer/build_scattering + RTProblem
+ * (R/grid.py:115-150, R/transfer.py:88-104, R/scattering.py:85-100,
+ * R/operator.py:28-45). */
+int rtk_problem_create_slab(const rtk_slab_desc* desc, rtk_problem** out);
+int rtk_problem_destroy(rtk_problem* p);
+int64_t rtk_problem_n_total(const rtk_problem* p);
+/* Re-upload inflow after a host-side edit (T/test_operator.py:88-110 mutate it). */
+int rtk_problem_set_inflow(rtk_problem* p, const double* inflow_host, int64_t n_rays);
+
+/* y = x - Lambda(Sigma x)  -- apply_A, R/operator.py:48-53.  x, y device, length n. */
+int rtk_apply_A(rtk_problem* p, const double* x_dev, double* y_dev, int64_t n, void* stream);
+/* apply_A with CUDA events between its kernels: ms_out[0..2] = moments, redistribution,
+ * sweep durations (ms) on `stream` (synchronises).  Measurement hook for bench.py. */
+int rtk_profile_apply_A(rtk_problem* p, const double* x_dev, double* y_dev, int64_t n, void* stream,
+                        float* ms_out);
+/* Same, host buffers in and out (H2D + matvec + D2H); the e2e path of the drop-in. */
+int rtk_apply_A_host(rtk_problem* p, const double* x_host, double* y_host, int64_t n, void* stream);
+/* s = Sigma x -- apply_scattering, R/scattering.py:126-148. */
+int rtk_apply_sigma(rtk_problem* p, const double* x_dev, double* s_dev, int64_t n, void* stream);
+/* y = Lambda s (homogeneous part) -- apply_transfer, R/transfer.py:134-141. */
+int rtk_apply_lambda(rtk_problem* p, const double* s_dev, double* y_dev, int64_t n, void* stream);
+/* y = boundary (inflow) term -- boundary_term, R/transfer.py:144-147 (overflow-free recursion). */
+int rtk_boundary(rtk_problem* p, double* y_dev, int64_t n, void* stream);
+/* b = Lambda thermal + boundary, or ones -- build_rhs, R/operator.py:56-64. */
+int rtk_build_rhs(rtk_problem* p, const double* thermal_dev, double* b_dev, int64_t n,
+                  int32_t override_ones, void* stream);
+/* s = Sigma I + thermal (returned source function; no reference helper, R/operator.py:35). */
+int rtk_source_function(rtk_problem* p, const double* intensity_dev, const double* thermal_dev,
+                        double* s_dev, int64_t n, void* stream);
+
+/* ---------------- Krylov (R/krylov.py) ---------------- */
+
+/* Matvec callback: y = A x on device vectors, on `stream`; returns a status code. */
+typedef int (*rtk_matvec_fn)(void* ctx, const double* x_dev, double* y_dev, int64_t n, void* stream);
+
+typedef struct rtk_solve_cfg {       /* SolveConfig, R/krylov.py:21-35 */
+    double rel_tol;
+    int32_t max_iter;
+    int32_t restart;                 /* <= 0: no restart (SolveConfig.restart = None) */
+    int32_t reorthogonalize;         /* accepted for API parity; Arnoldi is always CGS2 (two passes) */
+    int32_t reserved;
+} rtk_solve_cfg;
+
+typedef struct rtk_solve_report {    /* SolveReport, R/krylov.py:38-46 (solution stays on device) */
+    int32_t iterations;
+    int32_t converged;
+    int32_t breakdown;
+    int32_t n_history;               /* entries written to history_host (<= history_cap) */
+    double true_residual;
+    int32_t matvecs;                 /* total operator applications incl. restart/true-residual ones */
+    int32_t reserved;
+} rtk_solve_report;
+
+/* Restarted GMRES with the reference's exact control flow (R/krylov.py:56-158):
+ * x0 = 0, Givens least squares, recurrence-residual stop, true-residual guard
+ * at 10 tol, breakdown at 1e-14 ||b||.  Arnoldi is CGS2 with deterministic
+ * device reductions; the Krylov basis stays in HBM.  x_dev receives the
+ * solution. */
+int rtk_gmres(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b_dev, double* x_dev,
+              const rtk_solve_cfg* cfg, rtk_solve_report* report,
+              double* history_host, int32_t history_cap, void* stream);
+/* Same, with the problem's own fused matvec (no callback crossing). */
+int rtk_gmres_problem(rtk_problem* p, const double* b_dev, double* x_dev,
+                      const rtk_solve_cfg* cfg, rtk_solve_report* report,
+                      double* history_host, int32_t history_cap, void* stream);
+/* BiCGStab (R/krylov.py:180-256) on device vectors. */
+int rtk_bicgstab(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b_dev, double* x_dev,
+                 const rtk_solve_cfg* cfg, rtk_solve_report* report,
+                 double* history_host, int32_t history_cap, void* stream);
+/* rtk_matvec_fn adapter: ctx is an rtk_problem*. */
+int rtk_problem_matvec(void* problem, const double* x_dev, double* y_dev, int64_t n, void* stream);
+
+/* Device BLAS-1 used by the Krylov driver, exported for tests: deterministic
+ * fixed-order reductions, result written to host. */
+int rtk_dot(const double* x_dev, const double* y_dev, int64_t n, double* out_host, void* stream);
+int rtk_block_dot(const double* const* vecs_host, int32_t k, const double* w_dev, int64_t n,
+                  double* out_host, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RTK_B200_H */

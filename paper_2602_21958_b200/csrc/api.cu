@@ -1,0 +1,262 @@
+// C-ABI entry points of librtk_b200 (declared in include/rtk_b200.h): problem
+// lifetime, operator applications, RHS.  R/ = /root/reference/pkg/src/rtkrylov/.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "rtk_internal.cuh"
+
+struct rtk_problem {
+    rtk::Problem impl;
+};
+
+namespace rtk {
+
+static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+int set_error(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+    g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+    if (e == cudaErrorMemoryAllocation) return RTK_ERESOURCE;
+    return RTK_ECUDA;
+}
+
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+Problem::~Problem() {
+    double* bufs[] = {dt, phi, inv_mu, wy, yb, rwt, gamma, coeffs, inflow, mom, gmom, host_x, host_y};
+    for (double* b : bufs)
+        if (b) cudaFree(b);
+    if (dir_sign) cudaFree(dir_sign);
+}
+
+static int upload(double** dst, const double* src, size_t count) {
+    if (count == 0) count = 1;
+    RTK_CUDA_TRY(cudaMalloc(dst, count * sizeof(double)));
+    if (src) RTK_CUDA_TRY(cudaMemcpy(*dst, src, count * sizeof(double), cudaMemcpyHostToDevice));
+    else RTK_CUDA_TRY(cudaMemset(*dst, 0, count * sizeof(double)));
+    return RTK_OK;
+}
+
+int apply_A_dev(Problem& p, const double* x, double* y, cudaStream_t s) {
+    int rc;
+    if ((rc = launch_moments(p, x, s))) return rc;
+    if ((rc = launch_redistribute(p, s))) return rc;
+    return launch_sweep(p, SRC_MOMENTS, OUT_X_MINUS, false, nullptr, x, y, s);
+}
+
+}  // namespace rtk
+
+using rtk::Problem;
+using rtk::set_error;
+
+static int check_n(const rtk_problem* p, int64_t n) {
+    if (!p) return set_error(RTK_EINVAL, "null problem handle");
+    if (n != p->impl.n_total)
+        return set_error(RTK_EINVAL, "expected length " + std::to_string(p->impl.n_total) + ", got " + std::to_string(n));
+    return RTK_OK;
+}
+
+extern "C" {
+
+const char* rtk_last_error_message(void) { return rtk::g_last_error.c_str(); }
+
+int rtk_version(void) { return 1; }
+
+int64_t rtk_kernel_launch_count(void) { return rtk::g_launches.load(); }
+
+int rtk_problem_create_slab(const rtk_slab_desc* d, rtk_problem** out) {
+    if (!d || !out) return set_error(RTK_EINVAL, "null argument");
+    *out = nullptr;
+    if (d->n_space < 2) return set_error(RTK_EINVAL, "need at least 2 space nodes");
+    if (d->n_angles < 1 || d->n_freq < 1) return set_error(RTK_EINVAL, "need at least one angle and one frequency");
+    if (d->n_moments < 1 || d->n_moments > RTK_MAX_MOMENTS)
+        return set_error(RTK_EINVAL, "n_moments must be in 1.." + std::to_string(RTK_MAX_MOMENTS));
+    if (d->formal_solver < RTK_FS_IE || d->formal_solver > RTK_FS_EXP_PARABOLIC)
+        return set_error(RTK_EINVAL, "unknown formal solver");
+    if (!d->t_nodes || !d->mu || !d->ang_w || !d->phi || !d->freq_w || !d->ybasis || !d->coeffs ||
+        !d->redistribution || !d->gamma)
+        return set_error(RTK_EINVAL, "missing description array");
+    for (int64_t i = 0; i + 1 < d->n_space; ++i)
+        if (!(d->t_nodes[i + 1] > d->t_nodes[i])) return set_error(RTK_EINVAL, "t_nodes must be strictly increasing");
+    for (int a = 0; a < d->n_angles; ++a)
+        if (d->mu[a] == 0.0) return set_error(RTK_EINVAL, "mu = 0 is not an admissible direction");
+
+    rtk_problem* h = new (std::nothrow) rtk_problem();
+    if (!h) return set_error(RTK_ERESOURCE, "host allocation failed");
+    Problem& p = h->impl;
+    p.n_space = d->n_space;
+    p.n_angles = d->n_angles;
+    p.n_freq = d->n_freq;
+    p.n_mom = d->n_moments;
+    p.fs = d->formal_solver;
+    p.gamma_per_ray = d->gamma_per_ray ? 1 : 0;
+    p.n_rays = static_cast<int64_t>(p.n_angles) * p.n_freq;
+    p.n_total = p.n_space * p.n_rays;
+    p.h_mu.assign(d->mu, d->mu + p.n_angles);
+    p.h_coeffs.assign(d->coeffs, d->coeffs + p.n_mom);
+
+    // host-side table preparation (setup only, once per problem)
+    std::vector<double> dt(p.n_space - 1), inv_mu(p.n_angles), wy(p.n_mom * p.n_angles);
+    std::vector<double> rwt(static_cast<size_t>(p.n_freq) * p.n_freq);
+    std::vector<int> sign(p.n_angles);
+    for (int64_t i = 0; i + 1 < p.n_space; ++i) dt[i] = d->t_nodes[i + 1] - d->t_nodes[i];
+    for (int a = 0; a < p.n_angles; ++a) {
+        inv_mu[a] = 1.0 / std::fabs(d->mu[a]);
+        sign[a] = d->mu[a] < 0 ? -1 : 1;
+    }
+    for (int k = 0; k < p.n_mom; ++k)
+        for (int a = 0; a < p.n_angles; ++a) wy[k * p.n_angles + a] = d->ang_w[a] * d->ybasis[k * p.n_angles + a];
+    for (int f = 0; f < p.n_freq; ++f)
+        for (int g = 0; g < p.n_freq; ++g)
+            rwt[static_cast<size_t>(g) * p.n_freq + f] = d->redistribution[static_cast<size_t>(f) * p.n_freq + g] * d->freq_w[g];
+
+    int rc = RTK_OK;
+    const size_t gamma_count = static_cast<size_t>(p.n_space) * (p.gamma_per_ray ? p.n_rays : p.n_freq);
+    const size_t mom_count = static_cast<size_t>(p.n_space) * p.n_mom * p.n_freq;
+    if (!rc) rc = rtk::upload(&p.dt, dt.data(), dt.size());
+    if (!rc) rc = rtk::upload(&p.phi, d->phi, p.n_freq);
+    if (!rc) rc = rtk::upload(&p.inv_mu, inv_mu.data(), inv_mu.size());
+    if (!rc) rc = rtk::upload(&p.wy, wy.data(), wy.size());
+    if (!rc) rc = rtk::upload(&p.yb, d->ybasis, static_cast<size_t>(p.n_mom) * p.n_angles);
+    if (!rc) rc = rtk::upload(&p.rwt, rwt.data(), rwt.size());
+    if (!rc) rc = rtk::upload(&p.gamma, d->gamma, gamma_count);
+    if (!rc) rc = rtk::upload(&p.coeffs, d->coeffs, p.n_mom);
+    if (!rc) rc = rtk::upload(&p.inflow, d->inflow, p.n_rays);
+    if (!rc) rc = rtk::upload(&p.mom, nullptr, mom_count);
+    if (!rc) rc = rtk::upload(&p.gmom, nullptr, mom_count);
+    if (!rc) {
+        cudaError_t e = cudaMalloc(&p.dir_sign, sizeof(int) * p.n_angles);
+        if (e == cudaSuccess) e = cudaMemcpy(p.dir_sign, sign.data(), sizeof(int) * p.n_angles, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) rc = rtk::cuda_status(e, "dir_sign upload");
+    }
+    if (rc) {
+        delete h;
+        return rc;
+    }
+    *out = h;
+    return RTK_OK;
+}
+
+int rtk_problem_destroy(rtk_problem* p) {
+    delete p;
+    return RTK_OK;
+}
+
+int64_t rtk_problem_n_total(const rtk_problem* p) { return p ? p->impl.n_total : -1; }
+
+int rtk_problem_set_inflow(rtk_problem* p, const double* inflow_host, int64_t n_rays) {
+    if (!p) return set_error(RTK_EINVAL, "null problem handle");
+    if (n_rays != p->impl.n_rays) return set_error(RTK_EINVAL, "inflow length must equal n_rays");
+    if (inflow_host)
+        RTK_CUDA_TRY(cudaMemcpy(p->impl.inflow, inflow_host, sizeof(double) * n_rays, cudaMemcpyHostToDevice));
+    else
+        RTK_CUDA_TRY(cudaMemset(p->impl.inflow, 0, sizeof(double) * n_rays));
+    return RTK_OK;
+}
+
+int rtk_apply_A(rtk_problem* p, const double* x, double* y, int64_t n, void* stream) {
+    int rc = check_n(p, n);
+    if (rc) return rc;
+    return rtk::apply_A_dev(p->impl, x, y, static_cast<cudaStream_t>(stream));
+}
+
+int rtk_profile_apply_A(rtk_problem* p, const double* x, double* y, int64_t n, void* stream, float* ms_out) {
+    int rc = check_n(p, n);
+    if (rc) return rc;
+    if (!ms_out) return set_error(RTK_EINVAL, "null ms_out");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaEvent_t ev[4];
+    for (auto& e : ev) RTK_CUDA_TRY(cudaEventCreate(&e));
+    RTK_CUDA_TRY(cudaEventRecord(ev[0], s));
+    if (!rc) rc = rtk::launch_moments(p->impl, x, s);
+    RTK_CUDA_TRY(cudaEventRecord(ev[1], s));
+    if (!rc) rc = rtk::launch_redistribute(p->impl, s);
+    RTK_CUDA_TRY(cudaEventRecord(ev[2], s));
+    if (!rc) rc = rtk::launch_sweep(p->impl, rtk::SRC_MOMENTS, rtk::OUT_X_MINUS, false, nullptr, x, y, s);
+    RTK_CUDA_TRY(cudaEventRecord(ev[3], s));
+    RTK_CUDA_TRY(cudaEventSynchronize(ev[3]));
+    for (int k = 0; k < 3; ++k) cudaEventElapsedTime(&ms_out[k], ev[k], ev[k + 1]);
+    for (auto& e : ev) cudaEventDestroy(e);
+    return rc;
+}
+
+int rtk_problem_matvec(void* ctx, const double* x, double* y, int64_t n, void* stream) {
+    return rtk_apply_A(static_cast<rtk_problem*>(ctx), x, y, n, stream);
+}
+
+int rtk_apply_A_host(rtk_problem* p, const double* x_host, double* y_host, int64_t n, void* stream) {
+    int rc = check_n(p, n);
+    if (rc) return rc;
+    Problem& q = p->impl;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!q.host_x) RTK_CUDA_TRY(cudaMalloc(&q.host_x, sizeof(double) * q.n_total));
+    if (!q.host_y) RTK_CUDA_TRY(cudaMalloc(&q.host_y, sizeof(double) * q.n_total));
+    RTK_CUDA_TRY(cudaMemcpyAsync(q.host_x, x_host, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    if ((rc = rtk::apply_A_dev(q, q.host_x, q.host_y, s))) return rc;
+    RTK_CUDA_TRY(cudaMemcpyAsync(y_host, q.host_y, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    RTK_CUDA_TRY(cudaStreamSynchronize(s));
+    return RTK_OK;
+}
+
+int rtk_apply_sigma(rtk_problem* p, const double* x, double* s_out, int64_t n, void* stream) {
+    int rc = check_n(p, n);
+    if (rc) return rc;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if ((rc = rtk::launch_moments(p->impl, x, s))) return rc;
+    if ((rc = rtk::launch_redistribute(p->impl, s))) return rc;
+    return rtk::launch_expand_source(p->impl, nullptr, s_out, s);
+}
+
+int rtk_source_function(rtk_problem* p, const double* intensity, const double* thermal, double* s_out, int64_t n,
+                        void* stream) {
+    int rc = check_n(p, n);
+    if (rc) return rc;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if ((rc = rtk::launch_moments(p->impl, intensity, s))) return rc;
+    if ((rc = rtk::launch_redistribute(p->impl, s))) return rc;
+    return rtk::launch_expand_source(p->impl, thermal, s_out, s);
+}
+
+int rtk_apply_lambda(rtk_problem* p, const double* src, double* y, int64_t n, void* stream) {
+    int rc = check_n(p, n);
+    if (rc) return rc;
+    return rtk::launch_sweep(p->impl, rtk::SRC_VECTOR, rtk::OUT_ACC, false, src, nullptr, y,
+                             static_cast<cudaStream_t>(stream));
+}
+
+int rtk_boundary(rtk_problem* p, double* y, int64_t n, void* stream) {
+    int rc = check_n(p, n);
+    if (rc) return rc;
+    return rtk::launch_sweep(p->impl, rtk::SRC_ZERO, rtk::OUT_ACC, true, nullptr, nullptr, y,
+                             static_cast<cudaStream_t>(stream));
+}
+
+int rtk_build_rhs(rtk_problem* p, const double* thermal, double* b, int64_t n, int32_t override_ones, void* stream) {
+    int rc = check_n(p, n);
+    if (rc) return rc;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (override_ones) {
+        // b = 1 (named benchmark mode, R/operator.py:62-63)
+        std::vector<double> ones(static_cast<size_t>(n), 1.0);
+        RTK_CUDA_TRY(cudaMemcpyAsync(b, ones.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+        RTK_CUDA_TRY(cudaStreamSynchronize(s));
+        return RTK_OK;
+    }
+    // one recursion carrying the inflow value: Lambda thermal + decay * inflow
+    if (thermal)
+        return rtk::launch_sweep(p->impl, rtk::SRC_VECTOR, rtk::OUT_ACC, true, thermal, nullptr, b, s);
+    return rtk::launch_sweep(p->impl, rtk::SRC_ZERO, rtk::OUT_ACC, true, nullptr, nullptr, b, s);
+}
+
+}  // extern "C"

@@ -1,0 +1,696 @@
+// K3: Krylov solvers on device vectors.  GMRES and BiCGStab with the
+// reference's exact control flow (R/krylov.py:56-256); the vectors (Krylov
+// basis, iterate, residual) stay in HBM and only scalars cross to the host.
+//
+// Arnoldi uses classical Gram-Schmidt with one reorthogonalisation pass
+// (CGS2), fused into three streaming passes over the basis:
+//   pass 1  h1 = V^T w
+//   pass 2  w <- w - V h1 ;  h2 = V^T w          (same sweep over V)
+//   pass 3  w <- w - V h2 ;  ||w||^2
+// followed by v_{j+1} = w / ||w||.  Every reduction is a fixed-shape
+// two-level tree (warp shuffle -> block -> last-block serial sum over block
+// partials in index order), so results are bitwise reproducible run to run.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <vector>
+
+#include "rtk_internal.cuh"
+
+namespace rtk {
+namespace {
+
+constexpr int kRedThreads = 256;
+constexpr int kMaxRedBlocks = 296;   // 2 x 148 SMs
+constexpr int KMAX = 16;             // basis vectors handled per pass
+
+enum PassMode { MODE_DOT = 0, MODE_UPDATE_DOT = 1, MODE_UPDATE_NORM = 2, MODE_UPDATE = 3 };
+
+struct Workspace {
+    double* partials = nullptr;      // [KMAX][kMaxRedBlocks]
+    unsigned* counter = nullptr;
+    double* dev_scalars = nullptr;   // device-side coefficient / result scratch
+    double* pinned = nullptr;        // host pinned scratch
+    int dev_cap = 0, pin_cap = 0;
+    ~Workspace() {
+        if (partials) cudaFree(partials);
+        if (counter) cudaFree(counter);
+        if (dev_scalars) cudaFree(dev_scalars);
+        if (pinned) cudaFreeHost(pinned);
+    }
+    int init() {
+        RTK_CUDA_TRY(cudaMalloc(&partials, sizeof(double) * KMAX * kMaxRedBlocks));
+        RTK_CUDA_TRY(cudaMalloc(&counter, sizeof(unsigned)));
+        RTK_CUDA_TRY(cudaMemset(counter, 0, sizeof(unsigned)));
+        if (int rc = reserve_scalars(4 * KMAX)) return rc;
+        return reserve_pinned(4 * KMAX);
+    }
+    int reserve_scalars(int count) {
+        if (count <= dev_cap) return RTK_OK;
+        if (dev_scalars) cudaFree(dev_scalars);
+        dev_cap = count * 2;
+        RTK_CUDA_TRY(cudaMalloc(&dev_scalars, sizeof(double) * dev_cap));
+        return RTK_OK;
+    }
+    int reserve_pinned(int count) {
+        if (count <= pin_cap) return RTK_OK;
+        if (pinned) cudaFreeHost(pinned);
+        pin_cap = count * 2;
+        RTK_CUDA_TRY(cudaMallocHost(&pinned, sizeof(double) * pin_cap));
+        return RTK_OK;
+    }
+};
+
+int red_blocks(int64_t n) {
+    int64_t b = (n + kRedThreads * 4 - 1) / (kRedThreads * 4);
+    if (b < 1) b = 1;
+    if (b > kMaxRedBlocks) b = kMaxRedBlocks;
+    return static_cast<int>(b);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+struct PassArgs {
+    const double* v[KMAX];      // basis vectors of this pass
+    int kc;                     // how many of them
+    const double* coef;         // device coefficients (update modes), length kc
+    double* w;                  // vector updated in place (update modes) / read (dot)
+    const double* x;            // second operand for MODE_DOT when w is null... (unused)
+    int64_t n;
+    double* partials;
+    unsigned* counter;
+    double* out;                // device results: kc dots, or 1 norm^2
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kRedThreads) cgs_pass_kernel(PassArgs P) {
+    constexpr int NACC = (MODE == MODE_UPDATE_NORM) ? 1 : KMAX;
+    double acc[NACC];
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
+    double c[KMAX];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) c[k] = (MODE != MODE_DOT && k < P.kc) ? P.coef[k] : 0.0;
+
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < P.n; e += stride) {
+        double vv[KMAX];
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) vv[k] = (k < P.kc) ? __ldg(P.v[k] + e) : 0.0;
+        double we = P.w[e];
+        if (MODE != MODE_DOT) {
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k)
+                if (k < P.kc) we -= c[k] * vv[k];
+            P.w[e] = we;
+        }
+        if (MODE == MODE_UPDATE_NORM) {
+            acc[0] = fma(we, we, acc[0]);
+        } else if (MODE != MODE_UPDATE) {
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k)
+                if (k < P.kc) acc[k] = fma(vv[k], we, acc[k]);
+        }
+    }
+    if (MODE == MODE_UPDATE) return;
+
+    // block reduction of each accumulator, fixed order
+    __shared__ double red[kRedThreads / 32][NACC];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nk = (MODE == MODE_UPDATE_NORM) ? 1 : P.kc;
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) {
+        if (k < nk) {
+            const double s = warp_sum(acc[k]);
+            if (lane == 0) red[warp][k] = s;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < nk) {
+        double s = 0.0;
+        for (int w = 0; w < kRedThreads / 32; ++w) s += red[w][threadIdx.x];
+        P.partials[threadIdx.x * kMaxRedBlocks + blockIdx.x] = s;
+    }
+    // last block to finish sums the block partials in index order
+    __shared__ bool is_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned ticket = atomicAdd(P.counter, 1u);
+        is_last = (ticket == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (is_last) {
+        __threadfence();
+        if (threadIdx.x < nk) {
+            double s = 0.0;
+            const volatile double* pp = P.partials + threadIdx.x * kMaxRedBlocks;
+            for (unsigned b = 0; b < gridDim.x; ++b) s += pp[b];
+            P.out[threadIdx.x] = s;
+        }
+        if (threadIdx.x == 0) *P.counter = 0u;
+    }
+}
+
+// y = a * x  (a read from device: 1/sqrt(norm2) or a host scalar)
+__global__ void scale_kernel(const double* __restrict__ x, double* __restrict__ y, int64_t n, double a,
+                             const double* __restrict__ norm2) {
+    const double s = norm2 ? sqrt(*norm2) : a;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride) y[e] = x[e] / s;
+}
+
+// out = base + sum_k y_k V_k  (the reference's _combine, R/krylov.py:173-177, added to x)
+struct CombineArgs {
+    const double* v[KMAX];
+    double y[KMAX];
+    int kc;
+    const double* base;   // may be null (then 0)
+    double* out;
+    int64_t n;
+};
+__global__ void combine_kernel(CombineArgs C) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < C.n; e += stride) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+            if (k < C.kc) s = fma(C.y[k], __ldg(C.v[k] + e), s);
+        C.out[e] = (C.base ? C.base[e] : 0.0) + s;
+    }
+}
+
+// out = a - b
+__global__ void sub_kernel(const double* a, const double* b, double* out,
+                           int64_t n) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride) out[e] = a[e] - b[e];
+}
+
+// BiCGStab updates (R/krylov.py:211-233), same operation order as numpy
+__global__ void bicg_p_kernel(const double* __restrict__ r, double* __restrict__ p, const double* __restrict__ v,
+                              double beta, double omega, int64_t n) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride)
+        p[e] = r[e] + beta * (p[e] - omega * v[e]);
+}
+__global__ void axpy_out_kernel(const double* x, double a, const double* y,
+                                double* out, int64_t n) {   // out = x + a*y
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride)
+        out[e] = x[e] + a * y[e];
+}
+__global__ void bicg_x_kernel(double* __restrict__ x, double alpha, const double* __restrict__ p, double omega,
+                              const double* __restrict__ s, int64_t n) {   // x = x + alpha p + omega s
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride)
+        x[e] = (x[e] + alpha * p[e]) + omega * s[e];
+}
+
+unsigned elem_blocks(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    if (b < 1) b = 1;
+    return static_cast<unsigned>(b);
+}
+
+// ---------------------------------------------------------------------------
+
+class Engine {
+   public:
+    Engine(cudaStream_t s) : s_(s) {}
+    int init() { return ws_.init(); }
+    cudaStream_t stream() const { return s_; }
+
+    // results (dots or norm^2) land in out_dev[0 .. k)
+    int pass(int mode, const double* const* V, int k, const double* coef_dev, double* w, int64_t n, double* out_dev) {
+        PassArgs P;
+        for (int i = 0; i < KMAX; ++i) P.v[i] = (i < k) ? V[i] : nullptr;
+        P.kc = k;
+        P.coef = coef_dev;
+        P.w = w;
+        P.x = nullptr;
+        P.n = n;
+        P.partials = ws_.partials;
+        P.counter = ws_.counter;
+        P.out = out_dev;
+        const int blocks = red_blocks(n);
+        switch (mode) {
+            case MODE_DOT: cgs_pass_kernel<MODE_DOT><<<blocks, kRedThreads, 0, s_>>>(P); break;
+            case MODE_UPDATE_DOT: cgs_pass_kernel<MODE_UPDATE_DOT><<<blocks, kRedThreads, 0, s_>>>(P); break;
+            case MODE_UPDATE_NORM: cgs_pass_kernel<MODE_UPDATE_NORM><<<blocks, kRedThreads, 0, s_>>>(P); break;
+            default: cgs_pass_kernel<MODE_UPDATE><<<blocks, kRedThreads, 0, s_>>>(P); break;
+        }
+        RTK_LAUNCH_CHECK("cgs_pass_kernel");
+        return RTK_OK;
+    }
+
+    // host-visible dot product x.y (fixed-order reduction)
+    int dot(const double* x, const double* y, int64_t n, double* out) {
+        const double* V[1] = {x};
+        int rc = pass(MODE_DOT, V, 1, nullptr, const_cast<double*>(y), n, ws_.dev_scalars);
+        if (rc) return rc;
+        RTK_CUDA_TRY(cudaMemcpyAsync(ws_.pinned, ws_.dev_scalars, sizeof(double), cudaMemcpyDeviceToHost, s_));
+        RTK_CUDA_TRY(cudaStreamSynchronize(s_));
+        *out = ws_.pinned[0];
+        return RTK_OK;
+    }
+    int norm(const double* x, int64_t n, double* out) {
+        double d;
+        int rc = dot(x, x, n, &d);
+        *out = std::sqrt(d);
+        return rc;
+    }
+
+    // CGS2 Arnoldi step: w <- w - V h, h = h1 + h2 returned in col[0..j], col[j+1] = ||w||.
+    // Only one device->host transfer (the column) per step.
+    int cgs2(const std::vector<double*>& V, int jp1, double* w, int64_t n, double* col) {
+        int rc;
+        if ((rc = ws_.reserve_scalars(2 * jp1 + 1))) return rc;
+        double* h1 = ws_.dev_scalars;
+        double* h2 = ws_.dev_scalars + jp1;
+        double* nrm = ws_.dev_scalars + 2 * jp1;
+        if (jp1 <= KMAX) {
+            // pass 1: h1 = V^T w ; pass 2: w -= V h1, h2 = V^T w ; pass 3: w -= V h2, ||w||^2
+            if ((rc = pass(MODE_DOT, V.data(), jp1, nullptr, w, n, h1))) return rc;
+            if ((rc = pass(MODE_UPDATE_DOT, V.data(), jp1, h1, w, n, h2))) return rc;
+            if ((rc = pass(MODE_UPDATE_NORM, V.data(), jp1, h2, w, n, nrm))) return rc;
+        } else {
+            // long bases: chunked dot / update sweeps, still device-resident
+            for (int k0 = 0; k0 < jp1; k0 += KMAX)
+                if ((rc = pass(MODE_DOT, V.data() + k0, std::min(KMAX, jp1 - k0), nullptr, w, n, h1 + k0))) return rc;
+            for (int k0 = 0; k0 < jp1; k0 += KMAX)
+                if ((rc = pass(MODE_UPDATE, V.data() + k0, std::min(KMAX, jp1 - k0), h1 + k0, w, n, nullptr))) return rc;
+            for (int k0 = 0; k0 < jp1; k0 += KMAX)
+                if ((rc = pass(MODE_DOT, V.data() + k0, std::min(KMAX, jp1 - k0), nullptr, w, n, h2 + k0))) return rc;
+            for (int k0 = 0; k0 < jp1; k0 += KMAX) {
+                const int kc = std::min(KMAX, jp1 - k0);
+                const bool last = k0 + kc >= jp1;
+                if ((rc = pass(last ? MODE_UPDATE_NORM : MODE_UPDATE, V.data() + k0, kc, h2 + k0, w, n,
+                               last ? nrm : nullptr)))
+                    return rc;
+            }
+        }
+        if ((rc = ws_.reserve_pinned(2 * jp1 + 1))) return rc;
+        RTK_CUDA_TRY(cudaMemcpyAsync(ws_.pinned, ws_.dev_scalars, sizeof(double) * (2 * jp1 + 1),
+                                     cudaMemcpyDeviceToHost, s_));
+        RTK_CUDA_TRY(cudaStreamSynchronize(s_));
+        for (int i = 0; i < jp1; ++i) col[i] = ws_.pinned[i] + ws_.pinned[jp1 + i];
+        col[jp1] = std::sqrt(ws_.pinned[2 * jp1]);
+        return RTK_OK;
+    }
+
+    int scale(const double* x, double* y, int64_t n, double a) {
+        scale_kernel<<<elem_blocks(n), 256, 0, s_>>>(x, y, n, a, nullptr);
+        RTK_LAUNCH_CHECK("scale_kernel");
+        return RTK_OK;
+    }
+
+    // out = base + sum_k y_k V_k
+    int combine(const std::vector<double*>& V, const std::vector<double>& y, const double* base, double* out,
+                int64_t n) {
+        const int m = static_cast<int>(y.size());
+        const double* cur_base = base;
+        for (int k0 = 0; k0 < m || k0 == 0; k0 += KMAX) {
+            CombineArgs C;
+            const int kc = std::min(KMAX, m - k0);
+            for (int i = 0; i < KMAX; ++i) {
+                C.v[i] = (i < kc) ? V[k0 + i] : nullptr;
+                C.y[i] = (i < kc) ? y[k0 + i] : 0.0;
+            }
+            C.kc = kc > 0 ? kc : 0;
+            C.base = cur_base;
+            C.out = out;
+            C.n = n;
+            combine_kernel<<<elem_blocks(n), 256, 0, s_>>>(C);
+            RTK_LAUNCH_CHECK("combine_kernel");
+            cur_base = out;
+            if (m == 0) break;
+        }
+        return RTK_OK;
+    }
+
+    int sub(const double* a, const double* b, double* out, int64_t n) {
+        sub_kernel<<<elem_blocks(n), 256, 0, s_>>>(a, b, out, n);
+        RTK_LAUNCH_CHECK("sub_kernel");
+        return RTK_OK;
+    }
+
+    Workspace ws_;
+
+   private:
+    cudaStream_t s_;
+};
+
+struct DevBuf {
+    double* p = nullptr;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    int alloc(int64_t n) {
+        cudaError_t e = cudaMalloc(&p, sizeof(double) * (n > 0 ? n : 1));
+        if (e != cudaSuccess) return cuda_status(e, "Krylov workspace allocation");
+        return RTK_OK;
+    }
+};
+
+struct Basis {
+    std::vector<double*> v;
+    ~Basis() {
+        for (double* p : v)
+            if (p) cudaFree(p);
+    }
+    int ensure(size_t count, int64_t n) {
+        while (v.size() < count) {
+            double* p = nullptr;
+            cudaError_t e = cudaMalloc(&p, sizeof(double) * (n > 0 ? n : 1));
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                return set_error(RTK_ERESOURCE, "Krylov basis does not fit in device memory (" +
+                                                    std::to_string(v.size()) + " vectors allocated)");
+            }
+            v.push_back(p);
+        }
+        return RTK_OK;
+    }
+};
+
+void solve_upper(const std::vector<std::vector<double>>& h_cols, const std::vector<double>& g, int m,
+                 std::vector<double>& y) {
+    // R/krylov.py:161-170
+    y.assign(m, 0.0);
+    for (int i = m - 1; i >= 0; --i) {
+        double s = g[i];
+        for (int k = i + 1; k < m; ++k) s -= h_cols[k][i] * y[k];
+        y[i] = s / h_cols[i][i];
+    }
+}
+
+struct History {
+    double* out;
+    int cap;
+    int count = 0;
+    std::vector<double> all;
+    void push(double v) { all.push_back(v); }
+    void flush(rtk_solve_report* rep) {
+        const int n = static_cast<int>(all.size());
+        const int w = n < cap ? n : cap;
+        if (out)
+            for (int i = 0; i < w; ++i) out[i] = all[i];
+        rep->n_history = w;
+    }
+};
+
+int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, double* x, const rtk_solve_cfg* cfg,
+               rtk_solve_report* rep, double* hist_out, int hist_cap, cudaStream_t s) {
+    if (!cfg || !rep || !b || !x) return set_error(RTK_EINVAL, "null argument");
+    if (!(cfg->rel_tol > 0)) return set_error(RTK_EINVAL, "rel_tol must be positive");
+    if (cfg->max_iter < 1) return set_error(RTK_EINVAL, "max_iter must be >= 1");
+    *rep = rtk_solve_report{};
+    History hist{hist_out, hist_cap};
+    Engine E(s);
+    int rc;
+    if ((rc = E.init())) return rc;
+    int matvecs = 0;
+    auto A = [&](const double* in, double* out) -> int {
+        ++matvecs;
+        int r = apply(ctx, in, out, n, s);
+        if (r) return r;
+        return RTK_OK;
+    };
+    const double tol = cfg->rel_tol;
+    double b_norm;
+    if ((rc = E.norm(b, n, &b_norm))) return rc;
+    RTK_CUDA_TRY(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+    if (b_norm == 0.0) {   // R/krylov.py:64-68
+        hist.push(0.0);
+        hist.flush(rep);
+        rep->iterations = 0;
+        rep->converged = 1;
+        rep->true_residual = 0.0;
+        RTK_CUDA_TRY(cudaStreamSynchronize(s));
+        return RTK_OK;
+    }
+    DevBuf r, w, cand;
+    if ((rc = r.alloc(n)) || (rc = w.alloc(n)) || (rc = cand.alloc(n))) return rc;
+    RTK_CUDA_TRY(cudaMemcpyAsync(r.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    int total = 0;
+    const int cycle = cfg->restart > 0 ? cfg->restart : cfg->max_iter;
+    Basis V;
+    std::vector<double> col, y;
+    auto finish = [&](int iters, bool conv, bool brk, double tr) {
+        rep->iterations = iters;
+        rep->converged = conv ? 1 : 0;
+        rep->breakdown = brk ? 1 : 0;
+        rep->true_residual = tr;
+        rep->matvecs = matvecs;
+        hist.flush(rep);
+    };
+    while (total < cfg->max_iter) {
+        double beta;
+        if ((rc = E.norm(r.p, n, &beta))) return rc;
+        if (beta / b_norm <= tol) {   // R/krylov.py:77-83
+            hist.push(beta / b_norm);
+            finish(total > 1 ? total : 1, true, false, beta / b_norm);
+            return RTK_OK;
+        }
+        if ((rc = V.ensure(1, n))) return rc;
+        if ((rc = E.scale(r.p, V.v[0], n, beta))) return rc;
+        std::vector<std::vector<double>> h_cols;
+        std::vector<double> cs, sn, g{beta};
+        bool breakdown = false;
+        const int steps = std::min(cycle, cfg->max_iter - total);
+        int j = 0;
+        while (j < steps) {
+            if ((rc = A(V.v[j], w.p))) return rc;
+            col.assign(j + 2, 0.0);
+            if ((rc = E.cgs2(V.v, j + 1, w.p, n, col.data()))) return rc;
+            breakdown = col[j + 1] < 1e-14 * b_norm;
+            if (!breakdown) {
+                if ((rc = V.ensure(j + 2, n))) return rc;
+                if ((rc = E.scale(w.p, V.v[j + 1], n, col[j + 1]))) return rc;
+            }
+            // Givens (R/krylov.py:109-122), host scalars
+            for (int i = 0; i < j; ++i) {
+                const double tmp = cs[i] * col[i] + sn[i] * col[i + 1];
+                col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1];
+                col[i] = tmp;
+            }
+            const double denom = std::hypot(col[j], col[j + 1]);
+            const double cj = denom != 0.0 ? col[j] / denom : 1.0;
+            const double sj = denom != 0.0 ? col[j + 1] / denom : 0.0;
+            cs.push_back(cj);
+            sn.push_back(sj);
+            col[j] = denom;
+            h_cols.emplace_back(col.begin(), col.begin() + j + 1);
+            g.push_back(-sj * g[j]);
+            g[j] = cj * g[j];
+            ++total;
+            ++j;
+            const double rel = std::fabs(g[j]) / b_norm;
+            hist.push(rel);
+            if (rel <= tol || breakdown) {   // R/krylov.py:129-147
+                solve_upper(h_cols, g, j, y);
+                if ((rc = E.combine(V.v, y, x, cand.p, n))) return rc;
+                if ((rc = A(cand.p, w.p))) return rc;
+                if ((rc = E.sub(b, w.p, w.p, n))) return rc;
+                double tn;
+                if ((rc = E.norm(w.p, n, &tn))) return rc;
+                const double true_rel = tn / b_norm;
+                if (true_rel <= 10.0 * tol) {
+                    if (breakdown) hist.all.back() = true_rel;
+                    RTK_CUDA_TRY(cudaMemcpyAsync(x, cand.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+                    RTK_CUDA_TRY(cudaStreamSynchronize(s));
+                    finish(total, true, breakdown, true_rel);
+                    return RTK_OK;
+                }
+                if (breakdown) {
+                    RTK_CUDA_TRY(cudaMemcpyAsync(x, cand.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+                    RTK_CUDA_TRY(cudaStreamSynchronize(s));
+                    finish(total, false, true, true_rel);
+                    return RTK_OK;
+                }
+            }
+        }
+        // cycle exhausted: x += V y ; r = b - A x   (R/krylov.py:149-152)
+        solve_upper(h_cols, g, j, y);
+        if ((rc = E.combine(V.v, y, x, x, n))) return rc;
+        if ((rc = A(x, w.p))) return rc;
+        if ((rc = E.sub(b, w.p, r.p, n))) return rc;
+    }
+    double rn;
+    if ((rc = E.norm(r.p, n, &rn))) return rc;
+    finish(total, false, false, rn / b_norm);
+    RTK_CUDA_TRY(cudaStreamSynchronize(s));
+    return RTK_OK;
+}
+
+int bicgstab_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, double* x, const rtk_solve_cfg* cfg,
+                  rtk_solve_report* rep, double* hist_out, int hist_cap, cudaStream_t s) {
+    // R/krylov.py:180-256
+    if (!cfg || !rep || !b || !x) return set_error(RTK_EINVAL, "null argument");
+    if (!(cfg->rel_tol > 0)) return set_error(RTK_EINVAL, "rel_tol must be positive");
+    if (cfg->max_iter < 1) return set_error(RTK_EINVAL, "max_iter must be >= 1");
+    *rep = rtk_solve_report{};
+    History hist{hist_out, hist_cap};
+    Engine E(s);
+    int rc;
+    if ((rc = E.init())) return rc;
+    int matvecs = 0;
+    auto A = [&](const double* in, double* out) -> int {
+        ++matvecs;
+        return apply(ctx, in, out, n, s);
+    };
+    const double eps = 1e-30, tol = cfg->rel_tol;
+    double b_norm;
+    if ((rc = E.norm(b, n, &b_norm))) return rc;
+    RTK_CUDA_TRY(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+    if (b_norm == 0.0) {
+        hist.push(0.0);
+        hist.flush(rep);
+        rep->converged = 1;
+        RTK_CUDA_TRY(cudaStreamSynchronize(s));
+        return RTK_OK;
+    }
+    DevBuf r, rsh, v, p, sv, t;
+    if ((rc = r.alloc(n)) || (rc = rsh.alloc(n)) || (rc = v.alloc(n)) || (rc = p.alloc(n)) || (rc = sv.alloc(n)) ||
+        (rc = t.alloc(n)))
+        return rc;
+    RTK_CUDA_TRY(cudaMemcpyAsync(r.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    RTK_CUDA_TRY(cudaMemcpyAsync(rsh.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    RTK_CUDA_TRY(cudaMemsetAsync(v.p, 0, sizeof(double) * n, s));
+    RTK_CUDA_TRY(cudaMemsetAsync(p.p, 0, sizeof(double) * n, s));
+    double rho_prev = 1.0, alpha = 1.0, omega = 1.0;
+    bool breakdown = false, converged = false;
+    int it = 0;
+    const unsigned nb = elem_blocks(n);
+    while (it < cfg->max_iter) {
+        double rho;
+        if ((rc = E.dot(rsh.p, r.p, n, &rho))) return rc;
+        if (std::fabs(rho) < eps) {
+            breakdown = true;
+            break;
+        }
+        if (it == 0) {
+            RTK_CUDA_TRY(cudaMemcpyAsync(p.p, r.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+        } else {
+            const double beta = (rho / rho_prev) * (alpha / omega);
+            bicg_p_kernel<<<nb, 256, 0, s>>>(r.p, p.p, v.p, beta, omega, n);
+            RTK_LAUNCH_CHECK("bicg_p_kernel");
+        }
+        if ((rc = A(p.p, v.p))) return rc;
+        double denom;
+        if ((rc = E.dot(rsh.p, v.p, n, &denom))) return rc;
+        if (std::fabs(denom) < eps) {
+            breakdown = true;
+            break;
+        }
+        alpha = rho / denom;
+        axpy_out_kernel<<<nb, 256, 0, s>>>(r.p, -alpha, v.p, sv.p, n);   // s = r - alpha v
+        RTK_LAUNCH_CHECK("axpy_out_kernel");
+        ++it;
+        double s_norm;
+        if ((rc = E.norm(sv.p, n, &s_norm))) return rc;
+        if (s_norm / b_norm <= tol) {
+            axpy_out_kernel<<<nb, 256, 0, s>>>(x, alpha, p.p, x, n);
+            RTK_LAUNCH_CHECK("axpy_out_kernel");
+            hist.push(s_norm / b_norm);
+            converged = true;
+            break;
+        }
+        if ((rc = A(sv.p, t.p))) return rc;
+        double tt;
+        if ((rc = E.dot(t.p, t.p, n, &tt))) return rc;
+        if (tt < eps) {
+            breakdown = true;
+            break;
+        }
+        double ts;
+        if ((rc = E.dot(t.p, sv.p, n, &ts))) return rc;
+        omega = ts / tt;
+        if (std::fabs(omega) < eps) {
+            breakdown = true;
+            break;
+        }
+        bicg_x_kernel<<<nb, 256, 0, s>>>(x, alpha, p.p, omega, sv.p, n);
+        RTK_LAUNCH_CHECK("bicg_x_kernel");
+        axpy_out_kernel<<<nb, 256, 0, s>>>(sv.p, -omega, t.p, r.p, n);   // r = s - omega t
+        RTK_LAUNCH_CHECK("axpy_out_kernel");
+        rho_prev = rho;
+        double rn;
+        if ((rc = E.norm(r.p, n, &rn))) return rc;
+        hist.push(rn / b_norm);
+        if (rn / b_norm <= tol) {
+            converged = true;
+            break;
+        }
+    }
+    if ((rc = A(x, t.p))) return rc;
+    if ((rc = E.sub(b, t.p, t.p, n))) return rc;
+    double tn;
+    if ((rc = E.norm(t.p, n, &tn))) return rc;
+    const double true_rel = tn / b_norm;
+    if (converged) converged = true_rel <= 10.0 * tol;
+    if (hist.all.empty()) hist.push(true_rel);
+    rep->iterations = it;
+    rep->converged = converged ? 1 : 0;
+    rep->breakdown = breakdown ? 1 : 0;
+    rep->true_residual = true_rel;
+    rep->matvecs = matvecs;
+    hist.flush(rep);
+    RTK_CUDA_TRY(cudaStreamSynchronize(s));
+    return RTK_OK;
+}
+
+}  // namespace
+}  // namespace rtk
+
+extern "C" {
+
+int rtk_gmres(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, double* x, const rtk_solve_cfg* cfg,
+              rtk_solve_report* rep, double* hist, int32_t cap, void* stream) {
+    if (!apply) return rtk::set_error(RTK_EINVAL, "null matvec");
+    return rtk::gmres_impl(apply, ctx, n, b, x, cfg, rep, hist, cap, static_cast<cudaStream_t>(stream));
+}
+
+int rtk_gmres_problem(rtk_problem* p, const double* b, double* x, const rtk_solve_cfg* cfg, rtk_solve_report* rep,
+                      double* hist, int32_t cap, void* stream) {
+    if (!p) return rtk::set_error(RTK_EINVAL, "null problem handle");
+    return rtk::gmres_impl(rtk_problem_matvec, p, rtk_problem_n_total(p), b, x, cfg, rep, hist, cap,
+                           static_cast<cudaStream_t>(stream));
+}
+
+int rtk_bicgstab(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, double* x, const rtk_solve_cfg* cfg,
+                 rtk_solve_report* rep, double* hist, int32_t cap, void* stream) {
+    if (!apply) return rtk::set_error(RTK_EINVAL, "null matvec");
+    return rtk::bicgstab_impl(apply, ctx, n, b, x, cfg, rep, hist, cap, static_cast<cudaStream_t>(stream));
+}
+
+int rtk_dot(const double* x, const double* y, int64_t n, double* out_host, void* stream) {
+    rtk::Engine E(static_cast<cudaStream_t>(stream));
+    int rc = E.init();
+    if (rc) return rc;
+    return E.dot(x, y, n, out_host);
+}
+
+int rtk_block_dot(const double* const* vecs_host, int32_t k, const double* w, int64_t n, double* out_host,
+                  void* stream) {
+    rtk::Engine E(static_cast<cudaStream_t>(stream));
+    int rc = E.init();
+    if (rc) return rc;
+    for (int k0 = 0; k0 < k; k0 += rtk::KMAX) {
+        const int kc = std::min(rtk::KMAX, k - k0);
+        if ((rc = E.pass(rtk::MODE_DOT, vecs_host + k0, kc, nullptr, const_cast<double*>(w), n, E.ws_.dev_scalars)))
+            return rc;
+        RTK_CUDA_TRY(cudaMemcpyAsync(out_host + k0, E.ws_.dev_scalars, sizeof(double) * kc, cudaMemcpyDeviceToHost,
+                                     static_cast<cudaStream_t>(stream)));
+        RTK_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    }
+    return RTK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,72 @@
+// Internal declarations shared by the librtk_b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "rtk_b200.h"
+
+namespace rtk {
+
+// ---- error plumbing -------------------------------------------------------
+int set_error(int code, const std::string& msg);
+int cuda_status(cudaError_t e, const char* what);
+void count_launch(int n = 1);
+
+#define RTK_CUDA_TRY(expr)                                   \
+    do {                                                     \
+        cudaError_t _e = (expr);                             \
+        if (_e != cudaSuccess) return ::rtk::cuda_status(_e, #expr); \
+    } while (0)
+
+#define RTK_LAUNCH_CHECK(what)                               \
+    do {                                                     \
+        ::rtk::count_launch();                               \
+        cudaError_t _e = cudaGetLastError();                 \
+        if (_e != cudaSuccess) return ::rtk::cuda_status(_e, what); \
+    } while (0)
+
+// ---- device-resident slab operator ---------------------------------------
+//
+// HBM layout (all float64):
+//   dt      [n_space-1]          t_{i+1} - t_i
+//   phi     [n_freq]             profile at frequency nodes
+//   inv_mu  [n_angles]           1/|mu_a|
+//   wy      [n_mom][n_angles]    w_a * Y_k(a)      (moment reduction weights)
+//   yb      [n_mom][n_angles]    Y_k(a)            (source reconstruction)
+//   rwt     [n_freq][n_freq]     rwt[g][f] = R[f][g] * w_g   (K-major B operand)
+//   gamma   [n_space][n_freq] * coeff folded at use, or [n_space][n_rays]
+//   inflow  [n_rays]
+// workspace:
+//   mom     [n_space][n_mom][n_freq]   angular moments m
+//   gmom    [n_space][n_mom][n_freq]   G = c_k gamma R w m  (source moments)
+struct Problem {
+    int64_t n_space = 0;
+    int n_angles = 0, n_freq = 0, n_mom = 0, fs = 0, gamma_per_ray = 0;
+    int64_t n_rays = 0, n_total = 0;
+    std::vector<double> h_mu, h_coeffs;
+    double *dt = nullptr, *phi = nullptr, *inv_mu = nullptr, *wy = nullptr, *yb = nullptr;
+    double *rwt = nullptr, *gamma = nullptr, *coeffs = nullptr, *inflow = nullptr;
+    int* dir_sign = nullptr;     // [n_angles] -1 down (mu<0), +1 up
+    double *mom = nullptr, *gmom = nullptr;
+    double *host_x = nullptr, *host_y = nullptr;   // lazily allocated device staging for *_host calls
+    ~Problem();
+};
+
+// ---- kernel launchers (return status) --------------------------------------
+// sigma.cu
+int launch_moments(const Problem& p, const double* x, cudaStream_t s);
+int launch_redistribute(const Problem& p, cudaStream_t s);            // mom -> gmom
+int launch_expand_source(const Problem& p, const double* thermal, double* out, cudaStream_t s);
+// sweep1d.cu
+enum SweepSrc { SRC_MOMENTS = 0, SRC_VECTOR = 1, SRC_ZERO = 2 };
+enum SweepOut { OUT_X_MINUS = 0, OUT_ACC = 1 };
+int launch_sweep(const Problem& p, int src_mode, int out_mode, bool with_inflow,
+                 const double* src_vec, const double* x, double* y, cudaStream_t s);
+// krylov.cu
+int apply_A_dev(Problem& p, const double* x, double* y, cudaStream_t s);
+
+}  // namespace rtk

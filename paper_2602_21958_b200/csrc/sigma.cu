@@ -1,0 +1,187 @@
+// K2: the scattering operator Sigma = Gamma Psi W in moment form
+// (R/scattering.py:126-148), split as
+//   K2a  m[i,k,f]  = sum_a w_a Y_k(a) x[i,a,f]            angular moments  (HBM-bound)
+//   K2b  G[i,k,f]  = c_k gamma[i,f] sum_g R[f,g] w_g m[i,k,g]  redistribution (FP64 GEMM)
+// G is the "source moment" array the sweep kernel expands on the fly
+// (S[i,a,f] = sum_k Y_k(a) G[i,k,f]).  K2b is a (n_space*n_mom x n_freq) x
+// (n_freq x n_freq) GEMM; K = n_freq.
+#include <cuda_runtime.h>
+
+#include "rtk_internal.cuh"
+
+namespace rtk {
+namespace {
+
+constexpr int kMomThreads = 256;
+
+// one thread per (i, f); loops over the n_angles directions (coalesced in f)
+template <int NM>
+__global__ void __launch_bounds__(kMomThreads) moments_kernel(const double* __restrict__ x, const double* __restrict__ wy,
+                                                              double* __restrict__ mom, int64_t n_space, int n_angles,
+                                                              int n_freq) {
+    extern __shared__ double s_wy[];
+    for (int t = threadIdx.x; t < NM * n_angles; t += blockDim.x) s_wy[t] = wy[t];
+    __syncthreads();
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= n_space * n_freq) return;
+    const int64_t i = t / n_freq;
+    const int f = static_cast<int>(t - i * n_freq);
+    const int64_t n_rays = static_cast<int64_t>(n_angles) * n_freq;
+    const double* xp = x + i * n_rays + f;
+    double acc[NM];
+#pragma unroll
+    for (int k = 0; k < NM; ++k) acc[k] = 0.0;
+    int a = 0;
+    for (; a + 4 <= n_angles; a += 4) {
+        const double v0 = __ldg(xp + (int64_t)(a + 0) * n_freq);
+        const double v1 = __ldg(xp + (int64_t)(a + 1) * n_freq);
+        const double v2 = __ldg(xp + (int64_t)(a + 2) * n_freq);
+        const double v3 = __ldg(xp + (int64_t)(a + 3) * n_freq);
+#pragma unroll
+        for (int k = 0; k < NM; ++k) {
+            const double* w = s_wy + k * n_angles + a;
+            acc[k] = fma(w[0], v0, acc[k]);
+            acc[k] = fma(w[1], v1, acc[k]);
+            acc[k] = fma(w[2], v2, acc[k]);
+            acc[k] = fma(w[3], v3, acc[k]);
+        }
+    }
+    for (; a < n_angles; ++a) {
+        const double v = __ldg(xp + (int64_t)a * n_freq);
+#pragma unroll
+        for (int k = 0; k < NM; ++k) acc[k] = fma(s_wy[k * n_angles + a], v, acc[k]);
+    }
+    double* out = mom + i * NM * n_freq + f;
+#pragma unroll
+    for (int k = 0; k < NM; ++k) out[(int64_t)k * n_freq] = acc[k];
+}
+
+// ---- K2b: Out[c][f] = sum_g A[c][g] * B[g][f];  A = mom (rows c = (i,k)), B = rwt ----
+constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
+constexpr int kGemmThreads = (BM / TM) * (BN / TN);  // 256
+
+__global__ void __launch_bounds__(kGemmThreads) redistribute_kernel(const double* __restrict__ A, const double* __restrict__ B,
+                                                                    double* __restrict__ C, const double* __restrict__ gamma,
+                                                                    const double* __restrict__ coeffs, int64_t M, int N, int K,
+                                                                    int n_mom, int fold_gamma) {
+    __shared__ double As[BK][BM + 1];
+    __shared__ double Bs[BK][BN];
+    const int tx = threadIdx.x % (BN / TN);
+    const int ty = threadIdx.x / (BN / TN);
+    const int64_t row0 = static_cast<int64_t>(blockIdx.y) * BM;
+    const int col0 = blockIdx.x * BN;
+    double acc[TM][TN];
+#pragma unroll
+    for (int r = 0; r < TM; ++r)
+#pragma unroll
+        for (int c = 0; c < TN; ++c) acc[r][c] = 0.0;
+
+    for (int k0 = 0; k0 < K; k0 += BK) {
+        // A tile: BM x BK, stored transposed
+        for (int t = threadIdx.x; t < BM * BK; t += kGemmThreads) {
+            const int r = t / BK, kk = t % BK;
+            const int64_t gr = row0 + r;
+            const int gk = k0 + kk;
+            As[kk][r] = (gr < M && gk < K) ? A[gr * K + gk] : 0.0;
+        }
+        for (int t = threadIdx.x; t < BK * BN; t += kGemmThreads) {
+            const int kk = t / BN, c = t % BN;
+            const int gk = k0 + kk, gc = col0 + c;
+            Bs[kk][c] = (gk < K && gc < N) ? B[static_cast<int64_t>(gk) * N + gc] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+            double a[TM], b[TN];
+#pragma unroll
+            for (int r = 0; r < TM; ++r) a[r] = As[kk][ty * TM + r];
+#pragma unroll
+            for (int c = 0; c < TN; ++c) b[c] = Bs[kk][tx + c * (BN / TN)];
+#pragma unroll
+            for (int r = 0; r < TM; ++r)
+#pragma unroll
+                for (int c = 0; c < TN; ++c) acc[r][c] = fma(a[r], b[c], acc[r][c]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < TM; ++r) {
+        const int64_t gr = row0 + ty * TM + r;
+        if (gr >= M) continue;
+        const int64_t i = gr / n_mom;
+        const int k = static_cast<int>(gr - i * n_mom);
+        const double ck = coeffs[k];
+#pragma unroll
+        for (int c = 0; c < TN; ++c) {
+            const int gc = col0 + tx + c * (BN / TN);
+            if (gc >= N) continue;
+            double v = ck * acc[r][c];
+            if (fold_gamma) v *= gamma[i * N + gc];
+            C[gr * N + gc] = v;
+        }
+    }
+}
+
+// S[i,a,f] = sum_k Y_k(a) G[i,k,f]  (* per-ray gamma)  (+ thermal)
+__global__ void expand_kernel(const double* __restrict__ gmom, const double* __restrict__ yb,
+                              const double* __restrict__ gray, const double* __restrict__ thermal,
+                              double* __restrict__ out, int64_t n_total, int n_angles, int n_freq, int n_mom) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= n_total) return;
+    const int64_t n_rays = static_cast<int64_t>(n_angles) * n_freq;
+    const int64_t i = t / n_rays;
+    const int64_t ray = t - i * n_rays;
+    const int a = static_cast<int>(ray / n_freq);
+    const int f = static_cast<int>(ray - static_cast<int64_t>(a) * n_freq);
+    const double* g = gmom + i * n_mom * n_freq + f;
+    double s = 0.0;
+    for (int k = 0; k < n_mom; ++k) s = fma(yb[k * n_angles + a], g[(int64_t)k * n_freq], s);
+    if (gray) s *= gray[t];
+    if (thermal) s += thermal[t];
+    out[t] = s;
+}
+
+template <int NM>
+int launch_moments_t(const Problem& p, const double* x, cudaStream_t s) {
+    const int64_t work = p.n_space * p.n_freq;
+    const unsigned blocks = static_cast<unsigned>((work + kMomThreads - 1) / kMomThreads);
+    const size_t smem = sizeof(double) * NM * p.n_angles;
+    moments_kernel<NM><<<blocks, kMomThreads, smem, s>>>(x, p.wy, p.mom, p.n_space, p.n_angles, p.n_freq);
+    RTK_LAUNCH_CHECK("moments_kernel");
+    return RTK_OK;
+}
+
+}  // namespace
+
+int launch_moments(const Problem& p, const double* x, cudaStream_t s) {
+    switch (p.n_mom) {
+        case 1: return launch_moments_t<1>(p, x, s);
+        case 2: return launch_moments_t<2>(p, x, s);
+        case 3: return launch_moments_t<3>(p, x, s);
+        case 4: return launch_moments_t<4>(p, x, s);
+        case 5: return launch_moments_t<5>(p, x, s);
+        case 6: return launch_moments_t<6>(p, x, s);
+        case 7: return launch_moments_t<7>(p, x, s);
+        case 8: return launch_moments_t<8>(p, x, s);
+        default: return set_error(RTK_EINVAL, "moments: unsupported number of moments");
+    }
+}
+
+int launch_redistribute(const Problem& p, cudaStream_t s) {
+    const int64_t M = p.n_space * p.n_mom;
+    dim3 grid((p.n_freq + BN - 1) / BN, static_cast<unsigned>((M + BM - 1) / BM));
+    redistribute_kernel<<<grid, kGemmThreads, 0, s>>>(p.mom, p.rwt, p.gmom, p.gamma, p.coeffs, M, p.n_freq, p.n_freq,
+                                                      p.n_mom, p.gamma_per_ray ? 0 : 1);
+    RTK_LAUNCH_CHECK("redistribute_kernel");
+    return RTK_OK;
+}
+
+int launch_expand_source(const Problem& p, const double* thermal, double* out, cudaStream_t s) {
+    const unsigned blocks = static_cast<unsigned>((p.n_total + 255) / 256);
+    expand_kernel<<<blocks, 256, 0, s>>>(p.gmom, p.yb, p.gamma_per_ray ? p.gamma : nullptr, thermal, out, p.n_total,
+                                         p.n_angles, p.n_freq, p.n_mom);
+    RTK_LAUNCH_CHECK("expand_kernel");
+    return RTK_OK;
+}
+
+}  // namespace rtk

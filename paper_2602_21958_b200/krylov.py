@@ -1,0 +1,136 @@
+"""GMRES / BiCGStab on the B200 with the reference's semantics (R/krylov.py).
+
+`gmres(apply, b, cfg)` keeps the reference signature.  When `apply` is an
+RTProblem (or `operator(problem)`), the whole solve runs natively: matvec,
+CGS2 Arnoldi, Givens and restarts in librtk_b200 with the Krylov basis in
+HBM; only one Hessenberg column per iteration crosses to the host.  Any
+other callable is called back per matvec with vectors of the same kind as
+`b` (numpy arrays for numpy b, CUDA tensors for CUDA-tensor b) while the
+Krylov vectors still live on the device.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import numpy as np
+
+from paper_2602_21958_b200 import _device, _native
+
+
+@dataclass
+class SolveConfig:
+    method: str = "gmres"
+    rel_tol: float = 1e-12
+    max_iter: int = 1000
+    restart: Optional[int] = None
+    reorthogonalize: bool = False   # Arnoldi is always CGS2 on the device
+
+    def __post_init__(self):
+        if self.rel_tol <= 0:
+            raise ValueError("rel_tol must be positive")
+        if self.max_iter < 1:
+            raise ValueError("max_iter must be >= 1")
+        if self.restart is not None and self.restart < 1:
+            raise ValueError("restart must be >= 1 when given")
+
+
+@dataclass
+class SolveReport:
+    solution: object
+    iterations: int
+    residual_history: list
+    converged: bool
+    method: str
+    breakdown: bool = False
+    true_residual: Optional[float] = None
+    residual_kind: str = "recurrence"
+    matvecs: int = 0
+
+
+def _native_problem(apply):
+    from paper_2602_21958_b200.operator import DeviceOperator, RTProblem
+
+    if isinstance(apply, RTProblem):
+        return apply
+    if isinstance(apply, DeviceOperator):
+        return apply.problem
+    return None
+
+
+def _solve(method: str, apply, b, cfg: SolveConfig) -> SolveReport:
+    lib = _native.lib()
+    torch = _device.require_cuda()
+    n = int(b.numel()) if _device.is_tensor(b) else int(np.asarray(b).size)
+    bd, kind = _device.to_device(b, n)
+    x = _device.empty(n)
+    c = _native.SolveCfg(float(cfg.rel_tol), int(cfg.max_iter), int(cfg.restart or 0), int(cfg.reorthogonalize), 0)
+    rep = _native.SolveRep()
+    cap = int(cfg.max_iter) + 2
+    hist = np.zeros(cap)
+    stream = _device.stream_ptr()
+    problem = _native_problem(apply)
+    if problem is not None and method == "gmres":
+        if problem.n_total != n:
+            raise ValueError(f"expected length {problem.n_total}, got {n}")
+        rc = lib.rtk_gmres_problem(problem.device().h, _device.ptr(bd), _device.ptr(x), ctypes.byref(c),
+                                   ctypes.byref(rep), _device.dptr(hist), cap, stream)
+        _native.check(rc)
+    else:
+        if problem is not None:
+            from paper_2602_21958_b200.operator import apply_A
+
+            def fn_apply(v):
+                return apply_A(problem, v)
+
+            cb_kind = "cuda"
+        else:
+            fn_apply, cb_kind = apply, ("cuda" if kind == "cuda" else "numpy")
+        errors = []
+
+        def cb(ctx, xp, yp, nn, s):
+            try:
+                xv = _device.view(xp, nn)
+                yv = _device.view(yp, nn)
+                if cb_kind == "numpy":
+                    out = np.asarray(fn_apply(xv.cpu().numpy()), dtype=float).reshape(-1)
+                    yv.copy_(torch.from_numpy(out))
+                else:
+                    yv.copy_(fn_apply(xv).reshape(-1))
+                return 0
+            except Exception as e:  # re-raised after the C call returns
+                errors.append(e)
+                return 1
+
+        fn = _native.MATVEC_FN(cb)
+        entry = lib.rtk_gmres if method == "gmres" else lib.rtk_bicgstab
+        rc = entry(fn, None, n, _device.ptr(bd), _device.ptr(x), ctypes.byref(c), ctypes.byref(rep),
+                   _device.dptr(hist), cap, stream)
+        if errors:
+            raise errors[0]
+        _native.check(rc)
+    return SolveReport(solution=_device.from_device(x, kind), iterations=int(rep.iterations),
+                       residual_history=[float(h) for h in hist[: rep.n_history]], converged=bool(rep.converged),
+                       method=method, breakdown=bool(rep.breakdown), true_residual=float(rep.true_residual),
+                       matvecs=int(rep.matvecs))
+
+
+def gmres(apply, b, cfg: SolveConfig) -> SolveReport:
+    """Restarted GMRES, x0 = 0, Givens least squares, 10 tol true-residual guard (R/krylov.py:56-158)."""
+    return _solve("gmres", apply, b, cfg)
+
+
+def bicgstab(apply, b, cfg: SolveConfig) -> SolveReport:
+    """BiCGStab with shadow residual r0 (R/krylov.py:180-256)."""
+    return _solve("bicgstab", apply, b, cfg)
+
+
+def solve_system(apply: Callable, b, cfg: SolveConfig) -> SolveReport:
+    """Dispatch on cfg.method (R/krylov.py:259-266)."""
+    if cfg.method == "gmres":
+        return gmres(apply, b, cfg)
+    if cfg.method == "bicgstab":
+        return bicgstab(apply, b, cfg)
+    raise ValueError(f"unknown method {cfg.method!r}")

@@ -1,0 +1,150 @@
+"""Global operator A = I - Lambda Sigma on the B200 (R/operator.py).
+
+`apply_A(problem, v)` keeps the reference signature (R/operator.py:48-53):
+numpy in -> numpy out (one H2D, the fused device matvec, one D2H), or a torch
+CUDA float64 tensor in -> tensor out with no copies.  The device problem
+(tables + workspace) is uploaded once, on first use, and cached.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from paper_2602_21958_b200 import _device, _native
+from paper_2602_21958_b200.errors import DENSE_CAP_DEFAULT, ResourceLimitError
+from paper_2602_21958_b200.scattering import ScatteringOperator, slab_handle
+
+__all__ = ["DENSE_CAP_DEFAULT", "ResourceLimitError", "RTProblem", "DeviceOperator", "apply_A", "build_rhs",
+           "source_function", "operator", "spectral_radius_estimate", "materialize_A"]
+
+
+@dataclass
+class RTProblem:
+    """Grid, operators and thermal source of one setup (R/operator.py:28-45)."""
+
+    grid: object
+    transfer: object
+    scattering: ScatteringOperator
+    thermal: np.ndarray
+    descriptor: dict = field(default_factory=dict)
+    _handle: object = field(default=None, repr=False, compare=False)
+
+    def __post_init__(self):
+        self.thermal = np.asarray(self.thermal, dtype=float)
+        if self.thermal.size == 1 and self.grid.n_total != 1:
+            self.thermal = np.full(self.grid.n_total, float(self.thermal))
+        if self.thermal.size != self.grid.n_total:
+            raise ValueError("thermal source length does not match the grid")
+
+    @property
+    def n_total(self) -> int:
+        return self.grid.n_total
+
+    def device(self):
+        """The uploaded device operator (built once)."""
+        if self._handle is None:
+            self._handle = slab_handle(self.grid, self.scattering, self.transfer)
+        return self._handle
+
+    def invalidate(self):
+        """Drop the device copy after editing grid/kernel/gamma/formal solver on the host."""
+        self._handle = None
+
+
+class DeviceOperator:
+    """Callable v -> A v bound to a problem; lets gmres() run the fully native path."""
+
+    def __init__(self, problem: RTProblem):
+        self.problem = problem
+
+    def __call__(self, v):
+        return apply_A(self.problem, v)
+
+
+def operator(problem: RTProblem) -> DeviceOperator:
+    return DeviceOperator(problem)
+
+
+def apply_A(problem: RTProblem, v):
+    """v - Lambda(Sigma v), one fused device pass (R/operator.py:48-53)."""
+    n = problem.n_total
+    h = problem.device()
+    lib = _native.lib()
+    if _device.is_tensor(v) and v.is_cuda:
+        x, _ = _device.to_device(v, n)
+        y = _device.empty(n)
+        _native.check(lib.rtk_apply_A(h.h, _device.ptr(x), _device.ptr(y), n, _device.stream_ptr()))
+        return y
+    if _device.is_tensor(v):
+        return apply_A(problem, v.cuda()).cpu()
+    arr = np.ascontiguousarray(np.asarray(v, dtype=float).reshape(-1))
+    if arr.size != n:
+        raise ValueError(f"expected length {n}, got {arr.size}")
+    out = np.empty(n)
+    _native.check(lib.rtk_apply_A_host(h.h, _device.dptr(arr), _device.dptr(out), n, _device.stream_ptr()))
+    return out
+
+
+def build_rhs(problem: RTProblem, override_ones: bool = False, device: bool = False):
+    """Lambda thermal + boundary term, or ones (R/operator.py:56-64)."""
+    n = problem.n_total
+    if override_ones:
+        if device:
+            torch = _device.require_cuda()
+            return torch.ones(n, dtype=torch.float64, device="cuda")
+        return np.ones(n)
+    h = problem.device()
+    h.set_inflow(problem.transfer.inflow)
+    th, _ = _device.to_device(problem.thermal, n)
+    b = _device.empty(n)
+    _native.check(_native.lib().rtk_build_rhs(h.h, _device.ptr(th), _device.ptr(b), n, 0, _device.stream_ptr()))
+    return b if device else b.cpu().numpy()
+
+
+def source_function(problem: RTProblem, intensity):
+    """S = Sigma I + thermal, the quantity the reference never exposes (R/operator.py:35)."""
+    n = problem.n_total
+    h = problem.device()
+    x, kind = _device.to_device(intensity, n)
+    th, _ = _device.to_device(problem.thermal, n)
+    s = _device.empty(n)
+    _native.check(_native.lib().rtk_source_function(h.h, _device.ptr(x), _device.ptr(th), _device.ptr(s), n,
+                                                     _device.stream_ptr()))
+    return _device.from_device(s, kind)
+
+
+def spectral_radius_estimate(problem: RTProblem, iters: int = 50) -> float:
+    """Power iteration on Lambda Sigma = I - A (R/operator.py:89-109), device vectors."""
+    if iters < 1:
+        raise ValueError("iters must be >= 1")
+    torch = _device.require_cuda()
+    rng = np.random.default_rng(12345)
+    v = torch.from_numpy(rng.standard_normal(problem.n_total)).cuda()
+    v /= torch.linalg.vector_norm(v)
+    ratios = []
+    for _ in range(iters):
+        w = v - apply_A(problem, v)
+        norm = float(torch.linalg.vector_norm(w))
+        if norm == 0.0:
+            return 0.0
+        ratios.append(norm)
+        v = w / norm
+    tail = ratios[-min(5, len(ratios)):]
+    return float(np.exp(np.mean(np.log(tail))))
+
+
+def materialize_A(problem: RTProblem, dense_cap: int = DENSE_CAP_DEFAULT) -> np.ndarray:
+    """Dense A by device matvecs on unit vectors (R/operator.py:67-86); tiny grids only."""
+    n = problem.n_total
+    if n > dense_cap:
+        raise ResourceLimitError(f"dense operator of size {n} exceeds cap {dense_cap}")
+    torch = _device.require_cuda()
+    out = np.empty((n, n))
+    e = torch.zeros(n, dtype=torch.float64, device="cuda")
+    for j in range(n):
+        e.zero_()
+        e[j] = 1.0
+        out[:, j] = apply_A(problem, e).cpu().numpy()
+    return out

@@ -1,0 +1,137 @@
+"""GPU parity of the 1D (I - Lambda Sigma) path against the reference goldens and the oracle.
+
+Tolerance (BASELINE north_star): matvec <= 1e-11 relative L2 against the CPU
+oracle on identical seeded inputs; GMRES iterations within +-1 (unrestarted)
+and solution within 1e-7 relative.
+"""
+import numpy as np
+import pytest
+
+import paper_2602_21958_b200 as P
+from paper_2602_21958_b200 import configs
+from oracle import rt_oracle as ro
+from tests import _golden as G
+from tests._problems import oracle_desc, product_from_golden, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+MATVEC_TOL = 1e-11
+
+
+@pytest.mark.parametrize("key", G.CASES)
+def test_operator_pieces_match_reference_goldens(key):
+    z = G.load()
+    p = product_from_golden(key)
+    for v, sv, lv, av in zip(z[f"{key}/v"], z[f"{key}/Sigma_v"], z[f"{key}/Lambda_v"], z[f"{key}/Av"]):
+        assert rel_l2(P.apply_A(p, v), av) <= MATVEC_TOL
+        assert rel_l2(P.apply_scattering(p.scattering, v), sv) <= MATVEC_TOL
+        assert rel_l2(P.apply_transfer(p.transfer, v), lv) <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("key", G.CASES)
+def test_rhs_matches_reference_goldens(key):
+    z = G.load()
+    p = product_from_golden(key)
+    np.testing.assert_allclose(P.build_rhs(p), z[f"{key}/rhs"], rtol=1e-12, atol=1e-15)
+
+
+@pytest.mark.parametrize("key", ["mono", "coherent", "crd", "log_legendre", "log_crd", "cfg1_legendre", "cfg1_crd"])
+def test_gmres_matches_reference_goldens(key):
+    p = product_from_golden(key)
+    for case in G.gmres_cases(key):
+        cfg = P.SolveConfig(rel_tol=case["rel_tol"], max_iter=case["max_iter"], restart=case["restart"])
+        rep = P.gmres(p, case["b"], cfg)
+        assert rep.converged == case["converged"]
+        slack = 1 if case["restart"] is None else 15   # restarted counts: measured noise band
+        assert abs(rep.iterations - case["iterations"]) <= slack, (rep.iterations, case["iterations"])
+        k = min(len(rep.residual_history), len(case["history"]), 100)
+        np.testing.assert_allclose(rep.residual_history[:k], case["history"][:k], rtol=1e-8, atol=1e-13)
+        assert rel_l2(rep.solution, case["solution"]) <= 1e-7
+
+
+@pytest.mark.parametrize("fs", ["ie", "exp_linear", "exp_parabolic"])
+def test_cfg1_dipole_prd_matvec_matches_oracle(fs):
+    p = configs.slab_problem(1, formal_solver=fs)
+    d = oracle_desc(p)
+    rng = np.random.default_rng(21958 + 1)
+    for _ in range(3):
+        v = rng.standard_normal(p.n_total)
+        assert rel_l2(P.apply_A(p, v), ro.apply_A(d, v)) <= MATVEC_TOL
+    assert rel_l2(P.build_rhs(p), ro.build_rhs(d)) <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("fs", ["ie", "exp_linear"])
+def test_cfg2_full_size_matvec_matches_oracle(fs):
+    p = configs.slab_problem(2, formal_solver=fs)
+    d = oracle_desc(p)
+    v = np.random.default_rng(21958 + 2).standard_normal(p.n_total)
+    assert rel_l2(P.apply_A(p, v), ro.apply_A(d, v)) <= MATVEC_TOL
+
+
+def test_torch_tensor_path_equals_numpy_path():
+    import torch
+
+    p = configs.slab_problem(1)
+    v = np.random.default_rng(3).standard_normal(p.n_total)
+    yt = P.apply_A(p, torch.from_numpy(v).cuda())
+    assert yt.is_cuda
+    np.testing.assert_array_equal(yt.cpu().numpy(), P.apply_A(p, v))
+
+
+def test_gamma_zero_gives_identity():
+    p = configs.slab_problem(1)
+    p.scattering.gamma_table = np.zeros_like(p.scattering.gamma_table)
+    p.invalidate()
+    v = np.random.default_rng(4).standard_normal(p.n_total)
+    np.testing.assert_array_equal(P.apply_A(p, v), v)
+
+
+def test_linearity_cfg2():
+    import torch
+
+    p = configs.slab_problem(2)
+    rng = np.random.default_rng(5)
+    u = torch.from_numpy(rng.standard_normal(p.n_total)).cuda()
+    w = torch.from_numpy(rng.standard_normal(p.n_total)).cuda()
+    lhs = P.apply_A(p, 2.5 * u - 1.5 * w)
+    rhs = 2.5 * P.apply_A(p, u) - 1.5 * P.apply_A(p, w)
+    assert float(torch.linalg.vector_norm(lhs - rhs) / torch.linalg.vector_norm(rhs)) <= 1e-13
+
+
+def test_length_mismatch_raises_value_error():
+    p = configs.slab_problem(1)
+    with pytest.raises(ValueError):
+        P.apply_A(p, np.zeros(11))
+
+
+def test_cfg1_gmres_unrestarted_matches_oracle():
+    p = configs.slab_problem(1)
+    d = oracle_desc(p)
+    b = ro.build_rhs(d)
+    ref = ro.gmres(lambda v: ro.apply_A(d, v), b, rel_tol=1e-8, max_iter=2000)
+    rep = P.gmres(p, b, P.SolveConfig(rel_tol=1e-8, max_iter=2000))
+    assert rep.converged and ref.converged
+    assert abs(rep.iterations - ref.iterations) <= 1
+    np.testing.assert_allclose(rep.residual_history[:100], ref.residual_history[:100], rtol=1e-9, atol=1e-14)
+    assert rel_l2(rep.solution, ref.solution) <= 1e-7
+
+
+def test_callable_apply_path_matches_native_path():
+    p = configs.slab_problem(1)
+    b = P.build_rhs(p)
+    cfg = P.SolveConfig(rel_tol=1e-8, max_iter=300)
+    native = P.gmres(p, b, cfg)
+    cb = P.gmres(lambda v: P.apply_A(p, v), b, cfg)
+    assert native.iterations == cb.iterations
+    np.testing.assert_array_equal(native.solution, cb.solution)
+
+
+def test_bicgstab_matches_oracle_on_golden_crd():
+    p = product_from_golden("crd")
+    d = oracle_desc(p)
+    b = ro.build_rhs(d)
+    ref = ro.bicgstab(lambda v: ro.apply_A(d, v), b, rel_tol=1e-12, max_iter=500)
+    rep = P.bicgstab(P.operator(p), b, P.SolveConfig(method="bicgstab", rel_tol=1e-12, max_iter=500))
+    assert rep.converged == ref.converged
+    assert abs(rep.iterations - ref.iterations) <= 1
+    assert rel_l2(rep.solution, ref.solution) <= 1e-7
