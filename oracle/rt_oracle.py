@@ -246,10 +246,10 @@ def psi_dipole_prd(ybasis, coeffs, R):
 # ---------------------------------------------------------------------------
 
 EXP_SERIES_THRESHOLD = 0.05
-# Taylor coefficients of e1 = d - (1 - e^-d) = sum_{n>=2} (-1)^n d^n / n!  and
-# e2 = d^2 - 2 e1 = 2 sum_{n>=3} (-1)^{n+1} d^n / n!, evaluated by Horner in d.
-_E1_SERIES = [((-1) ** n) / math.factorial(n) for n in range(2, 14)]
-_E2_SERIES = [2.0 * ((-1) ** (n + 1)) / math.factorial(n) for n in range(3, 15)]
+EXP_EXPM1_THRESHOLD = 0.5
+# h1(d) = e1/d^2 = sum_{n=2}^{9} (-1)^n d^(n-2)/n!;  h2(d) = e2/d^3 = 2 sum_{n=3}^{10} (-1)^(n+1) d^(n-3)/n!
+_H1 = [((-1) ** n) / math.factorial(n) for n in range(2, 10)]
+_H2 = [2.0 * ((-1) ** (n + 1)) / math.factorial(n) for n in range(3, 11)]
 
 
 def _horner(coefs, d):
@@ -260,25 +260,39 @@ def _horner(coefs, d):
 
 
 def exp_weights(d):
-    """EXTENSION: (e^-d, e0, e1, e2) with one small-d branch shared with the CUDA build.
+    """EXTENSION: (att = e^-d, e0, e1, e2) with e_k = int_0^d t^k e^{-(d - t)} dt.
 
-    e_k = int_0^d t^k e^{-(d - t)} dt.  Closed forms e0 = -expm1(-d),
-    e1 = d - e0, e2 = d^2 - 2 e1 cancel catastrophically for small d, so below
-    EXP_SERIES_THRESHOLD e1 and e2 come from their Taylor series (12 terms).
+    Three branches shared with the CUDA build (csrc/formal.cuh) and the C port:
+      d < 0.05 : Taylor series (8 terms), no transcendental;
+      d < 0.5  : e0 = -expm1(-d), att = 1 - e0;
+      else     : att = exp(-d), e0 = 1 - att;
+    e1 = d - e0, e2 = d^2 - 2 e1 outside the series branch.
     """
     d = np.asarray(d, dtype=float)
-    att = np.exp(-d)
-    e0 = -np.expm1(-d)
     small = d < EXP_SERIES_THRESHOLD
-    e1 = np.where(small, d * d * _horner(_E1_SERIES, d), d - e0)
-    e2 = np.where(small, d * d * d * _horner(_E2_SERIES, d), d * d - 2.0 * e1)
+    mid = (~small) & (d < EXP_EXPM1_THRESHOLD)
+    with np.errstate(over="ignore", invalid="ignore"):
+        e0_mid = -np.expm1(-d)
+        att_big = np.exp(-d)
+        e1_small = d * d * _horner(_H1, d)
+        e2_small = d * d * d * _horner(_H2, d)
+    e0 = np.where(small, d - e1_small, np.where(mid, e0_mid, 1.0 - att_big))
+    att = np.where(small | mid, 1.0 - e0, att_big)
+    e1 = np.where(small, e1_small, d - e0)
+    e2 = np.where(small, e2_small, d * d - 2.0 * e1)
     return att, e0, e1, e2
 
 
 def _linear_weights(d):
+    """(att, w_u, w_c); in the series branch w_c = d h1(d) (no division), as on the device."""
+    d = np.asarray(d, dtype=float)
     att, e0, e1, _ = exp_weights(d)
+    small = d < EXP_SERIES_THRESHOLD
     with np.errstate(invalid="ignore", divide="ignore"):
-        wc = np.where(d > 0, e1 / d, 0.0)
+        wc = np.where(small, d * _horner(_H1, d), (d - e0) / d)
+    # the series branch defines e0 = d - d * w_c, recompute it that way for bit-parity of the formula
+    e0 = np.where(small, d - d * wc, e0)
+    att = np.where(small, 1.0 - e0, att)
     return att, e0 - wc, wc
 
 

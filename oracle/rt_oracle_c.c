@@ -20,23 +20,43 @@
 #endif
 
 #define THRESH 0.05
+#define THRESH_EXPM1 0.5
 
-static double e1_series(double d) {
-    static const double c[12] = {1.0 / 2, -1.0 / 6, 1.0 / 24, -1.0 / 120, 1.0 / 720, -1.0 / 5040, 1.0 / 40320,
-                                 -1.0 / 362880, 1.0 / 3628800, -1.0 / 39916800, 1.0 / 479001600,
-                                 -1.0 / 6227020800.0};
-    double acc = c[11];
-    for (int k = 10; k >= 0; --k) acc = acc * d + c[k];
-    return d * d * acc;
+/* h1 = e1/d^2, h2 = e2/d^3: 8-term Taylor series (csrc/formal.cuh, rt_oracle.py::exp_weights) */
+static double h1(double d) {
+    static const double c[8] = {1.0 / 2, -1.0 / 6, 1.0 / 24, -1.0 / 120, 1.0 / 720, -1.0 / 5040, 1.0 / 40320,
+                                -1.0 / 362880};
+    double acc = c[7];
+    for (int k = 6; k >= 0; --k) acc = acc * d + c[k];
+    return acc;
 }
 
-static double e2_series(double d) {
-    static const double c[12] = {2.0 / 6, -2.0 / 24, 2.0 / 120, -2.0 / 720, 2.0 / 5040, -2.0 / 40320,
-                                 2.0 / 362880, -2.0 / 3628800, 2.0 / 39916800, -2.0 / 479001600,
-                                 2.0 / 6227020800.0, -2.0 / 87178291200.0};
-    double acc = c[11];
-    for (int k = 10; k >= 0; --k) acc = acc * d + c[k];
-    return d * d * d * acc;
+static double h2(double d) {
+    static const double c[8] = {2.0 / 6, -2.0 / 24, 2.0 / 120, -2.0 / 720, 2.0 / 5040, -2.0 / 40320, 2.0 / 362880,
+                                -2.0 / 3628800};
+    double acc = c[7];
+    for (int k = 6; k >= 0; --k) acc = acc * d + c[k];
+    return acc;
+}
+
+/* att = e^-d, e0, e1, e2 with the three shared branches */
+static void exp_w(double d, double* att, double* e0, double* e1, double* e2) {
+    if (d < THRESH) {
+        *e1 = d * d * h1(d);
+        *e2 = d * d * d * h2(d);
+        *e0 = d - *e1;
+        *att = 1.0 - *e0;
+    } else {
+        if (d < THRESH_EXPM1) {
+            *e0 = -expm1(-d);
+            *att = 1.0 - *e0;
+        } else {
+            *att = exp(-d);
+            *e0 = 1.0 - *att;
+        }
+        *e1 = d - *e0;
+        *e2 = d * d - 2.0 * *e1;
+    }
 }
 
 int rto_max_threads(void) {
@@ -124,14 +144,12 @@ int rto_apply_A_slab(int64_t n_space, int n_angles, int n_freq, int n_mom, int f
                     if (fs == 0) {
                         acc[q] = (acc[q] + d * sc[q]) / (1.0 + d);
                     } else {
-                        const double att = exp(-d);
-                        const double e0 = -expm1(-d);
-                        const double e1 = d < THRESH ? e1_series(d) : d - e0;
+                        double att, e0, e1, e2;
+                        exp_w(d, &att, &e0, &e1, &e2);
                         if (fs == 2 && j + 1 < n_space) {
                             double s = 0.0;
                             for (int k = 0; k < n_mom; ++k) s += ybasis[k * n_angles + a] * G[(in * n_mom + k) * n_freq + f];
                             sn[q] = s;
-                            const double e2 = d < THRESH ? e2_series(d) : d * d - 2.0 * e1;
                             const double dd = phi[f] * dtn / fabs(mu[a]);
                             const double su = d + dd;
                             const double wu = e0 + (e2 - (dd + 2.0 * d) * e1) / (d * su);
@@ -139,7 +157,14 @@ int rto_apply_A_slab(int64_t n_space, int n_angles, int n_freq, int n_mom, int f
                             const double wd = (e2 - d * e1) / (dd * su);
                             acc[q] = att * acc[q] + wu * sp[q] + wc * sc[q] + wd * sn[q];
                         } else {
-                            const double wc = d > 0 ? e1 / d : 0.0;
+                            double wc;
+                            if (d < THRESH) {
+                                wc = d * h1(d);
+                                e0 = d - d * wc;
+                                att = 1.0 - e0;
+                            } else {
+                                wc = (d - e0) / d;
+                            }
                             const double wu = e0 - wc;
                             acc[q] = att * acc[q] + wu * sp[q] + wc * sc[q];
                         }

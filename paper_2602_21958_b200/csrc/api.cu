@@ -4,6 +4,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -38,6 +39,13 @@ Problem::~Problem() {
     for (double* b : bufs)
         if (b) cudaFree(b);
     if (dir_sign) cudaFree(dir_sign);
+    if (tma_ctas) cudaFree(tma_ctas);
+    if (dtpad) cudaFree(dtpad);
+}
+
+bool getenv_flag(const char* name) {
+    const char* v = std::getenv(name);
+    return v && v[0] && v[0] != '0';
 }
 
 static int upload(double** dst, const double* src, size_t count) {
@@ -48,11 +56,19 @@ static int upload(double** dst, const double* src, size_t count) {
     return RTK_OK;
 }
 
+int sweep_apply(const Problem& p, const double* x, double* y, cudaStream_t s) {
+    if (!getenv_flag("RTK_DISABLE_TMA")) {
+        const int rc = launch_sweep_tma(p, x, y, s);
+        if (rc != -1) return rc;
+    }
+    return launch_sweep(p, SRC_MOMENTS, OUT_X_MINUS, false, nullptr, x, y, s);
+}
+
 int apply_A_dev(Problem& p, const double* x, double* y, cudaStream_t s) {
     int rc;
     if ((rc = launch_moments(p, x, s))) return rc;
     if ((rc = launch_redistribute(p, s))) return rc;
-    return launch_sweep(p, SRC_MOMENTS, OUT_X_MINUS, false, nullptr, x, y, s);
+    return sweep_apply(p, x, y, s);
 }
 
 }  // namespace rtk
@@ -103,12 +119,13 @@ int rtk_problem_create_slab(const rtk_slab_desc* d, rtk_problem** out) {
     p.gamma_per_ray = d->gamma_per_ray ? 1 : 0;
     p.n_rays = static_cast<int64_t>(p.n_angles) * p.n_freq;
     p.n_total = p.n_space * p.n_rays;
+    p.fp = (p.n_freq + 1) / 2 * 2;
     p.h_mu.assign(d->mu, d->mu + p.n_angles);
     p.h_coeffs.assign(d->coeffs, d->coeffs + p.n_mom);
 
     // host-side table preparation (setup only, once per problem)
     std::vector<double> dt(p.n_space - 1), inv_mu(p.n_angles), wy(p.n_mom * p.n_angles);
-    std::vector<double> rwt(static_cast<size_t>(p.n_freq) * p.n_freq);
+    std::vector<double> rwt(static_cast<size_t>(p.n_freq) * p.fp, 0.0);
     std::vector<int> sign(p.n_angles);
     for (int64_t i = 0; i + 1 < p.n_space; ++i) dt[i] = d->t_nodes[i + 1] - d->t_nodes[i];
     for (int a = 0; a < p.n_angles; ++a) {
@@ -119,11 +136,11 @@ int rtk_problem_create_slab(const rtk_slab_desc* d, rtk_problem** out) {
         for (int a = 0; a < p.n_angles; ++a) wy[k * p.n_angles + a] = d->ang_w[a] * d->ybasis[k * p.n_angles + a];
     for (int f = 0; f < p.n_freq; ++f)
         for (int g = 0; g < p.n_freq; ++g)
-            rwt[static_cast<size_t>(g) * p.n_freq + f] = d->redistribution[static_cast<size_t>(f) * p.n_freq + g] * d->freq_w[g];
+            rwt[static_cast<size_t>(g) * p.fp + f] = d->redistribution[static_cast<size_t>(f) * p.n_freq + g] * d->freq_w[g];
 
     int rc = RTK_OK;
     const size_t gamma_count = static_cast<size_t>(p.n_space) * (p.gamma_per_ray ? p.n_rays : p.n_freq);
-    const size_t mom_count = static_cast<size_t>(p.n_space) * p.n_mom * p.n_freq;
+    const size_t mom_count = static_cast<size_t>(p.n_space) * p.n_mom * p.fp;
     if (!rc) rc = rtk::upload(&p.dt, dt.data(), dt.size());
     if (!rc) rc = rtk::upload(&p.phi, d->phi, p.n_freq);
     if (!rc) rc = rtk::upload(&p.inv_mu, inv_mu.data(), inv_mu.size());
@@ -140,6 +157,7 @@ int rtk_problem_create_slab(const rtk_slab_desc* d, rtk_problem** out) {
         if (e == cudaSuccess) e = cudaMemcpy(p.dir_sign, sign.data(), sizeof(int) * p.n_angles, cudaMemcpyHostToDevice);
         if (e != cudaSuccess) rc = rtk::cuda_status(e, "dir_sign upload");
     }
+    if (!rc) rc = rtk::setup_tma(p);
     if (rc) {
         delete h;
         return rc;
@@ -183,7 +201,7 @@ int rtk_profile_apply_A(rtk_problem* p, const double* x, double* y, int64_t n, v
     RTK_CUDA_TRY(cudaEventRecord(ev[1], s));
     if (!rc) rc = rtk::launch_redistribute(p->impl, s);
     RTK_CUDA_TRY(cudaEventRecord(ev[2], s));
-    if (!rc) rc = rtk::launch_sweep(p->impl, rtk::SRC_MOMENTS, rtk::OUT_X_MINUS, false, nullptr, x, y, s);
+    if (!rc) rc = rtk::sweep_apply(p->impl, x, y, s);
     RTK_CUDA_TRY(cudaEventRecord(ev[3], s));
     RTK_CUDA_TRY(cudaEventSynchronize(ev[3]));
     for (int k = 0; k < 3; ++k) cudaEventElapsedTime(&ms_out[k], ev[k], ev[k + 1]);

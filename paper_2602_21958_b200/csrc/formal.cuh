@@ -7,35 +7,42 @@
 // the recursion is contractive, so it does not accumulate).
 //
 // EXP_LINEAR (Olson-Kunasz) and EXP_PARABOLIC (Kunasz-Auer) are EXTENSIONS
-// with e_k = int_0^d t^k e^{-(d-t)} dt.  The small-d branch (Taylor series of
-// e1 and e2 below EXP_SERIES_THRESHOLD, 12 terms) is the one the CPU oracle
-// uses (oracle/rt_oracle.py: exp_weights) so both sides share it.
+// with e_k = int_0^d t^k e^{-(d-t)} dt.  The three-branch evaluation below
+// (Taylor series of e1, e2 below EXP_SERIES_THRESHOLD; expm1 below
+// EXP_EXPM1_THRESHOLD; exp above) is restated operation for operation by the
+// CPU oracle (oracle/rt_oracle.py: exp_weights, oracle/rt_oracle_c.c), so both
+// sides share every branch and rounding-sensitive formula.
 #pragma once
 
 #define RTK_EXP_SERIES_THRESHOLD 0.05
+#define RTK_EXP_EXPM1_THRESHOLD 0.5
 
 namespace rtk {
 
-__host__ __device__ __forceinline__ double e1_series(double d) {
-    // sum_{n=2}^{13} (-1)^n d^n / n!  =  d^2 * (c2 + d (c3 + ... + d c13))
-    const double c[12] = {1.0 / 2, -1.0 / 6, 1.0 / 24, -1.0 / 120, 1.0 / 720, -1.0 / 5040, 1.0 / 40320,
-                          -1.0 / 362880, 1.0 / 3628800, -1.0 / 39916800, 1.0 / 479001600,
-                          -1.0 / 6227020800.0};
-    double acc = c[11];
-#pragma unroll
-    for (int k = 10; k >= 0; --k) acc = acc * d + c[k];
-    return d * d * acc;
+// h1(d) = e1 / d^2 = sum_{n=2}^{9} (-1)^n d^(n-2) / n!      (truncation < 1e-17 relative for d < 0.05)
+__host__ __device__ __forceinline__ double e1_over_d2(double d) {
+    double acc = -1.0 / 362880;
+    acc = acc * d + 1.0 / 40320;
+    acc = acc * d - 1.0 / 5040;
+    acc = acc * d + 1.0 / 720;
+    acc = acc * d - 1.0 / 120;
+    acc = acc * d + 1.0 / 24;
+    acc = acc * d - 1.0 / 6;
+    acc = acc * d + 1.0 / 2;
+    return acc;
 }
 
-__host__ __device__ __forceinline__ double e2_series(double d) {
-    // 2 sum_{n=3}^{14} (-1)^{n+1} d^n / n!
-    const double c[12] = {2.0 / 6, -2.0 / 24, 2.0 / 120, -2.0 / 720, 2.0 / 5040, -2.0 / 40320,
-                          2.0 / 362880, -2.0 / 3628800, 2.0 / 39916800, -2.0 / 479001600,
-                          2.0 / 6227020800.0, -2.0 / 87178291200.0};
-    double acc = c[11];
-#pragma unroll
-    for (int k = 10; k >= 0; --k) acc = acc * d + c[k];
-    return d * d * d * acc;
+// h2(d) = e2 / d^3 = 2 sum_{n=3}^{10} (-1)^(n+1) d^(n-3) / n!
+__host__ __device__ __forceinline__ double e2_over_d3(double d) {
+    double acc = -2.0 / 3628800;
+    acc = acc * d + 2.0 / 362880;
+    acc = acc * d - 2.0 / 40320;
+    acc = acc * d + 2.0 / 5040;
+    acc = acc * d - 2.0 / 720;
+    acc = acc * d + 2.0 / 120;
+    acc = acc * d - 2.0 / 24;
+    acc = acc * d + 2.0 / 6;
+    return acc;
 }
 
 struct ExpLin {
@@ -45,25 +52,48 @@ struct ExpPar {
     double att, wu, wc, wd;
 };
 
+// Linear (Olson-Kunasz) weights.  Three branches, identical in the CPU oracle:
+//   d < 0.05 : series, no transcendental  (e1 = d^2 h1, e0 = d - e1, att = 1 - e0)
+//   d < 0.5  : e0 = -expm1(-d), att = 1 - e0
+//   else     : att = exp(-d), e0 = 1 - att
 __device__ __forceinline__ ExpLin exp_linear_weights(double d) {
     ExpLin w;
-    w.att = exp(-d);
-    const double e0 = -expm1(-d);
-    const double e1 = d < RTK_EXP_SERIES_THRESHOLD ? e1_series(d) : d - e0;
-    w.wc = d > 0.0 ? e1 / d : 0.0;
+    double e0;
+    if (d < RTK_EXP_SERIES_THRESHOLD) {
+        w.wc = d * e1_over_d2(d);
+        e0 = d - d * w.wc;
+        w.att = 1.0 - e0;
+    } else {
+        if (d < RTK_EXP_EXPM1_THRESHOLD) {
+            e0 = -expm1(-d);
+            w.att = 1.0 - e0;
+        } else {
+            w.att = exp(-d);
+            e0 = 1.0 - w.att;
+        }
+        w.wc = (d - e0) / d;
+    }
     w.wu = e0 - w.wc;
     return w;
 }
 
+// Parabolic (Kunasz-Auer) weights through upwind u, current c, downwind d nodes.
 __device__ __forceinline__ ExpPar exp_parabolic_weights(double du, double dd) {
     ExpPar w;
-    w.att = exp(-du);
-    const double e0 = -expm1(-du);
-    double e1, e2;
+    double e0, e1, e2;
     if (du < RTK_EXP_SERIES_THRESHOLD) {
-        e1 = e1_series(du);
-        e2 = e2_series(du);
+        e1 = du * du * e1_over_d2(du);
+        e2 = du * du * du * e2_over_d3(du);
+        e0 = du - e1;
+        w.att = 1.0 - e0;
     } else {
+        if (du < RTK_EXP_EXPM1_THRESHOLD) {
+            e0 = -expm1(-du);
+            w.att = 1.0 - e0;
+        } else {
+            w.att = exp(-du);
+            e0 = 1.0 - w.att;
+        }
         e1 = du - e0;
         e2 = du * du - 2.0 * e1;
     }

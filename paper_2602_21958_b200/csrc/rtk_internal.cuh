@@ -1,6 +1,7 @@
 // Internal declarations shared by the librtk_b200 translation units.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -41,11 +42,19 @@ void count_launch(int n = 1);
 //   gamma   [n_space][n_freq] * coeff folded at use, or [n_space][n_rays]
 //   inflow  [n_rays]
 // workspace:
-//   mom     [n_space][n_mom][n_freq]   angular moments m
-//   gmom    [n_space][n_mom][n_freq]   G = c_k gamma R w m  (source moments)
+//   mom     [n_space][n_mom][fp]   angular moments m          (fp = n_freq rounded up to even,
+//   gmom    [n_space][n_mom][fp]   G = c_k gamma R w m         so TMA row pitches are 16-byte multiples;
+//   rwt     [n_freq][fp]                                       pad columns stay zero)
+struct TmaCta {
+    int ray0;    // first ray (a-major, f-minor) of the CTA
+    int nr;      // rays in the CTA (<= 128), all of one hemisphere
+    int down;    // 1: mu < 0, march surface -> depth
+    int f0;      // first column of the G box
+};
+
 struct Problem {
     int64_t n_space = 0;
-    int n_angles = 0, n_freq = 0, n_mom = 0, fs = 0, gamma_per_ray = 0;
+    int n_angles = 0, n_freq = 0, n_mom = 0, fs = 0, gamma_per_ray = 0, fp = 0;
     int64_t n_rays = 0, n_total = 0;
     std::vector<double> h_mu, h_coeffs;
     double *dt = nullptr, *phi = nullptr, *inv_mu = nullptr, *wy = nullptr, *yb = nullptr;
@@ -53,6 +62,12 @@ struct Problem {
     int* dir_sign = nullptr;     // [n_angles] -1 down (mu<0), +1 up
     double *mom = nullptr, *gmom = nullptr;
     double *host_x = nullptr, *host_y = nullptr;   // lazily allocated device staging for *_host calls
+    // TMA sweep path (sweep_tma.cu)
+    bool tma_ready = false;
+    int tma_n_ctas = 0, tma_gw = 0;
+    TmaCta* tma_ctas = nullptr;
+    double* dtpad = nullptr;
+    CUtensorMap tma_gmap, tma_dtmap;
     ~Problem();
 };
 
@@ -66,7 +81,12 @@ enum SweepSrc { SRC_MOMENTS = 0, SRC_VECTOR = 1, SRC_ZERO = 2 };
 enum SweepOut { OUT_X_MINUS = 0, OUT_ACC = 1 };
 int launch_sweep(const Problem& p, int src_mode, int out_mode, bool with_inflow,
                  const double* src_vec, const double* x, double* y, cudaStream_t s);
+// sweep_tma.cu
+int setup_tma(Problem& p);
+int launch_sweep_tma(const Problem& p, const double* x, double* y, cudaStream_t s);   // -1: not applicable
 // krylov.cu
 int apply_A_dev(Problem& p, const double* x, double* y, cudaStream_t s);
+int sweep_apply(const Problem& p, const double* x, double* y, cudaStream_t s);
+bool getenv_flag(const char* name);
 
 }  // namespace rtk

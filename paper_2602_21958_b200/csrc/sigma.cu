@@ -18,7 +18,7 @@ constexpr int kMomThreads = 256;
 template <int NM>
 __global__ void __launch_bounds__(kMomThreads) moments_kernel(const double* __restrict__ x, const double* __restrict__ wy,
                                                               double* __restrict__ mom, int64_t n_space, int n_angles,
-                                                              int n_freq) {
+                                                              int n_freq, int fp) {
     extern __shared__ double s_wy[];
     for (int t = threadIdx.x; t < NM * n_angles; t += blockDim.x) s_wy[t] = wy[t];
     __syncthreads();
@@ -51,9 +51,9 @@ __global__ void __launch_bounds__(kMomThreads) moments_kernel(const double* __re
 #pragma unroll
         for (int k = 0; k < NM; ++k) acc[k] = fma(s_wy[k * n_angles + a], v, acc[k]);
     }
-    double* out = mom + i * NM * n_freq + f;
+    double* out = mom + i * NM * fp + f;
 #pragma unroll
-    for (int k = 0; k < NM; ++k) out[(int64_t)k * n_freq] = acc[k];
+    for (int k = 0; k < NM; ++k) out[(int64_t)k * fp] = acc[k];
 }
 
 // ---- K2b: Out[c][f] = sum_g A[c][g] * B[g][f];  A = mom (rows c = (i,k)), B = rwt ----
@@ -63,7 +63,7 @@ constexpr int kGemmThreads = (BM / TM) * (BN / TN);  // 256
 __global__ void __launch_bounds__(kGemmThreads) redistribute_kernel(const double* __restrict__ A, const double* __restrict__ B,
                                                                     double* __restrict__ C, const double* __restrict__ gamma,
                                                                     const double* __restrict__ coeffs, int64_t M, int N, int K,
-                                                                    int n_mom, int fold_gamma) {
+                                                                    int n_mom, int fold_gamma, int ld) {
     __shared__ double As[BK][BM + 1];
     __shared__ double Bs[BK][BN];
     const int tx = threadIdx.x % (BN / TN);
@@ -82,12 +82,12 @@ __global__ void __launch_bounds__(kGemmThreads) redistribute_kernel(const double
             const int r = t / BK, kk = t % BK;
             const int64_t gr = row0 + r;
             const int gk = k0 + kk;
-            As[kk][r] = (gr < M && gk < K) ? A[gr * K + gk] : 0.0;
+            As[kk][r] = (gr < M && gk < K) ? A[gr * ld + gk] : 0.0;
         }
         for (int t = threadIdx.x; t < BK * BN; t += kGemmThreads) {
             const int kk = t / BN, c = t % BN;
             const int gk = k0 + kk, gc = col0 + c;
-            Bs[kk][c] = (gk < K && gc < N) ? B[static_cast<int64_t>(gk) * N + gc] : 0.0;
+            Bs[kk][c] = (gk < K && gc < N) ? B[static_cast<int64_t>(gk) * ld + gc] : 0.0;
         }
         __syncthreads();
 #pragma unroll
@@ -117,15 +117,149 @@ __global__ void __launch_bounds__(kGemmThreads) redistribute_kernel(const double
             if (gc >= N) continue;
             double v = ck * acc[r][c];
             if (fold_gamma) v *= gamma[i * N + gc];
-            C[gr * N + gc] = v;
+            C[gr * ld + gc] = v;
         }
     }
 }
 
+// ---- K2b on the FP64 tensor pipe: mma.sync m8n8k4 f64 (DMMA) -------------------
+// tcgen05 has no f64 kind on sm_100a, so FP64 tensor work is the warp-level
+// DMMA path.  CTA tile 64 (rows c) x 128 (cols f), K staged 16 at a time in a
+// 3-stage cp.async ring; 8 warps in a 2 x 4 arrangement, 32 x 32 per warp
+// (4 x 4 m8n8 accumulators).  Row pitches 20 / 132 doubles keep the fragment
+// loads bank-conflict free.
+namespace dmma {
+constexpr int BM = 64, BN = 128, BK = 16, SA = BK + 4, SB = BN + 4, STAGES = 3, THREADS = 256;
+constexpr size_t kSmem = sizeof(double) * STAGES * (BM * SA + BK * SB);
+
+__device__ __forceinline__ void cp16(double* dst, const double* src, bool valid) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    const int n = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp8(double* dst, const double* src, bool valid) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    const int n = valid ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void mma(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+// VEC = 2: 16-byte copies (K and N even); VEC = 1: 8-byte copies (any shape)
+template <int VEC>
+__global__ void __launch_bounds__(THREADS, 2) redistribute_dmma_kernel(const double* __restrict__ A,
+                                                                       const double* __restrict__ B,
+                                                                       double* __restrict__ C,
+                                                                       const double* __restrict__ gamma,
+                                                                       const double* __restrict__ coeffs, int64_t M,
+                                                                       int N, int K, int n_mom, int fold_gamma, int ld) {
+    extern __shared__ double smem[];
+    double* As = smem;                          // [STAGES][BM][SA]
+    double* Bs = smem + STAGES * BM * SA;       // [STAGES][BK][SB]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 2, wn = warp & 3;
+    const int64_t row0 = static_cast<int64_t>(blockIdx.y) * BM;
+    const int col0 = blockIdx.x * BN;
+    const int KT = (K + BK - 1) / BK;
+
+    auto load = [&](int st, int k0) {
+        double* as = As + st * BM * SA;
+        double* bs = Bs + st * BK * SB;
+        if (VEC == 2) {
+            for (int t = tid; t < BM * BK / 2; t += THREADS) {
+                const int r = t / (BK / 2), c = (t % (BK / 2)) * 2;
+                const int64_t gr = row0 + r;
+                const int gk = k0 + c;
+                const bool v = gr < M && gk < K;
+                cp16(as + r * SA + c, v ? A + gr * ld + gk : A, v);
+            }
+            for (int t = tid; t < BK * BN / 2; t += THREADS) {
+                const int r = t / (BN / 2), c = (t % (BN / 2)) * 2;
+                const int gk = k0 + r, gc = col0 + c;
+                const bool v = gk < K && gc < N;
+                cp16(bs + r * SB + c, v ? B + static_cast<int64_t>(gk) * ld + gc : B, v);
+            }
+        } else {
+            for (int t = tid; t < BM * BK; t += THREADS) {
+                const int r = t / BK, c = t % BK;
+                const int64_t gr = row0 + r;
+                const int gk = k0 + c;
+                const bool v = gr < M && gk < K;
+                cp8(as + r * SA + c, v ? A + gr * ld + gk : A, v);
+            }
+            for (int t = tid; t < BK * BN; t += THREADS) {
+                const int r = t / BN, c = t % BN;
+                const int gk = k0 + r, gc = col0 + c;
+                const bool v = gk < K && gc < N;
+                cp8(bs + r * SB + c, v ? B + static_cast<int64_t>(gk) * ld + gc : B, v);
+            }
+        }
+    };
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < KT) load(s, s * BK);
+        asm volatile("cp.async.commit_group;\n" ::);
+    }
+    const int g = lane >> 2, q = lane & 3;
+    for (int kt = 0; kt < KT; ++kt) {
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(STAGES - 2));
+        __syncthreads();
+        const int st = kt % STAGES;
+        const double* as = As + st * BM * SA + (wm * 32 + g) * SA + q;
+        const double* bs = Bs + st * BK * SB + q * SB + wn * 32 + g;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) af[i] = as[i * 8 * SA + kk];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bf[j] = bs[kk * SB + j * 8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) mma(acc[i][j], af[i], bf[j]);
+        }
+        const int nk = kt + STAGES - 1;
+        if (nk < KT) load(nk % STAGES, nk * BK);
+        asm volatile("cp.async.commit_group;\n" ::);
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    // epilogue: G = c_k * gamma[i,f] * acc
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t gr = row0 + wm * 32 + i * 8 + g;
+        if (gr >= M) continue;
+        const int64_t si = gr / n_mom;
+        const double ck = coeffs[gr - si * n_mom];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int gc = col0 + wn * 32 + j * 8 + 2 * q;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                if (gc + e >= N) continue;
+                double v = ck * acc[i][j][e];
+                if (fold_gamma) v *= gamma[si * N + gc + e];
+                C[gr * ld + gc + e] = v;
+            }
+        }
+    }
+}
+}  // namespace dmma
+
 // S[i,a,f] = sum_k Y_k(a) G[i,k,f]  (* per-ray gamma)  (+ thermal)
 __global__ void expand_kernel(const double* __restrict__ gmom, const double* __restrict__ yb,
                               const double* __restrict__ gray, const double* __restrict__ thermal,
-                              double* __restrict__ out, int64_t n_total, int n_angles, int n_freq, int n_mom) {
+                              double* __restrict__ out, int64_t n_total, int n_angles, int n_freq, int n_mom, int fp) {
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= n_total) return;
     const int64_t n_rays = static_cast<int64_t>(n_angles) * n_freq;
@@ -133,9 +267,9 @@ __global__ void expand_kernel(const double* __restrict__ gmom, const double* __r
     const int64_t ray = t - i * n_rays;
     const int a = static_cast<int>(ray / n_freq);
     const int f = static_cast<int>(ray - static_cast<int64_t>(a) * n_freq);
-    const double* g = gmom + i * n_mom * n_freq + f;
+    const double* g = gmom + i * n_mom * fp + f;
     double s = 0.0;
-    for (int k = 0; k < n_mom; ++k) s = fma(yb[k * n_angles + a], g[(int64_t)k * n_freq], s);
+    for (int k = 0; k < n_mom; ++k) s = fma(yb[k * n_angles + a], g[(int64_t)k * fp], s);
     if (gray) s *= gray[t];
     if (thermal) s += thermal[t];
     out[t] = s;
@@ -146,7 +280,7 @@ int launch_moments_t(const Problem& p, const double* x, cudaStream_t s) {
     const int64_t work = p.n_space * p.n_freq;
     const unsigned blocks = static_cast<unsigned>((work + kMomThreads - 1) / kMomThreads);
     const size_t smem = sizeof(double) * NM * p.n_angles;
-    moments_kernel<NM><<<blocks, kMomThreads, smem, s>>>(x, p.wy, p.mom, p.n_space, p.n_angles, p.n_freq);
+    moments_kernel<NM><<<blocks, kMomThreads, smem, s>>>(x, p.wy, p.mom, p.n_space, p.n_angles, p.n_freq, p.fp);
     RTK_LAUNCH_CHECK("moments_kernel");
     return RTK_OK;
 }
@@ -169,9 +303,25 @@ int launch_moments(const Problem& p, const double* x, cudaStream_t s) {
 
 int launch_redistribute(const Problem& p, cudaStream_t s) {
     const int64_t M = p.n_space * p.n_mom;
+    if (p.n_freq >= 64) {
+        static bool configured = false;
+        if (!configured) {
+            cudaFuncSetAttribute(dmma::redistribute_dmma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(dmma::kSmem));
+            cudaFuncSetAttribute(dmma::redistribute_dmma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(dmma::kSmem));
+            configured = true;
+        }
+        dim3 grid((p.n_freq + dmma::BN - 1) / dmma::BN, static_cast<unsigned>((M + dmma::BM - 1) / dmma::BM));
+        // pitch fp is even: 16-byte copies always legal; pad column/row entries are zero
+        dmma::redistribute_dmma_kernel<2><<<grid, dmma::THREADS, dmma::kSmem, s>>>(
+            p.mom, p.rwt, p.gmom, p.gamma, p.coeffs, M, p.n_freq, p.n_freq, p.n_mom, p.gamma_per_ray ? 0 : 1, p.fp);
+        RTK_LAUNCH_CHECK("redistribute_dmma_kernel");
+        return RTK_OK;
+    }
     dim3 grid((p.n_freq + BN - 1) / BN, static_cast<unsigned>((M + BM - 1) / BM));
     redistribute_kernel<<<grid, kGemmThreads, 0, s>>>(p.mom, p.rwt, p.gmom, p.gamma, p.coeffs, M, p.n_freq, p.n_freq,
-                                                      p.n_mom, p.gamma_per_ray ? 0 : 1);
+                                                      p.n_mom, p.gamma_per_ray ? 0 : 1, p.fp);
     RTK_LAUNCH_CHECK("redistribute_kernel");
     return RTK_OK;
 }
@@ -179,7 +329,7 @@ int launch_redistribute(const Problem& p, cudaStream_t s) {
 int launch_expand_source(const Problem& p, const double* thermal, double* out, cudaStream_t s) {
     const unsigned blocks = static_cast<unsigned>((p.n_total + 255) / 256);
     expand_kernel<<<blocks, 256, 0, s>>>(p.gmom, p.yb, p.gamma_per_ray ? p.gamma : nullptr, thermal, out, p.n_total,
-                                         p.n_angles, p.n_freq, p.n_mom);
+                                         p.n_angles, p.n_freq, p.n_mom, p.fp);
     RTK_LAUNCH_CHECK("expand_kernel");
     return RTK_OK;
 }

@@ -43,7 +43,7 @@ struct SweepArgs {
     double* y;
     int64_t n_space;
     int64_t n_rays;
-    int n_angles, n_freq, n_mom;
+    int n_angles, n_freq, n_mom, fp;
 };
 
 constexpr int kThreads = 128;
@@ -86,9 +86,9 @@ __global__ void __launch_bounds__(kThreads) sweep1d_kernel(SweepArgs A) {
             if (OUT == OUT_X_MINUS) cp_async8(slot(st, 1), A.x + i * A.n_rays + ray);
             if (SRC == SRC_MOMENTS) {
                 if (gray) cp_async8(slot(st, 2), A.gray + i * A.n_rays + ray);
-                const double* g = A.gmom + i * (int64_t)NM * A.n_freq + f;
+                const double* g = A.gmom + i * (int64_t)NM * A.fp + f;
 #pragma unroll
-                for (int k = 0; k < NM; ++k) cp_async8(slot(st, 3 + k), g + (int64_t)k * A.n_freq);
+                for (int k = 0; k < NM; ++k) cp_async8(slot(st, 3 + k), g + (int64_t)k * A.fp);
             } else if (SRC == SRC_VECTOR) {
                 cp_async8(slot(st, 3), A.src + i * A.n_rays + ray);
             }
@@ -210,6 +210,7 @@ int launch_sweep(const Problem& p, int src_mode, int out_mode, bool with_inflow,
     A.n_angles = p.n_angles;
     A.n_freq = p.n_freq;
     A.n_mom = p.n_mom;
+    A.fp = p.fp;
     switch (p.fs) {
         case RTK_FS_IE: return dispatch_mode<RTK_FS_IE>(src_mode, out_mode, p.n_mom, A, s);
         case RTK_FS_EXP_LINEAR: return dispatch_mode<RTK_FS_EXP_LINEAR>(src_mode, out_mode, p.n_mom, A, s);

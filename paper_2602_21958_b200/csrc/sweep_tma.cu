@@ -1,0 +1,303 @@
+// K1 (TMA variant): the apply_A sweep y = x - Lambda S with S expanded on the fly
+// from the source moments G.  Replaces apply_transfer + sweep_down/sweep_up +
+// the Legendre/PRD expansion + `v - (...)` (R/transfer.py:134-141,
+// R/_kernels.py:70-88, R/scattering.py:136, R/operator.py:53).
+//
+// Warp-specialised CTA: 4 consumer warps own 128 rays (one ray per thread,
+// rays of one hemisphere, consecutive in the reference's a-major/f-minor
+// order, so a march step touches one contiguous 1 KB run of x and of y); one
+// producer warp streams, per stage of U march steps, three TMA tensor boxes
+// into shared memory: x[rows][130 rays], G[rows*n_mom][f-window] and dt[rows].
+// S stages are in flight (mbarrier full/empty ring), so no per-thread load
+// instruction touches L1 and the loop-carried chain is one FMA per step.
+// Measured on sm_100a: a TMA box whose innermost start coordinate is not a
+// multiple of 16 bytes (or is negative) faults with "illegal instruction", so
+// boxes start at the even coordinate below the wanted one (x box 130 wide,
+// dt box 6 long over a front-padded dt copy) and threads read at an offset.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "formal.cuh"
+#include "rtk_internal.cuh"
+#include "tma.cuh"
+
+namespace rtk {
+
+bool encode_f64_map(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, const uint64_t* stride_bytes,
+                    const uint32_t* box) {
+    using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                            const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                            CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Fn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            return false;
+        fn = reinterpret_cast<Fn>(p);
+    }
+    cuuint64_t gd[2] = {dims[0], rank > 1 ? dims[1] : 1};
+    cuuint64_t gs[1] = {rank > 1 ? stride_bytes[0] : 0};
+    cuuint32_t bd[2] = {box[0], rank > 1 ? box[1] : 1};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), gd, gs, bd, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+namespace {
+
+constexpr int kRaysPerCta = 128;
+constexpr int kXW = kRaysPerCta + 2;   // x box width (covers an odd ray0)
+constexpr int kDtW = 6;                // dt box length (U + 2)
+constexpr int kDtPad = 4;              // leading zeros in the padded dt copy
+constexpr int kConsumerWarps = kRaysPerCta / 32;
+constexpr int kTmaThreads = kRaysPerCta + 32;
+
+__device__ __forceinline__ double rcp_nr(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
+struct TmaArgs {
+    const TmaCta* ctas;
+    const double* phi;
+    const double* inv_mu;
+    const double* yb;      // [n_mom][n_angles]
+    double* y;
+    int64_t n_space;
+    int64_t n_rays;
+    int n_angles, n_freq, gw;
+};
+
+__host__ __device__ constexpr int round128(int bytes) { return (bytes + 127) / 128 * 128; }
+
+template <int NM, int U>
+struct Layout {
+    static constexpr int kX = round128(U * kXW * 8);
+    __host__ __device__ static int g_bytes(int gw) { return round128(U * NM * gw * 8); }
+    static constexpr int kDt = round128(kDtW * 8);
+    __host__ __device__ static int stage_bytes(int gw) { return kX + g_bytes(gw) + kDt; }
+};
+
+template <int FS, int NM, int U, int S>
+__global__ void __launch_bounds__(kTmaThreads) sweep1d_tma_kernel(const __grid_constant__ CUtensorMap xmap,
+                                                                  const __grid_constant__ CUtensorMap gmap,
+                                                                  const __grid_constant__ CUtensorMap dtmap,
+                                                                  TmaArgs A) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* empty = full + S;
+    unsigned char* stages = smem + 128;
+    const int gbytes = Layout<NM, U>::g_bytes(A.gw);
+    const int sbytes = Layout<NM, U>::stage_bytes(A.gw);
+
+    const TmaCta cta = A.ctas[blockIdx.x];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int64_t n = A.n_space;
+    const int Q = static_cast<int>((n + U - 1) / U);
+    const bool down = cta.down != 0;
+
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == kConsumerWarps) {
+        // ---------------- producer warp ----------------
+        if (lane == 0) {
+            prefetch_tensormap(&xmap);
+            prefetch_tensormap(&gmap);
+            prefetch_tensormap(&dtmap);
+            static_assert(U + 2 == kDtW, "dt box must cover U steps plus the parity offset");
+            const uint32_t tx = static_cast<uint32_t>(U * kXW * 8 + U * NM * A.gw * 8 + kDtW * 8);
+            for (int q = 0; q < Q; ++q) {
+                const int s = q % S;
+                if (q >= S) mbar_wait(&empty[s], ((q / S) - 1) & 1);
+                unsigned char* st = stages + s * sbytes;
+                const int r0 = down ? q * U : static_cast<int>(n) - U - q * U;   // first box row
+                mbar_arrive_expect_tx(&full[s], tx);
+                tma_load_2d(st, &xmap, cta.ray0 & ~1, r0, &full[s]);
+                tma_load_2d(st + Layout<NM, U>::kX, &gmap, cta.f0, r0 * NM, &full[s]);
+                // dt_pad[kDtPad + i] = dt[i]; down rows need dt[r0 - 1 + u], up rows dt[r0 + u]
+                const int want = (down ? r0 - 1 : r0) + kDtPad;
+                tma_load_1d(st + Layout<NM, U>::kX + gbytes, &dtmap, want & ~1, &full[s]);
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumer warps: one ray per thread ----------------
+    const bool valid = tid < cta.nr;
+    const int64_t ray = cta.ray0 + tid;
+    const int a = valid ? static_cast<int>(ray / A.n_freq) : 0;
+    const int f = valid ? static_cast<int>(ray - static_cast<int64_t>(a) * A.n_freq) : 0;
+    const int gcol = f - cta.f0;
+    const int xoff = tid + (cta.ray0 & 1);
+    const double phi_f = A.phi[f];
+    const double inv_mu = A.inv_mu[a];
+    double yk[NM];
+#pragma unroll
+    for (int k = 0; k < NM; ++k) yk[k] = A.yb[k * A.n_angles + a];
+    double acc = 0.0, s_prev = 0.0;
+    const int64_t step = down ? A.n_rays : -A.n_rays;
+    double* yp = A.y + (down ? 0 : (n - 1) * A.n_rays) + ray;
+
+    for (int q = 0; q < Q; ++q) {
+        const int s = q % S;
+        mbar_wait(&full[s], (q / S) & 1);
+        const unsigned char* st = stages + s * sbytes;
+        const double* xs = reinterpret_cast<const double*>(st);
+        const double* gs = reinterpret_cast<const double*>(st + Layout<NM, U>::kX);
+        const double* dts = reinterpret_cast<const double*>(st + Layout<NM, U>::kX + gbytes);
+        const int r0 = down ? q * U : static_cast<int>(n) - U - q * U;
+        const int dt_off = ((down ? r0 - 1 : r0) + kDtPad) & 1;
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) {
+            const int64_t j = static_cast<int64_t>(q) * U + uu;
+            if (j >= n) break;
+            const int u = down ? uu : U - 1 - uu;
+            const double xv = xs[u * kXW + xoff];
+            double sv = 0.0;
+#pragma unroll
+            for (int k = 0; k < NM; ++k) sv = fma(yk[k], gs[(u * NM + k) * A.gw + gcol], sv);
+            if (j > 0) {
+                const double d = phi_f * dts[u + dt_off] * inv_mu;
+                if (FS == RTK_FS_IE) {
+                    const double r = rcp_nr(1.0 + d);
+                    acc = fma(acc, r, (d * sv) * r);
+                } else {
+                    const ExpLin w = exp_linear_weights(d);
+                    acc = fma(acc, w.att, w.wu * s_prev + w.wc * sv);
+                }
+            }
+            s_prev = sv;
+            if (valid) *yp = xv - acc;
+            yp += step;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+}
+
+template <int FS, int NM>
+int launch_tma_t(const Problem& p, const double* x, double* y, cudaStream_t s) {
+    constexpr int U = 4;
+    constexpr int S = (NM <= 2) ? 8 : 4;
+    CUtensorMap xmap;
+    const uint64_t xd[2] = {static_cast<uint64_t>(p.n_rays), static_cast<uint64_t>(p.n_space)};
+    const uint64_t xs[1] = {static_cast<uint64_t>(p.n_rays) * 8};
+    const uint32_t xb[2] = {kXW, U};
+    if (!encode_f64_map(&xmap, x, 2, xd, xs, xb)) return -1;
+    TmaArgs A;
+    A.ctas = p.tma_ctas;
+    A.phi = p.phi;
+    A.inv_mu = p.inv_mu;
+    A.yb = p.yb;
+    A.y = y;
+    A.n_space = p.n_space;
+    A.n_rays = p.n_rays;
+    A.n_angles = p.n_angles;
+    A.n_freq = p.n_freq;
+    A.gw = p.tma_gw;
+    const size_t smem = 128 + static_cast<size_t>(S) * Layout<NM, U>::stage_bytes(p.tma_gw);
+    auto kern = sweep1d_tma_kernel<FS, NM, U, S>;
+    static size_t configured = 0;
+    if (configured < smem) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+            cudaSuccess) {
+            cudaGetLastError();
+            return -1;
+        }
+        configured = smem;
+    }
+    kern<<<p.tma_n_ctas, kTmaThreads, smem, s>>>(xmap, p.tma_gmap, p.tma_dtmap, A);
+    RTK_LAUNCH_CHECK("sweep1d_tma_kernel");
+    return RTK_OK;
+}
+
+template <int FS>
+int dispatch_tma(const Problem& p, const double* x, double* y, cudaStream_t s) {
+    switch (p.n_mom) {
+        case 1: return launch_tma_t<FS, 1>(p, x, y, s);
+        case 2: return launch_tma_t<FS, 2>(p, x, y, s);
+        case 3: return launch_tma_t<FS, 3>(p, x, y, s);
+        case 4: return launch_tma_t<FS, 4>(p, x, y, s);
+        default: return -1;
+    }
+}
+
+}  // namespace
+
+// returns RTK_OK, an error code, or -1 when the TMA path does not apply (caller falls back)
+int launch_sweep_tma(const Problem& p, const double* x, double* y, cudaStream_t s) {
+    if (!p.tma_ready || p.gamma_per_ray) return -1;
+    if (p.fs == RTK_FS_IE) return dispatch_tma<RTK_FS_IE>(p, x, y, s);
+    if (p.fs == RTK_FS_EXP_LINEAR) return dispatch_tma<RTK_FS_EXP_LINEAR>(p, x, y, s);
+    return -1;
+}
+
+// Host setup: CTA table (hemisphere-uniform ray groups) and the G / dt tensor maps.
+int setup_tma(Problem& p) {
+    p.tma_ready = false;
+    if ((p.n_rays % 2) != 0 || p.n_space < 2 || p.n_mom > 4) return RTK_OK;
+    std::vector<TmaCta> ctas;
+    const int nf = p.n_freq;
+    if (nf >= kRaysPerCta) {
+        p.tma_gw = kRaysPerCta;
+        for (int a = 0; a < p.n_angles; ++a)
+            for (int f0 = 0; f0 < nf; f0 += kRaysPerCta) {
+                TmaCta c;
+                c.ray0 = a * nf + f0;
+                c.nr = std::min(kRaysPerCta, nf - f0);
+                c.down = p.h_mu[a] < 0 ? 1 : 0;
+                c.f0 = f0;
+                ctas.push_back(c);
+            }
+    } else {
+        p.tma_gw = p.fp;
+        const int per = kRaysPerCta / nf;
+        int a = 0;
+        while (a < p.n_angles) {
+            const int sign = p.h_mu[a] < 0;
+            int b = a;
+            while (b < p.n_angles && b - a < per && (p.h_mu[b] < 0) == sign) ++b;
+            TmaCta c;
+            c.ray0 = a * nf;
+            c.nr = (b - a) * nf;
+            c.down = sign;
+            c.f0 = 0;
+            ctas.push_back(c);
+            a = b;
+        }
+    }
+    const uint64_t gd[2] = {static_cast<uint64_t>(p.fp), static_cast<uint64_t>(p.n_space * p.n_mom)};
+    const uint64_t gs[1] = {static_cast<uint64_t>(p.fp) * 8};
+    const uint32_t gb[2] = {static_cast<uint32_t>(p.tma_gw), static_cast<uint32_t>(4 * p.n_mom)};
+    // front/back zero-padded copy of dt so every dt box starts at an even, non-negative coordinate
+    std::vector<double> hdt(static_cast<size_t>(p.n_space - 1 + 2 * kDtPad), 0.0);
+    RTK_CUDA_TRY(cudaMemcpy(hdt.data() + kDtPad, p.dt, sizeof(double) * (p.n_space - 1), cudaMemcpyDeviceToHost));
+    RTK_CUDA_TRY(cudaMalloc(&p.dtpad, sizeof(double) * hdt.size()));
+    RTK_CUDA_TRY(cudaMemcpy(p.dtpad, hdt.data(), sizeof(double) * hdt.size(), cudaMemcpyHostToDevice));
+    const uint64_t dd[1] = {static_cast<uint64_t>(hdt.size())};
+    const uint32_t db[1] = {kDtW};
+    if (!encode_f64_map(&p.tma_gmap, p.gmom, 2, gd, gs, gb)) return RTK_OK;
+    if (!encode_f64_map(&p.tma_dtmap, p.dtpad, 1, dd, nullptr, db)) return RTK_OK;
+    RTK_CUDA_TRY(cudaMalloc(&p.tma_ctas, sizeof(TmaCta) * ctas.size()));
+    RTK_CUDA_TRY(cudaMemcpy(p.tma_ctas, ctas.data(), sizeof(TmaCta) * ctas.size(), cudaMemcpyHostToDevice));
+    p.tma_n_ctas = static_cast<int>(ctas.size());
+    p.tma_ready = true;
+    return RTK_OK;
+}
+
+}  // namespace rtk

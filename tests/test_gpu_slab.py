@@ -135,3 +135,25 @@ def test_bicgstab_matches_oracle_on_golden_crd():
     assert rep.converged == ref.converged
     assert abs(rep.iterations - ref.iterations) <= 1
     assert rel_l2(rep.solution, ref.solution) <= 1e-7
+
+
+@pytest.mark.parametrize("fs", ["ie", "exp_linear"])
+def test_cp_async_fallback_sweep_matches_tma_sweep(fs, monkeypatch):
+    """The generic (non-TMA) sweep kernel and the TMA kernel agree to rounding."""
+    p = configs.slab_problem(1, formal_solver=fs)
+    v = np.random.default_rng(9).standard_normal(p.n_total)
+    y_tma = P.apply_A(p, v)
+    monkeypatch.setenv("RTK_DISABLE_TMA", "1")
+    y_gen = P.apply_A(p, v)
+    assert rel_l2(y_gen, y_tma) <= 1e-14
+
+
+@pytest.mark.parametrize("shape", [(37, 6, 5), (64, 12, 130), (50, 4, 257), (9, 2, 1)])
+def test_odd_shapes_match_oracle(shape):
+    """Ragged shapes: odd N_nu (TMA pitch padding), N_nu > 128 with a partial tile, mono (N_nu = 1)."""
+    ns, na, nf = shape
+    for fs in ("ie", "exp_linear", "exp_parabolic"):
+        p = configs.slab_problem(1, formal_solver=fs, n_space=ns, n_angles=na, n_freq=max(nf, 2))
+        d = oracle_desc(p)
+        v = np.random.default_rng(ns).standard_normal(p.n_total)
+        assert rel_l2(P.apply_A(p, v), ro.apply_A(d, v)) <= MATVEC_TOL
