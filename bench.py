@@ -135,9 +135,9 @@ class ClockSampler:
 def cpu_port_timing(problem, target_s=12.0, max_steps=30):
     """The oracle's C/OpenMP restatement (oracle/librto.so) on this host's cores."""
     from oracle import cport
-    from tests._problems import oracle_desc
+    from oracle.rt_oracle import desc_from_problem
 
-    port = cport.SlabPort(oracle_desc(problem))
+    port = cport.SlabPort(desc_from_problem(problem))
     rng = np.random.default_rng(7)
     x = rng.standard_normal(problem.n_total)
     y = np.empty_like(x)
@@ -160,11 +160,11 @@ def run_reference(args):
     if rank != 0:
         return
     from oracle import cport
+    from oracle.rt_oracle import desc_from_problem
     from paper_2602_21958_b200 import configs
-    from tests._problems import oracle_desc
 
     problem = configs.slab_problem(CFG, formal_solver=args.formal_solver)
-    port = cport.SlabPort(oracle_desc(problem))
+    port = cport.SlabPort(desc_from_problem(problem))
     x = np.random.default_rng(7).standard_normal(problem.n_total)
     y = np.empty_like(x)
     for _ in range(max(args.warmup, 0)):
@@ -251,7 +251,7 @@ def run_b200(args):
     hbm = float(peaks["hbm_gbs"])
     sweep_bytes = 16 * n + 8 * mom_elems + 8 * g.n_space
     moments_bytes = 8 * n + 8 * mom_elems
-    r_flops = 2.0 * g.n_freq * g.n_freq * mom_elems
+    r_flops = 2.0 * g.n_freq * mom_elems   # 2 N_nu^2 n_mom N_s
     fp64_peak = 37.1  # DMMA TF/s measured by tools/peaks_fp64.cu (profiles/r01_peaks_fp64.json)
     kernels = {
         "sweep": {"ms": kms[2], "bytes": sweep_bytes, "achieved_gbs": sweep_bytes / kms[2] / 1e6,

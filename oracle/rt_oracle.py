@@ -24,7 +24,7 @@ __all__ = [
     "apply_transfer", "boundary_term", "apply_sigma", "apply_A", "build_rhs",
     "materialize", "psi_dipole_prd", "prd_matrix", "legendre_as_general",
     "crd_as_general", "coherent_as_general", "OracleSolveReport", "gmres",
-    "bicgstab", "source_function",
+    "bicgstab", "source_function", "desc_from_problem",
 ]
 
 
@@ -395,6 +395,35 @@ def build_rhs(d: SlabDesc, override_ones: bool = False) -> np.ndarray:
 def source_function(d: SlabDesc, intensity: np.ndarray) -> np.ndarray:
     """S = Sigma I + thermal (R/scattering.py:126 + R/operator.py:35; no reference helper)."""
     return apply_sigma(d, intensity) + d.thermal
+
+
+def desc_from_problem(problem) -> SlabDesc:
+    """Oracle description of a product-side (paper_2602_21958_b200) RTProblem, read by duck
+    typing: the same setup arrays, with the kernel mapped by this module's own restatement
+    (legendre_as_general / crd_as_general / coherent_as_general), not by product code."""
+    g = problem.grid
+    k = problem.scattering.kernel
+    kind = type(k).__name__
+    phi = np.asarray(g.profile(g.nu_nodes), dtype=float) * np.ones(g.n_freq)
+    if kind in ("LegendreKernel", "DipolePRDKernel"):
+        Y, c, R = legendre_as_general(k.coefficients, g.mu_nodes, g.n_freq)
+        if kind == "DipolePRDKernel":
+            R = np.asarray(k.redistribution, dtype=float)
+        keep = c != 0.0
+        Y, c = Y[keep], c[keep]
+    elif kind == "CRDKernel":
+        Y, c, R = crd_as_general(np.asarray(k.profile(g.nu_nodes), dtype=float) * np.ones(g.n_freq), g.mu_nodes)
+    elif kind == "CoherentKernel":
+        Y, c, R = coherent_as_general(np.asarray(k.profile(g.nu_nodes), dtype=float) * np.ones(g.n_freq),
+                                      g.frequency_weights, g.mu_nodes)
+    else:
+        raise TypeError(kind)
+    return SlabDesc(t_nodes=g.t_nodes, mu=g.mu_nodes, ang_w=g.angular_weights, nu=g.nu_nodes,
+                    freq_w=g.frequency_weights, phi=phi, ybasis=Y, coeffs=c, R=R,
+                    gamma=np.asarray(problem.scattering.gamma_table, dtype=float),
+                    thermal=np.asarray(problem.thermal, dtype=float),
+                    inflow=np.asarray(problem.transfer.inflow, dtype=float),
+                    formal_solver=problem.transfer.formal_solver)
 
 
 def materialize(apply: Callable[[np.ndarray], np.ndarray], n: int) -> np.ndarray:

@@ -39,12 +39,7 @@ def product_from_golden(key, formal_solver="ie"):
 
 def oracle_desc(problem):
     """Oracle description of a product problem (same arrays, independent arithmetic)."""
-    g = problem.grid
-    Y, c, R = P.separable_form(problem.scattering.kernel, g)
-    return ro.SlabDesc(t_nodes=g.t_nodes, mu=g.mu_nodes, ang_w=g.angular_weights, nu=g.nu_nodes,
-                       freq_w=g.frequency_weights, phi=g.profile_values(), ybasis=Y, coeffs=c, R=R,
-                       gamma=problem.scattering.gamma_table, thermal=problem.thermal,
-                       inflow=problem.transfer.inflow, formal_solver=problem.transfer.formal_solver)
+    return ro.desc_from_problem(problem)
 
 
 def rel_l2(a, b):
