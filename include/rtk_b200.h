@@ -67,6 +67,45 @@ typedef struct rtk_slab_desc {
     const double* inflow;         /* [n_angles*n_freq] boundary intensity per ray, or NULL for 0 (R/transfer.py:101-103) */
 } rtk_slab_desc;
 
+/* unknown layout of lattice problems */
+#define RTK_LAYOUT_INTENSITY 0
+#define RTK_LAYOUT_MOMENTS 1
+
+/*
+ * Periodic-lattice long characteristics on a 2D slab (ny = 1, y-invariant,
+ * periodic in x) or a 3D box (periodic in x and y): BASELINE configs 3-5.
+ * Generalises the reference's 2D long characteristics (R/multidim.py:127-360;
+ * operator defined in oracle/lattice.py and DESIGN.md section 11).  Nodes
+ * s = (k*ny + j)*nx + i, k = 0 the top layer.  Unknown layout:
+ *   RTK_LAYOUT_INTENSITY: I[s][a][f]  (n_total = n_space*n_dirs*n_freq)
+ *   RTK_LAYOUT_MOMENTS:   u[s][l][f]  redistributed angular moments
+ *                         u = sum_g R w_g m,  m = sum_a w_a Y_l(a) I
+ *                         (n_total = n_space*n_moments*n_freq);
+ *                         S[s][a][f] = gamma[s][f] sum_l coeffs[l] Y_l(a) u[s][l][f].
+ * For lattice problems rtk_build_rhs takes thermal as [n_space][n_freq]
+ * (isotropic thermal source).
+ */
+typedef struct rtk_lattice_desc {
+    int32_t nx, ny, nz;
+    int32_t n_dirs;
+    int32_t n_freq;
+    int32_t n_moments;            /* 1..RTK_MAX_MOMENTS */
+    int32_t formal_solver;        /* RTK_FS_IE or RTK_FS_EXP_LINEAR */
+    int32_t layout;               /* RTK_LAYOUT_* */
+    double dx, dy, dz;
+    const double* omega;          /* [n_dirs][3] unit vectors, omega_z != 0 */
+    const double* dir_w;          /* [n_dirs] quadrature weights */
+    const double* phi;            /* [n_freq] */
+    const double* freq_w;         /* [n_freq] */
+    const double* ybasis;         /* [n_moments][n_dirs] */
+    const double* coeffs;         /* [n_moments] */
+    const double* redistribution; /* [n_freq][n_freq] */
+    const double* gamma;          /* [n_space][n_freq] */
+    const double* chi;            /* [n_space] frequency-integrated opacity at nodes */
+    const double* inflow_top;     /* [n_freq] incident on omega_z < 0 rays at k = 0, or NULL (0) */
+    const double* inflow_bottom;  /* [n_freq] incident on omega_z > 0 rays at k = nz-1, or NULL (0) */
+} rtk_lattice_desc;
+
 const char* rtk_last_error_message(void);
 int rtk_version(void);
 /* Number of this library's kernels launched since load (bench / evidence counter). */
@@ -78,6 +117,9 @@ int64_t rtk_kernel_launch_count(void);
  * (R/grid.py:115-150, R/transfer.py:88-104, R/scattering.py:85-100,
  * R/operator.py:28-45). */
 int rtk_problem_create_slab(const rtk_slab_desc* desc, rtk_problem** out);
+/* Multi-D lattice problem (configs 3-5); replaces CartesianGrid2D + build_transfer_2d
+ * + build_scattering + RTProblem for the multi-D path (R/multidim.py:33-81, 322-360). */
+int rtk_problem_create_lattice(const rtk_lattice_desc* desc, rtk_problem** out);
 int rtk_problem_destroy(rtk_problem* p);
 int64_t rtk_problem_n_total(const rtk_problem* p);
 /* Re-upload inflow after a host-side edit (T/test_operator.py:88-110 mutate it). */

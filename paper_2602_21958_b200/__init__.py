@@ -23,6 +23,8 @@ from paper_2602_21958_b200.operator import (DeviceOperator, RTProblem, apply_A, 
                                             source_function, spectral_radius_estimate)
 from paper_2602_21958_b200.krylov import SolveConfig, SolveReport, bicgstab, gmres, solve_system
 from paper_2602_21958_b200.redistribution import gaussian_profile, prd_matrix
+from paper_2602_21958_b200.lattice import (LatticeProblem, dipole_harmonics, lattice_apply_A, lattice_build_rhs,
+                                           lattice_problem, product_quadrature)
 
 __all__ = [
     "DENSE_CAP_DEFAULT", "CoverageError", "ResourceLimitError",
@@ -36,4 +38,6 @@ __all__ = [
     "spectral_radius_estimate",
     "SolveConfig", "SolveReport", "bicgstab", "gmres", "solve_system",
     "gaussian_profile", "prd_matrix",
+    "LatticeProblem", "dipole_harmonics", "lattice_apply_A", "lattice_build_rhs", "lattice_problem",
+    "product_quadrature",
 ]

@@ -77,6 +77,7 @@ SIGNATURES = [
     ("rtk_version", ctypes.c_int, []),
     ("rtk_kernel_launch_count", _I64, []),
     ("rtk_problem_create_slab", ctypes.c_int, [ctypes.POINTER(SlabDesc), ctypes.POINTER(_P)]),
+    ("rtk_problem_create_lattice", ctypes.c_int, [_P, ctypes.POINTER(_P)]),
     ("rtk_problem_destroy", ctypes.c_int, [_P]),
     ("rtk_problem_n_total", _I64, [_P]),
     ("rtk_problem_set_inflow", ctypes.c_int, [_P, _P, _I64]),

@@ -41,6 +41,10 @@ Problem::~Problem() {
     if (dir_sign) cudaFree(dir_sign);
     if (tma_ctas) cudaFree(tma_ctas);
     if (dtpad) cudaFree(dtpad);
+    if (lat_dirs) cudaFree(lat_dirs);
+    double* lat[] = {lat_chi, lat_in_top, lat_in_bot, lat_state[0], lat_state[1], lat_src, lat_zero};
+    for (double* b : lat)
+        if (b) cudaFree(b);
 }
 
 bool getenv_flag(const char* name) {
@@ -48,7 +52,7 @@ bool getenv_flag(const char* name) {
     return v && v[0] && v[0] != '0';
 }
 
-static int upload(double** dst, const double* src, size_t count) {
+int upload(double** dst, const double* src, size_t count) {
     if (count == 0) count = 1;
     RTK_CUDA_TRY(cudaMalloc(dst, count * sizeof(double)));
     if (src) RTK_CUDA_TRY(cudaMemcpy(*dst, src, count * sizeof(double), cudaMemcpyHostToDevice));
@@ -66,6 +70,16 @@ int sweep_apply(const Problem& p, const double* x, double* y, cudaStream_t s) {
 
 int apply_A_dev(Problem& p, const double* x, double* y, cudaStream_t s) {
     int rc;
+    if (p.kind == KIND_LATTICE) {
+        if (p.layout == LAYOUT_MOMENTS) {
+            if ((rc = lattice_transfer_moments(p, 2 /*LSRC_U*/, false, x, p.mom, s))) return rc;
+            return launch_redistribute_ex(p, p.mom, y, p.n_freq, EPI_SUB, x, p.n_freq, s);
+        }
+        if ((rc = launch_moments(p, x, s))) return rc;
+        if ((rc = launch_redistribute(p, s))) return rc;
+        if ((rc = launch_expand_source(p, nullptr, p.lat_src, s))) return rc;
+        return lattice_transfer_intensity(p, 0 /*LSRC_VEC*/, OUT_X_MINUS, false, p.lat_src, x, y, s);
+    }
     if ((rc = launch_moments(p, x, s))) return rc;
     if ((rc = launch_redistribute(p, s))) return rc;
     return sweep_apply(p, x, y, s);
@@ -166,6 +180,77 @@ int rtk_problem_create_slab(const rtk_slab_desc* d, rtk_problem** out) {
     return RTK_OK;
 }
 
+int rtk_problem_create_lattice(const rtk_lattice_desc* d, rtk_problem** out) {
+    if (!d || !out) return set_error(RTK_EINVAL, "null argument");
+    *out = nullptr;
+    if (d->nx < 1 || d->ny < 1 || d->nz < 2) return set_error(RTK_EINVAL, "lattice needs nx, ny >= 1 and nz >= 2");
+    if (d->n_dirs < 1 || d->n_freq < 1) return set_error(RTK_EINVAL, "need at least one direction and frequency");
+    if (d->n_moments < 1 || d->n_moments > RTK_MAX_MOMENTS)
+        return set_error(RTK_EINVAL, "n_moments must be in 1.." + std::to_string(RTK_MAX_MOMENTS));
+    if (d->formal_solver != RTK_FS_IE && d->formal_solver != RTK_FS_EXP_LINEAR)
+        return set_error(RTK_EINVAL, "lattice problems support the IE and exp-linear formal solvers");
+    if (d->layout != RTK_LAYOUT_INTENSITY && d->layout != RTK_LAYOUT_MOMENTS)
+        return set_error(RTK_EINVAL, "unknown layout");
+    if (!(d->dx > 0 && d->dy > 0 && d->dz > 0)) return set_error(RTK_EINVAL, "spacings must be positive");
+    if (!d->omega || !d->dir_w || !d->phi || !d->freq_w || !d->ybasis || !d->coeffs || !d->redistribution ||
+        !d->gamma || !d->chi)
+        return set_error(RTK_EINVAL, "missing description array");
+    for (int a = 0; a < d->n_dirs; ++a)
+        if (d->omega[3 * a + 2] == 0.0) return set_error(RTK_EINVAL, "omega_z = 0 is not an admissible direction");
+    rtk_problem* h = new (std::nothrow) rtk_problem();
+    if (!h) return set_error(RTK_ERESOURCE, "host allocation failed");
+    Problem& p = h->impl;
+    p.kind = rtk::KIND_LATTICE;
+    p.layout = d->layout;
+    p.lat_nx = d->nx;
+    p.lat_ny = d->ny;
+    p.lat_nz = d->nz;
+    p.n_space = static_cast<int64_t>(d->nx) * d->ny * d->nz;
+    p.n_angles = d->n_dirs;
+    p.n_freq = d->n_freq;
+    p.n_mom = d->n_moments;
+    p.fs = d->formal_solver;
+    p.fp = (p.n_freq + 1) / 2 * 2;
+    p.n_rays = static_cast<int64_t>(p.n_angles) * p.n_freq;
+    p.n_total = p.layout == rtk::LAYOUT_MOMENTS ? p.n_space * p.n_mom * p.n_freq : p.n_space * p.n_rays;
+    p.h_coeffs.assign(d->coeffs, d->coeffs + p.n_mom);
+    std::vector<double> wy(p.n_mom * p.n_angles), rwt(static_cast<size_t>(p.n_freq) * p.fp, 0.0);
+    for (int k = 0; k < p.n_mom; ++k)
+        for (int a = 0; a < p.n_angles; ++a) wy[k * p.n_angles + a] = d->dir_w[a] * d->ybasis[k * p.n_angles + a];
+    for (int f = 0; f < p.n_freq; ++f)
+        for (int g = 0; g < p.n_freq; ++g)
+            rwt[static_cast<size_t>(g) * p.fp + f] = d->redistribution[static_cast<size_t>(f) * p.n_freq + g] * d->freq_w[g];
+    const size_t mom_count = static_cast<size_t>(p.n_space) * p.n_mom * p.fp;
+    int rc = RTK_OK;
+    if (!rc) rc = rtk::upload(&p.phi, d->phi, p.n_freq);
+    if (!rc) rc = rtk::upload(&p.wy, wy.data(), wy.size());
+    if (!rc) rc = rtk::upload(&p.yb, d->ybasis, static_cast<size_t>(p.n_mom) * p.n_angles);
+    if (!rc) rc = rtk::upload(&p.rwt, rwt.data(), rwt.size());
+    if (!rc) rc = rtk::upload(&p.gamma, d->gamma, static_cast<size_t>(p.n_space) * p.n_freq);
+    if (!rc) rc = rtk::upload(&p.coeffs, d->coeffs, p.n_mom);
+    if (!rc) rc = rtk::upload(&p.lat_chi, d->chi, p.n_space);
+    if (!rc) rc = rtk::upload(&p.lat_in_top, d->inflow_top, p.n_freq);
+    if (!rc) rc = rtk::upload(&p.lat_in_bot, d->inflow_bottom, p.n_freq);
+    if (!rc) rc = rtk::upload(&p.mom, nullptr, mom_count);
+    if (!rc && p.layout == rtk::LAYOUT_INTENSITY) {
+        rc = rtk::upload(&p.gmom, nullptr, mom_count);
+        if (!rc) rc = rtk::upload(&p.lat_src, nullptr, static_cast<size_t>(p.n_space) * p.n_rays);
+    }
+    if (!rc && p.layout == rtk::LAYOUT_MOMENTS) {
+        const size_t plane = static_cast<size_t>(p.n_angles) * d->nx * d->ny * p.n_freq;
+        rc = rtk::upload(&p.lat_state[0], nullptr, plane);
+        if (!rc) rc = rtk::upload(&p.lat_state[1], nullptr, plane);
+    }
+    if (!rc) rc = rtk::upload(&p.lat_zero, nullptr, static_cast<size_t>(p.n_space) * p.n_freq);
+    if (!rc) rc = rtk::setup_lattice(p, d);
+    if (rc) {
+        delete h;
+        return rc;
+    }
+    *out = h;
+    return RTK_OK;
+}
+
 int rtk_problem_destroy(rtk_problem* p) {
     delete p;
     return RTK_OK;
@@ -175,6 +260,7 @@ int64_t rtk_problem_n_total(const rtk_problem* p) { return p ? p->impl.n_total :
 
 int rtk_problem_set_inflow(rtk_problem* p, const double* inflow_host, int64_t n_rays) {
     if (!p) return set_error(RTK_EINVAL, "null problem handle");
+    if (p->impl.kind == rtk::KIND_LATTICE) return set_error(RTK_EINVAL, "lattice inflow is fixed at creation");
     if (n_rays != p->impl.n_rays) return set_error(RTK_EINVAL, "inflow length must equal n_rays");
     if (inflow_host)
         RTK_CUDA_TRY(cudaMemcpy(p->impl.inflow, inflow_host, sizeof(double) * n_rays, cudaMemcpyHostToDevice));
@@ -194,6 +280,20 @@ int rtk_profile_apply_A(rtk_problem* p, const double* x, double* y, int64_t n, v
     if (rc) return rc;
     if (!ms_out) return set_error(RTK_EINVAL, "null ms_out");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (p->impl.kind == rtk::KIND_LATTICE) {   // whole operator timed as one entry (ms_out[2])
+        cudaEvent_t e0, e1;
+        RTK_CUDA_TRY(cudaEventCreate(&e0));
+        RTK_CUDA_TRY(cudaEventCreate(&e1));
+        RTK_CUDA_TRY(cudaEventRecord(e0, s));
+        rc = rtk::apply_A_dev(p->impl, x, y, s);
+        RTK_CUDA_TRY(cudaEventRecord(e1, s));
+        RTK_CUDA_TRY(cudaEventSynchronize(e1));
+        ms_out[0] = ms_out[1] = 0.0f;
+        cudaEventElapsedTime(&ms_out[2], e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return rc;
+    }
     cudaEvent_t ev[4];
     for (auto& e : ev) RTK_CUDA_TRY(cudaEventCreate(&e));
     RTK_CUDA_TRY(cudaEventRecord(ev[0], s));
@@ -201,7 +301,7 @@ int rtk_profile_apply_A(rtk_problem* p, const double* x, double* y, int64_t n, v
     RTK_CUDA_TRY(cudaEventRecord(ev[1], s));
     if (!rc) rc = rtk::launch_redistribute(p->impl, s);
     RTK_CUDA_TRY(cudaEventRecord(ev[2], s));
-    if (!rc) rc = rtk::sweep_apply(p->impl, x, y, s);
+    if (!rc) rc = p->impl.kind == rtk::KIND_SLAB ? rtk::sweep_apply(p->impl, x, y, s) : RTK_OK;
     RTK_CUDA_TRY(cudaEventRecord(ev[3], s));
     RTK_CUDA_TRY(cudaEventSynchronize(ev[3]));
     for (int k = 0; k < 3; ++k) cudaEventElapsedTime(&ms_out[k], ev[k], ev[k + 1]);
@@ -230,6 +330,7 @@ int rtk_apply_A_host(rtk_problem* p, const double* x_host, double* y_host, int64
 int rtk_apply_sigma(rtk_problem* p, const double* x, double* s_out, int64_t n, void* stream) {
     int rc = check_n(p, n);
     if (rc) return rc;
+    if (p->impl.layout == rtk::LAYOUT_MOMENTS) return set_error(RTK_EINVAL, "apply_sigma needs the intensity layout");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if ((rc = rtk::launch_moments(p->impl, x, s))) return rc;
     if ((rc = rtk::launch_redistribute(p->impl, s))) return rc;
@@ -240,6 +341,7 @@ int rtk_source_function(rtk_problem* p, const double* intensity, const double* t
                         void* stream) {
     int rc = check_n(p, n);
     if (rc) return rc;
+    if (p->impl.kind == rtk::KIND_LATTICE) return set_error(RTK_EINVAL, "source_function is implemented for slabs");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if ((rc = rtk::launch_moments(p->impl, intensity, s))) return rc;
     if ((rc = rtk::launch_redistribute(p->impl, s))) return rc;
@@ -249,6 +351,11 @@ int rtk_source_function(rtk_problem* p, const double* intensity, const double* t
 int rtk_apply_lambda(rtk_problem* p, const double* src, double* y, int64_t n, void* stream) {
     int rc = check_n(p, n);
     if (rc) return rc;
+    if (p->impl.kind == rtk::KIND_LATTICE) {
+        if (p->impl.layout == rtk::LAYOUT_MOMENTS) return set_error(RTK_EINVAL, "apply_lambda needs the intensity layout");
+        return rtk::lattice_transfer_intensity(p->impl, 0, rtk::OUT_ACC, false, src, nullptr, y,
+                                               static_cast<cudaStream_t>(stream));
+    }
     return rtk::launch_sweep(p->impl, rtk::SRC_VECTOR, rtk::OUT_ACC, false, src, nullptr, y,
                              static_cast<cudaStream_t>(stream));
 }
@@ -256,6 +363,7 @@ int rtk_apply_lambda(rtk_problem* p, const double* src, double* y, int64_t n, vo
 int rtk_boundary(rtk_problem* p, double* y, int64_t n, void* stream) {
     int rc = check_n(p, n);
     if (rc) return rc;
+    if (p->impl.kind == rtk::KIND_LATTICE) return rtk_build_rhs(p, nullptr, y, n, 0, stream);
     return rtk::launch_sweep(p->impl, rtk::SRC_ZERO, rtk::OUT_ACC, true, nullptr, nullptr, y,
                              static_cast<cudaStream_t>(stream));
 }
@@ -270,6 +378,14 @@ int rtk_build_rhs(rtk_problem* p, const double* thermal, double* b, int64_t n, i
         RTK_CUDA_TRY(cudaMemcpyAsync(b, ones.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
         RTK_CUDA_TRY(cudaStreamSynchronize(s));
         return RTK_OK;
+    }
+    if (p->impl.kind == rtk::KIND_LATTICE) {
+        const double* th = thermal ? thermal : p->impl.lat_zero;   // [n_space][n_freq] isotropic
+        if (p->impl.layout == rtk::LAYOUT_MOMENTS) {
+            if ((rc = rtk::lattice_transfer_moments(p->impl, 1 /*LSRC_ISO*/, true, th, p->impl.mom, s))) return rc;
+            return rtk::launch_redistribute_ex(p->impl, p->impl.mom, b, p->impl.n_freq, rtk::EPI_PLAIN, nullptr, 0, s);
+        }
+        return rtk::lattice_transfer_intensity(p->impl, 1 /*LSRC_ISO*/, rtk::OUT_ACC, true, th, nullptr, b, s);
     }
     // one recursion carrying the inflow value: Lambda thermal + decay * inflow
     if (thermal)

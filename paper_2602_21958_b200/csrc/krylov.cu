@@ -220,10 +220,51 @@ unsigned elem_blocks(int64_t n) {
 
 // ---------------------------------------------------------------------------
 
+// Stream-ordered allocations from the device's default memory pool, kept cached
+// (release threshold = max), so per-solve buffers cost no cudaMalloc after warm-up.
+int pool_alloc(double** p, size_t count, cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        configured = true;
+    }
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(double) * (count > 0 ? count : 1), s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *p = nullptr;
+        return e == cudaErrorMemoryAllocation ? set_error(RTK_ERESOURCE, "device memory exhausted (Krylov workspace)")
+                                              : cuda_status(e, "cudaMallocAsync");
+    }
+    return RTK_OK;
+}
+
+// One reduction workspace per host thread, reused across solves (its allocation
+// -- cudaMallocHost in particular -- costs milliseconds).
+Workspace& thread_workspace(int* rc) {
+    thread_local Workspace ws;
+    thread_local bool ready = false;
+    *rc = RTK_OK;
+    if (!ready) {
+        *rc = ws.init();
+        ready = (*rc == RTK_OK);
+    }
+    return ws;
+}
+
 class Engine {
    public:
     Engine(cudaStream_t s) : s_(s) {}
-    int init() { return ws_.init(); }
+    int init() {
+        int rc;
+        wsp_ = &thread_workspace(&rc);
+        return rc;
+    }
     cudaStream_t stream() const { return s_; }
 
     // results (dots or norm^2) land in out_dev[0 .. k)
@@ -235,8 +276,8 @@ class Engine {
         P.w = w;
         P.x = nullptr;
         P.n = n;
-        P.partials = ws_.partials;
-        P.counter = ws_.counter;
+        P.partials = wsp_->partials;
+        P.counter = wsp_->counter;
         P.out = out_dev;
         const int blocks = red_blocks(n);
         switch (mode) {
@@ -252,11 +293,11 @@ class Engine {
     // host-visible dot product x.y (fixed-order reduction)
     int dot(const double* x, const double* y, int64_t n, double* out) {
         const double* V[1] = {x};
-        int rc = pass(MODE_DOT, V, 1, nullptr, const_cast<double*>(y), n, ws_.dev_scalars);
+        int rc = pass(MODE_DOT, V, 1, nullptr, const_cast<double*>(y), n, wsp_->dev_scalars);
         if (rc) return rc;
-        RTK_CUDA_TRY(cudaMemcpyAsync(ws_.pinned, ws_.dev_scalars, sizeof(double), cudaMemcpyDeviceToHost, s_));
+        RTK_CUDA_TRY(cudaMemcpyAsync(wsp_->pinned, wsp_->dev_scalars, sizeof(double), cudaMemcpyDeviceToHost, s_));
         RTK_CUDA_TRY(cudaStreamSynchronize(s_));
-        *out = ws_.pinned[0];
+        *out = wsp_->pinned[0];
         return RTK_OK;
     }
     int norm(const double* x, int64_t n, double* out) {
@@ -270,10 +311,10 @@ class Engine {
     // Only one device->host transfer (the column) per step.
     int cgs2(const std::vector<double*>& V, int jp1, double* w, int64_t n, double* col) {
         int rc;
-        if ((rc = ws_.reserve_scalars(2 * jp1 + 1))) return rc;
-        double* h1 = ws_.dev_scalars;
-        double* h2 = ws_.dev_scalars + jp1;
-        double* nrm = ws_.dev_scalars + 2 * jp1;
+        if ((rc = wsp_->reserve_scalars(2 * jp1 + 1))) return rc;
+        double* h1 = wsp_->dev_scalars;
+        double* h2 = wsp_->dev_scalars + jp1;
+        double* nrm = wsp_->dev_scalars + 2 * jp1;
         if (jp1 <= KMAX) {
             // pass 1: h1 = V^T w ; pass 2: w -= V h1, h2 = V^T w ; pass 3: w -= V h2, ||w||^2
             if ((rc = pass(MODE_DOT, V.data(), jp1, nullptr, w, n, h1))) return rc;
@@ -295,12 +336,12 @@ class Engine {
                     return rc;
             }
         }
-        if ((rc = ws_.reserve_pinned(2 * jp1 + 1))) return rc;
-        RTK_CUDA_TRY(cudaMemcpyAsync(ws_.pinned, ws_.dev_scalars, sizeof(double) * (2 * jp1 + 1),
+        if ((rc = wsp_->reserve_pinned(2 * jp1 + 1))) return rc;
+        RTK_CUDA_TRY(cudaMemcpyAsync(wsp_->pinned, wsp_->dev_scalars, sizeof(double) * (2 * jp1 + 1),
                                      cudaMemcpyDeviceToHost, s_));
         RTK_CUDA_TRY(cudaStreamSynchronize(s_));
-        for (int i = 0; i < jp1; ++i) col[i] = ws_.pinned[i] + ws_.pinned[jp1 + i];
-        col[jp1] = std::sqrt(ws_.pinned[2 * jp1]);
+        for (int i = 0; i < jp1; ++i) col[i] = wsp_->pinned[i] + wsp_->pinned[jp1 + i];
+        col[jp1] = std::sqrt(wsp_->pinned[2 * jp1]);
         return RTK_OK;
     }
 
@@ -340,7 +381,7 @@ class Engine {
         return RTK_OK;
     }
 
-    Workspace ws_;
+    Workspace* wsp_ = nullptr;
 
    private:
     cudaStream_t s_;
@@ -348,31 +389,30 @@ class Engine {
 
 struct DevBuf {
     double* p = nullptr;
+    cudaStream_t s = nullptr;
     ~DevBuf() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, s);
     }
-    int alloc(int64_t n) {
-        cudaError_t e = cudaMalloc(&p, sizeof(double) * (n > 0 ? n : 1));
-        if (e != cudaSuccess) return cuda_status(e, "Krylov workspace allocation");
-        return RTK_OK;
+    int alloc(int64_t n, cudaStream_t st) {
+        s = st;
+        return pool_alloc(&p, static_cast<size_t>(n), st);
     }
 };
 
 struct Basis {
     std::vector<double*> v;
+    cudaStream_t s = nullptr;
+    explicit Basis(cudaStream_t st) : s(st) {}
     ~Basis() {
         for (double* p : v)
-            if (p) cudaFree(p);
+            if (p) cudaFreeAsync(p, s);
     }
     int ensure(size_t count, int64_t n) {
         while (v.size() < count) {
             double* p = nullptr;
-            cudaError_t e = cudaMalloc(&p, sizeof(double) * (n > 0 ? n : 1));
-            if (e != cudaSuccess) {
-                cudaGetLastError();
+            if (pool_alloc(&p, static_cast<size_t>(n), s) != RTK_OK)
                 return set_error(RTK_ERESOURCE, "Krylov basis does not fit in device memory (" +
                                                     std::to_string(v.size()) + " vectors allocated)");
-            }
             v.push_back(p);
         }
         return RTK_OK;
@@ -436,11 +476,11 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
         return RTK_OK;
     }
     DevBuf r, w, cand;
-    if ((rc = r.alloc(n)) || (rc = w.alloc(n)) || (rc = cand.alloc(n))) return rc;
+    if ((rc = r.alloc(n, s)) || (rc = w.alloc(n, s)) || (rc = cand.alloc(n, s))) return rc;
     RTK_CUDA_TRY(cudaMemcpyAsync(r.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     int total = 0;
     const int cycle = cfg->restart > 0 ? cfg->restart : cfg->max_iter;
-    Basis V;
+    Basis V(s);
     std::vector<double> col, y;
     auto finish = [&](int iters, bool conv, bool brk, double tr) {
         rep->iterations = iters;
@@ -557,8 +597,8 @@ int bicgstab_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, do
         return RTK_OK;
     }
     DevBuf r, rsh, v, p, sv, t;
-    if ((rc = r.alloc(n)) || (rc = rsh.alloc(n)) || (rc = v.alloc(n)) || (rc = p.alloc(n)) || (rc = sv.alloc(n)) ||
-        (rc = t.alloc(n)))
+    if ((rc = r.alloc(n, s)) || (rc = rsh.alloc(n, s)) || (rc = v.alloc(n, s)) || (rc = p.alloc(n, s)) ||
+        (rc = sv.alloc(n, s)) || (rc = t.alloc(n, s)))
         return rc;
     RTK_CUDA_TRY(cudaMemcpyAsync(r.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     RTK_CUDA_TRY(cudaMemcpyAsync(rsh.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
@@ -684,9 +724,9 @@ int rtk_block_dot(const double* const* vecs_host, int32_t k, const double* w, in
     if (rc) return rc;
     for (int k0 = 0; k0 < k; k0 += rtk::KMAX) {
         const int kc = std::min(rtk::KMAX, k - k0);
-        if ((rc = E.pass(rtk::MODE_DOT, vecs_host + k0, kc, nullptr, const_cast<double*>(w), n, E.ws_.dev_scalars)))
+        if ((rc = E.pass(rtk::MODE_DOT, vecs_host + k0, kc, nullptr, const_cast<double*>(w), n, E.wsp_->dev_scalars)))
             return rc;
-        RTK_CUDA_TRY(cudaMemcpyAsync(out_host + k0, E.ws_.dev_scalars, sizeof(double) * kc, cudaMemcpyDeviceToHost,
+        RTK_CUDA_TRY(cudaMemcpyAsync(out_host + k0, E.wsp_->dev_scalars, sizeof(double) * kc, cudaMemcpyDeviceToHost,
                                      static_cast<cudaStream_t>(stream)));
         RTK_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
     }

@@ -52,7 +52,22 @@ struct TmaCta {
     int f0;      // first column of the G box
 };
 
+// per-direction lattice geometry (lattice.cu)
+struct LatDir {
+    int down;         // Omega_z < 0: enters at the top layer
+    int n_sub;        // sub-segments per layer step
+    double sx, sy;    // horizontal cells moved per layer step
+    double sub_len;   // path length of one sub-segment
+    double wy[8];     // w_a Y_l(a)   (moment accumulation)
+    double cy[8];     // c_l Y_l(a)   (source expansion)
+};
+
+enum ProblemKind { KIND_SLAB = 1, KIND_LATTICE = 2 };
+enum Layout { LAYOUT_INTENSITY = 0, LAYOUT_MOMENTS = 1 };
+
 struct Problem {
+    int kind = KIND_SLAB;
+    int layout = LAYOUT_INTENSITY;
     int64_t n_space = 0;
     int n_angles = 0, n_freq = 0, n_mom = 0, fs = 0, gamma_per_ray = 0, fp = 0;
     int64_t n_rays = 0, n_total = 0;
@@ -67,6 +82,13 @@ struct Problem {
     int tma_n_ctas = 0, tma_gw = 0;
     TmaCta* tma_ctas = nullptr;
     double* dtpad = nullptr;
+    // lattice (multi-D) state
+    int lat_nx = 0, lat_ny = 0, lat_nz = 0;
+    LatDir* lat_dirs = nullptr;
+    double *lat_chi = nullptr, *lat_in_top = nullptr, *lat_in_bot = nullptr;
+    double* lat_state[2] = {nullptr, nullptr};   // [dir][line][freq] line values (moment layout)
+    double* lat_src = nullptr;                   // full source vector (intensity layout)
+    double* lat_zero = nullptr;                  // [n_space][n_freq] zeros (boundary-only RHS)
     CUtensorMap tma_gmap, tma_dtmap;
     ~Problem();
 };
@@ -84,9 +106,20 @@ int launch_sweep(const Problem& p, int src_mode, int out_mode, bool with_inflow,
 // sweep_tma.cu
 int setup_tma(Problem& p);
 int launch_sweep_tma(const Problem& p, const double* x, double* y, cudaStream_t s);   // -1: not applicable
+// lattice.cu
+int setup_lattice(Problem& p, const rtk_lattice_desc* d);
+int lattice_transfer_intensity(const Problem& p, int src_mode, int out_mode, bool with_inflow, const double* src,
+                               const double* x, double* y, cudaStream_t s);
+int lattice_transfer_moments(const Problem& p, int src_mode, bool with_inflow, const double* src, double* mom,
+                             cudaStream_t s);
+// sigma.cu GEMM epilogues: C = c_k gamma acc | c_k acc | U - acc | acc
+enum Epilogue { EPI_GAMMA = 0, EPI_COEF = 1, EPI_SUB = 2, EPI_PLAIN = 3 };
+int launch_redistribute_ex(const Problem& p, const double* A, double* C, int ldc, int epi, const double* U, int ldu,
+                           cudaStream_t s);
 // krylov.cu
 int apply_A_dev(Problem& p, const double* x, double* y, cudaStream_t s);
 int sweep_apply(const Problem& p, const double* x, double* y, cudaStream_t s);
 bool getenv_flag(const char* name);
+int upload(double** dst, const double* src, size_t count);
 
 }  // namespace rtk

@@ -56,6 +56,17 @@ __global__ void __launch_bounds__(kMomThreads) moments_kernel(const double* __re
     for (int k = 0; k < NM; ++k) out[(int64_t)k * fp] = acc[k];
 }
 
+// GEMM epilogues (Epilogue in rtk_internal.cuh)
+__device__ __forceinline__ double epilogue(int epi, double acc, double ck, const double* gamma, int64_t gidx,
+                                           const double* U, int64_t uidx) {
+    switch (epi) {
+        case EPI_GAMMA: return ck * acc * gamma[gidx];
+        case EPI_COEF: return ck * acc;
+        case EPI_SUB: return U[uidx] - acc;
+        default: return acc;
+    }
+}
+
 // ---- K2b: Out[c][f] = sum_g A[c][g] * B[g][f];  A = mom (rows c = (i,k)), B = rwt ----
 constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
 constexpr int kGemmThreads = (BM / TM) * (BN / TN);  // 256
@@ -63,7 +74,8 @@ constexpr int kGemmThreads = (BM / TM) * (BN / TN);  // 256
 __global__ void __launch_bounds__(kGemmThreads) redistribute_kernel(const double* __restrict__ A, const double* __restrict__ B,
                                                                     double* __restrict__ C, const double* __restrict__ gamma,
                                                                     const double* __restrict__ coeffs, int64_t M, int N, int K,
-                                                                    int n_mom, int fold_gamma, int ld) {
+                                                                    int n_mom, int epi, int ld, int ldc,
+                                                                    const double* __restrict__ U, int ldu) {
     __shared__ double As[BK][BM + 1];
     __shared__ double Bs[BK][BN];
     const int tx = threadIdx.x % (BN / TN);
@@ -115,9 +127,7 @@ __global__ void __launch_bounds__(kGemmThreads) redistribute_kernel(const double
         for (int c = 0; c < TN; ++c) {
             const int gc = col0 + tx + c * (BN / TN);
             if (gc >= N) continue;
-            double v = ck * acc[r][c];
-            if (fold_gamma) v *= gamma[i * N + gc];
-            C[gr * ld + gc] = v;
+            C[gr * ldc + gc] = epilogue(epi, acc[r][c], ck, gamma, i * N + gc, U, gr * ldu + gc);
         }
     }
 }
@@ -155,7 +165,8 @@ __global__ void __launch_bounds__(THREADS, 2) redistribute_dmma_kernel(const dou
                                                                        double* __restrict__ C,
                                                                        const double* __restrict__ gamma,
                                                                        const double* __restrict__ coeffs, int64_t M,
-                                                                       int N, int K, int n_mom, int fold_gamma, int ld) {
+                                                                       int N, int K, int n_mom, int epi, int ld, int ldc,
+                                                                       const double* __restrict__ U, int ldu) {
     extern __shared__ double smem[];
     double* As = smem;                          // [STAGES][BM][SA]
     double* Bs = smem + STAGES * BM * SA;       // [STAGES][BK][SB]
@@ -247,9 +258,7 @@ __global__ void __launch_bounds__(THREADS, 2) redistribute_dmma_kernel(const dou
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 if (gc + e >= N) continue;
-                double v = ck * acc[i][j][e];
-                if (fold_gamma) v *= gamma[si * N + gc + e];
-                C[gr * ld + gc + e] = v;
+                C[gr * ldc + gc + e] = epilogue(epi, acc[i][j][e], ck, gamma, si * N + gc + e, U, gr * ldu + gc + e);
             }
         }
     }
@@ -301,29 +310,32 @@ int launch_moments(const Problem& p, const double* x, cudaStream_t s) {
     }
 }
 
-int launch_redistribute(const Problem& p, cudaStream_t s) {
+int launch_redistribute_ex(const Problem& p, const double* A, double* C, int ldc, int epi, const double* U, int ldu,
+                           cudaStream_t s) {
     const int64_t M = p.n_space * p.n_mom;
     if (p.n_freq >= 64) {
         static bool configured = false;
         if (!configured) {
             cudaFuncSetAttribute(dmma::redistribute_dmma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(dmma::kSmem));
-            cudaFuncSetAttribute(dmma::redistribute_dmma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(dmma::kSmem));
             configured = true;
         }
         dim3 grid((p.n_freq + dmma::BN - 1) / dmma::BN, static_cast<unsigned>((M + dmma::BM - 1) / dmma::BM));
         // pitch fp is even: 16-byte copies always legal; pad column/row entries are zero
         dmma::redistribute_dmma_kernel<2><<<grid, dmma::THREADS, dmma::kSmem, s>>>(
-            p.mom, p.rwt, p.gmom, p.gamma, p.coeffs, M, p.n_freq, p.n_freq, p.n_mom, p.gamma_per_ray ? 0 : 1, p.fp);
+            A, p.rwt, C, p.gamma, p.coeffs, M, p.n_freq, p.n_freq, p.n_mom, epi, p.fp, ldc, U, ldu);
         RTK_LAUNCH_CHECK("redistribute_dmma_kernel");
         return RTK_OK;
     }
     dim3 grid((p.n_freq + BN - 1) / BN, static_cast<unsigned>((M + BM - 1) / BM));
-    redistribute_kernel<<<grid, kGemmThreads, 0, s>>>(p.mom, p.rwt, p.gmom, p.gamma, p.coeffs, M, p.n_freq, p.n_freq,
-                                                      p.n_mom, p.gamma_per_ray ? 0 : 1, p.fp);
+    redistribute_kernel<<<grid, kGemmThreads, 0, s>>>(A, p.rwt, C, p.gamma, p.coeffs, M, p.n_freq, p.n_freq, p.n_mom,
+                                                      epi, p.fp, ldc, U, ldu);
     RTK_LAUNCH_CHECK("redistribute_kernel");
     return RTK_OK;
+}
+
+int launch_redistribute(const Problem& p, cudaStream_t s) {
+    return launch_redistribute_ex(p, p.mom, p.gmom, p.fp, p.gamma_per_ray ? EPI_COEF : EPI_GAMMA, nullptr, 0, s);
 }
 
 int launch_expand_source(const Problem& p, const double* thermal, double* out, cudaStream_t s) {

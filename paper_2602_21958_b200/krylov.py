@@ -51,9 +51,10 @@ class SolveReport:
 
 
 def _native_problem(apply):
+    from paper_2602_21958_b200.lattice import LatticeProblem
     from paper_2602_21958_b200.operator import DeviceOperator, RTProblem
 
-    if isinstance(apply, RTProblem):
+    if isinstance(apply, (RTProblem, LatticeProblem)):
         return apply
     if isinstance(apply, DeviceOperator):
         return apply.problem

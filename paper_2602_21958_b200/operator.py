@@ -69,6 +69,10 @@ def operator(problem: RTProblem) -> DeviceOperator:
 
 def apply_A(problem: RTProblem, v):
     """v - Lambda(Sigma v), one fused device pass (R/operator.py:48-53)."""
+    from paper_2602_21958_b200.lattice import LatticeProblem, lattice_apply_A
+
+    if isinstance(problem, LatticeProblem):
+        return lattice_apply_A(problem, v)
     n = problem.n_total
     h = problem.device()
     lib = _native.lib()
@@ -89,7 +93,11 @@ def apply_A(problem: RTProblem, v):
 
 def build_rhs(problem: RTProblem, override_ones: bool = False, device: bool = False):
     """Lambda thermal + boundary term, or ones (R/operator.py:56-64)."""
+    from paper_2602_21958_b200.lattice import LatticeProblem, lattice_build_rhs
+
     n = problem.n_total
+    if isinstance(problem, LatticeProblem) and not override_ones:
+        return lattice_build_rhs(problem, device=device)
     if override_ones:
         if device:
             torch = _device.require_cuda()
