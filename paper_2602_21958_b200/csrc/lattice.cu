@@ -84,22 +84,24 @@ struct LatArgs {
 
 enum LatSrc { LSRC_VEC = 0, LSRC_ISO = 1, LSRC_U = 2 };
 
-// source value at node s (layer-relative index c within layer k) for direction a, frequency f
-template <int SRC>
-__device__ __forceinline__ double node_source(const LatArgs& A, int64_t s, int a, int f, const double* cy) {
+// source value at node s for direction a, frequency f (NM: number of moments, compile-time)
+template <int SRC, int NM>
+__device__ __forceinline__ double node_source(const LatArgs& A, int64_t s, int a, int f, const double (&cy)[NM]) {
     if (SRC == LSRC_VEC) return __ldg(A.src + (s * A.n_dirs + a) * A.n_freq + f);
     if (SRC == LSRC_ISO) return __ldg(A.src + s * A.n_freq + f);
-    const double* u = A.src + s * A.n_mom * A.n_freq + f;
+    const double* u = A.src + s * NM * A.n_freq + f;
     double v = 0.0;
-    for (int l = 0; l < A.n_mom; ++l) v = fma(cy[l], __ldg(u + l * A.n_freq), v);
+#pragma unroll
+    for (int l = 0; l < NM; ++l) v = fma(cy[l], __ldg(u + l * A.n_freq), v);
     return v * __ldg(A.gamma + s * A.n_freq + f);
 }
 
 // One formal-solver pass of a line from layer k to k2 (geometry of direction D),
 // starting at horizontal position (X0, Y0) = line position at the start layer.
-template <int FS, int SRC>
+template <int FS, int SRC, int NM>
 __device__ __forceinline__ double advance_line(const LatArgs& A, const LatDir& D, double acc, double lx, double ly,
-                                               int t, int k, int k2, int a, int f, double phi_f, const double* cy) {
+                                               int t, int k, int k2, int a, int f, double phi_f,
+                                               const double (&cy)[NM]) {
     const int64_t base_a = static_cast<int64_t>(k) * A.nxy;
     const int64_t base_b = static_cast<int64_t>(k2) * A.nxy;
     double prev_s = 0.0, prev_c = 0.0;
@@ -113,14 +115,14 @@ __device__ __forceinline__ double advance_line(const LatArgs& A, const LatDir& D
                           st.w01 * __ldg(A.chi + base_a + st.c01) + st.w11 * __ldg(A.chi + base_a + st.c11);
         const double cb = st.w00 * __ldg(A.chi + base_b + st.c00) + st.w10 * __ldg(A.chi + base_b + st.c10) +
                           st.w01 * __ldg(A.chi + base_b + st.c01) + st.w11 * __ldg(A.chi + base_b + st.c11);
-        const double sa = st.w00 * node_source<SRC>(A, base_a + st.c00, a, f, cy) +
-                          st.w10 * node_source<SRC>(A, base_a + st.c10, a, f, cy) +
-                          st.w01 * node_source<SRC>(A, base_a + st.c01, a, f, cy) +
-                          st.w11 * node_source<SRC>(A, base_a + st.c11, a, f, cy);
-        const double sb = st.w00 * node_source<SRC>(A, base_b + st.c00, a, f, cy) +
-                          st.w10 * node_source<SRC>(A, base_b + st.c10, a, f, cy) +
-                          st.w01 * node_source<SRC>(A, base_b + st.c01, a, f, cy) +
-                          st.w11 * node_source<SRC>(A, base_b + st.c11, a, f, cy);
+        const double sa = st.w00 * node_source<SRC, NM>(A, base_a + st.c00, a, f, cy) +
+                          st.w10 * node_source<SRC, NM>(A, base_a + st.c10, a, f, cy) +
+                          st.w01 * node_source<SRC, NM>(A, base_a + st.c01, a, f, cy) +
+                          st.w11 * node_source<SRC, NM>(A, base_a + st.c11, a, f, cy);
+        const double sb = st.w00 * node_source<SRC, NM>(A, base_b + st.c00, a, f, cy) +
+                          st.w10 * node_source<SRC, NM>(A, base_b + st.c10, a, f, cy) +
+                          st.w01 * node_source<SRC, NM>(A, base_b + st.c01, a, f, cy) +
+                          st.w11 * node_source<SRC, NM>(A, base_b + st.c11, a, f, cy);
         const double c_m = (1 - wz) * ca + wz * cb;
         const double s_m = (1 - wz) * sa + wz * sb;
         if (m > 0) {
@@ -153,8 +155,7 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_kernel(LatArgs A, int
     const int slot = threadIdx.x / kFC;
     const LatDir D = A.dirs[a];
     const double phi_f = fvalid ? A.phi[f] : 0.0;
-    double cy[8];
-    for (int l = 0; l < 8; ++l) cy[l] = (l < A.n_mom) ? D.cy[l] : 0.0;
+    const double cy[1] = {0.0};   // VEC / ISO sources do not expand moments
     double inflow = 0.0;
     if (with_inflow && fvalid) {
         const double* in = D.down ? A.inflow_top : A.inflow_bottom;
@@ -181,15 +182,15 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_kernel(LatArgs A, int
         for (int64_t c = slot; c < A.nxy; c += slots) {
             const double lx = static_cast<double>(c % A.nx), ly = static_cast<double>(c / A.nx);
             double acc = lines[c * kFC + fq];
-            if (fvalid) acc = advance_line<FS, SRC>(A, D, acc, lx, ly, t, k, k2, a, f, phi_f, cy);
+            if (fvalid) acc = advance_line<FS, SRC, 1>(A, D, acc, lx, ly, t, k, k2, a, f, phi_f, cy);
             lines[c * kFC + fq] = acc;
         }
     }
 }
 
 // ---------------- moment layout: layer-synchronous step ----------------
-// thread = (line c, frequency f); loops over all directions.
-template <int FS, int SRC>
+// thread = (line c, frequency f); loops over all directions.  NM moments, compile-time.
+template <int FS, int SRC, int NM>
 __global__ void __launch_bounds__(256) lattice_mom_step_kernel(LatArgs A, int t, const double* __restrict__ st_in,
                                                                 double* __restrict__ st_out, double* __restrict__ mom,
                                                                 int with_inflow, int fp) {
@@ -199,57 +200,66 @@ __global__ void __launch_bounds__(256) lattice_mom_step_kernel(LatArgs A, int t,
     const int64_t c = tid / A.n_freq;
     const int i = static_cast<int>(c % A.nx), j = static_cast<int>(c / A.nx);
     const double phi_f = A.phi[f];
-    const int n_mom = A.n_mom;
-    double m_dn[8], m_up[8];
-    for (int l = 0; l < 8; ++l) m_dn[l] = m_up[l] = 0.0;
+    double m_dn[NM], m_up[NM];
+#pragma unroll
+    for (int l = 0; l < NM; ++l) m_dn[l] = m_up[l] = 0.0;
     const int k_dn = t, k_up = A.nz - 1 - t;
     const int64_t plane = A.nxy * A.n_freq;
+    const double in_top = (with_inflow && A.inflow_top) ? A.inflow_top[f] : 0.0;
+    const double in_bot = (with_inflow && A.inflow_bottom) ? A.inflow_bottom[f] : 0.0;
     for (int a = 0; a < A.n_dirs; ++a) {
-        const LatDir D = A.dirs[a];
+        const LatDir& D = A.dirs[a];
+        const bool down = D.down != 0;
+        const double sx = D.sx, sy = D.sy;
+        double wy[NM], cy[NM];
+#pragma unroll
+        for (int l = 0; l < NM; ++l) {
+            wy[l] = D.wy[l];
+            cy[l] = D.cy[l];
+        }
         const double* sin_a = st_in + a * plane;
         // T_RC gather for node (i, j) at this direction's current layer
         double v;
         if (t == 0) {
-            const double* in = D.down ? A.inflow_top : A.inflow_bottom;
-            v = (with_inflow && in) ? in[f] : 0.0;
+            v = down ? in_top : in_bot;
         } else {
-            const Stencil st = stencil(i - t * D.sx, j - t * D.sy, A.nx, A.ny);
+            const Stencil st = stencil(i - t * sx, j - t * sy, A.nx, A.ny);
             v = st.w00 * sin_a[st.c00 * A.n_freq + f] + st.w10 * sin_a[st.c10 * A.n_freq + f] +
                 st.w01 * sin_a[st.c01 * A.n_freq + f] + st.w11 * sin_a[st.c11 * A.n_freq + f];
         }
-        double* macc = D.down ? m_dn : m_up;
-        for (int l = 0; l < n_mom; ++l) macc[l] = fma(D.wy[l], v, macc[l]);
+        if (down) {
+#pragma unroll
+            for (int l = 0; l < NM; ++l) m_dn[l] = fma(wy[l], v, m_dn[l]);
+        } else {
+#pragma unroll
+            for (int l = 0; l < NM; ++l) m_up[l] = fma(wy[l], v, m_up[l]);
+        }
         // advance own line (c) to the next layer
         if (t < A.nz - 1) {
-            const int k = D.down ? t : A.nz - 1 - t;
-            const int k2 = D.down ? k + 1 : k - 1;
-            double acc;
-            if (t == 0) {
-                const double* in = D.down ? A.inflow_top : A.inflow_bottom;
-                acc = (with_inflow && in) ? in[f] : 0.0;
-            } else {
-                acc = sin_a[c * A.n_freq + f];
-            }
-            acc = advance_line<FS, SRC>(A, D, acc, static_cast<double>(i), static_cast<double>(j), t, k, k2, a, f,
-                                        phi_f, D.cy);
+            const int k = down ? t : A.nz - 1 - t;
+            const int k2 = down ? k + 1 : k - 1;
+            double acc = (t == 0) ? (down ? in_top : in_bot) : sin_a[c * A.n_freq + f];
+            const LatDir Dl = D;
+            acc = advance_line<FS, SRC, NM>(A, Dl, acc, static_cast<double>(i), static_cast<double>(j), t, k, k2, a, f,
+                                            phi_f, cy);
             st_out[a * plane + c * A.n_freq + f] = acc;
         }
     }
     // layer k receives its down part at step k and its up part at step nz-1-k: the later step adds
-    auto put = [&](int k, const double* mv, bool first) {
-        double* out = mom + (static_cast<int64_t>(k) * A.nxy + c) * n_mom * fp + f;   // pitch fp (GEMM operand)
-        for (int l = 0; l < n_mom; ++l) {
-            const double cur = first ? 0.0 : out[static_cast<int64_t>(l) * fp];
-            out[static_cast<int64_t>(l) * fp] = cur + mv[l];
-        }
-    };
+    double* out_dn = mom + (static_cast<int64_t>(k_dn) * A.nxy + c) * NM * fp + f;   // pitch fp (GEMM operand)
+    double* out_up = mom + (static_cast<int64_t>(k_up) * A.nxy + c) * NM * fp + f;
     if (k_dn == k_up) {
-        double both[8];
-        for (int l = 0; l < n_mom; ++l) both[l] = m_dn[l] + m_up[l];
-        put(k_dn, both, true);
+#pragma unroll
+        for (int l = 0; l < NM; ++l) out_dn[static_cast<int64_t>(l) * fp] = m_dn[l] + m_up[l];
     } else {
-        put(k_dn, m_dn, k_dn < k_up ? true : false);
-        put(k_up, m_up, k_up < k_dn ? false : true);
+        // step t is the first visit of both layers t and nz-1-t iff t < nz-1-t
+        const bool first = k_dn < k_up;
+#pragma unroll
+        for (int l = 0; l < NM; ++l) {
+            const int64_t o = static_cast<int64_t>(l) * fp;
+            out_dn[o] = first ? m_dn[l] : out_dn[o] + m_dn[l];
+            out_up[o] = first ? m_up[l] : out_up[o] + m_up[l];
+        }
     }
 }
 
@@ -332,33 +342,47 @@ int lattice_transfer_intensity(const Problem& p, int src_mode, int out_mode, boo
     return set_error(RTK_EINVAL, "lattice: unsupported source/output mode");
 }
 
-// moment layout: mom[s][l][f] = sum_a w_a Y_l(a) (Lambda S)(s, a, f); S from u (SRC_U) or thermal (SRC_ISO)
-int lattice_transfer_moments(const Problem& p, int src_mode, bool with_inflow, const double* src, double* mom,
-                             cudaStream_t s) {
-    LatArgs A = lat_args(p, src, nullptr, nullptr);
+template <int FS, int SRC, int NM>
+static int launch_mom_steps(const Problem& p, const LatArgs& A, bool with_inflow, double* mom, cudaStream_t s) {
     const int64_t threads = A.nxy * A.n_freq;
     const unsigned blocks = static_cast<unsigned>((threads + 255) / 256);
     double* a = p.lat_state[0];
     double* b = p.lat_state[1];
     for (int t = 0; t < A.nz; ++t) {
-        if (p.fs == RTK_FS_IE) {
-            if (src_mode == LSRC_U)
-                lattice_mom_step_kernel<RTK_FS_IE, LSRC_U><<<blocks, 256, 0, s>>>(A, t, a, b, mom, with_inflow, p.fp);
-            else
-                lattice_mom_step_kernel<RTK_FS_IE, LSRC_ISO><<<blocks, 256, 0, s>>>(A, t, a, b, mom, with_inflow, p.fp);
-        } else {
-            if (src_mode == LSRC_U)
-                lattice_mom_step_kernel<RTK_FS_EXP_LINEAR, LSRC_U><<<blocks, 256, 0, s>>>(A, t, a, b, mom, with_inflow, p.fp);
-            else
-                lattice_mom_step_kernel<RTK_FS_EXP_LINEAR, LSRC_ISO><<<blocks, 256, 0, s>>>(A, t, a, b, mom,
-                                                                                            with_inflow, p.fp);
-        }
+        lattice_mom_step_kernel<FS, SRC, NM><<<blocks, 256, 0, s>>>(A, t, a, b, mom, with_inflow ? 1 : 0, p.fp);
         RTK_LAUNCH_CHECK("lattice_mom_step_kernel");
         double* tmp = a;
         a = b;
         b = tmp;
     }
     return RTK_OK;
+}
+
+template <int FS, int SRC>
+static int dispatch_mom_nm(const Problem& p, const LatArgs& A, bool with_inflow, double* mom, cudaStream_t s) {
+    switch (p.n_mom) {
+        case 1: return launch_mom_steps<FS, SRC, 1>(p, A, with_inflow, mom, s);
+        case 2: return launch_mom_steps<FS, SRC, 2>(p, A, with_inflow, mom, s);
+        case 3: return launch_mom_steps<FS, SRC, 3>(p, A, with_inflow, mom, s);
+        case 4: return launch_mom_steps<FS, SRC, 4>(p, A, with_inflow, mom, s);
+        case 5: return launch_mom_steps<FS, SRC, 5>(p, A, with_inflow, mom, s);
+        case 6: return launch_mom_steps<FS, SRC, 6>(p, A, with_inflow, mom, s);
+        case 7: return launch_mom_steps<FS, SRC, 7>(p, A, with_inflow, mom, s);
+        case 8: return launch_mom_steps<FS, SRC, 8>(p, A, with_inflow, mom, s);
+        default: return set_error(RTK_EINVAL, "lattice: unsupported number of moments");
+    }
+}
+
+// moment layout: mom[s][l][f] = sum_a w_a Y_l(a) (Lambda S)(s, a, f); S from u (SRC_U) or thermal (SRC_ISO)
+int lattice_transfer_moments(const Problem& p, int src_mode, bool with_inflow, const double* src, double* mom,
+                             cudaStream_t s) {
+    LatArgs A = lat_args(p, src, nullptr, nullptr);
+    if (p.fs == RTK_FS_IE) {
+        if (src_mode == LSRC_U) return dispatch_mom_nm<RTK_FS_IE, LSRC_U>(p, A, with_inflow, mom, s);
+        return dispatch_mom_nm<RTK_FS_IE, LSRC_ISO>(p, A, with_inflow, mom, s);
+    }
+    if (src_mode == LSRC_U) return dispatch_mom_nm<RTK_FS_EXP_LINEAR, LSRC_U>(p, A, with_inflow, mom, s);
+    return dispatch_mom_nm<RTK_FS_EXP_LINEAR, LSRC_ISO>(p, A, with_inflow, mom, s);
 }
 
 }  // namespace rtk

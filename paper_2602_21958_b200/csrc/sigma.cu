@@ -80,8 +80,8 @@ __global__ void __launch_bounds__(kGemmThreads) redistribute_kernel(const double
     __shared__ double Bs[BK][BN];
     const int tx = threadIdx.x % (BN / TN);
     const int ty = threadIdx.x / (BN / TN);
-    const int64_t row0 = static_cast<int64_t>(blockIdx.y) * BM;
-    const int col0 = blockIdx.x * BN;
+    const int64_t row0 = static_cast<int64_t>(blockIdx.x) * BM;
+    const int col0 = blockIdx.y * BN;
     double acc[TM][TN];
 #pragma unroll
     for (int r = 0; r < TM; ++r)
@@ -172,8 +172,8 @@ __global__ void __launch_bounds__(THREADS, 2) redistribute_dmma_kernel(const dou
     double* Bs = smem + STAGES * BM * SA;       // [STAGES][BK][SB]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp >> 2, wn = warp & 3;
-    const int64_t row0 = static_cast<int64_t>(blockIdx.y) * BM;
-    const int col0 = blockIdx.x * BN;
+    const int64_t row0 = static_cast<int64_t>(blockIdx.x) * BM;
+    const int col0 = blockIdx.y * BN;
     const int KT = (K + BK - 1) / BK;
 
     auto load = [&](int st, int k0) {
@@ -320,14 +320,14 @@ int launch_redistribute_ex(const Problem& p, const double* A, double* C, int ldc
                                  static_cast<int>(dmma::kSmem));
             configured = true;
         }
-        dim3 grid((p.n_freq + dmma::BN - 1) / dmma::BN, static_cast<unsigned>((M + dmma::BM - 1) / dmma::BM));
+        dim3 grid(static_cast<unsigned>((M + dmma::BM - 1) / dmma::BM), (p.n_freq + dmma::BN - 1) / dmma::BN);
         // pitch fp is even: 16-byte copies always legal; pad column/row entries are zero
         dmma::redistribute_dmma_kernel<2><<<grid, dmma::THREADS, dmma::kSmem, s>>>(
             A, p.rwt, C, p.gamma, p.coeffs, M, p.n_freq, p.n_freq, p.n_mom, epi, p.fp, ldc, U, ldu);
         RTK_LAUNCH_CHECK("redistribute_dmma_kernel");
         return RTK_OK;
     }
-    dim3 grid((p.n_freq + BN - 1) / BN, static_cast<unsigned>((M + BM - 1) / BM));
+    dim3 grid(static_cast<unsigned>((M + BM - 1) / BM), (p.n_freq + BN - 1) / BN);
     redistribute_kernel<<<grid, kGemmThreads, 0, s>>>(A, p.rwt, C, p.gamma, p.coeffs, M, p.n_freq, p.n_freq, p.n_mom,
                                                       epi, p.fp, ldc, U, ldu);
     RTK_LAUNCH_CHECK("redistribute_kernel");

@@ -1,0 +1,38 @@
+"""Time the lattice matvec at the BASELINE config sizes (development tool)."""
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, ".")
+import paper_2602_21958_b200 as P  # noqa: E402
+from paper_2602_21958_b200 import lattice as L  # noqa: E402
+
+CFGS = {
+    3: dict(nx=256, ny=1, nz=256, n_polar=8, n_azimuth=16, n_freq=41, corr_len=16.0, eps=1e-4, layout="intensity"),
+    4: dict(nx=64, ny=64, nz=64, n_polar=8, n_azimuth=16, n_freq=31, corr_len=8.0, eps=1e-4, layout="moments"),
+    5: dict(nx=128, ny=128, nz=128, n_polar=8, n_azimuth=12, n_freq=41, corr_len=16.0, eps=1e-5, layout="moments"),
+}
+which = [int(a) for a in sys.argv[1:]] or [3, 4, 5]
+for cfg in which:
+    kw = dict(CFGS[cfg])
+    t0 = time.time()
+    p = L.lattice_problem(seed=21958 + cfg, **kw)
+    p.device()
+    setup = time.time() - t0
+    x = torch.randn(p.n_total, dtype=torch.float64, device="cuda")
+    y = P.apply_A(p, x)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3 if cfg == 5 else 5
+    e0.record()
+    for _ in range(reps):
+        y = P.apply_A(p, x)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    dof = p.n_space * p.n_dirs * p.n_freq
+    print(f"cfg{cfg} {kw['layout']:9s} unknowns={p.n_total:>11d} DOF={dof:>11d} setup {setup:6.1f}s  matvec {ms:9.2f} ms"
+          f"  {dof / ms / 1e6:8.2f} GDOF/s", flush=True)
+    del p, x, y
+    torch.cuda.empty_cache()
