@@ -42,7 +42,8 @@ Problem::~Problem() {
     if (tma_ctas) cudaFree(tma_ctas);
     if (dtpad) cudaFree(dtpad);
     if (lat_dirs) cudaFree(lat_dirs);
-    double* lat[] = {lat_chi, lat_in_top, lat_in_bot, lat_state[0], lat_state[1], lat_src, lat_zero};
+    double* lat[] = {lat_chi, lat_in_top, lat_in_bot, lat_state[0], lat_state[1], lat_src, lat_zero, lat_splane[0],
+                     lat_splane[1]};
     for (double* b : lat)
         if (b) cudaFree(b);
 }
@@ -240,6 +241,8 @@ int rtk_problem_create_lattice(const rtk_lattice_desc* d, rtk_problem** out) {
         const size_t plane = static_cast<size_t>(p.n_angles) * d->nx * d->ny * p.n_freq;
         rc = rtk::upload(&p.lat_state[0], nullptr, plane);
         if (!rc) rc = rtk::upload(&p.lat_state[1], nullptr, plane);
+        if (!rc) rc = rtk::upload(&p.lat_splane[0], nullptr, plane);
+        if (!rc) rc = rtk::upload(&p.lat_splane[1], nullptr, plane);
     }
     if (!rc) rc = rtk::upload(&p.lat_zero, nullptr, static_cast<size_t>(p.n_space) * p.n_freq);
     if (!rc) rc = rtk::setup_lattice(p, d);

@@ -84,45 +84,30 @@ struct LatArgs {
 
 enum LatSrc { LSRC_VEC = 0, LSRC_ISO = 1, LSRC_U = 2 };
 
-// source value at node s for direction a, frequency f (NM: number of moments, compile-time)
-template <int SRC, int NM>
-__device__ __forceinline__ double node_source(const LatArgs& A, int64_t s, int a, int f, const double (&cy)[NM]) {
-    if (SRC == LSRC_VEC) return __ldg(A.src + (s * A.n_dirs + a) * A.n_freq + f);
-    if (SRC == LSRC_ISO) return __ldg(A.src + s * A.n_freq + f);
-    const double* u = A.src + s * NM * A.n_freq + f;
-    double v = 0.0;
-#pragma unroll
-    for (int l = 0; l < NM; ++l) v = fma(cy[l], __ldg(u + l * A.n_freq), v);
-    return v * __ldg(A.gamma + s * A.n_freq + f);
-}
-
-// One formal-solver pass of a line from layer k to k2 (geometry of direction D),
-// starting at horizontal position (X0, Y0) = line position at the start layer.
-template <int FS, int SRC, int NM>
-__device__ __forceinline__ double advance_line(const LatArgs& A, const LatDir& D, double acc, double lx, double ly,
-                                               int t, int k, int k2, int a, int f, double phi_f,
-                                               const double (&cy)[NM]) {
-    const int64_t base_a = static_cast<int64_t>(k) * A.nxy;
-    const int64_t base_b = static_cast<int64_t>(k2) * A.nxy;
+// One formal-solver pass of a line between two layers.  The line sits at horizontal
+// position (lx + t sx, ly + t sy) on the start layer; chi_a/chi_b are the opacity
+// planes and Sa/Sb the source planes (node c at Sa[c * ss]) of the start and end layers.
+template <int FS>
+__device__ __forceinline__ double advance_line(const LatDir& D, double acc, double lx, double ly, int t, int nx,
+                                               int ny, const double* __restrict__ chi_a,
+                                               const double* __restrict__ chi_b, const double* __restrict__ Sa,
+                                               const double* __restrict__ Sb, int64_t ss, double phi_f) {
     double prev_s = 0.0, prev_c = 0.0;
+    const double inv_sub = 1.0 / D.n_sub;
     for (int m = 0; m <= D.n_sub; ++m) {
         const double tt = t + static_cast<double>(m) / D.n_sub;
         // no FMA contraction: same rounding as the oracle's lx + tt * sx
         const double X = __dadd_rn(lx, __dmul_rn(tt, D.sx)), Y = __dadd_rn(ly, __dmul_rn(tt, D.sy));
         const double wz = static_cast<double>(m) / D.n_sub;
-        const Stencil st = stencil(X, Y, A.nx, A.ny);
-        const double ca = st.w00 * __ldg(A.chi + base_a + st.c00) + st.w10 * __ldg(A.chi + base_a + st.c10) +
-                          st.w01 * __ldg(A.chi + base_a + st.c01) + st.w11 * __ldg(A.chi + base_a + st.c11);
-        const double cb = st.w00 * __ldg(A.chi + base_b + st.c00) + st.w10 * __ldg(A.chi + base_b + st.c10) +
-                          st.w01 * __ldg(A.chi + base_b + st.c01) + st.w11 * __ldg(A.chi + base_b + st.c11);
-        const double sa = st.w00 * node_source<SRC, NM>(A, base_a + st.c00, a, f, cy) +
-                          st.w10 * node_source<SRC, NM>(A, base_a + st.c10, a, f, cy) +
-                          st.w01 * node_source<SRC, NM>(A, base_a + st.c01, a, f, cy) +
-                          st.w11 * node_source<SRC, NM>(A, base_a + st.c11, a, f, cy);
-        const double sb = st.w00 * node_source<SRC, NM>(A, base_b + st.c00, a, f, cy) +
-                          st.w10 * node_source<SRC, NM>(A, base_b + st.c10, a, f, cy) +
-                          st.w01 * node_source<SRC, NM>(A, base_b + st.c01, a, f, cy) +
-                          st.w11 * node_source<SRC, NM>(A, base_b + st.c11, a, f, cy);
+        const Stencil st = stencil(X, Y, nx, ny);
+        const double ca = st.w00 * __ldg(chi_a + st.c00) + st.w10 * __ldg(chi_a + st.c10) +
+                          st.w01 * __ldg(chi_a + st.c01) + st.w11 * __ldg(chi_a + st.c11);
+        const double cb = st.w00 * __ldg(chi_b + st.c00) + st.w10 * __ldg(chi_b + st.c10) +
+                          st.w01 * __ldg(chi_b + st.c01) + st.w11 * __ldg(chi_b + st.c11);
+        const double sa = st.w00 * __ldg(Sa + st.c00 * ss) + st.w10 * __ldg(Sa + st.c10 * ss) +
+                          st.w01 * __ldg(Sa + st.c01 * ss) + st.w11 * __ldg(Sa + st.c11 * ss);
+        const double sb = st.w00 * __ldg(Sb + st.c00 * ss) + st.w10 * __ldg(Sb + st.c10 * ss) +
+                          st.w01 * __ldg(Sb + st.c01 * ss) + st.w11 * __ldg(Sb + st.c11 * ss);
         const double c_m = (1 - wz) * ca + wz * cb;
         const double s_m = (1 - wz) * sa + wz * sb;
         if (m > 0) {
@@ -138,6 +123,7 @@ __device__ __forceinline__ double advance_line(const LatArgs& A, const LatDir& D
         prev_s = s_m;
         prev_c = c_m;
     }
+    (void)inv_sub;
     return acc;
 }
 
@@ -155,7 +141,6 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_kernel(LatArgs A, int
     const int slot = threadIdx.x / kFC;
     const LatDir D = A.dirs[a];
     const double phi_f = fvalid ? A.phi[f] : 0.0;
-    const double cy[1] = {0.0};   // VEC / ISO sources do not expand moments
     double inflow = 0.0;
     if (with_inflow && fvalid) {
         const double* in = D.down ? A.inflow_top : A.inflow_bottom;
@@ -179,10 +164,17 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_kernel(LatArgs A, int
         if (t == A.nz - 1) break;
         __syncthreads();
         const int k2 = D.down ? k + 1 : k - 1;
+        // source planes of layers k and k2 for (a, f): S[s][a][f] (VEC) or thermal[s][f] (ISO)
+        const int64_t ss = (SRC == LSRC_VEC) ? static_cast<int64_t>(A.n_dirs) * A.n_freq : A.n_freq;
+        const int64_t off = (SRC == LSRC_VEC) ? static_cast<int64_t>(a) * A.n_freq + f : f;
+        const double* Sa = A.src + static_cast<int64_t>(k) * A.nxy * ss + off;
+        const double* Sb = A.src + static_cast<int64_t>(k2) * A.nxy * ss + off;
+        const double* chi_a = A.chi + static_cast<int64_t>(k) * A.nxy;
+        const double* chi_b = A.chi + static_cast<int64_t>(k2) * A.nxy;
         for (int64_t c = slot; c < A.nxy; c += slots) {
             const double lx = static_cast<double>(c % A.nx), ly = static_cast<double>(c / A.nx);
             double acc = lines[c * kFC + fq];
-            if (fvalid) acc = advance_line<FS, SRC, 1>(A, D, acc, lx, ly, t, k, k2, a, f, phi_f, cy);
+            if (fvalid) acc = advance_line<FS>(D, acc, lx, ly, t, A.nx, A.ny, chi_a, chi_b, Sa, Sb, ss, phi_f);
             lines[c * kFC + fq] = acc;
         }
     }
@@ -190,10 +182,12 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_kernel(LatArgs A, int
 
 // ---------------- moment layout: layer-synchronous step ----------------
 // thread = (line c, frequency f); loops over all directions.  NM moments, compile-time.
-template <int FS, int SRC, int NM>
+template <int FS, int NM>
 __global__ void __launch_bounds__(256) lattice_mom_step_kernel(LatArgs A, int t, const double* __restrict__ st_in,
                                                                 double* __restrict__ st_out, double* __restrict__ mom,
-                                                                int with_inflow, int fp) {
+                                                                int with_inflow, int fp,
+                                                                const double* __restrict__ plane_cur,
+                                                                const double* __restrict__ plane_next) {
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (tid >= A.nxy * A.n_freq) return;
     const int f = static_cast<int>(tid % A.n_freq);
@@ -211,12 +205,9 @@ __global__ void __launch_bounds__(256) lattice_mom_step_kernel(LatArgs A, int t,
         const LatDir& D = A.dirs[a];
         const bool down = D.down != 0;
         const double sx = D.sx, sy = D.sy;
-        double wy[NM], cy[NM];
+        double wy[NM];
 #pragma unroll
-        for (int l = 0; l < NM; ++l) {
-            wy[l] = D.wy[l];
-            cy[l] = D.cy[l];
-        }
+        for (int l = 0; l < NM; ++l) wy[l] = D.wy[l];
         const double* sin_a = st_in + a * plane;
         // T_RC gather for node (i, j) at this direction's current layer
         double v;
@@ -240,8 +231,9 @@ __global__ void __launch_bounds__(256) lattice_mom_step_kernel(LatArgs A, int t,
             const int k2 = down ? k + 1 : k - 1;
             double acc = (t == 0) ? (down ? in_top : in_bot) : sin_a[c * A.n_freq + f];
             const LatDir Dl = D;
-            acc = advance_line<FS, SRC, NM>(A, Dl, acc, static_cast<double>(i), static_cast<double>(j), t, k, k2, a, f,
-                                            phi_f, cy);
+            acc = advance_line<FS>(Dl, acc, static_cast<double>(i), static_cast<double>(j), t, A.nx, A.ny,
+                                   A.chi + static_cast<int64_t>(k) * A.nxy, A.chi + static_cast<int64_t>(k2) * A.nxy,
+                                   plane_cur + a * plane + f, plane_next + a * plane + f, A.n_freq, phi_f);
             st_out[a * plane + c * A.n_freq + f] = acc;
         }
     }
@@ -259,6 +251,61 @@ __global__ void __launch_bounds__(256) lattice_mom_step_kernel(LatArgs A, int t,
             const int64_t o = static_cast<int64_t>(l) * fp;
             out_dn[o] = first ? m_dn[l] : out_dn[o] + m_dn[l];
             out_up[o] = first ? m_up[l] : out_up[o] + m_up[l];
+        }
+    }
+}
+
+// Source planes: for every direction a, S_a on the layer it reaches next (down: t+1,
+// up: nz-2-t), and at t = 0 also on its entry layer; S = gamma sum_l c_l Y_l(a) u_l
+// (SRC_U) or the isotropic thermal source (SRC_ISO).  Layout plane[a][c][f].
+template <int SRC, int NM>
+__global__ void __launch_bounds__(256) lattice_splane_kernel(LatArgs A, int t, double* __restrict__ plane_cur,
+                                                              double* __restrict__ plane_next, int fill_cur) {
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (tid >= A.nxy * A.n_freq) return;
+    const int f = static_cast<int>(tid % A.n_freq);
+    const int64_t c = tid / A.n_freq;
+    const int64_t plane = A.nxy * A.n_freq;
+    // layers: [0] down-current, [1] up-current, [2] down-next, [3] up-next
+    const int layers[4] = {t, A.nz - 1 - t, t + 1, A.nz - 2 - t};
+    double uval[4][NM], g[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (q < 2 && !fill_cur) {
+            g[q] = 0.0;
+#pragma unroll
+            for (int l = 0; l < NM; ++l) uval[q][l] = 0.0;
+            continue;
+        }
+        const int64_t sidx = static_cast<int64_t>(layers[q]) * A.nxy + c;
+        if (SRC == LSRC_U) {
+#pragma unroll
+            for (int l = 0; l < NM; ++l) uval[q][l] = __ldg(A.src + (sidx * NM + l) * A.n_freq + f);
+            g[q] = __ldg(A.gamma + sidx * A.n_freq + f);
+        } else {
+            g[q] = __ldg(A.src + sidx * A.n_freq + f);
+        }
+    }
+    for (int a = 0; a < A.n_dirs; ++a) {
+        const LatDir& D = A.dirs[a];
+        const int qd = D.down ? 0 : 1;
+        double cy[NM];
+#pragma unroll
+        for (int l = 0; l < NM; ++l) cy[l] = D.cy[l];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if ((q & 1) != qd || (q < 2 && !fill_cur)) continue;
+            double v;
+            if (SRC == LSRC_U) {
+                v = 0.0;
+#pragma unroll
+                for (int l = 0; l < NM; ++l) v = fma(cy[l], uval[q][l], v);
+                v *= g[q];
+            } else {
+                v = g[q];
+            }
+            double* dst = (q < 2) ? plane_cur : plane_next;
+            dst[a * plane + c * A.n_freq + f] = v;
         }
     }
 }
@@ -349,7 +396,13 @@ static int launch_mom_steps(const Problem& p, const LatArgs& A, bool with_inflow
     double* a = p.lat_state[0];
     double* b = p.lat_state[1];
     for (int t = 0; t < A.nz; ++t) {
-        lattice_mom_step_kernel<FS, SRC, NM><<<blocks, 256, 0, s>>>(A, t, a, b, mom, with_inflow ? 1 : 0, p.fp);
+        double* cur = p.lat_splane[t & 1];
+        double* nxt = p.lat_splane[(t + 1) & 1];
+        if (t < A.nz - 1) {
+            lattice_splane_kernel<SRC, NM><<<blocks, 256, 0, s>>>(A, t, cur, nxt, t == 0 ? 1 : 0);
+            RTK_LAUNCH_CHECK("lattice_splane_kernel");
+        }
+        lattice_mom_step_kernel<FS, NM><<<blocks, 256, 0, s>>>(A, t, a, b, mom, with_inflow ? 1 : 0, p.fp, cur, nxt);
         RTK_LAUNCH_CHECK("lattice_mom_step_kernel");
         double* tmp = a;
         a = b;

@@ -89,6 +89,7 @@ struct Problem {
     double* lat_state[2] = {nullptr, nullptr};   // [dir][line][freq] line values (moment layout)
     double* lat_src = nullptr;                   // full source vector (intensity layout)
     double* lat_zero = nullptr;                  // [n_space][n_freq] zeros (boundary-only RHS)
+    double* lat_splane[2] = {nullptr, nullptr};  // [dir][line][freq] source planes (moment layout ring)
     CUtensorMap tma_gmap, tma_dtmap;
     ~Problem();
 };
