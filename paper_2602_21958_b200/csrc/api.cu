@@ -238,7 +238,7 @@ int rtk_problem_create_lattice(const rtk_lattice_desc* d, rtk_problem** out) {
         if (!rc) rc = rtk::upload(&p.lat_src, nullptr, static_cast<size_t>(p.n_space) * p.n_rays);
     }
     if (!rc && p.layout == rtk::LAYOUT_MOMENTS) {
-        const size_t plane = static_cast<size_t>(p.n_angles) * d->nx * d->ny * p.n_freq;
+        const size_t plane = static_cast<size_t>(p.n_angles) * d->nx * d->ny * p.fp;   // pitch fp (pairs)
         rc = rtk::upload(&p.lat_state[0], nullptr, plane);
         if (!rc) rc = rtk::upload(&p.lat_state[1], nullptr, plane);
         if (!rc) rc = rtk::upload(&p.lat_splane[0], nullptr, plane);

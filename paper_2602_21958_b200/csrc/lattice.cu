@@ -40,31 +40,49 @@ __device__ __forceinline__ double rcp_nr(double x) {
     return fma(r, e, r);
 }
 
-__device__ __forceinline__ int wrap(int v, int n) {
-    v %= n;
-    return v < 0 ? v + n : v;
-}
-
-// bilinear stencil of a horizontal position (periodic): 4 column indices + weights
+// bilinear stencil of a horizontal position (periodic): 4 node indices + weights
 struct Stencil {
     int c00, c10, c01, c11;
     double w00, w10, w01, w11;
 };
 
-__device__ __forceinline__ Stencil stencil(double X, double Y, int nx, int ny) {
-    const double fx = floor(X), fy = floor(Y);
-    const double ax = X - fx, ay = Y - fy;
-    const int i0 = wrap(static_cast<int>(fx), nx), j0 = wrap(static_cast<int>(fy), ny);
+// Lattice regularity: every line of a direction has the same fractional offset at a
+// given (layer step, sub-node), so the interpolation weights and the integer shift
+// are warp-uniform; only the line's own column enters per lane.
+struct Shift {
+    int bx, by;       // floor(offset) mod n
+    double ax, ay;    // fractional part
+};
+
+__device__ __forceinline__ Shift shift_of(double offx, double offy, int nx, int ny) {
+    Shift s;
+    const double fx = floor(offx), fy = floor(offy);
+    s.ax = offx - fx;
+    s.ay = offy - fy;
+    s.bx = static_cast<int>(fx - nx * floor(fx / nx));
+    s.by = static_cast<int>(fy - ny * floor(fy / ny));
+    if (s.bx >= nx) s.bx -= nx;   // guard the rounding edge of floor(fx / nx)
+    if (s.by >= ny) s.by -= ny;
+    if (s.bx < 0) s.bx += nx;
+    if (s.by < 0) s.by += ny;
+    return s;
+}
+
+__device__ __forceinline__ Stencil stencil_at(int lx, int ly, const Shift& sh, int nx, int ny) {
+    int i0 = lx + sh.bx;
+    if (i0 >= nx) i0 -= nx;
+    int j0 = ly + sh.by;
+    if (j0 >= ny) j0 -= ny;
     const int i1 = (i0 + 1 == nx) ? 0 : i0 + 1, j1 = (j0 + 1 == ny) ? 0 : j0 + 1;
     Stencil s;
     s.c00 = j0 * nx + i0;
     s.c10 = j0 * nx + i1;
     s.c01 = j1 * nx + i0;
     s.c11 = j1 * nx + i1;
-    s.w00 = (1 - ax) * (1 - ay);
-    s.w10 = ax * (1 - ay);
-    s.w01 = (1 - ax) * ay;
-    s.w11 = ax * ay;
+    s.w00 = (1 - sh.ax) * (1 - sh.ay);
+    s.w10 = sh.ax * (1 - sh.ay);
+    s.w01 = (1 - sh.ax) * sh.ay;
+    s.w11 = sh.ax * sh.ay;
     return s;
 }
 
@@ -88,18 +106,16 @@ enum LatSrc { LSRC_VEC = 0, LSRC_ISO = 1, LSRC_U = 2 };
 // position (lx + t sx, ly + t sy) on the start layer; chi_a/chi_b are the opacity
 // planes and Sa/Sb the source planes (node c at Sa[c * ss]) of the start and end layers.
 template <int FS>
-__device__ __forceinline__ double advance_line(const LatDir& D, double acc, double lx, double ly, int t, int nx,
+__device__ __forceinline__ double advance_line(const LatDir& D, double acc, int lx, int ly, int t, int nx,
                                                int ny, const double* __restrict__ chi_a,
                                                const double* __restrict__ chi_b, const double* __restrict__ Sa,
                                                const double* __restrict__ Sb, int64_t ss, double phi_f) {
     double prev_s = 0.0, prev_c = 0.0;
-    const double inv_sub = 1.0 / D.n_sub;
     for (int m = 0; m <= D.n_sub; ++m) {
         const double tt = t + static_cast<double>(m) / D.n_sub;
-        // no FMA contraction: same rounding as the oracle's lx + tt * sx
-        const double X = __dadd_rn(lx, __dmul_rn(tt, D.sx)), Y = __dadd_rn(ly, __dmul_rn(tt, D.sy));
         const double wz = static_cast<double>(m) / D.n_sub;
-        const Stencil st = stencil(X, Y, nx, ny);
+        const Shift sh = shift_of(__dmul_rn(tt, D.sx), __dmul_rn(tt, D.sy), nx, ny);
+        const Stencil st = stencil_at(lx, ly, sh, nx, ny);
         const double ca = st.w00 * __ldg(chi_a + st.c00) + st.w10 * __ldg(chi_a + st.c10) +
                           st.w01 * __ldg(chi_a + st.c01) + st.w11 * __ldg(chi_a + st.c11);
         const double cb = st.w00 * __ldg(chi_b + st.c00) + st.w10 * __ldg(chi_b + st.c10) +
@@ -123,7 +139,6 @@ __device__ __forceinline__ double advance_line(const LatDir& D, double acc, doub
         prev_s = s_m;
         prev_c = c_m;
     }
-    (void)inv_sub;
     return acc;
 }
 
@@ -146,14 +161,15 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_kernel(LatArgs A, int
         const double* in = D.down ? A.inflow_top : A.inflow_bottom;
         inflow = in ? in[f] : 0.0;
     }
-    for (int64_t l = slot; l < A.nxy; l += slots) lines[l * kFC + fq] = inflow;
+    for (int l = slot; l < A.nxy; l += slots) lines[l * kFC + fq] = inflow;
     for (int t = 0; t < A.nz; ++t) {
         const int k = D.down ? t : A.nz - 1 - t;
         __syncthreads();
         // T_RC gather for the nodes of layer k
-        for (int64_t c = slot; c < A.nxy; c += slots) {
-            const int i = static_cast<int>(c % A.nx), j = static_cast<int>(c / A.nx);
-            const Stencil st = stencil(i - t * D.sx, j - t * D.sy, A.nx, A.ny);
+        const Shift gsh = shift_of(-t * D.sx, -t * D.sy, A.nx, A.ny);
+        for (int c = slot; c < A.nxy; c += slots) {
+            const int j = c / A.nx, i = c - j * A.nx;
+            const Stencil st = stencil_at(i, j, gsh, A.nx, A.ny);
             const double v = st.w00 * lines[st.c00 * kFC + fq] + st.w10 * lines[st.c10 * kFC + fq] +
                              st.w01 * lines[st.c01 * kFC + fq] + st.w11 * lines[st.c11 * kFC + fq];
             if (fvalid) {
@@ -171,8 +187,8 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_kernel(LatArgs A, int
         const double* Sb = A.src + static_cast<int64_t>(k2) * A.nxy * ss + off;
         const double* chi_a = A.chi + static_cast<int64_t>(k) * A.nxy;
         const double* chi_b = A.chi + static_cast<int64_t>(k2) * A.nxy;
-        for (int64_t c = slot; c < A.nxy; c += slots) {
-            const double lx = static_cast<double>(c % A.nx), ly = static_cast<double>(c / A.nx);
+        for (int c = slot; c < A.nxy; c += slots) {
+            const int ly = c / A.nx, lx = c - ly * A.nx;
             double acc = lines[c * kFC + fq];
             if (fvalid) acc = advance_line<FS>(D, acc, lx, ly, t, A.nx, A.ny, chi_a, chi_b, Sa, Sb, ss, phi_f);
             lines[c * kFC + fq] = acc;
@@ -180,77 +196,131 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_kernel(LatArgs A, int
     }
 }
 
-// ---------------- moment layout: layer-synchronous step ----------------
-// thread = (line c, frequency f); loops over all directions.  NM moments, compile-time.
+// Two frequencies per thread: the lattice geometry (shift, stencil, trilinear
+// opacity, dt) is frequency-independent and computed once for the pair; the
+// internal planes use the even pitch fp so the pair moves as one 16-byte load.
+template <int FS>
+__device__ __forceinline__ double2 advance_line2(const LatDir& D, double2 acc, int lx, int ly, int t, int nx,
+                                                 int ny, const double* __restrict__ chi_a,
+                                                 const double* __restrict__ chi_b, const double2* __restrict__ Sa,
+                                                 const double2* __restrict__ Sb, int64_t ss, double phi0,
+                                                 double phi1) {
+    double2 prev_s = make_double2(0.0, 0.0);
+    double prev_c = 0.0;
+    for (int m = 0; m <= D.n_sub; ++m) {
+        const double tt = t + static_cast<double>(m) / D.n_sub;
+        const double wz = static_cast<double>(m) / D.n_sub;
+        const Shift sh = shift_of(__dmul_rn(tt, D.sx), __dmul_rn(tt, D.sy), nx, ny);
+        const Stencil st = stencil_at(lx, ly, sh, nx, ny);
+        const double ca = st.w00 * __ldg(chi_a + st.c00) + st.w10 * __ldg(chi_a + st.c10) +
+                          st.w01 * __ldg(chi_a + st.c01) + st.w11 * __ldg(chi_a + st.c11);
+        const double cb = st.w00 * __ldg(chi_b + st.c00) + st.w10 * __ldg(chi_b + st.c10) +
+                          st.w01 * __ldg(chi_b + st.c01) + st.w11 * __ldg(chi_b + st.c11);
+        const double2 a00 = __ldg(Sa + st.c00 * ss), a10 = __ldg(Sa + st.c10 * ss);
+        const double2 a01 = __ldg(Sa + st.c01 * ss), a11 = __ldg(Sa + st.c11 * ss);
+        const double2 b00 = __ldg(Sb + st.c00 * ss), b10 = __ldg(Sb + st.c10 * ss);
+        const double2 b01 = __ldg(Sb + st.c01 * ss), b11 = __ldg(Sb + st.c11 * ss);
+        const double c_m = (1 - wz) * ca + wz * cb;
+        double2 s_m;
+        s_m.x = (1 - wz) * (st.w00 * a00.x + st.w10 * a10.x + st.w01 * a01.x + st.w11 * a11.x) +
+                wz * (st.w00 * b00.x + st.w10 * b10.x + st.w01 * b01.x + st.w11 * b11.x);
+        s_m.y = (1 - wz) * (st.w00 * a00.y + st.w10 * a10.y + st.w01 * a01.y + st.w11 * a11.y) +
+                wz * (st.w00 * b00.y + st.w10 * b10.y + st.w01 * b01.y + st.w11 * b11.y);
+        if (m > 0) {
+            const double dt = D.sub_len * (prev_c + c_m) * 0.5;
+            const double d0 = phi0 * dt, d1 = phi1 * dt;
+            if (FS == RTK_FS_IE) {
+                const double r0 = rcp_nr(1.0 + d0), r1 = rcp_nr(1.0 + d1);
+                acc.x = fma(acc.x, r0, (d0 * s_m.x) * r0);
+                acc.y = fma(acc.y, r1, (d1 * s_m.y) * r1);
+            } else {
+                const ExpLin w0 = exp_linear_weights(d0), w1 = exp_linear_weights(d1);
+                acc.x = fma(acc.x, w0.att, w0.wu * prev_s.x + w0.wc * s_m.x);
+                acc.y = fma(acc.y, w1.att, w1.wu * prev_s.y + w1.wc * s_m.y);
+            }
+        }
+        prev_s = s_m;
+        prev_c = c_m;
+    }
+    return acc;
+}
+
+// thread = (line c, frequency pair q): f0 = 2q, f1 = 2q + 1 (f1 may be padding).
+// Directions are processed hemisphere by hemisphere so only NM x 2 moment
+// accumulators are live; layer t gets the down part, layer nz-1-t the up part.
 template <int FS, int NM>
-__global__ void __launch_bounds__(256) lattice_mom_step_kernel(LatArgs A, int t, const double* __restrict__ st_in,
+__global__ void __launch_bounds__(256) lattice_mom_pair_kernel(LatArgs A, int t, const double* __restrict__ st_in,
                                                                 double* __restrict__ st_out, double* __restrict__ mom,
                                                                 int with_inflow, int fp,
                                                                 const double* __restrict__ plane_cur,
                                                                 const double* __restrict__ plane_next) {
+    const int hp = fp >> 1;
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (tid >= A.nxy * A.n_freq) return;
-    const int f = static_cast<int>(tid % A.n_freq);
-    const int64_t c = tid / A.n_freq;
-    const int i = static_cast<int>(c % A.nx), j = static_cast<int>(c / A.nx);
-    const double phi_f = A.phi[f];
-    double m_dn[NM], m_up[NM];
-#pragma unroll
-    for (int l = 0; l < NM; ++l) m_dn[l] = m_up[l] = 0.0;
-    const int k_dn = t, k_up = A.nz - 1 - t;
-    const int64_t plane = A.nxy * A.n_freq;
-    const double in_top = (with_inflow && A.inflow_top) ? A.inflow_top[f] : 0.0;
-    const double in_bot = (with_inflow && A.inflow_bottom) ? A.inflow_bottom[f] : 0.0;
-    for (int a = 0; a < A.n_dirs; ++a) {
-        const LatDir& D = A.dirs[a];
-        const bool down = D.down != 0;
-        const double sx = D.sx, sy = D.sy;
-        double wy[NM];
-#pragma unroll
-        for (int l = 0; l < NM; ++l) wy[l] = D.wy[l];
-        const double* sin_a = st_in + a * plane;
-        // T_RC gather for node (i, j) at this direction's current layer
-        double v;
-        if (t == 0) {
-            v = down ? in_top : in_bot;
-        } else {
-            const Stencil st = stencil(i - t * sx, j - t * sy, A.nx, A.ny);
-            v = st.w00 * sin_a[st.c00 * A.n_freq + f] + st.w10 * sin_a[st.c10 * A.n_freq + f] +
-                st.w01 * sin_a[st.c01 * A.n_freq + f] + st.w11 * sin_a[st.c11 * A.n_freq + f];
-        }
-        if (down) {
-#pragma unroll
-            for (int l = 0; l < NM; ++l) m_dn[l] = fma(wy[l], v, m_dn[l]);
-        } else {
-#pragma unroll
-            for (int l = 0; l < NM; ++l) m_up[l] = fma(wy[l], v, m_up[l]);
-        }
-        // advance own line (c) to the next layer
-        if (t < A.nz - 1) {
-            const int k = down ? t : A.nz - 1 - t;
-            const int k2 = down ? k + 1 : k - 1;
-            double acc = (t == 0) ? (down ? in_top : in_bot) : sin_a[c * A.n_freq + f];
-            const LatDir Dl = D;
-            acc = advance_line<FS>(Dl, acc, static_cast<double>(i), static_cast<double>(j), t, A.nx, A.ny,
-                                   A.chi + static_cast<int64_t>(k) * A.nxy, A.chi + static_cast<int64_t>(k2) * A.nxy,
-                                   plane_cur + a * plane + f, plane_next + a * plane + f, A.n_freq, phi_f);
-            st_out[a * plane + c * A.n_freq + f] = acc;
-        }
+    if (tid >= A.nxy * hp) return;
+    const int c = static_cast<int>(tid / hp);
+    const int q = static_cast<int>(tid - static_cast<int64_t>(c) * hp);
+    const int f0 = 2 * q, f1 = 2 * q + 1;
+    const bool v1 = f1 < A.n_freq;
+    const int j = c / A.nx, i = c - j * A.nx;
+    const double phi0 = A.phi[f0], phi1 = v1 ? A.phi[f1] : 0.0;
+    const int64_t plane2 = A.nxy * static_cast<int64_t>(hp);   // double2 per direction plane
+    const double2* sin2 = reinterpret_cast<const double2*>(st_in);
+    double2* sout2 = reinterpret_cast<double2*>(st_out);
+    const double2* pc2 = reinterpret_cast<const double2*>(plane_cur);
+    const double2* pn2 = reinterpret_cast<const double2*>(plane_next);
+    double2 in_top = make_double2(0.0, 0.0), in_bot = make_double2(0.0, 0.0);
+    if (with_inflow) {
+        if (A.inflow_top) in_top = make_double2(A.inflow_top[f0], v1 ? A.inflow_top[f1] : 0.0);
+        if (A.inflow_bottom) in_bot = make_double2(A.inflow_bottom[f0], v1 ? A.inflow_bottom[f1] : 0.0);
     }
-    // layer k receives its down part at step k and its up part at step nz-1-k: the later step adds
-    double* out_dn = mom + (static_cast<int64_t>(k_dn) * A.nxy + c) * NM * fp + f;   // pitch fp (GEMM operand)
-    double* out_up = mom + (static_cast<int64_t>(k_up) * A.nxy + c) * NM * fp + f;
-    if (k_dn == k_up) {
+    for (int hemi = 0; hemi < 2; ++hemi) {       // 0: down (layer t), 1: up (layer nz-1-t)
+        const int k = hemi == 0 ? t : A.nz - 1 - t;
+        double m0[NM], m1[NM];
 #pragma unroll
-        for (int l = 0; l < NM; ++l) out_dn[static_cast<int64_t>(l) * fp] = m_dn[l] + m_up[l];
-    } else {
-        // step t is the first visit of both layers t and nz-1-t iff t < nz-1-t
-        const bool first = k_dn < k_up;
+        for (int l = 0; l < NM; ++l) m0[l] = m1[l] = 0.0;
+        for (int a = 0; a < A.n_dirs; ++a) {
+            const LatDir& D = A.dirs[a];
+            if ((D.down != 0) != (hemi == 0)) continue;
+            const double2* sa = sin2 + a * plane2;
+            double2 v;
+            if (t == 0) {
+                v = hemi == 0 ? in_top : in_bot;
+            } else {
+                const Stencil st = stencil_at(i, j, shift_of(-t * D.sx, -t * D.sy, A.nx, A.ny), A.nx, A.ny);
+                const double2 s00 = sa[st.c00 * hp + q], s10 = sa[st.c10 * hp + q];
+                const double2 s01 = sa[st.c01 * hp + q], s11 = sa[st.c11 * hp + q];
+                v.x = st.w00 * s00.x + st.w10 * s10.x + st.w01 * s01.x + st.w11 * s11.x;
+                v.y = st.w00 * s00.y + st.w10 * s10.y + st.w01 * s01.y + st.w11 * s11.y;
+            }
+#pragma unroll
+            for (int l = 0; l < NM; ++l) {
+                const double w = D.wy[l];
+                m0[l] = fma(w, v.x, m0[l]);
+                m1[l] = fma(w, v.y, m1[l]);
+            }
+            if (t < A.nz - 1) {
+                const int k2 = hemi == 0 ? k + 1 : k - 1;
+                double2 acc = (t == 0) ? (hemi == 0 ? in_top : in_bot) : sa[static_cast<int64_t>(c) * hp + q];
+                const LatDir Dl = D;
+                acc = advance_line2<FS>(Dl, acc, i, j, t, A.nx, A.ny, A.chi + static_cast<int64_t>(k) * A.nxy,
+                                        A.chi + static_cast<int64_t>(k2) * A.nxy, pc2 + a * plane2 + q,
+                                        pn2 + a * plane2 + q, hp, phi0, phi1);
+                sout2[a * plane2 + static_cast<int64_t>(c) * hp + q] = acc;
+            }
+        }
+        // step t is the first visit of layers t and nz-1-t iff t < nz-1-t; the middle layer
+        // (odd nz) gets both parts in this thread, up added to down
+        const bool first = (hemi == 0) ? (t <= A.nz - 1 - t) : (t < A.nz - 1 - t);
+        double2* out = reinterpret_cast<double2*>(mom + (static_cast<int64_t>(k) * A.nxy + c) * NM * fp) + q;
 #pragma unroll
         for (int l = 0; l < NM; ++l) {
-            const int64_t o = static_cast<int64_t>(l) * fp;
-            out_dn[o] = first ? m_dn[l] : out_dn[o] + m_dn[l];
-            out_up[o] = first ? m_up[l] : out_up[o] + m_up[l];
+            double2 val = make_double2(m0[l], v1 ? m1[l] : 0.0);
+            if (!first) {
+                const double2 old = out[l * hp];
+                val.x += old.x;
+                val.y += old.y;
+            }
+            out[l * hp] = val;
         }
     }
 }
@@ -260,12 +330,14 @@ __global__ void __launch_bounds__(256) lattice_mom_step_kernel(LatArgs A, int t,
 // (SRC_U) or the isotropic thermal source (SRC_ISO).  Layout plane[a][c][f].
 template <int SRC, int NM>
 __global__ void __launch_bounds__(256) lattice_splane_kernel(LatArgs A, int t, double* __restrict__ plane_cur,
-                                                              double* __restrict__ plane_next, int fill_cur) {
+                                                              double* __restrict__ plane_next, int fill_cur, int fp) {
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (tid >= A.nxy * A.n_freq) return;
-    const int f = static_cast<int>(tid % A.n_freq);
-    const int64_t c = tid / A.n_freq;
-    const int64_t plane = A.nxy * A.n_freq;
+    if (tid >= A.nxy * fp) return;
+    const int64_t c = tid / fp;
+    const int fpad = static_cast<int>(tid - c * fp);
+    const bool fvalid = fpad < A.n_freq;
+    const int f = fvalid ? fpad : 0;
+    const int64_t plane = A.nxy * fp;
     // layers: [0] down-current, [1] up-current, [2] down-next, [3] up-next
     const int layers[4] = {t, A.nz - 1 - t, t + 1, A.nz - 2 - t};
     double uval[4][NM], g[4];
@@ -305,7 +377,7 @@ __global__ void __launch_bounds__(256) lattice_splane_kernel(LatArgs A, int t, d
                 v = g[q];
             }
             double* dst = (q < 2) ? plane_cur : plane_next;
-            dst[a * plane + c * A.n_freq + f] = v;
+            dst[a * plane + c * fp + fpad] = fvalid ? v : 0.0;
         }
     }
 }
@@ -391,19 +463,19 @@ int lattice_transfer_intensity(const Problem& p, int src_mode, int out_mode, boo
 
 template <int FS, int SRC, int NM>
 static int launch_mom_steps(const Problem& p, const LatArgs& A, bool with_inflow, double* mom, cudaStream_t s) {
-    const int64_t threads = A.nxy * A.n_freq;
-    const unsigned blocks = static_cast<unsigned>((threads + 255) / 256);
+    const unsigned pblocks = static_cast<unsigned>((A.nxy * p.fp + 255) / 256);
+    const unsigned sblocks = static_cast<unsigned>((A.nxy * (p.fp / 2) + 255) / 256);
     double* a = p.lat_state[0];
     double* b = p.lat_state[1];
     for (int t = 0; t < A.nz; ++t) {
         double* cur = p.lat_splane[t & 1];
         double* nxt = p.lat_splane[(t + 1) & 1];
         if (t < A.nz - 1) {
-            lattice_splane_kernel<SRC, NM><<<blocks, 256, 0, s>>>(A, t, cur, nxt, t == 0 ? 1 : 0);
+            lattice_splane_kernel<SRC, NM><<<pblocks, 256, 0, s>>>(A, t, cur, nxt, t == 0 ? 1 : 0, p.fp);
             RTK_LAUNCH_CHECK("lattice_splane_kernel");
         }
-        lattice_mom_step_kernel<FS, NM><<<blocks, 256, 0, s>>>(A, t, a, b, mom, with_inflow ? 1 : 0, p.fp, cur, nxt);
-        RTK_LAUNCH_CHECK("lattice_mom_step_kernel");
+        lattice_mom_pair_kernel<FS, NM><<<sblocks, 256, 0, s>>>(A, t, a, b, mom, with_inflow ? 1 : 0, p.fp, cur, nxt);
+        RTK_LAUNCH_CHECK("lattice_mom_pair_kernel");
         double* tmp = a;
         a = b;
         b = tmp;

@@ -13,8 +13,9 @@ CFGS = {
     4: dict(nx=64, ny=64, nz=64, n_polar=8, n_azimuth=16, n_freq=31, corr_len=8.0, eps=1e-4, layout="moments"),
     5: dict(nx=128, ny=128, nz=128, n_polar=8, n_azimuth=12, n_freq=41, corr_len=16.0, eps=1e-5, layout="moments"),
 }
-which = [int(a) for a in sys.argv[1:]] or [3, 4, 5]
-for cfg in which:
+def main():
+  which = [int(a) for a in sys.argv[1:]] or [3, 4, 5]
+  for cfg in which:
     kw = dict(CFGS[cfg])
     t0 = time.time()
     p = L.lattice_problem(seed=21958 + cfg, **kw)
@@ -36,3 +37,7 @@ for cfg in which:
           f"  {dof / ms / 1e6:8.2f} GDOF/s", flush=True)
     del p, x, y
     torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
