@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--formal-solver", default="ie", choices=["ie", "exp_linear", "exp_parabolic"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gmres", action="store_true")
+    ap.add_argument("--no-lattice", action="store_true")
     return ap.parse_args()
 
 
@@ -291,6 +292,9 @@ def run_b200(args):
     extra = {}
     if rank == 0 and not args.no_gmres:
         extra["gmres"] = gmres_timings(torch)
+        extra["krylov_cfg2"] = krylov_cfg2(torch, problem, ms_per_step, hbm)
+    if rank == 0 and not args.no_lattice:
+        extra["lattice"] = lattice_timings(torch)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -329,6 +333,62 @@ def gmres_timings(torch):
         el = time.perf_counter() - t0
         out[name] = {"iterations": rep.iterations, "converged": rep.converged, "time_s": el,
                      "true_residual": rep.true_residual, "matvecs": rep.matvecs}
+    return out
+
+
+def krylov_cfg2(torch, problem, matvec_ms, hbm):
+    """30 GMRES(30) iterations on cfg2: per-iteration time and the CGS2 passes' achieved bandwidth."""
+    import paper_2602_21958_b200 as P
+
+    n = problem.n_total
+    b = torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator(device="cuda").manual_seed(5))
+    cfg = P.SolveConfig(rel_tol=1e-30, max_iter=30, restart=30)
+    P.gmres(problem, b, P.SolveConfig(rel_tol=1e-30, max_iter=30, restart=30))   # warm the memory pool
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rep = P.gmres(problem, b, cfg)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    its = rep.iterations
+    orth_s = el - rep.matvecs * matvec_ms / 1e3
+    # CGS2 + normalisation traffic per step j: 3(j+1) basis reads + 7 vector reads/writes
+    orth_bytes = sum((3 * (j + 1) + 7) * 8 * n for j in range(its))
+    return {"iterations": its, "matvecs": rep.matvecs, "time_s": el, "ms_per_iteration": el / its * 1e3,
+            "orth_s": orth_s, "orth_algorithmic_bytes": orth_bytes,
+            "orth_achieved_gbs": orth_bytes / orth_s / 1e9 if orth_s > 0 else None,
+            "orth_frac_hbm": orth_bytes / orth_s / 1e9 / hbm if orth_s > 0 else None}
+
+
+def lattice_timings(torch):
+    """Matvec time of the multi-D configurations (cfg3 intensity layout, cfg4/5 moment layout)."""
+    import paper_2602_21958_b200 as P
+    from paper_2602_21958_b200 import lattice as L
+
+    cfgs = {3: dict(nx=256, ny=1, nz=256, n_polar=8, n_azimuth=16, n_freq=41, corr_len=16.0, eps=1e-4,
+                    layout="intensity"),
+            4: dict(nx=64, ny=64, nz=64, n_polar=8, n_azimuth=16, n_freq=31, corr_len=8.0, eps=1e-4,
+                    layout="moments"),
+            5: dict(nx=128, ny=128, nz=128, n_polar=8, n_azimuth=12, n_freq=41, corr_len=16.0, eps=1e-5,
+                    layout="moments")}
+    out = {}
+    for cfg, kw in cfgs.items():
+        p = L.lattice_problem(seed=21958 + cfg, **kw)
+        x = torch.randn(p.n_total, dtype=torch.float64, device="cuda")
+        P.apply_A(p, x)
+        torch.cuda.synchronize()
+        reps = 2 if cfg == 5 else 4
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            P.apply_A(p, x)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        dof = p.n_space * p.n_dirs * p.n_freq
+        out[f"cfg{cfg}"] = {"layout": kw["layout"], "unknowns": p.n_total, "dof": dof, "ms_per_matvec": ms,
+                            "matvecs_per_s": 1e3 / ms, "gdof_per_s": dof / ms / 1e6}
+        del p, x
+        torch.cuda.empty_cache()
     return out
 
 

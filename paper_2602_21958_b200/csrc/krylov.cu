@@ -12,7 +12,9 @@
 // partials in index order), so results are bitwise reproducible run to run.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "rtk_internal.cuh"
@@ -21,8 +23,8 @@ namespace rtk {
 namespace {
 
 constexpr int kRedThreads = 256;
-constexpr int kMaxRedBlocks = 296;   // 2 x 148 SMs
-constexpr int KMAX = 16;             // basis vectors handled per pass
+constexpr int kMaxRedBlocks = 592;   // 4 x 148 SMs
+constexpr int KMAX = 32;             // basis vectors handled per pass (restart <= 31 runs fully fused)
 
 enum PassMode { MODE_DOT = 0, MODE_UPDATE_DOT = 1, MODE_UPDATE_NORM = 2, MODE_UPDATE = 3 };
 
@@ -61,10 +63,12 @@ struct Workspace {
     }
 };
 
-int red_blocks(int64_t n) {
+// one full wave: 148 SMs x resident blocks of the pass kernel for this bucket size
+int red_blocks(int64_t n, int kb = 4) {
+    const int per_sm = kb <= 8 ? 4 : (kb <= 16 ? 2 : 1);
     int64_t b = (n + kRedThreads * 4 - 1) / (kRedThreads * 4);
     if (b < 1) b = 1;
-    if (b > kMaxRedBlocks) b = kMaxRedBlocks;
+    if (b > 148 * per_sm) b = 148 * per_sm;
     return static_cast<int>(b);
 }
 
@@ -86,40 +90,40 @@ struct PassArgs {
     double* out;                // device results: kc dots, or 1 norm^2
 };
 
-template <int MODE>
+// KB = compile-time bucket >= kc: all KB loads of an element are issued back to back
+// (predicated off beyond kc), so each thread keeps KB independent requests in flight.
+template <int MODE, int KB>
 __global__ void __launch_bounds__(kRedThreads) cgs_pass_kernel(PassArgs P) {
-    constexpr int NACC = (MODE == MODE_UPDATE_NORM) ? 1 : KMAX;
+    constexpr int NACC = (MODE == MODE_UPDATE_NORM) ? 1 : KB;
+    __shared__ double coef[KMAX];
+    if (threadIdx.x < KMAX) coef[threadIdx.x] = (MODE != MODE_DOT && threadIdx.x < P.kc) ? P.coef[threadIdx.x] : 0.0;
+    __syncthreads();
     double acc[NACC];
 #pragma unroll
     for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
-    double c[KMAX];
-#pragma unroll
-    for (int k = 0; k < KMAX; ++k) c[k] = (MODE != MODE_DOT && k < P.kc) ? P.coef[k] : 0.0;
 
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < P.n; e += stride) {
-        double vv[KMAX];
+        double vv[KB];
 #pragma unroll
-        for (int k = 0; k < KMAX; ++k) vv[k] = (k < P.kc) ? __ldg(P.v[k] + e) : 0.0;
+        for (int k = 0; k < KB; ++k) vv[k] = (k < P.kc) ? __ldg(P.v[k] + e) : 0.0;
         double we = P.w[e];
         if (MODE != MODE_DOT) {
 #pragma unroll
-            for (int k = 0; k < KMAX; ++k)
-                if (k < P.kc) we -= c[k] * vv[k];
+            for (int k = 0; k < KB; ++k) we = fma(-coef[k], vv[k], we);
             P.w[e] = we;
         }
         if (MODE == MODE_UPDATE_NORM) {
             acc[0] = fma(we, we, acc[0]);
         } else if (MODE != MODE_UPDATE) {
 #pragma unroll
-            for (int k = 0; k < KMAX; ++k)
-                if (k < P.kc) acc[k] = fma(vv[k], we, acc[k]);
+            for (int k = 0; k < KB; ++k) acc[k] = fma(vv[k], we, acc[k]);
         }
     }
     if (MODE == MODE_UPDATE) return;
 
     // block reduction of each accumulator, fixed order
-    __shared__ double red[kRedThreads / 32][NACC];
+    __shared__ double red[kRedThreads / 32][KMAX];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nk = (MODE == MODE_UPDATE_NORM) ? 1 : P.kc;
 #pragma unroll
@@ -279,15 +283,25 @@ class Engine {
         P.partials = wsp_->partials;
         P.counter = wsp_->counter;
         P.out = out_dev;
-        const int blocks = red_blocks(n);
-        switch (mode) {
-            case MODE_DOT: cgs_pass_kernel<MODE_DOT><<<blocks, kRedThreads, 0, s_>>>(P); break;
-            case MODE_UPDATE_DOT: cgs_pass_kernel<MODE_UPDATE_DOT><<<blocks, kRedThreads, 0, s_>>>(P); break;
-            case MODE_UPDATE_NORM: cgs_pass_kernel<MODE_UPDATE_NORM><<<blocks, kRedThreads, 0, s_>>>(P); break;
-            default: cgs_pass_kernel<MODE_UPDATE><<<blocks, kRedThreads, 0, s_>>>(P); break;
-        }
+        const int kb = k <= 4 ? 4 : (k <= 8 ? 8 : (k <= 16 ? 16 : 32));
+        const char* ov = std::getenv("RTK_PASS_BLOCKS");   // tuning hook: fixed block count for every pass
+        const int blocks = ov ? std::max(1, std::min(kMaxRedBlocks, std::atoi(ov))) : red_blocks(n, kb);
+        if (k <= 4) launch_pass<4>(mode, blocks, P);
+        else if (k <= 8) launch_pass<8>(mode, blocks, P);
+        else if (k <= 16) launch_pass<16>(mode, blocks, P);
+        else launch_pass<32>(mode, blocks, P);
         RTK_LAUNCH_CHECK("cgs_pass_kernel");
         return RTK_OK;
+    }
+
+    template <int KB>
+    void launch_pass(int mode, int blocks, const PassArgs& P) {
+        switch (mode) {
+            case MODE_DOT: cgs_pass_kernel<MODE_DOT, KB><<<blocks, kRedThreads, 0, s_>>>(P); break;
+            case MODE_UPDATE_DOT: cgs_pass_kernel<MODE_UPDATE_DOT, KB><<<blocks, kRedThreads, 0, s_>>>(P); break;
+            case MODE_UPDATE_NORM: cgs_pass_kernel<MODE_UPDATE_NORM, KB><<<blocks, kRedThreads, 0, s_>>>(P); break;
+            default: cgs_pass_kernel<MODE_UPDATE, KB><<<blocks, kRedThreads, 0, s_>>>(P); break;
+        }
     }
 
     // host-visible dot product x.y (fixed-order reduction)
