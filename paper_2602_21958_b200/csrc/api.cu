@@ -39,6 +39,11 @@ Problem::~Problem() {
     for (double* b : bufs)
         if (b) cudaFree(b);
     if (dir_sign) cudaFree(dir_sign);
+    if (aux) cudaStreamDestroy(aux);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    for (auto e : ev_chunk)
+        if (e) cudaEventDestroy(e);
     if (tma_ctas) cudaFree(tma_ctas);
     if (dtpad) cudaFree(dtpad);
     if (lat_dirs) cudaFree(lat_dirs);
@@ -80,6 +85,29 @@ int apply_A_dev(Problem& p, const double* x, double* y, cudaStream_t s) {
         if ((rc = launch_redistribute(p, s))) return rc;
         if ((rc = launch_expand_source(p, nullptr, p.lat_src, s))) return rc;
         return lattice_transfer_intensity(p, 0 /*LSRC_VEC*/, OUT_X_MINUS, false, p.lat_src, x, y, s);
+    }
+    if (getenv_flag("RTK_OVERLAP") && p.n_space >= 64) {   // opt-in: measured slower on cfg2
+        // Chunked fork/join: moments of chunk c+1 (HBM-bound, user stream) run while the DMMA
+        // GEMM of chunk c (FP64-bound, auxiliary stream) runs; the sweep waits for all chunks.
+        const int NC = getenv_flag("RTK_OVERLAP4") ? 4 : 2;
+        if (!p.aux) {
+            RTK_CUDA_TRY(cudaStreamCreateWithFlags(&p.aux, cudaStreamNonBlocking));
+            RTK_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming));
+            RTK_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming));
+            for (int c = 0; c < NC; ++c) RTK_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_chunk[c], cudaEventDisableTiming));
+        }
+        RTK_CUDA_TRY(cudaEventRecord(p.ev_fork, s));
+        RTK_CUDA_TRY(cudaStreamWaitEvent(p.aux, p.ev_fork, 0));
+        for (int c = 0; c < NC; ++c) {
+            const int64_t i0 = p.n_space * c / NC, i1 = p.n_space * (c + 1) / NC;
+            if ((rc = launch_moments_range(p, x, i0, i1, s))) return rc;
+            RTK_CUDA_TRY(cudaEventRecord(p.ev_chunk[c], s));
+            RTK_CUDA_TRY(cudaStreamWaitEvent(p.aux, p.ev_chunk[c], 0));
+            if ((rc = launch_redistribute_range(p, i0, i1, p.aux))) return rc;
+        }
+        RTK_CUDA_TRY(cudaEventRecord(p.ev_join, p.aux));
+        RTK_CUDA_TRY(cudaStreamWaitEvent(s, p.ev_join, 0));
+        return sweep_apply(p, x, y, s);
     }
     if ((rc = launch_moments(p, x, s))) return rc;
     if ((rc = launch_redistribute(p, s))) return rc;

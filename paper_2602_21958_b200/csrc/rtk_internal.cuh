@@ -90,6 +90,9 @@ struct Problem {
     double* lat_src = nullptr;                   // full source vector (intensity layout)
     double* lat_zero = nullptr;                  // [n_space][n_freq] zeros (boundary-only RHS)
     double* lat_splane[2] = {nullptr, nullptr};  // [dir][line][freq] source planes (moment layout ring)
+    // overlap of the HBM-bound moment reduction with the FP64 redistribution GEMM (slab apply_A)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chunk[8] = {};
     CUtensorMap tma_gmap, tma_dtmap;
     ~Problem();
 };
@@ -116,7 +119,9 @@ int lattice_transfer_moments(const Problem& p, int src_mode, bool with_inflow, c
 // sigma.cu GEMM epilogues: C = c_k gamma acc | c_k acc | U - acc | acc
 enum Epilogue { EPI_GAMMA = 0, EPI_COEF = 1, EPI_SUB = 2, EPI_PLAIN = 3 };
 int launch_redistribute_ex(const Problem& p, const double* A, double* C, int ldc, int epi, const double* U, int ldu,
-                           cudaStream_t s);
+                           cudaStream_t s, int64_t nodes = -1, const double* gamma = nullptr);
+int launch_moments_range(const Problem& p, const double* x, int64_t i0, int64_t i1, cudaStream_t s);
+int launch_redistribute_range(const Problem& p, int64_t i0, int64_t i1, cudaStream_t s);
 // krylov.cu
 int apply_A_dev(Problem& p, const double* x, double* y, cudaStream_t s);
 int sweep_apply(const Problem& p, const double* x, double* y, cudaStream_t s);
