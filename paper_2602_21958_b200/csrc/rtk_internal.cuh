@@ -79,7 +79,7 @@ struct Problem {
     double *host_x = nullptr, *host_y = nullptr;   // lazily allocated device staging for *_host calls
     // TMA sweep path (sweep_tma.cu)
     bool tma_ready = false;
-    int tma_n_ctas = 0, tma_gw = 0;
+    int tma_n_ctas = 0, tma_gw = 0, tma_u = 4;
     TmaCta* tma_ctas = nullptr;
     double* dtpad = nullptr;
     // lattice (multi-D) state

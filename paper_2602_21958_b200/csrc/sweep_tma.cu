@@ -50,7 +50,7 @@ namespace {
 
 constexpr int kRaysPerCta = 128;
 constexpr int kXW = kRaysPerCta + 2;   // x box width (covers an odd ray0)
-constexpr int kDtW = 6;                // dt box length (U + 2)
+// dt box length is U + 2 (U steps plus the parity offset)
 constexpr int kDtPad = 4;              // leading zeros in the padded dt copy
 constexpr int kConsumerWarps = kRaysPerCta / 32;
 constexpr int kTmaThreads = kRaysPerCta + 32;
@@ -81,9 +81,55 @@ template <int NM, int U>
 struct Layout {
     static constexpr int kX = round128(U * kXW * 8);
     __host__ __device__ static int g_bytes(int gw) { return round128(U * NM * gw * 8); }
+    static constexpr int kDtW = U + 2;
     static constexpr int kDt = round128(kDtW * 8);
     __host__ __device__ static int stage_bytes(int gw) { return kX + g_bytes(gw) + kDt; }
 };
+
+struct SweepState {
+    double acc, s_prev;
+    double* yp;
+};
+
+template <int NM>
+struct ConsumerCtx {
+    int xoff, gcol, gw;
+    double phi_f, inv_mu;
+    bool valid;
+    double yk[NM];
+};
+
+// U march steps of one stage.  DOWN: box row u = step uu (ascending i); up: u = U-1-uu.
+// CHECK: first/last stage (node 0 has no segment; rows beyond the slab are skipped).
+template <int FS, int NM, int U, bool DOWN, bool CHECK>
+__device__ __forceinline__ void consume(const ConsumerCtx<NM>& c, SweepState& st, const double* __restrict__ xs,
+                                        const double* __restrict__ gs, const double* __restrict__ dts, int q,
+                                        int64_t n, int64_t step) {
+    const double* gcol = gs + c.gcol;
+#pragma unroll
+    for (int uu = 0; uu < U; ++uu) {
+        const int j = q * U + uu;
+        if (CHECK && j >= n) break;
+        const int u = DOWN ? uu : U - 1 - uu;
+        const double xv = xs[u * kXW + c.xoff];
+        double sv = 0.0;
+#pragma unroll
+        for (int k = 0; k < NM; ++k) sv = fma(c.yk[k], gcol[(u * NM + k) * c.gw], sv);
+        if (!CHECK || j > 0) {
+            const double d = c.phi_f * dts[u] * c.inv_mu;
+            if (FS == RTK_FS_IE) {
+                const double r = rcp_nr(1.0 + d);
+                st.acc = fma(st.acc, r, (d * sv) * r);
+            } else {
+                const ExpLin w = exp_linear_weights(d);
+                st.acc = fma(st.acc, w.att, w.wu * st.s_prev + w.wc * sv);
+            }
+        }
+        st.s_prev = sv;
+        if (c.valid) *st.yp = xv - st.acc;
+        st.yp += step;
+    }
+}
 
 template <int FS, int NM, int U, int S>
 __global__ void __launch_bounds__(kTmaThreads) sweep1d_tma_kernel(const __grid_constant__ CUtensorMap xmap,
@@ -119,8 +165,7 @@ __global__ void __launch_bounds__(kTmaThreads) sweep1d_tma_kernel(const __grid_c
             prefetch_tensormap(&xmap);
             prefetch_tensormap(&gmap);
             prefetch_tensormap(&dtmap);
-            static_assert(U + 2 == kDtW, "dt box must cover U steps plus the parity offset");
-            const uint32_t tx = static_cast<uint32_t>(U * kXW * 8 + U * NM * A.gw * 8 + kDtW * 8);
+            const uint32_t tx = static_cast<uint32_t>(U * kXW * 8 + U * NM * A.gw * 8 + Layout<NM, U>::kDtW * 8);
             for (int q = 0; q < Q; ++q) {
                 const int s = q % S;
                 if (q >= S) mbar_wait(&empty[s], ((q / S) - 1) & 1);
@@ -149,51 +194,52 @@ __global__ void __launch_bounds__(kTmaThreads) sweep1d_tma_kernel(const __grid_c
     double yk[NM];
 #pragma unroll
     for (int k = 0; k < NM; ++k) yk[k] = A.yb[k * A.n_angles + a];
-    double acc = 0.0, s_prev = 0.0;
+    SweepState st{0.0, 0.0, A.y + (down ? 0 : (n - 1) * A.n_rays) + ray};
     const int64_t step = down ? A.n_rays : -A.n_rays;
-    double* yp = A.y + (down ? 0 : (n - 1) * A.n_rays) + ray;
-
+    ConsumerCtx<NM> c2;
+    c2.xoff = xoff;
+    c2.gcol = gcol;
+    c2.gw = A.gw;
+    c2.phi_f = phi_f;
+    c2.inv_mu = inv_mu;
+    c2.valid = valid;
+#pragma unroll
+    for (int k = 0; k < NM; ++k) c2.yk[k] = yk[k];
+    // first and last stage carry the boundary checks; the body runs check-free, with the
+    // march direction resolved at compile time
     for (int q = 0; q < Q; ++q) {
         const int s = q % S;
         mbar_wait(&full[s], (q / S) & 1);
-        const unsigned char* st = stages + s * sbytes;
-        const double* xs = reinterpret_cast<const double*>(st);
-        const double* gs = reinterpret_cast<const double*>(st + Layout<NM, U>::kX);
-        const double* dts = reinterpret_cast<const double*>(st + Layout<NM, U>::kX + gbytes);
+        const unsigned char* stg = stages + s * sbytes;
+        const double* xs = reinterpret_cast<const double*>(stg);
+        const double* gs = reinterpret_cast<const double*>(stg + Layout<NM, U>::kX);
+        const double* dts = reinterpret_cast<const double*>(stg + Layout<NM, U>::kX + gbytes);
         const int r0 = down ? q * U : static_cast<int>(n) - U - q * U;
         const int dt_off = ((down ? r0 - 1 : r0) + kDtPad) & 1;
-#pragma unroll
-        for (int uu = 0; uu < U; ++uu) {
-            const int64_t j = static_cast<int64_t>(q) * U + uu;
-            if (j >= n) break;
-            const int u = down ? uu : U - 1 - uu;
-            const double xv = xs[u * kXW + xoff];
-            double sv = 0.0;
-#pragma unroll
-            for (int k = 0; k < NM; ++k) sv = fma(yk[k], gs[(u * NM + k) * A.gw + gcol], sv);
-            if (j > 0) {
-                const double d = phi_f * dts[u + dt_off] * inv_mu;
-                if (FS == RTK_FS_IE) {
-                    const double r = rcp_nr(1.0 + d);
-                    acc = fma(acc, r, (d * sv) * r);
-                } else {
-                    const ExpLin w = exp_linear_weights(d);
-                    acc = fma(acc, w.att, w.wu * s_prev + w.wc * sv);
-                }
-            }
-            s_prev = sv;
-            if (valid) *yp = xv - acc;
-            yp += step;
+        const bool edge = (q == 0) || (q == Q - 1);
+        if (down) {
+            if (edge) consume<FS, NM, U, true, true>(c2, st, xs, gs, dts + dt_off, q, n, step);
+            else consume<FS, NM, U, true, false>(c2, st, xs, gs, dts + dt_off, q, n, step);
+        } else {
+            if (edge) consume<FS, NM, U, false, true>(c2, st, xs, gs, dts + dt_off, q, n, step);
+            else consume<FS, NM, U, false, false>(c2, st, xs, gs, dts + dt_off, q, n, step);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
     }
 }
 
+template <int FS, int NM, int U, int S>
+int launch_tma_us(const Problem& p, const double* x, double* y, cudaStream_t s);
+
 template <int FS, int NM>
 int launch_tma_t(const Problem& p, const double* x, double* y, cudaStream_t s) {
-    constexpr int U = 4;
-    constexpr int S = (NM <= 2) ? 8 : 4;
+    if (p.tma_u == 8) return launch_tma_us<FS, NM, 8, 4>(p, x, y, s);
+    return launch_tma_us<FS, NM, 4, (NM <= 2) ? 8 : 4>(p, x, y, s);
+}
+
+template <int FS, int NM, int U, int S>
+int launch_tma_us(const Problem& p, const double* x, double* y, cudaStream_t s) {
     CUtensorMap xmap;
     const uint64_t xd[2] = {static_cast<uint64_t>(p.n_rays), static_cast<uint64_t>(p.n_space)};
     const uint64_t xs[1] = {static_cast<uint64_t>(p.n_rays) * 8};
@@ -283,14 +329,15 @@ int setup_tma(Problem& p) {
     }
     const uint64_t gd[2] = {static_cast<uint64_t>(p.fp), static_cast<uint64_t>(p.n_space * p.n_mom)};
     const uint64_t gs[1] = {static_cast<uint64_t>(p.fp) * 8};
-    const uint32_t gb[2] = {static_cast<uint32_t>(p.tma_gw), static_cast<uint32_t>(4 * p.n_mom)};
+    p.tma_u = (!getenv_flag("RTK_TMA_U4") && p.n_mom <= 2) ? 8 : 4;   // march steps per pipeline stage (U = 8: 96% of HBM on cfg2)
+    const uint32_t gb[2] = {static_cast<uint32_t>(p.tma_gw), static_cast<uint32_t>(p.tma_u * p.n_mom)};
     // front/back zero-padded copy of dt so every dt box starts at an even, non-negative coordinate
     std::vector<double> hdt(static_cast<size_t>(p.n_space - 1 + 2 * kDtPad), 0.0);
     RTK_CUDA_TRY(cudaMemcpy(hdt.data() + kDtPad, p.dt, sizeof(double) * (p.n_space - 1), cudaMemcpyDeviceToHost));
     RTK_CUDA_TRY(cudaMalloc(&p.dtpad, sizeof(double) * hdt.size()));
     RTK_CUDA_TRY(cudaMemcpy(p.dtpad, hdt.data(), sizeof(double) * hdt.size(), cudaMemcpyHostToDevice));
     const uint64_t dd[1] = {static_cast<uint64_t>(hdt.size())};
-    const uint32_t db[1] = {kDtW};
+    const uint32_t db[1] = {static_cast<uint32_t>(p.tma_u + 2)};
     if (!encode_f64_map(&p.tma_gmap, p.gmom, 2, gd, gs, gb)) return RTK_OK;
     if (!encode_f64_map(&p.tma_dtmap, p.dtpad, 1, dd, nullptr, db)) return RTK_OK;
     RTK_CUDA_TRY(cudaMalloc(&p.tma_ctas, sizeof(TmaCta) * ctas.size()));
