@@ -55,3 +55,23 @@ def test_cfg3_full_size_linearity_and_layout_identity():
     lhs = P.apply_A(p, 2.0 * u - 0.5 * w)
     rhs = 2.0 * P.apply_A(p, u) - 0.5 * P.apply_A(p, w)
     assert float(torch.linalg.vector_norm(lhs - rhs) / torch.linalg.vector_norm(rhs)) <= 1e-13
+
+
+def test_lattice_bicgstab_matches_oracle():
+    p = L.lattice_problem(6, 1, 8, 4, 8, 5, corr_len=2.0, seed=9, layout="moments")
+    d = OL.desc_from_lattice_problem(p)
+    b = OL.build_rhs(d, "moments")
+    ref = ro.bicgstab(lambda v: OL.apply_A(d, "moments", v), b, rel_tol=1e-9, max_iter=300)
+    rep = P.bicgstab(p, b, P.SolveConfig(method="bicgstab", rel_tol=1e-9, max_iter=300))
+    assert rep.converged == ref.converged
+    assert abs(rep.iterations - ref.iterations) <= 1
+    assert rel_l2(rep.solution, ref.solution) <= 1e-7
+
+
+def test_lattice_rejects_bad_arguments():
+    p = L.lattice_problem(4, 1, 4, 4, 4, 3, corr_len=1.0)
+    with pytest.raises(ValueError):
+        P.apply_A(p, np.zeros(7))
+    q = L.lattice_problem(4, 1, 4, 4, 4, 3, corr_len=1.0, formal_solver="exp_parabolic")
+    with pytest.raises(ValueError):
+        q.device()

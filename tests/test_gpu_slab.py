@@ -157,3 +157,61 @@ def test_odd_shapes_match_oracle(shape):
         d = oracle_desc(p)
         v = np.random.default_rng(ns).standard_normal(p.n_total)
         assert rel_l2(P.apply_A(p, v), ro.apply_A(d, v)) <= MATVEC_TOL
+
+
+def test_reduced_cfg2_gmres_history_prefix_matches_oracle():
+    """cfg2 construction at N_z = 300, 16 mu, 64 nu: first 60 history entries within 1e-9
+    (the sharp GMRES parity check), solution within 1e-7."""
+    p = configs.slab_problem(2, n_space=300, n_angles=16, n_freq=64)
+    d = oracle_desc(p)
+    b = ro.build_rhs(d)
+    cfg = dict(rel_tol=1e-8, max_iter=60, restart=30)
+    ref = ro.gmres(lambda v: ro.apply_A(d, v), b, **cfg)
+    rep = P.gmres(p, b, P.SolveConfig(**cfg))
+    k = min(len(ref.residual_history), len(rep.residual_history))
+    np.testing.assert_allclose(rep.residual_history[:k], ref.residual_history[:k], rtol=1e-9, atol=1e-15)
+    assert rep.iterations == ref.iterations
+    assert rel_l2(rep.solution, ref.solution) <= 1e-7
+
+
+def test_source_function_and_boundary_match_oracle():
+    p = configs.slab_problem(1)
+    p.transfer.inflow = np.random.default_rng(2).uniform(0, 1, p.grid.n_rays)
+    d = oracle_desc(p)
+    I = np.random.default_rng(8).standard_normal(p.n_total)
+    assert rel_l2(P.source_function(p, I), ro.source_function(d, I)) <= MATVEC_TOL
+    assert rel_l2(P.boundary_term(p.transfer).values, ro.boundary_term(d)) <= MATVEC_TOL
+    assert rel_l2(P.build_rhs(p), ro.build_rhs(d)) <= MATVEC_TOL
+
+
+def test_spectral_radius_estimate_matches_oracle_power_iteration():
+    p = configs.slab_problem(1, n_space=40, n_angles=8, n_freq=11)
+    d = oracle_desc(p)
+    rng = np.random.default_rng(12345)
+    v = rng.standard_normal(d.n_total)
+    v /= np.linalg.norm(v)
+    ratios = []
+    for _ in range(30):
+        w = v - ro.apply_A(d, v)
+        nrm = np.linalg.norm(w)
+        ratios.append(nrm)
+        v = w / nrm
+    ref = float(np.exp(np.mean(np.log(ratios[-5:]))))
+    assert abs(P.spectral_radius_estimate(p, iters=30) - ref) <= 1e-9 * ref
+
+
+def test_materialize_A_matches_oracle_dense():
+    p = configs.slab_problem(1, n_space=6, n_angles=4, n_freq=5)
+    d = oracle_desc(p)
+    np.testing.assert_allclose(P.materialize_A(p), ro.materialize(lambda v: ro.apply_A(d, v), d.n_total),
+                               atol=1e-13)
+
+
+def test_field_vector_ray_major_round_trip():
+    p = configs.slab_problem(1, n_space=10, n_angles=4, n_freq=3)
+    v = np.random.default_rng(1).standard_normal(p.n_total)
+    fv = P.permute(p.grid, P.FieldVector(v, P.Ordering.SPACE_MAJOR), P.Ordering.RAY_MAJOR)
+    out = P.apply_transfer(p.transfer, fv)
+    assert out.ordering is P.Ordering.RAY_MAJOR
+    back = P.permute(p.grid, out, P.Ordering.SPACE_MAJOR).values
+    np.testing.assert_allclose(back, P.apply_transfer(p.transfer, v), rtol=1e-15, atol=1e-16)
