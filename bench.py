@@ -315,6 +315,22 @@ def run_b200(args):
         torch.distributed.destroy_process_group()
 
 
+def cpu_gmres_cfg1(p, b_host):
+    """The reference GMRES algorithm (oracle restatement of R/krylov.py:56-158, numpy MGS) with the
+    numpy oracle matvec on one host core: CPU time-to-1e-8 on cfg1 (the OpenMP C port is slower at
+    this tiny size: thread start-up dominates a 50k-DOF matvec)."""
+    from oracle import rt_oracle as ro
+
+    d = ro.desc_from_problem(p)
+    out = {}
+    for name, restart in (("cfg1_gmres30", 30), ("cfg1_gmres_full", None)):
+        t0 = time.perf_counter()
+        rep = ro.gmres(lambda v: ro.apply_A(d, v), b_host, rel_tol=1e-8, max_iter=6000, restart=restart)
+        out[name] = {"iterations": rep.iterations, "converged": rep.converged, "time_s": time.perf_counter() - t0,
+                     "cores": 1, "kind": "port"}
+    return out
+
+
 def gmres_timings(torch):
     """Time-to-1e-8 of the device GMRES on cfg1 (restart 30 and unrestarted)."""
     import paper_2602_21958_b200 as P
@@ -322,7 +338,7 @@ def gmres_timings(torch):
 
     p = configs.slab_problem(1)
     b = P.build_rhs(p, device=True)
-    out = {}
+    out = {"cpu": cpu_gmres_cfg1(p, b.cpu().numpy())}
     for name, restart in (("cfg1_gmres30", 30), ("cfg1_gmres_full", None)):
         cfg = P.SolveConfig(rel_tol=1e-8, max_iter=6000, restart=restart)
         P.gmres(p, b, P.SolveConfig(rel_tol=1e-8, max_iter=5, restart=restart))   # warm-up
