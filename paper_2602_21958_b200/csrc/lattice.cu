@@ -142,6 +142,142 @@ __device__ __forceinline__ double advance_line(const LatDir& D, double acc, int 
     return acc;
 }
 
+// Shared-memory variant of advance_line for kFC frequencies at once: the geometry
+// (shift, stencil, trilinear opacity, dt) is computed once per line and sub-node and
+// reused for the kFC frequencies of the chunk.  Planes: chi [nxy], S [nxy][kFC].
+template <int FS>
+__device__ __forceinline__ void advance_line_smem4(const LatDir& D, double (&acc)[kFC], int lx, int ly, int t,
+                                                   int nx, int ny, const double* chi_a, const double* chi_b,
+                                                   const double* Sa, const double* Sb, const double (&phi)[kFC]) {
+    double prev_s[kFC], prev_c = 0.0;
+#pragma unroll
+    for (int q = 0; q < kFC; ++q) prev_s[q] = 0.0;
+    for (int m = 0; m <= D.n_sub; ++m) {
+        const double tt = t + static_cast<double>(m) / D.n_sub;
+        const double wz = static_cast<double>(m) / D.n_sub;
+        const Shift sh = shift_of(__dmul_rn(tt, D.sx), __dmul_rn(tt, D.sy), nx, ny);
+        const Stencil st = stencil_at(lx, ly, sh, nx, ny);
+        const double ca = st.w00 * chi_a[st.c00] + st.w10 * chi_a[st.c10] + st.w01 * chi_a[st.c01] +
+                          st.w11 * chi_a[st.c11];
+        const double cb = st.w00 * chi_b[st.c00] + st.w10 * chi_b[st.c10] + st.w01 * chi_b[st.c01] +
+                          st.w11 * chi_b[st.c11];
+        const double c_m = (1 - wz) * ca + wz * cb;
+        const double dt = D.sub_len * (prev_c + c_m) * 0.5;
+        const double2* a00 = reinterpret_cast<const double2*>(Sa + st.c00 * kFC);
+        const double2* a10 = reinterpret_cast<const double2*>(Sa + st.c10 * kFC);
+        const double2* a01 = reinterpret_cast<const double2*>(Sa + st.c01 * kFC);
+        const double2* a11 = reinterpret_cast<const double2*>(Sa + st.c11 * kFC);
+        const double2* b00 = reinterpret_cast<const double2*>(Sb + st.c00 * kFC);
+        const double2* b10 = reinterpret_cast<const double2*>(Sb + st.c10 * kFC);
+        const double2* b01 = reinterpret_cast<const double2*>(Sb + st.c01 * kFC);
+        const double2* b11 = reinterpret_cast<const double2*>(Sb + st.c11 * kFC);
+#pragma unroll
+        for (int h = 0; h < kFC / 2; ++h) {
+            const double2 p00 = a00[h], p10 = a10[h], p01 = a01[h], p11 = a11[h];
+            const double2 q00 = b00[h], q10 = b10[h], q01 = b01[h], q11 = b11[h];
+            double s2[2];
+            s2[0] = (1 - wz) * (st.w00 * p00.x + st.w10 * p10.x + st.w01 * p01.x + st.w11 * p11.x) +
+                    wz * (st.w00 * q00.x + st.w10 * q10.x + st.w01 * q01.x + st.w11 * q11.x);
+            s2[1] = (1 - wz) * (st.w00 * p00.y + st.w10 * p10.y + st.w01 * p01.y + st.w11 * p11.y) +
+                    wz * (st.w00 * q00.y + st.w10 * q10.y + st.w01 * q01.y + st.w11 * q11.y);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int q = 2 * h + e;
+                if (m > 0) {
+                    const double dtau = phi[q] * dt;
+                    if (FS == RTK_FS_IE) {
+                        const double r = rcp_nr(1.0 + dtau);
+                        acc[q] = fma(acc[q], r, (dtau * s2[e]) * r);
+                    } else {
+                        const ExpLin w = exp_linear_weights(dtau);
+                        acc[q] = fma(acc[q], w.att, w.wu * prev_s[q] + w.wc * s2[e]);
+                    }
+                }
+                prev_s[q] = s2[e];
+            }
+        }
+        prev_c = c_m;
+    }
+}
+
+// Intensity layout, small layers (nxy <= ~1500, e.g. the 2D slab): one CTA per
+// (direction, 4-frequency chunk), one thread per line handling the 4 frequencies;
+// the two source and opacity planes the lines cross are staged in shared memory once
+// per layer (ring of two), so every trilinear T_CR sample reads smem.
+template <int FS, int SRC, int OUT>
+__global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A, int with_inflow) {
+    extern __shared__ __align__(16) double sm[];
+    const int nxy = static_cast<int>(A.nxy);
+    double* lines = sm;                         // [nxy][kFC]
+    double* splane = lines + nxy * kFC;         // [2][nxy][kFC]
+    double* cplane = splane + 2 * nxy * kFC;    // [2][nxy]
+    const int nfc = (A.n_freq + kFC - 1) / kFC;
+    const int a = blockIdx.x / nfc;
+    const int f0 = (blockIdx.x % nfc) * kFC;
+    const LatDir D = A.dirs[a];
+    double phi[kFC], inflow[kFC];
+#pragma unroll
+    for (int q = 0; q < kFC; ++q) {
+        const int f = f0 + q;
+        const bool fv = f < A.n_freq;
+        phi[q] = fv ? A.phi[f] : 0.0;
+        const double* in = D.down ? A.inflow_top : A.inflow_bottom;
+        inflow[q] = (with_inflow && fv && in) ? in[f] : 0.0;
+    }
+    auto load_planes = [&](int k, int ring) {
+        const int64_t base = static_cast<int64_t>(k) * A.nxy;
+        double* sp = splane + ring * nxy * kFC;
+        double* cp = cplane + ring * nxy;
+        for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) {
+            const int c = e / kFC, q = e - c * kFC, f = f0 + q;
+            double v = 0.0;
+            if (f < A.n_freq) {
+                if (SRC == LSRC_VEC) v = __ldg(A.src + ((base + c) * A.n_dirs + a) * A.n_freq + f);
+                else v = __ldg(A.src + (base + c) * A.n_freq + f);
+            }
+            sp[e] = v;
+        }
+        for (int c = threadIdx.x; c < nxy; c += blockDim.x) cp[c] = __ldg(A.chi + base + c);
+    };
+    for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) lines[e] = inflow[e % kFC];
+    load_planes(D.down ? 0 : A.nz - 1, 0);
+    for (int t = 0; t < A.nz; ++t) {
+        const int k = D.down ? t : A.nz - 1 - t;
+        __syncthreads();
+        // T_RC gather: one thread per (node, frequency) for coalesced y writes
+        const Shift gsh = shift_of(-t * D.sx, -t * D.sy, A.nx, A.ny);
+        for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) {
+            const int c = e / kFC, q = e - c * kFC, f = f0 + q;
+            const int j = c / A.nx, i = c - j * A.nx;
+            const Stencil st = stencil_at(i, j, gsh, A.nx, A.ny);
+            const double v = st.w00 * lines[st.c00 * kFC + q] + st.w10 * lines[st.c10 * kFC + q] +
+                             st.w01 * lines[st.c01 * kFC + q] + st.w11 * lines[st.c11 * kFC + q];
+            if (f < A.n_freq) {
+                const int64_t idx = ((static_cast<int64_t>(k) * A.nxy + c) * A.n_dirs + a) * A.n_freq + f;
+                A.y[idx] = (OUT == OUT_X_MINUS) ? A.x[idx] - v : v;
+            }
+        }
+        if (t == A.nz - 1) break;
+        const int k2 = D.down ? k + 1 : k - 1;
+        load_planes(k2, (t + 1) & 1);
+        __syncthreads();
+        const int cur = t & 1, nxt = (t + 1) & 1;
+        const double* Sa = splane + cur * nxy * kFC;
+        const double* Sb = splane + nxt * nxy * kFC;
+        const double* ca = cplane + cur * nxy;
+        const double* cb = cplane + nxt * nxy;
+        for (int c = threadIdx.x; c < nxy; c += blockDim.x) {
+            const int ly = c / A.nx, lx = c - ly * A.nx;
+            double acc[kFC];
+#pragma unroll
+            for (int q = 0; q < kFC; ++q) acc[q] = lines[c * kFC + q];
+            advance_line_smem4<FS>(D, acc, lx, ly, t, A.nx, A.ny, ca, cb, Sa, Sb, phi);
+#pragma unroll
+            for (int q = 0; q < kFC; ++q) lines[c * kFC + q] = acc[q];
+        }
+    }
+}
+
 // ---------------- intensity layout: one CTA per (direction, frequency chunk) ----------------
 template <int FS, int SRC, int OUT>
 __global__ void __launch_bounds__(kIntThreads) lattice_int_kernel(LatArgs A, int with_inflow) {
@@ -429,6 +565,18 @@ static LatArgs lat_args(const Problem& p, const double* src, const double* x, do
 
 template <int FS, int SRC, int OUT>
 static int launch_int(const Problem& p, const LatArgs& A, int with_inflow, cudaStream_t s) {
+    const size_t smem_planes = sizeof(double) * A.nxy * (3 * kFC + 2);
+    if (smem_planes <= 160 * 1024 && !getenv_flag("RTK_LATTICE_NO_SMEM")) {
+        auto kern = lattice_int_smem_kernel<FS, SRC, OUT>;
+        if (smem_planes > 48 * 1024 &&
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_planes)) !=
+                cudaSuccess)
+            return set_error(RTK_ERESOURCE, "lattice planes do not fit in shared memory");
+        const int nfc = (A.n_freq + kFC - 1) / kFC;
+        kern<<<A.n_dirs * nfc, kIntThreads, smem_planes, s>>>(A, with_inflow);
+        RTK_LAUNCH_CHECK("lattice_int_smem_kernel");
+        return RTK_OK;
+    }
     const size_t smem = sizeof(double) * A.nxy * kFC;
     auto kern = lattice_int_kernel<FS, SRC, OUT>;
     if (smem > 48 * 1024) {
