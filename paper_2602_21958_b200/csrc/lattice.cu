@@ -332,17 +332,17 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_kernel(LatArgs A, int
     }
 }
 
-// Two frequencies per thread: the lattice geometry (shift, stencil, trilinear
-// opacity, dt) is frequency-independent and computed once for the pair; the
-// internal planes use the even pitch fp so the pair moves as one 16-byte load.
-template <int FS>
-__device__ __forceinline__ double2 advance_line2(const LatDir& D, double2 acc, int lx, int ly, int t, int nx,
-                                                 int ny, const double* __restrict__ chi_a,
-                                                 const double* __restrict__ chi_b, const double2* __restrict__ Sa,
-                                                 const double2* __restrict__ Sb, int64_t ss, double phi0,
-                                                 double phi1) {
-    double2 prev_s = make_double2(0.0, 0.0);
-    double prev_c = 0.0;
+// F frequencies per thread (F even): the lattice geometry (shift, stencil, trilinear
+// opacity, dt) is frequency-independent and computed once for the group; the internal
+// planes use the even pitch fp so each group moves as F/2 16-byte loads.
+template <int FS, int F>
+__device__ __forceinline__ void advance_lineF(const LatDir& D, double (&acc)[F], int lx, int ly, int t, int nx,
+                                              int ny, const double* __restrict__ chi_a,
+                                              const double* __restrict__ chi_b, const double2* __restrict__ Sa,
+                                              const double2* __restrict__ Sb, int64_t ss, const double (&phi)[F]) {
+    double prev_s[F], prev_c = 0.0;
+#pragma unroll
+    for (int q = 0; q < F; ++q) prev_s[q] = 0.0;
     for (int m = 0; m <= D.n_sub; ++m) {
         const double tt = t + static_cast<double>(m) / D.n_sub;
         const double wz = static_cast<double>(m) / D.n_sub;
@@ -352,111 +352,156 @@ __device__ __forceinline__ double2 advance_line2(const LatDir& D, double2 acc, i
                           st.w01 * __ldg(chi_a + st.c01) + st.w11 * __ldg(chi_a + st.c11);
         const double cb = st.w00 * __ldg(chi_b + st.c00) + st.w10 * __ldg(chi_b + st.c10) +
                           st.w01 * __ldg(chi_b + st.c01) + st.w11 * __ldg(chi_b + st.c11);
-        const double2 a00 = __ldg(Sa + st.c00 * ss), a10 = __ldg(Sa + st.c10 * ss);
-        const double2 a01 = __ldg(Sa + st.c01 * ss), a11 = __ldg(Sa + st.c11 * ss);
-        const double2 b00 = __ldg(Sb + st.c00 * ss), b10 = __ldg(Sb + st.c10 * ss);
-        const double2 b01 = __ldg(Sb + st.c01 * ss), b11 = __ldg(Sb + st.c11 * ss);
         const double c_m = (1 - wz) * ca + wz * cb;
-        double2 s_m;
-        s_m.x = (1 - wz) * (st.w00 * a00.x + st.w10 * a10.x + st.w01 * a01.x + st.w11 * a11.x) +
-                wz * (st.w00 * b00.x + st.w10 * b10.x + st.w01 * b01.x + st.w11 * b11.x);
-        s_m.y = (1 - wz) * (st.w00 * a00.y + st.w10 * a10.y + st.w01 * a01.y + st.w11 * a11.y) +
-                wz * (st.w00 * b00.y + st.w10 * b10.y + st.w01 * b01.y + st.w11 * b11.y);
-        if (m > 0) {
-            const double dt = D.sub_len * (prev_c + c_m) * 0.5;
-            const double d0 = phi0 * dt, d1 = phi1 * dt;
-            if (FS == RTK_FS_IE) {
-                const double r0 = rcp_nr(1.0 + d0), r1 = rcp_nr(1.0 + d1);
-                acc.x = fma(acc.x, r0, (d0 * s_m.x) * r0);
-                acc.y = fma(acc.y, r1, (d1 * s_m.y) * r1);
-            } else {
-                const ExpLin w0 = exp_linear_weights(d0), w1 = exp_linear_weights(d1);
-                acc.x = fma(acc.x, w0.att, w0.wu * prev_s.x + w0.wc * s_m.x);
-                acc.y = fma(acc.y, w1.att, w1.wu * prev_s.y + w1.wc * s_m.y);
+        const double dt = D.sub_len * (prev_c + c_m) * 0.5;
+#pragma unroll
+        for (int h = 0; h < F / 2; ++h) {
+            const double2 a00 = __ldg(Sa + st.c00 * ss + h), a10 = __ldg(Sa + st.c10 * ss + h);
+            const double2 a01 = __ldg(Sa + st.c01 * ss + h), a11 = __ldg(Sa + st.c11 * ss + h);
+            const double2 b00 = __ldg(Sb + st.c00 * ss + h), b10 = __ldg(Sb + st.c10 * ss + h);
+            const double2 b01 = __ldg(Sb + st.c01 * ss + h), b11 = __ldg(Sb + st.c11 * ss + h);
+            double s2[2];
+            s2[0] = (1 - wz) * (st.w00 * a00.x + st.w10 * a10.x + st.w01 * a01.x + st.w11 * a11.x) +
+                    wz * (st.w00 * b00.x + st.w10 * b10.x + st.w01 * b01.x + st.w11 * b11.x);
+            s2[1] = (1 - wz) * (st.w00 * a00.y + st.w10 * a10.y + st.w01 * a01.y + st.w11 * a11.y) +
+                    wz * (st.w00 * b00.y + st.w10 * b10.y + st.w01 * b01.y + st.w11 * b11.y);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int q = 2 * h + e;
+                if (m > 0) {
+                    const double dtau = phi[q] * dt;
+                    if (FS == RTK_FS_IE) {
+                        const double r = rcp_nr(1.0 + dtau);
+                        acc[q] = fma(acc[q], r, (dtau * s2[e]) * r);
+                    } else {
+                        const ExpLin w = exp_linear_weights(dtau);
+                        acc[q] = fma(acc[q], w.att, w.wu * prev_s[q] + w.wc * s2[e]);
+                    }
+                }
+                prev_s[q] = s2[e];
             }
         }
-        prev_s = s_m;
         prev_c = c_m;
     }
-    return acc;
 }
 
-// thread = (line c, frequency pair q): f0 = 2q, f1 = 2q + 1 (f1 may be padding).
-// Directions are processed hemisphere by hemisphere so only NM x 2 moment
-// accumulators are live; layer t gets the down part, layer nz-1-t the up part.
-template <int FS, int NM>
-__global__ void __launch_bounds__(256) lattice_mom_pair_kernel(LatArgs A, int t, const double* __restrict__ st_in,
-                                                                double* __restrict__ st_out, double* __restrict__ mom,
-                                                                int with_inflow, int fp,
-                                                                const double* __restrict__ plane_cur,
-                                                                const double* __restrict__ plane_next) {
-    const int hp = fp >> 1;
+// thread = (line c, frequency group q of F): f = F q .. F q + F - 1 (the tail may be padding).
+// Directions are processed hemisphere by hemisphere so only NM x F moment accumulators
+// are live; layer t gets the down part, layer nz-1-t the up part.
+template <int FS, int NM, int F>
+__global__ void __launch_bounds__(256) lattice_mom_group_kernel(LatArgs A, int t, const double* __restrict__ st_in,
+                                                                 double* __restrict__ st_out, double* __restrict__ mom,
+                                                                 int with_inflow, int fp,
+                                                                 const double* __restrict__ plane_cur,
+                                                                 const double* __restrict__ plane_next) {
+    const int ng = (fp + F - 1) / F;       // groups per line
+    const int hp = fp >> 1;                // double2 per line in the [dir][line][fp] planes
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (tid >= A.nxy * hp) return;
-    const int c = static_cast<int>(tid / hp);
-    const int q = static_cast<int>(tid - static_cast<int64_t>(c) * hp);
-    const int f0 = 2 * q, f1 = 2 * q + 1;
-    const bool v1 = f1 < A.n_freq;
+    if (tid >= A.nxy * ng) return;
+    const int c = static_cast<int>(tid / ng);
+    const int g = static_cast<int>(tid - static_cast<int64_t>(c) * ng);
+    const int f0 = F * g;
     const int j = c / A.nx, i = c - j * A.nx;
-    const double phi0 = A.phi[f0], phi1 = v1 ? A.phi[f1] : 0.0;
-    const int64_t plane2 = A.nxy * static_cast<int64_t>(hp);   // double2 per direction plane
+    double phi[F], in_top[F], in_bot[F];
+    bool fv[F];
+#pragma unroll
+    for (int q = 0; q < F; ++q) {
+        const int f = f0 + q;
+        fv[q] = f < A.n_freq;
+        phi[q] = fv[q] ? A.phi[f] : 0.0;
+        in_top[q] = (with_inflow && fv[q] && A.inflow_top) ? A.inflow_top[f] : 0.0;
+        in_bot[q] = (with_inflow && fv[q] && A.inflow_bottom) ? A.inflow_bottom[f] : 0.0;
+    }
+    // the last group of a line may reach past fp when F does not divide fp: clamp its loads
+    const bool full_group = f0 + F <= fp;
+    const int64_t plane2 = A.nxy * static_cast<int64_t>(hp);
     const double2* sin2 = reinterpret_cast<const double2*>(st_in);
     double2* sout2 = reinterpret_cast<double2*>(st_out);
     const double2* pc2 = reinterpret_cast<const double2*>(plane_cur);
     const double2* pn2 = reinterpret_cast<const double2*>(plane_next);
-    double2 in_top = make_double2(0.0, 0.0), in_bot = make_double2(0.0, 0.0);
-    if (with_inflow) {
-        if (A.inflow_top) in_top = make_double2(A.inflow_top[f0], v1 ? A.inflow_top[f1] : 0.0);
-        if (A.inflow_bottom) in_bot = make_double2(A.inflow_bottom[f0], v1 ? A.inflow_bottom[f1] : 0.0);
-    }
+    const int g2 = f0 >> 1;               // first double2 of the group within a line
     for (int hemi = 0; hemi < 2; ++hemi) {       // 0: down (layer t), 1: up (layer nz-1-t)
         const int k = hemi == 0 ? t : A.nz - 1 - t;
-        double m0[NM], m1[NM];
+        double mo[NM][F];
 #pragma unroll
-        for (int l = 0; l < NM; ++l) m0[l] = m1[l] = 0.0;
+        for (int l = 0; l < NM; ++l)
+#pragma unroll
+            for (int q = 0; q < F; ++q) mo[l][q] = 0.0;
         for (int a = 0; a < A.n_dirs; ++a) {
             const LatDir& D = A.dirs[a];
             if ((D.down != 0) != (hemi == 0)) continue;
-            const double2* sa = sin2 + a * plane2;
-            double2 v;
+            const double2* sa = sin2 + a * plane2 + g2;
+            double v[F];
             if (t == 0) {
-                v = hemi == 0 ? in_top : in_bot;
+#pragma unroll
+                for (int q = 0; q < F; ++q) v[q] = hemi == 0 ? in_top[q] : in_bot[q];
             } else {
                 const Stencil st = stencil_at(i, j, shift_of(-t * D.sx, -t * D.sy, A.nx, A.ny), A.nx, A.ny);
-                const double2 s00 = sa[st.c00 * hp + q], s10 = sa[st.c10 * hp + q];
-                const double2 s01 = sa[st.c01 * hp + q], s11 = sa[st.c11 * hp + q];
-                v.x = st.w00 * s00.x + st.w10 * s10.x + st.w01 * s01.x + st.w11 * s11.x;
-                v.y = st.w00 * s00.y + st.w10 * s10.y + st.w01 * s01.y + st.w11 * s11.y;
+#pragma unroll
+                for (int h = 0; h < F / 2; ++h) {
+                    if (!full_group && g2 + h >= hp) {
+                        v[2 * h] = v[2 * h + 1] = 0.0;
+                        continue;
+                    }
+                    const double2 s00 = sa[st.c00 * hp + h], s10 = sa[st.c10 * hp + h];
+                    const double2 s01 = sa[st.c01 * hp + h], s11 = sa[st.c11 * hp + h];
+                    v[2 * h] = st.w00 * s00.x + st.w10 * s10.x + st.w01 * s01.x + st.w11 * s11.x;
+                    v[2 * h + 1] = st.w00 * s00.y + st.w10 * s10.y + st.w01 * s01.y + st.w11 * s11.y;
+                }
             }
 #pragma unroll
             for (int l = 0; l < NM; ++l) {
                 const double w = D.wy[l];
-                m0[l] = fma(w, v.x, m0[l]);
-                m1[l] = fma(w, v.y, m1[l]);
+#pragma unroll
+                for (int q = 0; q < F; ++q) mo[l][q] = fma(w, v[q], mo[l][q]);
             }
             if (t < A.nz - 1) {
                 const int k2 = hemi == 0 ? k + 1 : k - 1;
-                double2 acc = (t == 0) ? (hemi == 0 ? in_top : in_bot) : sa[static_cast<int64_t>(c) * hp + q];
+                double acc[F];
+#pragma unroll
+                for (int h = 0; h < F / 2; ++h) {
+                    double2 s2;
+                    if (t == 0) s2 = hemi == 0 ? make_double2(in_top[2 * h], in_top[2 * h + 1])
+                                                : make_double2(in_bot[2 * h], in_bot[2 * h + 1]);
+                    else s2 = (!full_group && g2 + h >= hp) ? make_double2(0.0, 0.0)
+                                                            : sa[static_cast<int64_t>(c) * hp + h];
+                    acc[2 * h] = s2.x;
+                    acc[2 * h + 1] = s2.y;
+                }
                 const LatDir Dl = D;
-                acc = advance_line2<FS>(Dl, acc, i, j, t, A.nx, A.ny, A.chi + static_cast<int64_t>(k) * A.nxy,
-                                        A.chi + static_cast<int64_t>(k2) * A.nxy, pc2 + a * plane2 + q,
-                                        pn2 + a * plane2 + q, hp, phi0, phi1);
-                sout2[a * plane2 + static_cast<int64_t>(c) * hp + q] = acc;
+                if (full_group) {
+                    advance_lineF<FS, F>(Dl, acc, i, j, t, A.nx, A.ny, A.chi + static_cast<int64_t>(k) * A.nxy,
+                                         A.chi + static_cast<int64_t>(k2) * A.nxy, pc2 + a * plane2 + g2,
+                                         pn2 + a * plane2 + g2, hp, phi);
+#pragma unroll
+                    for (int h = 0; h < F / 2; ++h)
+                        sout2[a * plane2 + static_cast<int64_t>(c) * hp + g2 + h] = make_double2(acc[2 * h], acc[2 * h + 1]);
+                } else {
+                    // tail group: process as pairs within the pitch
+                    for (int h = 0; h < F / 2 && g2 + h < hp; ++h) {
+                        double ap[2] = {acc[2 * h], acc[2 * h + 1]};
+                        const double pp[2] = {phi[2 * h], phi[2 * h + 1]};
+                        advance_lineF<FS, 2>(Dl, ap, i, j, t, A.nx, A.ny, A.chi + static_cast<int64_t>(k) * A.nxy,
+                                             A.chi + static_cast<int64_t>(k2) * A.nxy, pc2 + a * plane2 + g2 + h,
+                                             pn2 + a * plane2 + g2 + h, hp, pp);
+                        sout2[a * plane2 + static_cast<int64_t>(c) * hp + g2 + h] = make_double2(ap[0], ap[1]);
+                    }
+                }
             }
         }
         // step t is the first visit of layers t and nz-1-t iff t < nz-1-t; the middle layer
         // (odd nz) gets both parts in this thread, up added to down
         const bool first = (hemi == 0) ? (t <= A.nz - 1 - t) : (t < A.nz - 1 - t);
-        double2* out = reinterpret_cast<double2*>(mom + (static_cast<int64_t>(k) * A.nxy + c) * NM * fp) + q;
+        double* out = mom + (static_cast<int64_t>(k) * A.nxy + c) * NM * fp + f0;
 #pragma unroll
         for (int l = 0; l < NM; ++l) {
-            double2 val = make_double2(m0[l], v1 ? m1[l] : 0.0);
-            if (!first) {
-                const double2 old = out[l * hp];
-                val.x += old.x;
-                val.y += old.y;
+#pragma unroll
+            for (int q = 0; q < F; ++q) {
+                if (f0 + q >= fp) continue;
+                const double val = fv[q] ? mo[l][q] : 0.0;
+                double* o = out + static_cast<int64_t>(l) * fp + q;
+                *o = first ? val : *o + val;
             }
-            out[l * hp] = val;
         }
     }
 }
@@ -612,7 +657,8 @@ int lattice_transfer_intensity(const Problem& p, int src_mode, int out_mode, boo
 template <int FS, int SRC, int NM>
 static int launch_mom_steps(const Problem& p, const LatArgs& A, bool with_inflow, double* mom, cudaStream_t s) {
     const unsigned pblocks = static_cast<unsigned>((A.nxy * p.fp + 255) / 256);
-    const unsigned sblocks = static_cast<unsigned>((A.nxy * (p.fp / 2) + 255) / 256);
+    constexpr int F = 2;   // F = 4 measured slower (176 registers, 1 block/SM; cfg5 854 vs 487 ms)
+    const unsigned sblocks = static_cast<unsigned>((A.nxy * ((p.fp + F - 1) / F) + 255) / 256);
     double* a = p.lat_state[0];
     double* b = p.lat_state[1];
     for (int t = 0; t < A.nz; ++t) {
@@ -622,8 +668,9 @@ static int launch_mom_steps(const Problem& p, const LatArgs& A, bool with_inflow
             lattice_splane_kernel<SRC, NM><<<pblocks, 256, 0, s>>>(A, t, cur, nxt, t == 0 ? 1 : 0, p.fp);
             RTK_LAUNCH_CHECK("lattice_splane_kernel");
         }
-        lattice_mom_pair_kernel<FS, NM><<<sblocks, 256, 0, s>>>(A, t, a, b, mom, with_inflow ? 1 : 0, p.fp, cur, nxt);
-        RTK_LAUNCH_CHECK("lattice_mom_pair_kernel");
+        lattice_mom_group_kernel<FS, NM, F><<<sblocks, 256, 0, s>>>(A, t, a, b, mom, with_inflow ? 1 : 0, p.fp, cur,
+                                                                    nxt);
+        RTK_LAUNCH_CHECK("lattice_mom_group_kernel");
         double* tmp = a;
         a = b;
         b = tmp;
