@@ -133,6 +133,11 @@ int rtk_profile_apply_A(rtk_problem* p, const double* x_dev, double* y_dev, int6
                         float* ms_out);
 /* Same, host buffers in and out (H2D + matvec + D2H); the e2e path of the drop-in. */
 int rtk_apply_A_host(rtk_problem* p, const double* x_host, double* y_host, int64_t n, void* stream);
+/* Batched host-buffer apply_A: y_k = A x_k for k < count.  Two device buffer pairs and two
+ * streams alternate, so the H2D copy of x_{k+1} overlaps the D2H copy of y_k (PCIe is full
+ * duplex).  Host buffers should be pinned for the copies to be asynchronous. */
+int rtk_apply_A_host_batch(rtk_problem* p, const double* const* x_host, double* const* y_host, int32_t count,
+                           int64_t n);
 /* s = Sigma x -- apply_scattering, R/scattering.py:126-148. */
 int rtk_apply_sigma(rtk_problem* p, const double* x_dev, double* s_dev, int64_t n, void* stream);
 /* y = Lambda s (homogeneous part) -- apply_transfer, R/transfer.py:134-141. */

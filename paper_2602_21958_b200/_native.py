@@ -83,6 +83,7 @@ SIGNATURES = [
     ("rtk_problem_set_inflow", ctypes.c_int, [_P, _P, _I64]),
     ("rtk_apply_A", ctypes.c_int, [_P, _P, _P, _I64, _P]),
     ("rtk_apply_A_host", ctypes.c_int, [_P, _P, _P, _I64, _P]),
+    ("rtk_apply_A_host_batch", ctypes.c_int, [_P, _P, _P, _I32, _I64]),
     ("rtk_profile_apply_A", ctypes.c_int, [_P, _P, _P, _I64, _P, ctypes.POINTER(ctypes.c_float)]),
     ("rtk_apply_sigma", ctypes.c_int, [_P, _P, _P, _I64, _P]),
     ("rtk_apply_lambda", ctypes.c_int, [_P, _P, _P, _I64, _P]),

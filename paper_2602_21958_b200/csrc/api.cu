@@ -35,7 +35,11 @@ int cuda_status(cudaError_t e, const char* what) {
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 Problem::~Problem() {
-    double* bufs[] = {dt, phi, inv_mu, wy, yb, rwt, gamma, coeffs, inflow, mom, gmom, host_x, host_y};
+    double* bufs[] = {dt, phi, inv_mu, wy, yb, rwt, gamma, coeffs, inflow, mom, gmom, host_x, host_y, host_x2, host_y2};
+    for (auto st : io)
+        if (st) cudaStreamDestroy(st);
+    for (auto ev : io_done)
+        if (ev) cudaEventDestroy(ev);
     for (double* b : bufs)
         if (b) cudaFree(b);
     if (dir_sign) cudaFree(dir_sign);
@@ -355,6 +359,36 @@ int rtk_apply_A_host(rtk_problem* p, const double* x_host, double* y_host, int64
     if ((rc = rtk::apply_A_dev(q, q.host_x, q.host_y, s))) return rc;
     RTK_CUDA_TRY(cudaMemcpyAsync(y_host, q.host_y, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
     RTK_CUDA_TRY(cudaStreamSynchronize(s));
+    return RTK_OK;
+}
+
+int rtk_apply_A_host_batch(rtk_problem* p, const double* const* xs, double* const* ys, int32_t count, int64_t n) {
+    int rc = check_n(p, n);
+    if (rc) return rc;
+    if (count < 0 || (count > 0 && (!xs || !ys))) return set_error(RTK_EINVAL, "bad batch arguments");
+    Problem& q = p->impl;
+    if (!q.host_x) RTK_CUDA_TRY(cudaMalloc(&q.host_x, sizeof(double) * q.n_total));
+    if (!q.host_y) RTK_CUDA_TRY(cudaMalloc(&q.host_y, sizeof(double) * q.n_total));
+    if (!q.host_x2) RTK_CUDA_TRY(cudaMalloc(&q.host_x2, sizeof(double) * q.n_total));
+    if (!q.host_y2) RTK_CUDA_TRY(cudaMalloc(&q.host_y2, sizeof(double) * q.n_total));
+    if (!q.io[0]) {
+        for (auto& st : q.io) RTK_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        for (auto& ev : q.io_done) RTK_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    const size_t bytes = sizeof(double) * n;
+    for (int k = 0; k < count; ++k) {
+        const int b = k & 1;
+        cudaStream_t st = q.io[b];
+        double* dx = b ? q.host_x2 : q.host_x;
+        double* dy = b ? q.host_y2 : q.host_y;
+        RTK_CUDA_TRY(cudaMemcpyAsync(dx, xs[k], bytes, cudaMemcpyHostToDevice, st));
+        // the two streams share the operator's workspace (moments, G): serialise the compute parts
+        if (k > 0) RTK_CUDA_TRY(cudaStreamWaitEvent(st, q.io_done[1 - b], 0));
+        if ((rc = rtk::apply_A_dev(q, dx, dy, st))) return rc;
+        RTK_CUDA_TRY(cudaEventRecord(q.io_done[b], st));
+        RTK_CUDA_TRY(cudaMemcpyAsync(ys[k], dy, bytes, cudaMemcpyDeviceToHost, st));
+    }
+    for (auto st : q.io) RTK_CUDA_TRY(cudaStreamSynchronize(st));
     return RTK_OK;
 }
 

@@ -77,6 +77,9 @@ struct Problem {
     int* dir_sign = nullptr;     // [n_angles] -1 down (mu<0), +1 up
     double *mom = nullptr, *gmom = nullptr;
     double *host_x = nullptr, *host_y = nullptr;   // lazily allocated device staging for *_host calls
+    double *host_x2 = nullptr, *host_y2 = nullptr; // second staging pair (batched host calls)
+    cudaStream_t io[2] = {nullptr, nullptr};
+    cudaEvent_t io_done[2] = {nullptr, nullptr};
     // TMA sweep path (sweep_tma.cu)
     bool tma_ready = false;
     int tma_n_ctas = 0, tma_gw = 0, tma_u = 4;

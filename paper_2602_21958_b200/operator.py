@@ -16,7 +16,8 @@ from paper_2602_21958_b200 import _device, _native
 from paper_2602_21958_b200.errors import DENSE_CAP_DEFAULT, ResourceLimitError
 from paper_2602_21958_b200.scattering import ScatteringOperator, slab_handle
 
-__all__ = ["DENSE_CAP_DEFAULT", "ResourceLimitError", "RTProblem", "DeviceOperator", "apply_A", "build_rhs",
+__all__ = ["DENSE_CAP_DEFAULT", "ResourceLimitError", "RTProblem", "DeviceOperator", "apply_A", "apply_A_batch",
+           "build_rhs",
            "source_function", "operator", "spectral_radius_estimate", "materialize_A"]
 
 
@@ -89,6 +90,25 @@ def apply_A(problem: RTProblem, v):
     out = np.empty(n)
     _native.check(lib.rtk_apply_A_host(h.h, _device.dptr(arr), _device.dptr(out), n, _device.stream_ptr()))
     return out
+
+
+def apply_A_batch(problem: RTProblem, vs, out=None):
+    """[A v for v in vs] for host (numpy) vectors, with the H2D copy of the next vector
+    overlapping the D2H copy of the previous result (rtk_apply_A_host_batch).  Pass
+    pinned-memory arrays (e.g. torch.empty(n, pin_memory=True).numpy()) for full overlap."""
+    import ctypes
+
+    n = problem.n_total
+    h = problem.device()
+    xs = [np.ascontiguousarray(np.asarray(v, dtype=float).reshape(-1)) for v in vs]
+    for x in xs:
+        if x.size != n:
+            raise ValueError(f"expected length {n}, got {x.size}")
+    ys = out if out is not None else [np.empty(n) for _ in xs]
+    xp = (ctypes.c_void_p * len(xs))(*[x.ctypes.data for x in xs])
+    yp = (ctypes.c_void_p * len(ys))(*[y.ctypes.data for y in ys])
+    _native.check(_native.lib().rtk_apply_A_host_batch(h.h, xp, yp, len(xs), n))
+    return ys
 
 
 def build_rhs(problem: RTProblem, override_ones: bool = False, device: bool = False):

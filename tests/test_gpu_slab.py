@@ -215,3 +215,30 @@ def test_field_vector_ray_major_round_trip():
     assert out.ordering is P.Ordering.RAY_MAJOR
     back = P.permute(p.grid, out, P.Ordering.SPACE_MAJOR).values
     np.testing.assert_allclose(back, P.apply_transfer(p.transfer, v), rtol=1e-15, atol=1e-16)
+
+
+def test_cfg2_full_size_gmres_history_prefix_matches_oracle():
+    """Full cfg2 (N = 65.5M): the first 12 GMRES(30) iterations agree with the oracle GMRES
+    (reference MGS control flow) driving the C/OpenMP port's matvec (itself pinned to the numpy
+    oracle in tests/test_oracle_extensions.py)."""
+    from oracle import cport
+
+    p = configs.slab_problem(2)
+    d = oracle_desc(p)
+    port = cport.SlabPort(d)
+    b = np.random.default_rng(21958).standard_normal(p.n_total)
+    ref = ro.gmres(port.apply_A, b, rel_tol=1e-30, max_iter=12, restart=30)
+    rep = P.gmres(p, b, P.SolveConfig(rel_tol=1e-30, max_iter=12, restart=30))
+    np.testing.assert_allclose(rep.residual_history, ref.residual_history, rtol=1e-9)
+    assert rel_l2(rep.solution, ref.solution) <= 1e-7
+
+
+def test_apply_A_batch_matches_single_calls():
+    import torch
+
+    p = configs.slab_problem(2, n_space=200, n_angles=16, n_freq=130)
+    rng = np.random.default_rng(4)
+    xs = [torch.from_numpy(rng.standard_normal(p.n_total)).pin_memory().numpy() for _ in range(5)]
+    ys = P.apply_A_batch(p, xs)
+    for x, y in zip(xs, ys):
+        np.testing.assert_array_equal(y, P.apply_A(p, x))
