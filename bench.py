@@ -155,6 +155,18 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def aggregate(ms_local: float, steps: int, world: int, device: str):
+    """Max of the timed region over ranks; whole-job throughput = world * steps / max time
+    (weak scaling: every rank runs the full per-GPU workload)."""
+    import torch
+
+    t = torch.tensor([ms_local], dtype=torch.float64, device=device)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(t.item())
+    return ms_max, world * steps / (ms_max / 1e3)
+
+
 def cpu_port_timing(problem, target_s=12.0, max_steps=30):
     """The oracle's C/OpenMP restatement (oracle/librto.so) on this host's cores."""
     from oracle import cport
@@ -252,12 +264,8 @@ def run_b200(args):
     if world > 1:
         torch.distributed.barrier()
     clk = clocks.stop()
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max, value = aggregate(ms, args.steps, world, "cuda")
     ms_per_step = ms_max / args.steps
-    value = world * args.steps / (ms_max / 1e3)
 
     # per-kernel durations inside the same matvec (events on the launching stream)
     kms = np.zeros(3)
