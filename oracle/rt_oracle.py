@@ -246,7 +246,6 @@ def psi_dipole_prd(ybasis, coeffs, R):
 # ---------------------------------------------------------------------------
 
 EXP_SERIES_THRESHOLD = 0.05
-EXP_EXPM1_THRESHOLD = 0.5
 # h1(d) = e1/d^2 = sum_{n=2}^{9} (-1)^n d^(n-2)/n!;  h2(d) = e2/d^3 = 2 sum_{n=3}^{10} (-1)^(n+1) d^(n-3)/n!
 _H1 = [((-1) ** n) / math.factorial(n) for n in range(2, 10)]
 _H2 = [2.0 * ((-1) ** (n + 1)) / math.factorial(n) for n in range(3, 11)]
@@ -262,37 +261,36 @@ def _horner(coefs, d):
 def exp_weights(d):
     """EXTENSION: (att = e^-d, e0, e1, e2) with e_k = int_0^d t^k e^{-(d - t)} dt.
 
-    Three branches shared with the CUDA build (csrc/formal.cuh) and the C port:
-      d < 0.05 : Taylor series (8 terms), no transcendental;
-      d < 0.5  : e0 = -expm1(-d), att = 1 - e0;
-      else     : att = exp(-d), e0 = 1 - att;
-    e1 = d - e0, e2 = d^2 - 2 e1 outside the series branch.
+    Shared with the CUDA build (csrc/formal.cuh) and the C port:
+      d < 0.05 : e1 = d^2 h1(d), e2 = d^3 h2(d) (8-term Taylor series), e0 = d - e1, att = 1 - e0;
+      else     : att = exp(-d), e0 = 1 - att, e1 = d - e0, e2 = d^2 - 2 e1.
     """
     d = np.asarray(d, dtype=float)
     small = d < EXP_SERIES_THRESHOLD
-    mid = (~small) & (d < EXP_EXPM1_THRESHOLD)
     with np.errstate(over="ignore", invalid="ignore"):
-        e0_mid = -np.expm1(-d)
         att_big = np.exp(-d)
         e1_small = d * d * _horner(_H1, d)
         e2_small = d * d * d * _horner(_H2, d)
-    e0 = np.where(small, d - e1_small, np.where(mid, e0_mid, 1.0 - att_big))
-    att = np.where(small | mid, 1.0 - e0, att_big)
+    e0 = np.where(small, d - e1_small, 1.0 - att_big)
+    att = np.where(small, 1.0 - e0, att_big)
     e1 = np.where(small, e1_small, d - e0)
     e2 = np.where(small, e2_small, d * d - 2.0 * e1)
     return att, e0, e1, e2
 
 
 def _linear_weights(d):
-    """(att, w_u, w_c); in the series branch w_c = d h1(d) (no division), as on the device."""
+    """(att, w_u, w_c) as csrc/formal.cuh: series path w_c = d h1(d), e0 = d - d w_c, att = 1 - e0;
+    transcendental path att = exp(-d), e0 = 1 - att, w_c = (d - e0) / d."""
     d = np.asarray(d, dtype=float)
-    att, e0, e1, _ = exp_weights(d)
     small = d < EXP_SERIES_THRESHOLD
-    with np.errstate(invalid="ignore", divide="ignore"):
-        wc = np.where(small, d * _horner(_H1, d), (d - e0) / d)
-    # the series branch defines e0 = d - d * w_c, recompute it that way for bit-parity of the formula
-    e0 = np.where(small, d - d * wc, e0)
-    att = np.where(small, 1.0 - e0, att)
+    with np.errstate(over="ignore", invalid="ignore", divide="ignore"):
+        wc_s = d * _horner(_H1, d)
+        att_b = np.exp(-d)
+        e0_b = 1.0 - att_b
+        wc_b = (d - e0_b) / d
+    e0 = np.where(small, d - d * wc_s, e0_b)
+    att = np.where(small, 1.0 - e0, att_b)
+    wc = np.where(small, wc_s, wc_b)
     return att, e0 - wc, wc
 
 

@@ -20,7 +20,6 @@
 #endif
 
 #define THRESH 0.05
-#define THRESH_EXPM1 0.5
 
 /* h1 = e1/d^2, h2 = e2/d^3: 8-term Taylor series (csrc/formal.cuh, rt_oracle.py::exp_weights) */
 static double h1(double d) {
@@ -39,7 +38,7 @@ static double h2(double d) {
     return acc;
 }
 
-/* att = e^-d, e0, e1, e2 with the three shared branches */
+/* att = e^-d, e0, e1, e2 (csrc/formal.cuh): series below THRESH, exp(-d) and closed forms above */
 static void exp_w(double d, double* att, double* e0, double* e1, double* e2) {
     if (d < THRESH) {
         *e1 = d * d * h1(d);
@@ -47,13 +46,8 @@ static void exp_w(double d, double* att, double* e0, double* e1, double* e2) {
         *e0 = d - *e1;
         *att = 1.0 - *e0;
     } else {
-        if (d < THRESH_EXPM1) {
-            *e0 = -expm1(-d);
-            *att = 1.0 - *e0;
-        } else {
-            *att = exp(-d);
-            *e0 = 1.0 - *att;
-        }
+        *att = exp(-d);
+        *e0 = 1.0 - *att;
         *e1 = d - *e0;
         *e2 = d * d - 2.0 * *e1;
     }

@@ -131,6 +131,48 @@ __device__ __forceinline__ void consume(const ConsumerCtx<NM>& c, SweepState& st
     }
 }
 
+// Exp-parabolic needs the downwind source S_{j+1}: node j-1 is finalised while node j
+// is being read (one-node delay), the last node with the linear weights afterwards.
+struct ParState {
+    double acc, s_m2, s_m1, d_m2, x_m1;
+    double* yp;   // node to be finalised next
+};
+
+template <int NM, int U, bool DOWN, bool CHECK>
+__device__ __forceinline__ void consume_par(const ConsumerCtx<NM>& c, ParState& st, const double* __restrict__ xs,
+                                            const double* __restrict__ gs, const double* __restrict__ dts, int q,
+                                            int64_t n, int64_t step) {
+    const double* gcol = gs + c.gcol;
+#pragma unroll
+    for (int uu = 0; uu < U; ++uu) {
+        const int j = q * U + uu;
+        if (CHECK && j >= n) break;
+        const int u = DOWN ? uu : U - 1 - uu;
+        const double xv = xs[u * kXW + c.xoff];
+        double sv = 0.0;
+#pragma unroll
+        for (int k = 0; k < NM; ++k) sv = fma(c.yk[k], gcol[(u * NM + k) * c.gw], sv);
+        if (CHECK && j == 0) {
+            if (c.valid) *st.yp = xv - st.acc;
+            st.yp += step;
+            st.s_m1 = sv;
+            st.x_m1 = xv;
+            continue;
+        }
+        const double d_m1 = c.phi_f * dts[u] * c.inv_mu;   // segment j-1 -> j
+        if (!(CHECK && j == 1)) {
+            const ExpPar w = exp_parabolic_weights(st.d_m2, d_m1);
+            st.acc = fma(st.acc, w.att, w.wu * st.s_m2 + w.wc * st.s_m1 + w.wd * sv);
+            if (c.valid) *st.yp = st.x_m1 - st.acc;
+            st.yp += step;
+        }
+        st.s_m2 = st.s_m1;
+        st.s_m1 = sv;
+        st.d_m2 = d_m1;
+        st.x_m1 = xv;
+    }
+}
+
 template <int FS, int NM, int U, int S>
 __global__ void __launch_bounds__(kTmaThreads) sweep1d_tma_kernel(const __grid_constant__ CUtensorMap xmap,
                                                                   const __grid_constant__ CUtensorMap gmap,
@@ -195,6 +237,7 @@ __global__ void __launch_bounds__(kTmaThreads) sweep1d_tma_kernel(const __grid_c
 #pragma unroll
     for (int k = 0; k < NM; ++k) yk[k] = A.yb[k * A.n_angles + a];
     SweepState st{0.0, 0.0, A.y + (down ? 0 : (n - 1) * A.n_rays) + ray};
+    ParState ps{0.0, 0.0, 0.0, 0.0, 0.0, st.yp};
     const int64_t step = down ? A.n_rays : -A.n_rays;
     ConsumerCtx<NM> c2;
     c2.xoff = xoff;
@@ -217,7 +260,15 @@ __global__ void __launch_bounds__(kTmaThreads) sweep1d_tma_kernel(const __grid_c
         const int r0 = down ? q * U : static_cast<int>(n) - U - q * U;
         const int dt_off = ((down ? r0 - 1 : r0) + kDtPad) & 1;
         const bool edge = (q == 0) || (q == Q - 1);
-        if (down) {
+        if (FS == RTK_FS_EXP_PARABOLIC) {
+            if (down) {
+                if (edge) consume_par<NM, U, true, true>(c2, ps, xs, gs, dts + dt_off, q, n, step);
+                else consume_par<NM, U, true, false>(c2, ps, xs, gs, dts + dt_off, q, n, step);
+            } else {
+                if (edge) consume_par<NM, U, false, true>(c2, ps, xs, gs, dts + dt_off, q, n, step);
+                else consume_par<NM, U, false, false>(c2, ps, xs, gs, dts + dt_off, q, n, step);
+            }
+        } else if (down) {
             if (edge) consume<FS, NM, U, true, true>(c2, st, xs, gs, dts + dt_off, q, n, step);
             else consume<FS, NM, U, true, false>(c2, st, xs, gs, dts + dt_off, q, n, step);
         } else {
@@ -226,6 +277,11 @@ __global__ void __launch_bounds__(kTmaThreads) sweep1d_tma_kernel(const __grid_c
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (FS == RTK_FS_EXP_PARABOLIC && n >= 2) {   // last node: linear weights on the last segment
+        const ExpLin w = exp_linear_weights(ps.d_m2);
+        ps.acc = fma(ps.acc, w.att, w.wu * ps.s_m2 + w.wc * ps.s_m1);
+        if (valid) *ps.yp = ps.x_m1 - ps.acc;
     }
 }
 
@@ -290,6 +346,7 @@ int launch_sweep_tma(const Problem& p, const double* x, double* y, cudaStream_t 
     if (!p.tma_ready || p.gamma_per_ray) return -1;
     if (p.fs == RTK_FS_IE) return dispatch_tma<RTK_FS_IE>(p, x, y, s);
     if (p.fs == RTK_FS_EXP_LINEAR) return dispatch_tma<RTK_FS_EXP_LINEAR>(p, x, y, s);
+    if (p.fs == RTK_FS_EXP_PARABOLIC) return dispatch_tma<RTK_FS_EXP_PARABOLIC>(p, x, y, s);
     return -1;
 }
 
