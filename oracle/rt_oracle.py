@@ -297,9 +297,10 @@ def _linear_weights(d):
 def _parabolic_weights(du, dd):
     att, e0, e1, e2 = exp_weights(du)
     s = du + dd
-    wu = e0 + (e2 - (dd + 2.0 * du) * e1) / (du * s)
-    wc = (s * e1 - e2) / (du * dd)
-    wd = (e2 - du * e1) / (dd * s)
+    r = 1.0 / (du * dd * s)          # one division shared by the three weights (csrc/formal.cuh)
+    wu = e0 + (e2 - (dd + 2.0 * du) * e1) * (dd * r)
+    wc = (s * e1 - e2) * (s * r)
+    wd = (e2 - du * e1) * (du * r)
     return att, wu, wc, wd
 
 

@@ -146,9 +146,10 @@ int rto_apply_A_slab(int64_t n_space, int n_angles, int n_freq, int n_mom, int f
                             sn[q] = s;
                             const double dd = phi[f] * dtn / fabs(mu[a]);
                             const double su = d + dd;
-                            const double wu = e0 + (e2 - (dd + 2.0 * d) * e1) / (d * su);
-                            const double wc = (su * e1 - e2) / (d * dd);
-                            const double wd = (e2 - d * e1) / (dd * su);
+                            const double r = 1.0 / (d * dd * su);
+                            const double wu = e0 + (e2 - (dd + 2.0 * d) * e1) * (dd * r);
+                            const double wc = (su * e1 - e2) * (su * r);
+                            const double wd = (e2 - d * e1) * (d * r);
                             acc[q] = att * acc[q] + wu * sp[q] + wc * sc[q] + wd * sn[q];
                         } else {
                             double wc;

@@ -88,10 +88,12 @@ __device__ __forceinline__ ExpPar exp_parabolic_weights(double du, double dd) {
         e1 = du - e0;
         e2 = du * du - 2.0 * e1;
     }
+    // one division: 1/(du dd s) shared by the three Lagrange weights
     const double s = du + dd;
-    w.wu = e0 + (e2 - (dd + 2.0 * du) * e1) / (du * s);
-    w.wc = (s * e1 - e2) / (du * dd);
-    w.wd = (e2 - du * e1) / (dd * s);
+    const double r = 1.0 / (du * dd * s);
+    w.wu = e0 + (e2 - (dd + 2.0 * du) * e1) * (dd * r);
+    w.wc = (s * e1 - e2) * (s * r);
+    w.wd = (e2 - du * e1) * (du * r);
     return w;
 }
 
