@@ -51,6 +51,8 @@ Problem::~Problem() {
     if (tma_ctas) cudaFree(tma_ctas);
     if (dtpad) cudaFree(dtpad);
     if (lat_dirs) cudaFree(lat_dirs);
+    if (lat_sub_shift) cudaFree(lat_sub_shift);
+    if (lat_gat_shift) cudaFree(lat_gat_shift);
     double* lat[] = {lat_chi, lat_in_top, lat_in_bot, lat_state[0], lat_state[1], lat_src, lat_zero, lat_splane[0],
                      lat_splane[1]};
     for (double* b : lat)

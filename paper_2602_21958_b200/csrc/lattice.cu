@@ -54,7 +54,7 @@ struct Shift {
     double ax, ay;    // fractional part
 };
 
-__device__ __forceinline__ Shift shift_of(double offx, double offy, int nx, int ny) {
+__host__ __device__ __forceinline__ Shift shift_of(double offx, double offy, int nx, int ny) {
     Shift s;
     const double fx = floor(offx), fy = floor(offy);
     s.ax = offx - fx;
@@ -88,6 +88,8 @@ __device__ __forceinline__ Stencil stencil_at(int lx, int ly, const Shift& sh, i
 
 struct LatArgs {
     const LatDir* dirs;
+    const Shift* sub_shift;   // [dir: shift_off + t * (n_sub + 1) + m] sub-node shifts
+    const Shift* gat_shift;   // [dir * nz + t] T_RC gather shifts
     const double* chi;      // [n_space]
     const double* phi;      // [n_freq]
     const double* src;      // SRC_VEC: S[s][a][f]; SRC_ISO: thermal[s][f]; SRC_U: u[s][l][f]
@@ -106,15 +108,14 @@ enum LatSrc { LSRC_VEC = 0, LSRC_ISO = 1, LSRC_U = 2 };
 // position (lx + t sx, ly + t sy) on the start layer; chi_a/chi_b are the opacity
 // planes and Sa/Sb the source planes (node c at Sa[c * ss]) of the start and end layers.
 template <int FS>
-__device__ __forceinline__ double advance_line(const LatDir& D, double acc, int lx, int ly, int t, int nx,
-                                               int ny, const double* __restrict__ chi_a,
+__device__ __forceinline__ double advance_line(const LatDir& D, const Shift* __restrict__ sub, double acc, int lx,
+                                               int ly, int t, int nx, int ny, const double* __restrict__ chi_a,
                                                const double* __restrict__ chi_b, const double* __restrict__ Sa,
                                                const double* __restrict__ Sb, int64_t ss, double phi_f) {
     double prev_s = 0.0, prev_c = 0.0;
     for (int m = 0; m <= D.n_sub; ++m) {
-        const double tt = t + static_cast<double>(m) / D.n_sub;
         const double wz = static_cast<double>(m) / D.n_sub;
-        const Shift sh = shift_of(__dmul_rn(tt, D.sx), __dmul_rn(tt, D.sy), nx, ny);
+        const Shift sh = sub[m];   // warp-uniform, precomputed at setup (same arithmetic as shift_of)
         const Stencil st = stencil_at(lx, ly, sh, nx, ny);
         const double ca = st.w00 * __ldg(chi_a + st.c00) + st.w10 * __ldg(chi_a + st.c10) +
                           st.w01 * __ldg(chi_a + st.c01) + st.w11 * __ldg(chi_a + st.c11);
@@ -146,16 +147,16 @@ __device__ __forceinline__ double advance_line(const LatDir& D, double acc, int 
 // (shift, stencil, trilinear opacity, dt) is computed once per line and sub-node and
 // reused for the kFC frequencies of the chunk.  Planes: chi [nxy], S [nxy][kFC].
 template <int FS>
-__device__ __forceinline__ void advance_line_smem4(const LatDir& D, double (&acc)[kFC], int lx, int ly, int t,
-                                                   int nx, int ny, const double* chi_a, const double* chi_b,
+__device__ __forceinline__ void advance_line_smem4(const LatDir& D, const Shift* __restrict__ sub,
+                                                   double (&acc)[kFC], int lx, int ly, int t, int nx, int ny,
+                                                   const double* chi_a, const double* chi_b,
                                                    const double* Sa, const double* Sb, const double (&phi)[kFC]) {
     double prev_s[kFC], prev_c = 0.0;
 #pragma unroll
     for (int q = 0; q < kFC; ++q) prev_s[q] = 0.0;
     for (int m = 0; m <= D.n_sub; ++m) {
-        const double tt = t + static_cast<double>(m) / D.n_sub;
         const double wz = static_cast<double>(m) / D.n_sub;
-        const Shift sh = shift_of(__dmul_rn(tt, D.sx), __dmul_rn(tt, D.sy), nx, ny);
+        const Shift sh = sub[m];   // warp-uniform, precomputed at setup (same arithmetic as shift_of)
         const Stencil st = stencil_at(lx, ly, sh, nx, ny);
         const double ca = st.w00 * chi_a[st.c00] + st.w10 * chi_a[st.c10] + st.w01 * chi_a[st.c01] +
                           st.w11 * chi_a[st.c11];
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
         const int k = D.down ? t : A.nz - 1 - t;
         __syncthreads();
         // T_RC gather: one thread per (node, frequency) for coalesced y writes
-        const Shift gsh = shift_of(-t * D.sx, -t * D.sy, A.nx, A.ny);
+        const Shift gsh = A.gat_shift[a * A.nz + t];
         for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) {
             const int c = e / kFC, q = e - c * kFC, f = f0 + q;
             const int j = c / A.nx, i = c - j * A.nx;
@@ -271,7 +272,8 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
             double acc[kFC];
 #pragma unroll
             for (int q = 0; q < kFC; ++q) acc[q] = lines[c * kFC + q];
-            advance_line_smem4<FS>(D, acc, lx, ly, t, A.nx, A.ny, ca, cb, Sa, Sb, phi);
+            advance_line_smem4<FS>(D, A.sub_shift + D.shift_off + t * (D.n_sub + 1), acc, lx, ly, t, A.nx, A.ny, ca,
+                                   cb, Sa, Sb, phi);
 #pragma unroll
             for (int q = 0; q < kFC; ++q) lines[c * kFC + q] = acc[q];
         }
@@ -302,7 +304,7 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_kernel(LatArgs A, int
         const int k = D.down ? t : A.nz - 1 - t;
         __syncthreads();
         // T_RC gather for the nodes of layer k
-        const Shift gsh = shift_of(-t * D.sx, -t * D.sy, A.nx, A.ny);
+        const Shift gsh = A.gat_shift[a * A.nz + t];
         for (int c = slot; c < A.nxy; c += slots) {
             const int j = c / A.nx, i = c - j * A.nx;
             const Stencil st = stencil_at(i, j, gsh, A.nx, A.ny);
@@ -326,7 +328,9 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_kernel(LatArgs A, int
         for (int c = slot; c < A.nxy; c += slots) {
             const int ly = c / A.nx, lx = c - ly * A.nx;
             double acc = lines[c * kFC + fq];
-            if (fvalid) acc = advance_line<FS>(D, acc, lx, ly, t, A.nx, A.ny, chi_a, chi_b, Sa, Sb, ss, phi_f);
+            if (fvalid)
+                acc = advance_line<FS>(D, A.sub_shift + D.shift_off + t * (D.n_sub + 1), acc, lx, ly, t, A.nx, A.ny,
+                                       chi_a, chi_b, Sa, Sb, ss, phi_f);
             lines[c * kFC + fq] = acc;
         }
     }
@@ -336,17 +340,16 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_kernel(LatArgs A, int
 // opacity, dt) is frequency-independent and computed once for the group; the internal
 // planes use the even pitch fp so each group moves as F/2 16-byte loads.
 template <int FS, int F>
-__device__ __forceinline__ void advance_lineF(const LatDir& D, double (&acc)[F], int lx, int ly, int t, int nx,
-                                              int ny, const double* __restrict__ chi_a,
+__device__ __forceinline__ void advance_lineF(const LatDir& D, const Shift* __restrict__ sub, double (&acc)[F],
+                                              int lx, int ly, int t, int nx, int ny, const double* __restrict__ chi_a,
                                               const double* __restrict__ chi_b, const double2* __restrict__ Sa,
                                               const double2* __restrict__ Sb, int64_t ss, const double (&phi)[F]) {
     double prev_s[F], prev_c = 0.0;
 #pragma unroll
     for (int q = 0; q < F; ++q) prev_s[q] = 0.0;
     for (int m = 0; m <= D.n_sub; ++m) {
-        const double tt = t + static_cast<double>(m) / D.n_sub;
         const double wz = static_cast<double>(m) / D.n_sub;
-        const Shift sh = shift_of(__dmul_rn(tt, D.sx), __dmul_rn(tt, D.sy), nx, ny);
+        const Shift sh = sub[m];   // warp-uniform, precomputed at setup (same arithmetic as shift_of)
         const Stencil st = stencil_at(lx, ly, sh, nx, ny);
         const double ca = st.w00 * __ldg(chi_a + st.c00) + st.w10 * __ldg(chi_a + st.c10) +
                           st.w01 * __ldg(chi_a + st.c01) + st.w11 * __ldg(chi_a + st.c11);
@@ -436,7 +439,7 @@ __global__ void __launch_bounds__(256) lattice_mom_group_kernel(LatArgs A, int t
 #pragma unroll
                 for (int q = 0; q < F; ++q) v[q] = hemi == 0 ? in_top[q] : in_bot[q];
             } else {
-                const Stencil st = stencil_at(i, j, shift_of(-t * D.sx, -t * D.sy, A.nx, A.ny), A.nx, A.ny);
+                const Stencil st = stencil_at(i, j, A.gat_shift[a * A.nz + t], A.nx, A.ny);
 #pragma unroll
                 for (int h = 0; h < F / 2; ++h) {
                     if (!full_group && g2 + h >= hp) {
@@ -470,7 +473,8 @@ __global__ void __launch_bounds__(256) lattice_mom_group_kernel(LatArgs A, int t
                 }
                 const LatDir Dl = D;
                 if (full_group) {
-                    advance_lineF<FS, F>(Dl, acc, i, j, t, A.nx, A.ny, A.chi + static_cast<int64_t>(k) * A.nxy,
+                    advance_lineF<FS, F>(Dl, A.sub_shift + Dl.shift_off + t * (Dl.n_sub + 1), acc, i, j, t, A.nx,
+                                         A.ny, A.chi + static_cast<int64_t>(k) * A.nxy,
                                          A.chi + static_cast<int64_t>(k2) * A.nxy, pc2 + a * plane2 + g2,
                                          pn2 + a * plane2 + g2, hp, phi);
 #pragma unroll
@@ -481,7 +485,8 @@ __global__ void __launch_bounds__(256) lattice_mom_group_kernel(LatArgs A, int t
                     for (int h = 0; h < F / 2 && g2 + h < hp; ++h) {
                         double ap[2] = {acc[2 * h], acc[2 * h + 1]};
                         const double pp[2] = {phi[2 * h], phi[2 * h + 1]};
-                        advance_lineF<FS, 2>(Dl, ap, i, j, t, A.nx, A.ny, A.chi + static_cast<int64_t>(k) * A.nxy,
+                        advance_lineF<FS, 2>(Dl, A.sub_shift + Dl.shift_off + t * (Dl.n_sub + 1), ap, i, j, t, A.nx,
+                                             A.ny, A.chi + static_cast<int64_t>(k) * A.nxy,
                                              A.chi + static_cast<int64_t>(k2) * A.nxy, pc2 + a * plane2 + g2 + h,
                                              pn2 + a * plane2 + g2 + h, hp, pp);
                         sout2[a * plane2 + static_cast<int64_t>(c) * hp + g2 + h] = make_double2(ap[0], ap[1]);
@@ -582,6 +587,23 @@ int setup_lattice(Problem& p, const rtk_lattice_desc* d) {
             D.cy[l] = in ? d->coeffs[l] * d->ybasis[l * d->n_dirs + a] : 0.0;
         }
     }
+    // warp-uniform interpolation shifts, tabulated once (same arithmetic as the device's shift_of)
+    std::vector<Shift> sub, gat(static_cast<size_t>(d->n_dirs) * d->nz);
+    for (int a = 0; a < d->n_dirs; ++a) {
+        LatDir& D = dirs[a];
+        D.shift_off = static_cast<int>(sub.size());
+        for (int t = 0; t < d->nz - 1; ++t)
+            for (int m = 0; m <= D.n_sub; ++m) {
+                const double tt = t + static_cast<double>(m) / D.n_sub;
+                sub.push_back(shift_of(tt * D.sx, tt * D.sy, d->nx, d->ny));
+            }
+        for (int t = 0; t < d->nz; ++t) gat[static_cast<size_t>(a) * d->nz + t] = shift_of(-t * D.sx, -t * D.sy, d->nx, d->ny);
+    }
+    if (sub.empty()) sub.push_back(Shift{});
+    RTK_CUDA_TRY(cudaMalloc(&p.lat_sub_shift, sizeof(Shift) * sub.size()));
+    RTK_CUDA_TRY(cudaMemcpy(p.lat_sub_shift, sub.data(), sizeof(Shift) * sub.size(), cudaMemcpyHostToDevice));
+    RTK_CUDA_TRY(cudaMalloc(&p.lat_gat_shift, sizeof(Shift) * gat.size()));
+    RTK_CUDA_TRY(cudaMemcpy(p.lat_gat_shift, gat.data(), sizeof(Shift) * gat.size(), cudaMemcpyHostToDevice));
     RTK_CUDA_TRY(cudaMalloc(&p.lat_dirs, sizeof(LatDir) * dirs.size()));
     RTK_CUDA_TRY(cudaMemcpy(p.lat_dirs, dirs.data(), sizeof(LatDir) * dirs.size(), cudaMemcpyHostToDevice));
     return RTK_OK;
@@ -590,6 +612,8 @@ int setup_lattice(Problem& p, const rtk_lattice_desc* d) {
 static LatArgs lat_args(const Problem& p, const double* src, const double* x, double* y) {
     LatArgs A;
     A.dirs = p.lat_dirs;
+    A.sub_shift = reinterpret_cast<const Shift*>(p.lat_sub_shift);
+    A.gat_shift = reinterpret_cast<const Shift*>(p.lat_gat_shift);
     A.chi = p.lat_chi;
     A.phi = p.phi;
     A.src = src;

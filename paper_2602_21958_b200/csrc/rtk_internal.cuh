@@ -56,6 +56,7 @@ struct TmaCta {
 struct LatDir {
     int down;         // Omega_z < 0: enters at the top layer
     int n_sub;        // sub-segments per layer step
+    int shift_off;    // first entry of this direction in the sub-node shift table
     double sx, sy;    // horizontal cells moved per layer step
     double sub_len;   // path length of one sub-segment
     double wy[8];     // w_a Y_l(a)   (moment accumulation)
@@ -93,6 +94,8 @@ struct Problem {
     double* lat_src = nullptr;                   // full source vector (intensity layout)
     double* lat_zero = nullptr;                  // [n_space][n_freq] zeros (boundary-only RHS)
     double* lat_splane[2] = {nullptr, nullptr};  // [dir][line][freq] source planes (moment layout ring)
+    void* lat_sub_shift = nullptr;               // Shift table (lattice.cu), sub-nodes
+    void* lat_gat_shift = nullptr;               // Shift table, T_RC gathers
     // overlap of the HBM-bound moment reduction with the FP64 redistribution GEMM (slab apply_A)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chunk[8] = {};
