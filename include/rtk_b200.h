@@ -36,6 +36,11 @@ extern "C" {
 
 #define RTK_MAX_MOMENTS 8
 
+/* unknown layout of slab and lattice problems */
+#define RTK_LAYOUT_INTENSITY 0
+#define RTK_LAYOUT_MOMENTS 1
+
+
 typedef struct rtk_problem rtk_problem;
 
 /*
@@ -54,7 +59,9 @@ typedef struct rtk_slab_desc {
     int32_t n_moments;        /* rows of ybasis, 1..RTK_MAX_MOMENTS */
     int32_t formal_solver;    /* RTK_FS_* */
     int32_t gamma_per_ray;    /* 0: gamma[n_space][n_freq]; 1: gamma[n_space][n_angles*n_freq] (R/grid.py:107-112) */
-    int32_t reserved;
+    int32_t layout;           /* RTK_LAYOUT_INTENSITY (the reference's I[i][a][f]) or RTK_LAYOUT_MOMENTS
+                                 (u[i][k][f] = sum_g R w_g m, m = sum_a w_a Y_k(a) I; 2 N_nu N_s values for
+                                 the dipole kernel; IE / exp-linear, n_moments <= 3, gamma[n_space][n_freq]) */
     const double* t_nodes;        /* [n_space] strictly increasing optical-depth scale (R/grid.py:68) */
     const double* mu;             /* [n_angles] direction cosines, none zero */
     const double* ang_w;          /* [n_angles] angular weights */
@@ -66,10 +73,6 @@ typedef struct rtk_slab_desc {
     const double* gamma;          /* see gamma_per_ray */
     const double* inflow;         /* [n_angles*n_freq] boundary intensity per ray, or NULL for 0 (R/transfer.py:101-103) */
 } rtk_slab_desc;
-
-/* unknown layout of lattice problems */
-#define RTK_LAYOUT_INTENSITY 0
-#define RTK_LAYOUT_MOMENTS 1
 
 /*
  * Periodic-lattice long characteristics on a 2D slab (ny = 1, y-invariant,
@@ -138,6 +141,11 @@ int rtk_apply_A_host(rtk_problem* p, const double* x_host, double* y_host, int64
  * duplex).  Host buffers should be pinned for the copies to be asynchronous. */
 int rtk_apply_A_host_batch(rtk_problem* p, const double* const* x_host, double* const* y_host, int32_t count,
                            int64_t n);
+/* Moment-layout problems: intensities I = Lambda(S(u) + thermal) + inflow term from a
+ * moment vector u (the returned intensities of a moment-layout solve); thermal_dev and
+ * I_dev are intensity-layout vectors of n_intensity = n_space * n_rays entries. */
+int rtk_intensity_from_moments(rtk_problem* p, const double* u_dev, const double* thermal_dev, double* I_dev,
+                               int64_t n_intensity, void* stream);
 /* s = Sigma x -- apply_scattering, R/scattering.py:126-148. */
 int rtk_apply_sigma(rtk_problem* p, const double* x_dev, double* s_dev, int64_t n, void* stream);
 /* y = Lambda s (homogeneous part) -- apply_transfer, R/transfer.py:134-141. */

@@ -24,7 +24,8 @@ __all__ = [
     "apply_transfer", "boundary_term", "apply_sigma", "apply_A", "build_rhs",
     "materialize", "psi_dipole_prd", "prd_matrix", "legendre_as_general",
     "crd_as_general", "coherent_as_general", "OracleSolveReport", "gmres",
-    "bicgstab", "source_function", "desc_from_problem",
+    "bicgstab", "source_function", "desc_from_problem", "moments_of", "source_from_moments",
+    "apply_A_moments", "build_rhs_moments", "intensity_from_moments",
 ]
 
 
@@ -389,6 +390,34 @@ def build_rhs(d: SlabDesc, override_ones: bool = False) -> np.ndarray:
     if override_ones:
         return np.ones(d.n_total)
     return apply_transfer(d, d.thermal) + boundary_term(d)
+
+
+def moments_of(d: SlabDesc, I: np.ndarray) -> np.ndarray:
+    """EXTENSION (moment layout): u = R_w M I, u[i,k,f] = sum_g R[f,g] w_g sum_a w_a Y_k(a) I[i,a,g]."""
+    cube = np.asarray(I, dtype=float).reshape(d.n_space, d.n_angles, d.n_freq)
+    m = np.einsum("saf,ka->skf", cube, d.ybasis * d.ang_w[None, :])
+    return np.einsum("fg,skg->skf", d.R * d.freq_w[None, :], m).reshape(-1)
+
+
+def source_from_moments(d: SlabDesc, u: np.ndarray) -> np.ndarray:
+    """S[i,a,f] = gamma[i,(a,f)] sum_k c_k Y_k(a) u[i,k,f]."""
+    u3 = np.asarray(u, dtype=float).reshape(d.n_space, d.ybasis.shape[0], d.n_freq)
+    S = np.einsum("ka,skf->saf", d.coeffs[:, None] * d.ybasis, u3)
+    return (d.gamma * S.reshape(d.n_space, d.n_rays)).ravel()
+
+
+def apply_A_moments(d: SlabDesc, u: np.ndarray) -> np.ndarray:
+    """EXTENSION: y = u - R_w M Lambda S(u), the operator in moment coordinates."""
+    return np.asarray(u, dtype=float) - moments_of(d, apply_transfer(d, source_from_moments(d, u)))
+
+
+def build_rhs_moments(d: SlabDesc) -> np.ndarray:
+    return moments_of(d, build_rhs(d))
+
+
+def intensity_from_moments(d: SlabDesc, u: np.ndarray) -> np.ndarray:
+    """I = Lambda(S(u) + thermal) + inflow term."""
+    return apply_transfer(d, source_from_moments(d, u) + d.thermal, with_boundary=True)
 
 
 def source_function(d: SlabDesc, intensity: np.ndarray) -> np.ndarray:

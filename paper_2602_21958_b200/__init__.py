@@ -20,7 +20,7 @@ from paper_2602_21958_b200.scattering import (CoherentKernel, CRDKernel, DipoleP
                                               build_scattering, kernel_normalization, materialize_scattering,
                                               psi_matrix, separable_form)
 from paper_2602_21958_b200.operator import (DeviceOperator, RTProblem, apply_A, apply_A_batch, build_rhs,
-                                            materialize_A, operator,
+                                            intensity_from_moments, materialize_A, operator,
                                             source_function, spectral_radius_estimate)
 from paper_2602_21958_b200.krylov import SolveConfig, SolveReport, bicgstab, gmres, solve_system
 from paper_2602_21958_b200.redistribution import gaussian_profile, prd_matrix
@@ -35,7 +35,7 @@ __all__ = [
     "CoherentKernel", "CRDKernel", "DipolePRDKernel", "LegendreKernel", "ScatteringOperator",
     "ScatteringStrengthWarning", "apply_scattering", "build_scattering", "kernel_normalization",
     "materialize_scattering", "psi_matrix", "separable_form",
-    "DeviceOperator", "RTProblem", "apply_A", "apply_A_batch", "build_rhs", "materialize_A", "operator", "source_function",
+    "DeviceOperator", "RTProblem", "apply_A", "apply_A_batch", "build_rhs", "intensity_from_moments", "materialize_A", "operator", "source_function",
     "spectral_radius_estimate",
     "SolveConfig", "SolveReport", "bicgstab", "gmres", "solve_system",
     "gaussian_profile", "prd_matrix",

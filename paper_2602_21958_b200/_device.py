@@ -98,7 +98,7 @@ class SlabHandle:
     """Owns one rtk_problem (device-resident tables + workspace)."""
 
     def __init__(self, arrays: dict, formal_solver: str, gamma_per_ray: bool, n_space: int, n_angles: int,
-                 n_freq: int, n_moments: int):
+                 n_freq: int, n_moments: int, layout: str = "intensity"):
         require_cuda()
         lib = _native.lib()
         self._keep = {k: np.ascontiguousarray(v, dtype=float) for k, v in arrays.items() if v is not None}
@@ -108,6 +108,7 @@ class SlabHandle:
             raise ValueError(f"unknown formal solver {formal_solver!r}")
         d.formal_solver = _native.FS_CODES[formal_solver]
         d.gamma_per_ray = 1 if gamma_per_ray else 0
+        d.layout = 1 if layout == "moments" else 0
         for name in ("t_nodes", "mu", "ang_w", "phi", "freq_w", "ybasis", "coeffs", "redistribution", "gamma",
                      "inflow"):
             if name in self._keep:

@@ -29,7 +29,7 @@ class SlabDesc(ctypes.Structure):
         ("n_moments", ctypes.c_int32),
         ("formal_solver", ctypes.c_int32),
         ("gamma_per_ray", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("layout", ctypes.c_int32),
         ("t_nodes", c_double_p),
         ("mu", c_double_p),
         ("ang_w", c_double_p),
@@ -85,6 +85,7 @@ SIGNATURES = [
     ("rtk_apply_A_host", ctypes.c_int, [_P, _P, _P, _I64, _P]),
     ("rtk_apply_A_host_batch", ctypes.c_int, [_P, _P, _P, _I32, _I64]),
     ("rtk_profile_apply_A", ctypes.c_int, [_P, _P, _P, _I64, _P, ctypes.POINTER(ctypes.c_float)]),
+    ("rtk_intensity_from_moments", ctypes.c_int, [_P, _P, _P, _P, _I64, _P]),
     ("rtk_apply_sigma", ctypes.c_int, [_P, _P, _P, _I64, _P]),
     ("rtk_apply_lambda", ctypes.c_int, [_P, _P, _P, _I64, _P]),
     ("rtk_boundary", ctypes.c_int, [_P, _P, _I64, _P]),

@@ -41,7 +41,8 @@ def slab_t_nodes(n_space: int, t_range, sigma: float, seed: int) -> np.ndarray:
 
 
 def slab_problem(cfg: int = 1, formal_solver: str = "ie", n_space: int = None, n_angles: int = None,
-                 n_freq: int = None, coherence: float = PRD_COHERENCE, kernel=None) -> RTProblem:
+                 n_freq: int = None, coherence: float = PRD_COHERENCE, kernel=None,
+                 layout: str = "intensity") -> RTProblem:
     """1D slab with dipole x PRD scattering, Planck B = 1, zero incident intensity.
 
     gamma = (1 - eps) / (2 phi) (s_d = 2 in 1D), thermal = eps B; R is the
@@ -74,6 +75,7 @@ def slab_problem(cfg: int = 1, formal_solver: str = "ie", n_space: int = None, n
         warnings.simplefilter("ignore")
         scattering = build_scattering(grid, kernel, gamma)
     return RTProblem(grid=grid, transfer=transfer, scattering=scattering, thermal=np.full(grid.n_total, eps),
+                     layout=layout,
                      descriptor=dict(config=cfg, formal_solver=formal_solver, eps=eps, coherence=coherence,
                                      restart=c["restart"], **{k: c[k] for k in ("n_space", "n_angles", "n_freq")}))
 

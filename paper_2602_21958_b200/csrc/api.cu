@@ -51,6 +51,9 @@ Problem::~Problem() {
     if (tma_ctas) cudaFree(tma_ctas);
     if (dtpad) cudaFree(dtpad);
     if (lat_dirs) cudaFree(lat_dirs);
+    if (mom_ctas) cudaFree(mom_ctas);
+    if (mom_partial) cudaFree(mom_partial);
+    if (dtpad_mom) cudaFree(dtpad_mom);
     if (lat_sub_shift) cudaFree(lat_sub_shift);
     if (lat_gat_shift) cudaFree(lat_gat_shift);
     double* lat[] = {lat_chi, lat_in_top, lat_in_bot, lat_state[0], lat_state[1], lat_src, lat_zero, lat_splane[0],
@@ -82,6 +85,10 @@ int sweep_apply(const Problem& p, const double* x, double* y, cudaStream_t s) {
 
 int apply_A_dev(Problem& p, const double* x, double* y, cudaStream_t s) {
     int rc;
+    if (p.kind == KIND_SLAB && p.layout == LAYOUT_MOMENTS) {
+        if ((rc = slab_moment_transfer(p, x, s))) return rc;
+        return launch_redistribute_ex(p, p.mom, y, p.n_freq, EPI_SUB, x, p.n_freq, s);
+    }
     if (p.kind == KIND_LATTICE) {
         if (p.layout == LAYOUT_MOMENTS) {
             if ((rc = lattice_transfer_moments(p, 2 /*LSRC_U*/, false, x, p.mom, s))) return rc;
@@ -166,9 +173,19 @@ int rtk_problem_create_slab(const rtk_slab_desc* d, rtk_problem** out) {
     p.n_mom = d->n_moments;
     p.fs = d->formal_solver;
     p.gamma_per_ray = d->gamma_per_ray ? 1 : 0;
+    p.layout = d->layout == RTK_LAYOUT_MOMENTS ? rtk::LAYOUT_MOMENTS : rtk::LAYOUT_INTENSITY;
+    if (d->layout != RTK_LAYOUT_INTENSITY && d->layout != RTK_LAYOUT_MOMENTS) {
+        delete h;
+        return set_error(RTK_EINVAL, "unknown layout");
+    }
+    if (p.layout == rtk::LAYOUT_MOMENTS && p.gamma_per_ray) {
+        delete h;
+        return set_error(RTK_EINVAL, "the moment layout needs a mu-independent gamma");
+    }
     p.n_rays = static_cast<int64_t>(p.n_angles) * p.n_freq;
     p.n_total = p.n_space * p.n_rays;
     p.fp = (p.n_freq + 1) / 2 * 2;
+    if (p.layout == rtk::LAYOUT_MOMENTS) p.n_total = p.n_space * p.n_mom * p.n_freq;
     p.h_mu.assign(d->mu, d->mu + p.n_angles);
     p.h_coeffs.assign(d->coeffs, d->coeffs + p.n_mom);
 
@@ -206,7 +223,7 @@ int rtk_problem_create_slab(const rtk_slab_desc* d, rtk_problem** out) {
         if (e == cudaSuccess) e = cudaMemcpy(p.dir_sign, sign.data(), sizeof(int) * p.n_angles, cudaMemcpyHostToDevice);
         if (e != cudaSuccess) rc = rtk::cuda_status(e, "dir_sign upload");
     }
-    if (!rc) rc = rtk::setup_tma(p);
+    if (!rc) rc = p.layout == rtk::LAYOUT_MOMENTS ? rtk::setup_slab_moments(p) : rtk::setup_tma(p);
     if (rc) {
         delete h;
         return rc;
@@ -317,7 +334,7 @@ int rtk_profile_apply_A(rtk_problem* p, const double* x, double* y, int64_t n, v
     if (rc) return rc;
     if (!ms_out) return set_error(RTK_EINVAL, "null ms_out");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (p->impl.kind == rtk::KIND_LATTICE) {   // whole operator timed as one entry (ms_out[2])
+    if (p->impl.kind == rtk::KIND_LATTICE || p->impl.layout == rtk::LAYOUT_MOMENTS) {   // whole operator (ms_out[2])
         cudaEvent_t e0, e1;
         RTK_CUDA_TRY(cudaEventCreate(&e0));
         RTK_CUDA_TRY(cudaEventCreate(&e1));
@@ -394,10 +411,33 @@ int rtk_apply_A_host_batch(rtk_problem* p, const double* const* xs, double* cons
     return RTK_OK;
 }
 
+int rtk_intensity_from_moments(rtk_problem* p, const double* u, const double* thermal, double* I, int64_t n_int,
+                               void* stream) {
+    if (!p) return set_error(RTK_EINVAL, "null problem handle");
+    Problem& q = p->impl;
+    if (q.kind != rtk::KIND_SLAB || q.layout != rtk::LAYOUT_MOMENTS)
+        return set_error(RTK_EINVAL, "intensity_from_moments needs a slab problem in the moment layout");
+    if (n_int != q.n_space * q.n_rays) return set_error(RTK_EINVAL, "intensity length must be n_space * n_rays");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // G = c gamma u (pitch fp) -> S = sum_k Y_k G + thermal (intensity layout, into I) -> I = Lambda S + inflow
+    int rc = rtk::slab_moment_fold(q, u, s);
+    if (rc) return rc;
+    double* tmp = nullptr;
+    RTK_CUDA_TRY(cudaMalloc(&tmp, sizeof(double) * n_int));
+    rc = rtk::launch_expand_source(q, thermal, tmp, s);
+    if (!rc) rc = rtk::launch_sweep(q, rtk::SRC_VECTOR, rtk::OUT_ACC, true, tmp, nullptr, I, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    cudaFree(tmp);
+    if (!rc && e != cudaSuccess) rc = rtk::cuda_status(e, "intensity_from_moments");
+    return rc;
+}
+
 int rtk_apply_sigma(rtk_problem* p, const double* x, double* s_out, int64_t n, void* stream) {
     int rc = check_n(p, n);
     if (rc) return rc;
     if (p->impl.layout == rtk::LAYOUT_MOMENTS) return set_error(RTK_EINVAL, "apply_sigma needs the intensity layout");
+    if (p->impl.kind == rtk::KIND_SLAB && p->impl.layout == rtk::LAYOUT_MOMENTS)
+        return set_error(RTK_EINVAL, "apply_sigma needs the intensity layout");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if ((rc = rtk::launch_moments(p->impl, x, s))) return rc;
     if ((rc = rtk::launch_redistribute(p->impl, s))) return rc;
@@ -418,6 +458,8 @@ int rtk_source_function(rtk_problem* p, const double* intensity, const double* t
 int rtk_apply_lambda(rtk_problem* p, const double* src, double* y, int64_t n, void* stream) {
     int rc = check_n(p, n);
     if (rc) return rc;
+    if (p->impl.kind == rtk::KIND_SLAB && p->impl.layout == rtk::LAYOUT_MOMENTS)
+        return set_error(RTK_EINVAL, "apply_lambda needs the intensity layout");
     if (p->impl.kind == rtk::KIND_LATTICE) {
         if (p->impl.layout == rtk::LAYOUT_MOMENTS) return set_error(RTK_EINVAL, "apply_lambda needs the intensity layout");
         return rtk::lattice_transfer_intensity(p->impl, 0, rtk::OUT_ACC, false, src, nullptr, y,
@@ -430,6 +472,8 @@ int rtk_apply_lambda(rtk_problem* p, const double* src, double* y, int64_t n, vo
 int rtk_boundary(rtk_problem* p, double* y, int64_t n, void* stream) {
     int rc = check_n(p, n);
     if (rc) return rc;
+    if (p->impl.kind == rtk::KIND_SLAB && p->impl.layout == rtk::LAYOUT_MOMENTS)
+        return set_error(RTK_EINVAL, "boundary needs the intensity layout");
     if (p->impl.kind == rtk::KIND_LATTICE) return rtk_build_rhs(p, nullptr, y, n, 0, stream);
     return rtk::launch_sweep(p->impl, rtk::SRC_ZERO, rtk::OUT_ACC, true, nullptr, nullptr, y,
                              static_cast<cudaStream_t>(stream));
@@ -453,6 +497,20 @@ int rtk_build_rhs(rtk_problem* p, const double* thermal, double* b, int64_t n, i
             return rtk::launch_redistribute_ex(p->impl, p->impl.mom, b, p->impl.n_freq, rtk::EPI_PLAIN, nullptr, 0, s);
         }
         return rtk::lattice_transfer_intensity(p->impl, 1 /*LSRC_ISO*/, rtk::OUT_ACC, true, th, nullptr, b, s);
+    }
+    if (p->impl.layout == rtk::LAYOUT_MOMENTS) {
+        // b_u = R_w M (Lambda thermal + inflow term): through a transient intensity vector (one-time setup)
+        Problem& q = p->impl;
+        double* tmp = nullptr;
+        RTK_CUDA_TRY(cudaMalloc(&tmp, sizeof(double) * q.n_space * q.n_rays));
+        if (thermal) rc = rtk::launch_sweep(q, rtk::SRC_VECTOR, rtk::OUT_ACC, true, thermal, nullptr, tmp, s);
+        else rc = rtk::launch_sweep(q, rtk::SRC_ZERO, rtk::OUT_ACC, true, nullptr, nullptr, tmp, s);
+        if (!rc) rc = rtk::launch_moments(q, tmp, s);
+        if (!rc) rc = rtk::launch_redistribute_ex(q, q.mom, b, q.n_freq, rtk::EPI_PLAIN, nullptr, 0, s);
+        cudaError_t e = cudaStreamSynchronize(s);
+        cudaFree(tmp);
+        if (!rc && e != cudaSuccess) rc = rtk::cuda_status(e, "moment RHS");
+        return rc;
     }
     // one recursion carrying the inflow value: Lambda thermal + decay * inflow
     if (thermal)

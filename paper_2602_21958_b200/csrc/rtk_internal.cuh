@@ -66,6 +66,10 @@ struct LatDir {
 enum ProblemKind { KIND_SLAB = 1, KIND_LATTICE = 2 };
 enum Layout { LAYOUT_INTENSITY = 0, LAYOUT_MOMENTS = 1 };
 
+struct MomCta {
+    int a0, nd, down, f0, group;   // 1D moment-layout sweep: directions [a0, a0+nd), 16-frequency tile at f0
+};
+
 struct Problem {
     int kind = KIND_SLAB;
     int layout = LAYOUT_INTENSITY;
@@ -94,6 +98,12 @@ struct Problem {
     double* lat_src = nullptr;                   // full source vector (intensity layout)
     double* lat_zero = nullptr;                  // [n_space][n_freq] zeros (boundary-only RHS)
     double* lat_splane[2] = {nullptr, nullptr};  // [dir][line][freq] source planes (moment layout ring)
+    // slab moment layout (sweep_mom.cu)
+    MomCta* mom_ctas = nullptr;
+    int mom_n_ctas = 0, mom_n_groups = 0;
+    double* mom_partial = nullptr;               // [group][n_space][n_mom][fp]
+    double* dtpad_mom = nullptr;
+    CUtensorMap mom_gmap, tma_dtmap_mom;
     void* lat_sub_shift = nullptr;               // Shift table (lattice.cu), sub-nodes
     void* lat_gat_shift = nullptr;               // Shift table, T_RC gathers
     // overlap of the HBM-bound moment reduction with the FP64 redistribution GEMM (slab apply_A)
@@ -116,6 +126,12 @@ int launch_sweep(const Problem& p, int src_mode, int out_mode, bool with_inflow,
 // sweep_tma.cu
 int setup_tma(Problem& p);
 int launch_sweep_tma(const Problem& p, const double* x, double* y, cudaStream_t s);   // -1: not applicable
+// sweep_mom.cu
+int setup_slab_moments(Problem& p);
+int slab_moment_transfer(const Problem& p, const double* u, cudaStream_t s);   // p.mom = M Lambda S(u)
+int slab_moment_fold(const Problem& p, const double* u, cudaStream_t s);       // p.gmom = c gamma u
+bool encode_f64_map(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, const uint64_t* stride_bytes,
+                    const uint32_t* box);
 // lattice.cu
 int setup_lattice(Problem& p, const rtk_lattice_desc* d);
 int lattice_transfer_intensity(const Problem& p, int src_mode, int out_mode, bool with_inflow, const double* src,

@@ -371,8 +371,9 @@ int launch_redistribute(const Problem& p, cudaStream_t s) {
 }
 
 int launch_expand_source(const Problem& p, const double* thermal, double* out, cudaStream_t s) {
-    const unsigned blocks = static_cast<unsigned>((p.n_total + 255) / 256);
-    expand_kernel<<<blocks, 256, 0, s>>>(p.gmom, p.yb, p.gamma_per_ray ? p.gamma : nullptr, thermal, out, p.n_total,
+    const int64_t n_int = p.n_space * p.n_rays;   // intensity-layout length (n_total differs in the moment layout)
+    const unsigned blocks = static_cast<unsigned>((n_int + 255) / 256);
+    expand_kernel<<<blocks, 256, 0, s>>>(p.gmom, p.yb, p.gamma_per_ray ? p.gamma : nullptr, thermal, out, n_int,
                                          p.n_angles, p.n_freq, p.n_mom, p.fp);
     RTK_LAUNCH_CHECK("expand_kernel");
     return RTK_OK;

@@ -18,7 +18,8 @@ from paper_2602_21958_b200.scattering import ScatteringOperator, slab_handle
 
 __all__ = ["DENSE_CAP_DEFAULT", "ResourceLimitError", "RTProblem", "DeviceOperator", "apply_A", "apply_A_batch",
            "build_rhs",
-           "source_function", "operator", "spectral_radius_estimate", "materialize_A"]
+           "source_function", "operator", "spectral_radius_estimate", "materialize_A",
+           "intensity_from_moments"]
 
 
 @dataclass
@@ -30,6 +31,7 @@ class RTProblem:
     scattering: ScatteringOperator
     thermal: np.ndarray
     descriptor: dict = field(default_factory=dict)
+    layout: str = "intensity"     # or "moments": unknown u = R_w M I, 2 N_nu N_s values
     _handle: object = field(default=None, repr=False, compare=False)
 
     def __post_init__(self):
@@ -38,15 +40,22 @@ class RTProblem:
             self.thermal = np.full(self.grid.n_total, float(self.thermal))
         if self.thermal.size != self.grid.n_total:
             raise ValueError("thermal source length does not match the grid")
+        if self.layout not in ("intensity", "moments"):
+            raise ValueError(f"unknown layout {self.layout!r}")
 
     @property
     def n_total(self) -> int:
+        """Length of the unknown: the intensity vector, or the moment vector in the moment layout."""
+        if self.layout == "moments":
+            from paper_2602_21958_b200.scattering import separable_form
+
+            return self.grid.n_space * separable_form(self.scattering.kernel, self.grid)[0].shape[0] * self.grid.n_freq
         return self.grid.n_total
 
     def device(self):
         """The uploaded device operator (built once)."""
         if self._handle is None:
-            self._handle = slab_handle(self.grid, self.scattering, self.transfer)
+            self._handle = slab_handle(self.grid, self.scattering, self.transfer, self.layout)
         return self._handle
 
     def invalidate(self):
@@ -125,10 +134,25 @@ def build_rhs(problem: RTProblem, override_ones: bool = False, device: bool = Fa
         return np.ones(n)
     h = problem.device()
     h.set_inflow(problem.transfer.inflow)
-    th, _ = _device.to_device(problem.thermal, n)
+    th, _ = _device.to_device(problem.thermal, problem.grid.n_total)
     b = _device.empty(n)
     _native.check(_native.lib().rtk_build_rhs(h.h, _device.ptr(th), _device.ptr(b), n, 0, _device.stream_ptr()))
     return b if device else b.cpu().numpy()
+
+
+def intensity_from_moments(problem: RTProblem, u):
+    """Moment layout: intensities I = Lambda(S(u) + thermal) + inflow term of a moment vector u."""
+    if problem.layout != "moments":
+        raise ValueError("intensity_from_moments needs a moment-layout problem")
+    h = problem.device()
+    h.set_inflow(problem.transfer.inflow)
+    x, kind = _device.to_device(u, problem.n_total)
+    ni = problem.grid.n_total
+    th, _ = _device.to_device(problem.thermal, ni)
+    out = _device.empty(ni)
+    _native.check(_native.lib().rtk_intensity_from_moments(h.h, _device.ptr(x), _device.ptr(th), _device.ptr(out), ni,
+                                                            _device.stream_ptr()))
+    return _device.from_device(out, kind)
 
 
 def source_function(problem: RTProblem, intensity):

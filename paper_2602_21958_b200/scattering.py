@@ -146,7 +146,7 @@ class ScatteringOperator:
         return self._handle
 
 
-def slab_handle(grid, scattering, transfer):
+def slab_handle(grid, scattering, transfer, layout: str = "intensity"):
     """Upload one slab problem; scattering or transfer may be None (identity-free stand-ins)."""
     if scattering is not None:
         Y, d, R = separable_form(scattering.kernel, grid)
@@ -158,7 +158,7 @@ def slab_handle(grid, scattering, transfer):
     inflow = transfer.inflow if transfer is not None else None
     arrays = dict(t_nodes=grid.t_nodes, mu=grid.mu_nodes, ang_w=grid.angular_weights, phi=grid.profile_values(),
                   freq_w=grid.frequency_weights, ybasis=Y, coeffs=d, redistribution=R, gamma=gamma, inflow=inflow)
-    return _device.SlabHandle(arrays, fs, per_ray, grid.n_space, grid.n_angles, grid.n_freq, Y.shape[0])
+    return _device.SlabHandle(arrays, fs, per_ray, grid.n_space, grid.n_angles, grid.n_freq, Y.shape[0], layout)
 
 
 def build_scattering(grid, kernel: Kernel, gamma) -> ScatteringOperator:

@@ -242,3 +242,31 @@ def test_apply_A_batch_matches_single_calls():
     ys = P.apply_A_batch(p, xs)
     for x, y in zip(xs, ys):
         np.testing.assert_array_equal(y, P.apply_A(p, x))
+
+
+@pytest.mark.parametrize("fs", ["ie", "exp_linear"])
+@pytest.mark.parametrize("shape", [(1, None), (2, dict(n_space=300, n_angles=16, n_freq=130)), (2, None)])
+def test_moment_layout_matvec_matches_oracle(fs, shape):
+    cfg, kw = shape
+    p = configs.slab_problem(cfg, formal_solver=fs, layout="moments", **(kw or {}))
+    d = oracle_desc(p)
+    u = np.random.default_rng(31).standard_normal(p.n_total)
+    assert rel_l2(P.apply_A(p, u), ro.apply_A_moments(d, u)) <= MATVEC_TOL
+    if cfg == 1:
+        assert rel_l2(P.build_rhs(p), ro.build_rhs_moments(d)) <= MATVEC_TOL
+
+
+def test_moment_layout_solve_reproduces_intensity_solve():
+    """Unrestarted GMRES: same iteration count (+-1) in both layouts, and I(u*) equals the
+    intensity-layout solution."""
+    pi = configs.slab_problem(1)
+    pm = configs.slab_problem(1, layout="moments")
+    cfg = P.SolveConfig(rel_tol=1e-10, max_iter=500)
+    ri = P.gmres(pi, P.build_rhs(pi), cfg)
+    rm = P.gmres(pm, P.build_rhs(pm), cfg)
+    assert ri.converged and rm.converged
+    assert abs(ri.iterations - rm.iterations) <= 1
+    I = P.intensity_from_moments(pm, rm.solution)
+    assert rel_l2(I, ri.solution) <= 1e-8
+    d = oracle_desc(pm)
+    assert rel_l2(I, ro.intensity_from_moments(d, rm.solution)) <= 1e-11
