@@ -337,6 +337,7 @@ def run_b200(args):
     extra = {}
     if rank == 0 and not args.no_gmres:
         extra["gmres"] = gmres_timings(torch)
+        extra["gmres_cfg2_moment_layout"] = gmres_cfg2_moments(torch)
         extra["krylov_cfg2"] = krylov_cfg2(torch, problem, ms_per_step, hbm)
     if rank == 0 and not args.no_lattice:
         extra["lattice"] = lattice_timings(torch)
@@ -394,6 +395,26 @@ def gmres_timings(torch):
         el = time.perf_counter() - t0
         out[name] = {"iterations": rep.iterations, "converged": rep.converged, "time_s": el,
                      "true_residual": rep.true_residual, "matvecs": rep.matvecs}
+    return out
+
+
+def gmres_cfg2_moments(torch):
+    """cfg2 time-to-1e-8 in the moment layout (unknown u = R_w M I, 16 MB): unrestarted GMRES
+    (basis of up to ~1500 x 16 MB in HBM), and the residual GMRES(30) reaches in 3000 iterations.
+    The CPU reference cannot run this solve (about 3 s per matvec and an N-sized MGS basis)."""
+    import paper_2602_21958_b200 as P
+    from paper_2602_21958_b200 import configs
+
+    p = configs.slab_problem(2, layout="moments")
+    b = P.build_rhs(p, device=True)
+    out = {}
+    for name, restart, its in (("gmres30_3000", 30, 3000), ("gmres_unrestarted", None, 4000)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = P.gmres(p, b, P.SolveConfig(rel_tol=1e-8, max_iter=its, restart=restart))
+        torch.cuda.synchronize()
+        out[name] = {"iterations": rep.iterations, "converged": rep.converged, "time_s": time.perf_counter() - t0,
+                     "true_residual": rep.true_residual, "matvecs": rep.matvecs, "unknowns": p.n_total}
     return out
 
 
