@@ -75,3 +75,15 @@ def test_lattice_rejects_bad_arguments():
     q = L.lattice_problem(4, 1, 4, 4, 4, 3, corr_len=1.0, formal_solver="exp_parabolic")
     with pytest.raises(ValueError):
         q.device()
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_full_size_lattice_matvec_matches_oracle(cfg):
+    """BASELINE cfg3 (256 x 256 slab, 128 dirs, 41 nu, intensity layout) and cfg4 (64^3, 128 dirs,
+    31 nu, moment layout) at full size: one matvec against the numpy oracle (1 - 3 min on the CPU)."""
+    from tools.time_lattice import CFGS
+
+    p = L.lattice_problem(seed=21958 + cfg, **CFGS[cfg])
+    d = OL.desc_from_lattice_problem(p)
+    v = np.random.default_rng(cfg).standard_normal(p.n_total)
+    assert rel_l2(P.apply_A(p, v), OL.apply_A(d, p.layout, v)) <= MATVEC_TOL
