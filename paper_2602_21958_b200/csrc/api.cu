@@ -56,6 +56,7 @@ Problem::~Problem() {
     if (dtpad_mom) cudaFree(dtpad_mom);
     if (lat_sub_shift) cudaFree(lat_sub_shift);
     if (lat_gat_shift) cudaFree(lat_gat_shift);
+    if (lat_dtab) cudaFree(lat_dtab);
     double* lat[] = {lat_chi, lat_in_top, lat_in_bot, lat_state[0], lat_state[1], lat_src, lat_zero, lat_splane[0],
                      lat_splane[1]};
     for (double* b : lat)

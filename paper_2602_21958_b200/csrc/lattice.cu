@@ -90,6 +90,7 @@ struct LatArgs {
     const LatDir* dirs;
     const Shift* sub_shift;   // [dir: shift_off + t * (n_sub + 1) + m] sub-node shifts
     const Shift* gat_shift;   // [dir * nz + t] T_RC gather shifts
+    const double* dtab;       // sub-segment optical paths (moment layout), see lattice_dtab_kernel
     const double* chi;      // [n_space]
     const double* phi;      // [n_freq]
     const double* src;      // SRC_VEC: S[s][a][f]; SRC_ISO: thermal[s][f]; SRC_U: u[s][l][f]
@@ -339,11 +340,25 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_kernel(LatArgs A, int
 // F frequencies per thread (F even): the lattice geometry (shift, stencil, trilinear
 // opacity, dt) is frequency-independent and computed once for the group; the internal
 // planes use the even pitch fp so each group moves as F/2 16-byte loads.
-template <int FS, int F>
+// Trilinear opacity at sub-node m of a line (T_CR on the two opacity planes).
+__device__ __forceinline__ double chi_at(const Stencil& st, double wz, const double* __restrict__ chi_a,
+                                         const double* __restrict__ chi_b) {
+    const double ca = st.w00 * __ldg(chi_a + st.c00) + st.w10 * __ldg(chi_a + st.c10) +
+                      st.w01 * __ldg(chi_a + st.c01) + st.w11 * __ldg(chi_a + st.c11);
+    const double cb = st.w00 * __ldg(chi_b + st.c00) + st.w10 * __ldg(chi_b + st.c10) +
+                      st.w01 * __ldg(chi_b + st.c01) + st.w11 * __ldg(chi_b + st.c11);
+    return (1 - wz) * ca + wz * cb;
+}
+
+// DTAB: the frequency-independent sub-segment optical paths dt are read from the
+// precomputed [dir][layer step][sub-segment][line] table (one coalesced load instead of
+// eight opacity samples); dtab points at (direction, step t, line) and has stride nxy.
+template <int FS, int F, bool DTAB>
 __device__ __forceinline__ void advance_lineF(const LatDir& D, const Shift* __restrict__ sub, double (&acc)[F],
                                               int lx, int ly, int t, int nx, int ny, const double* __restrict__ chi_a,
                                               const double* __restrict__ chi_b, const double2* __restrict__ Sa,
-                                              const double2* __restrict__ Sb, int64_t ss, const double (&phi)[F]) {
+                                              const double2* __restrict__ Sb, int64_t ss, const double (&phi)[F],
+                                              const double* __restrict__ dtab, int64_t nxy) {
     double prev_s[F], prev_c = 0.0;
 #pragma unroll
     for (int q = 0; q < F; ++q) prev_s[q] = 0.0;
@@ -351,12 +366,13 @@ __device__ __forceinline__ void advance_lineF(const LatDir& D, const Shift* __re
         const double wz = static_cast<double>(m) / D.n_sub;
         const Shift sh = sub[m];   // warp-uniform, precomputed at setup (same arithmetic as shift_of)
         const Stencil st = stencil_at(lx, ly, sh, nx, ny);
-        const double ca = st.w00 * __ldg(chi_a + st.c00) + st.w10 * __ldg(chi_a + st.c10) +
-                          st.w01 * __ldg(chi_a + st.c01) + st.w11 * __ldg(chi_a + st.c11);
-        const double cb = st.w00 * __ldg(chi_b + st.c00) + st.w10 * __ldg(chi_b + st.c10) +
-                          st.w01 * __ldg(chi_b + st.c01) + st.w11 * __ldg(chi_b + st.c11);
-        const double c_m = (1 - wz) * ca + wz * cb;
-        const double dt = D.sub_len * (prev_c + c_m) * 0.5;
+        double dt = 0.0, c_m = 0.0;
+        if (DTAB) {
+            if (m > 0) dt = __ldg(dtab + static_cast<int64_t>(m - 1) * nxy);
+        } else {
+            c_m = chi_at(st, wz, chi_a, chi_b);
+            dt = D.sub_len * (prev_c + c_m) * 0.5;
+        }
 #pragma unroll
         for (int h = 0; h < F / 2; ++h) {
             const double2 a00 = __ldg(Sa + st.c00 * ss + h), a10 = __ldg(Sa + st.c10 * ss + h);
@@ -384,6 +400,33 @@ __device__ __forceinline__ void advance_lineF(const LatDir& D, const Shift* __re
                 prev_s[q] = s2[e];
             }
         }
+        prev_c = c_m;
+    }
+}
+
+// dt table: dtab[D.dtab_off + (t * n_sub + m - 1) * nxy + c] = sub_len (chi(m-1) + chi(m)) / 2,
+// computed with the same expressions as the on-the-fly path.
+__global__ void lattice_dtab_kernel(const LatDir* __restrict__ dirs, const Shift* __restrict__ sub_shift,
+                                    const double* __restrict__ chi, double* __restrict__ dtab, int n_dirs, int nx,
+                                    int ny, int nz) {
+    const int64_t nxy = static_cast<int64_t>(nx) * ny;
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int a = blockIdx.y;
+    if (tid >= nxy * (nz - 1) || a >= n_dirs) return;
+    const int t = static_cast<int>(tid / nxy);
+    const int c = static_cast<int>(tid - static_cast<int64_t>(t) * nxy);
+    const LatDir D = dirs[a];
+    const int k = D.down ? t : nz - 1 - t;
+    const int k2 = D.down ? k + 1 : k - 1;
+    const int ly = c / nx, lx = c - ly * nx;
+    const Shift* sub = sub_shift + D.shift_off + t * (D.n_sub + 1);
+    double prev_c = 0.0;
+    for (int m = 0; m <= D.n_sub; ++m) {
+        const double wz = static_cast<double>(m) / D.n_sub;
+        const Stencil st = stencil_at(lx, ly, sub[m], nx, ny);
+        const double c_m = chi_at(st, wz, chi + static_cast<int64_t>(k) * nxy, chi + static_cast<int64_t>(k2) * nxy);
+        if (m > 0)
+            dtab[D.dtab_off + (static_cast<int64_t>(t) * D.n_sub + m - 1) * nxy + c] = D.sub_len * (prev_c + c_m) * 0.5;
         prev_c = c_m;
     }
 }
@@ -473,10 +516,11 @@ __global__ void __launch_bounds__(256) lattice_mom_group_kernel(LatArgs A, int t
                 }
                 const LatDir Dl = D;
                 if (full_group) {
-                    advance_lineF<FS, F>(Dl, A.sub_shift + Dl.shift_off + t * (Dl.n_sub + 1), acc, i, j, t, A.nx,
-                                         A.ny, A.chi + static_cast<int64_t>(k) * A.nxy,
-                                         A.chi + static_cast<int64_t>(k2) * A.nxy, pc2 + a * plane2 + g2,
-                                         pn2 + a * plane2 + g2, hp, phi);
+                    advance_lineF<FS, F, true>(Dl, A.sub_shift + Dl.shift_off + t * (Dl.n_sub + 1), acc, i, j, t,
+                                               A.nx, A.ny, nullptr, nullptr, pc2 + a * plane2 + g2,
+                                               pn2 + a * plane2 + g2, hp, phi,
+                                               A.dtab + Dl.dtab_off + static_cast<int64_t>(t) * Dl.n_sub * A.nxy + c,
+                                               A.nxy);
 #pragma unroll
                     for (int h = 0; h < F / 2; ++h)
                         sout2[a * plane2 + static_cast<int64_t>(c) * hp + g2 + h] = make_double2(acc[2 * h], acc[2 * h + 1]);
@@ -485,10 +529,11 @@ __global__ void __launch_bounds__(256) lattice_mom_group_kernel(LatArgs A, int t
                     for (int h = 0; h < F / 2 && g2 + h < hp; ++h) {
                         double ap[2] = {acc[2 * h], acc[2 * h + 1]};
                         const double pp[2] = {phi[2 * h], phi[2 * h + 1]};
-                        advance_lineF<FS, 2>(Dl, A.sub_shift + Dl.shift_off + t * (Dl.n_sub + 1), ap, i, j, t, A.nx,
-                                             A.ny, A.chi + static_cast<int64_t>(k) * A.nxy,
-                                             A.chi + static_cast<int64_t>(k2) * A.nxy, pc2 + a * plane2 + g2 + h,
-                                             pn2 + a * plane2 + g2 + h, hp, pp);
+                        advance_lineF<FS, 2, true>(Dl, A.sub_shift + Dl.shift_off + t * (Dl.n_sub + 1), ap, i, j, t,
+                                                   A.nx, A.ny, nullptr, nullptr, pc2 + a * plane2 + g2 + h,
+                                                   pn2 + a * plane2 + g2 + h, hp, pp,
+                                                   A.dtab + Dl.dtab_off + static_cast<int64_t>(t) * Dl.n_sub * A.nxy + c,
+                                                   A.nxy);
                         sout2[a * plane2 + static_cast<int64_t>(c) * hp + g2 + h] = make_double2(ap[0], ap[1]);
                     }
                 }
@@ -604,8 +649,24 @@ int setup_lattice(Problem& p, const rtk_lattice_desc* d) {
     RTK_CUDA_TRY(cudaMemcpy(p.lat_sub_shift, sub.data(), sizeof(Shift) * sub.size(), cudaMemcpyHostToDevice));
     RTK_CUDA_TRY(cudaMalloc(&p.lat_gat_shift, sizeof(Shift) * gat.size()));
     RTK_CUDA_TRY(cudaMemcpy(p.lat_gat_shift, gat.data(), sizeof(Shift) * gat.size(), cudaMemcpyHostToDevice));
+    int64_t dtab_count = 0;
+    const int64_t nxy = static_cast<int64_t>(d->nx) * d->ny;
+    for (auto& D : dirs) {
+        D.dtab_off = dtab_count;
+        dtab_count += static_cast<int64_t>(D.n_sub) * (d->nz - 1) * nxy;
+    }
     RTK_CUDA_TRY(cudaMalloc(&p.lat_dirs, sizeof(LatDir) * dirs.size()));
     RTK_CUDA_TRY(cudaMemcpy(p.lat_dirs, dirs.data(), sizeof(LatDir) * dirs.size(), cudaMemcpyHostToDevice));
+    if (d->layout == RTK_LAYOUT_MOMENTS) {
+        // frequency-independent sub-segment optical paths, streamed by the moment-layout sweep
+        cudaError_t e = cudaMalloc(&p.lat_dtab, sizeof(double) * std::max<int64_t>(1, dtab_count));
+        if (e != cudaSuccess) return cuda_status(e, "lattice dt table");
+        dim3 grid(static_cast<unsigned>((nxy * (d->nz - 1) + 255) / 256), d->n_dirs);
+        lattice_dtab_kernel<<<grid, 256>>>(p.lat_dirs, reinterpret_cast<const Shift*>(p.lat_sub_shift), p.lat_chi,
+                                           p.lat_dtab, d->n_dirs, d->nx, d->ny, d->nz);
+        RTK_LAUNCH_CHECK("lattice_dtab_kernel");
+        RTK_CUDA_TRY(cudaDeviceSynchronize());
+    }
     return RTK_OK;
 }
 
@@ -614,6 +675,7 @@ static LatArgs lat_args(const Problem& p, const double* src, const double* x, do
     A.dirs = p.lat_dirs;
     A.sub_shift = reinterpret_cast<const Shift*>(p.lat_sub_shift);
     A.gat_shift = reinterpret_cast<const Shift*>(p.lat_gat_shift);
+    A.dtab = p.lat_dtab;
     A.chi = p.lat_chi;
     A.phi = p.phi;
     A.src = src;

@@ -57,6 +57,7 @@ struct LatDir {
     int down;         // Omega_z < 0: enters at the top layer
     int n_sub;        // sub-segments per layer step
     int shift_off;    // first entry of this direction in the sub-node shift table
+    long long dtab_off;   // first entry of this direction in the dt table (moment layout)
     double sx, sy;    // horizontal cells moved per layer step
     double sub_len;   // path length of one sub-segment
     double wy[8];     // w_a Y_l(a)   (moment accumulation)
@@ -106,6 +107,7 @@ struct Problem {
     CUtensorMap mom_gmap, tma_dtmap_mom;
     void* lat_sub_shift = nullptr;               // Shift table (lattice.cu), sub-nodes
     void* lat_gat_shift = nullptr;               // Shift table, T_RC gathers
+    double* lat_dtab = nullptr;                  // [dir][t][m][line] sub-segment optical paths (moment layout)
     // overlap of the HBM-bound moment reduction with the FP64 redistribution GEMM (slab apply_A)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chunk[8] = {};
