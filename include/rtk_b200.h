@@ -131,7 +131,9 @@ int rtk_problem_set_inflow(rtk_problem* p, const double* inflow_host, int64_t n_
 /* y = x - Lambda(Sigma x)  -- apply_A, R/operator.py:48-53.  x, y device, length n. */
 int rtk_apply_A(rtk_problem* p, const double* x_dev, double* y_dev, int64_t n, void* stream);
 /* apply_A with CUDA events between its kernels: ms_out[0..2] = moments, redistribution,
- * sweep durations (ms) on `stream` (synchronises).  Measurement hook for bench.py. */
+ * sweep durations (ms) on `stream` (synchronises).  When moments and redistribution ran
+ * as the single fused kernel, ms_out[0] is its duration and ms_out[1] = -1.
+ * Measurement hook for bench.py. */
 int rtk_profile_apply_A(rtk_problem* p, const double* x_dev, double* y_dev, int64_t n, void* stream,
                         float* ms_out);
 /* Same, host buffers in and out (H2D + matvec + D2H); the e2e path of the drop-in. */

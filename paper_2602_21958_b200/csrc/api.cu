@@ -95,8 +95,7 @@ int apply_A_dev(Problem& p, const double* x, double* y, cudaStream_t s) {
             if ((rc = lattice_transfer_moments(p, 2 /*LSRC_U*/, false, x, p.mom, s))) return rc;
             return launch_redistribute_ex(p, p.mom, y, p.n_freq, EPI_SUB, x, p.n_freq, s);
         }
-        if ((rc = launch_moments(p, x, s))) return rc;
-        if ((rc = launch_redistribute(p, s))) return rc;
+        if ((rc = launch_sigma(p, x, s))) return rc;
         if ((rc = launch_expand_source(p, nullptr, p.lat_src, s))) return rc;
         return lattice_transfer_intensity(p, 0 /*LSRC_VEC*/, OUT_X_MINUS, false, p.lat_src, x, y, s);
     }
@@ -123,8 +122,7 @@ int apply_A_dev(Problem& p, const double* x, double* y, cudaStream_t s) {
         RTK_CUDA_TRY(cudaStreamWaitEvent(s, p.ev_join, 0));
         return sweep_apply(p, x, y, s);
     }
-    if ((rc = launch_moments(p, x, s))) return rc;
-    if ((rc = launch_redistribute(p, s))) return rc;
+    if ((rc = launch_sigma(p, x, s))) return rc;
     return sweep_apply(p, x, y, s);
 }
 
@@ -352,14 +350,20 @@ int rtk_profile_apply_A(rtk_problem* p, const double* x, double* y, int64_t n, v
     cudaEvent_t ev[4];
     for (auto& e : ev) RTK_CUDA_TRY(cudaEventCreate(&e));
     RTK_CUDA_TRY(cudaEventRecord(ev[0], s));
-    if (!rc) rc = rtk::launch_moments(p->impl, x, s);
+    bool fused = false;
+    if (!rc) {
+        rc = rtk::launch_sigma_fused(p->impl, x, s);
+        fused = rc != -1;
+        if (!fused) rc = rtk::launch_moments(p->impl, x, s);
+    }
     RTK_CUDA_TRY(cudaEventRecord(ev[1], s));
-    if (!rc) rc = rtk::launch_redistribute(p->impl, s);
+    if (!rc && !fused) rc = rtk::launch_redistribute(p->impl, s);
     RTK_CUDA_TRY(cudaEventRecord(ev[2], s));
     if (!rc) rc = p->impl.kind == rtk::KIND_SLAB ? rtk::sweep_apply(p->impl, x, y, s) : RTK_OK;
     RTK_CUDA_TRY(cudaEventRecord(ev[3], s));
     RTK_CUDA_TRY(cudaEventSynchronize(ev[3]));
     for (int k = 0; k < 3; ++k) cudaEventElapsedTime(&ms_out[k], ev[k], ev[k + 1]);
+    if (fused) ms_out[1] = -1.0f;   // moments and redistribution ran as one kernel, timed in ms_out[0]
     for (auto& e : ev) cudaEventDestroy(e);
     return rc;
 }
@@ -440,8 +444,7 @@ int rtk_apply_sigma(rtk_problem* p, const double* x, double* s_out, int64_t n, v
     if (p->impl.kind == rtk::KIND_SLAB && p->impl.layout == rtk::LAYOUT_MOMENTS)
         return set_error(RTK_EINVAL, "apply_sigma needs the intensity layout");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if ((rc = rtk::launch_moments(p->impl, x, s))) return rc;
-    if ((rc = rtk::launch_redistribute(p->impl, s))) return rc;
+    if ((rc = rtk::launch_sigma(p->impl, x, s))) return rc;
     return rtk::launch_expand_source(p->impl, nullptr, s_out, s);
 }
 
@@ -451,8 +454,7 @@ int rtk_source_function(rtk_problem* p, const double* intensity, const double* t
     if (rc) return rc;
     if (p->impl.kind == rtk::KIND_LATTICE) return set_error(RTK_EINVAL, "source_function is implemented for slabs");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if ((rc = rtk::launch_moments(p->impl, intensity, s))) return rc;
-    if ((rc = rtk::launch_redistribute(p->impl, s))) return rc;
+    if ((rc = rtk::launch_sigma(p->impl, intensity, s))) return rc;
     return rtk::launch_expand_source(p->impl, thermal, s_out, s);
 }
 

@@ -119,6 +119,8 @@ struct Problem {
 // sigma.cu
 int launch_moments(const Problem& p, const double* x, cudaStream_t s);
 int launch_redistribute(const Problem& p, cudaStream_t s);            // mom -> gmom
+int launch_sigma_fused(const Problem& p, const double* x, cudaStream_t s);   // x -> gmom; -1: not applicable
+int launch_sigma(const Problem& p, const double* x, cudaStream_t s);         // x -> gmom (fused or K2a + K2b)
 int launch_expand_source(const Problem& p, const double* thermal, double* out, cudaStream_t s);
 // sweep1d.cu
 enum SweepSrc { SRC_MOMENTS = 0, SRC_VECTOR = 1, SRC_ZERO = 2 };

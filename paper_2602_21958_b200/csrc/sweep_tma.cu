@@ -36,12 +36,37 @@ bool encode_f64_map(CUtensorMap* map, const void* base, int rank, const uint64_t
             return false;
         fn = reinterpret_cast<Fn>(p);
     }
-    cuuint64_t gd[2] = {dims[0], rank > 1 ? dims[1] : 1};
-    cuuint64_t gs[1] = {rank > 1 ? stride_bytes[0] : 0};
-    cuuint32_t bd[2] = {box[0], rank > 1 ? box[1] : 1};
-    cuuint32_t es[2] = {1, 1};
+    if (rank < 1 || rank > 3) return false;
+    cuuint64_t gd[3] = {dims[0], rank > 1 ? dims[1] : 1, rank > 2 ? dims[2] : 1};
+    cuuint64_t gs[2] = {rank > 1 ? stride_bytes[0] : 0, rank > 2 ? stride_bytes[1] : 0};
+    cuuint32_t bd[3] = {box[0], rank > 1 ? box[1] : 1, rank > 2 ? box[2] : 1};
+    cuuint32_t es[3] = {1, 1, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), gd, gs, bd, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// 2D f64 map with 128-byte swizzle (box inner extent must be 16 doubles)
+bool encode_f64_map_sw128(CUtensorMap* map, const void* base, const uint64_t* dims, uint64_t row_stride_bytes,
+                          const uint32_t* box) {
+    using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                            const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                            CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Fn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            return false;
+        fn = reinterpret_cast<Fn>(p);
+    }
+    cuuint64_t gd[2] = {dims[0], dims[1]};
+    cuuint64_t gs[1] = {row_stride_bytes};
+    cuuint32_t bd[2] = {box[0], box[1]};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), gd, gs, bd, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }

@@ -61,14 +61,42 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+            smem_addr(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar))
+        : "memory");
+}
+
+// L2 evict-first policy for streamed-once operands (keeps reused tables resident)
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
+                                                 uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, "
+        "%4}], [%5], %6;\n" ::"r"(smem_addr(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar)), "l"(policy)
+        : "memory");
+}
+
 __device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(map) : "memory");
 }
 
 // ---------------- host side ----------------
-// Encode a row-major f64 tensor map: dims[0] contiguous.  rank 1 or 2.
+// Encode a row-major f64 tensor map: dims[0] contiguous.  rank 1, 2 or 3.
 // Returns false if the driver rejects the shape (caller falls back).
 bool encode_f64_map(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, const uint64_t* stride_bytes,
                     const uint32_t* box);
+// 2D f64 map with CU_TENSOR_MAP_SWIZZLE_128B: box[0] = 16 doubles; in shared memory the
+// 16-byte chunk c of row r sits at chunk c ^ (r % 8) (destination 1024-byte aligned).
+bool encode_f64_map_sw128(CUtensorMap* map, const void* base, const uint64_t* dims, uint64_t row_stride_bytes,
+                          const uint32_t* box);
 
 }  // namespace rtk

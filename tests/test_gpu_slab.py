@@ -159,6 +159,27 @@ def test_odd_shapes_match_oracle(shape):
         assert rel_l2(P.apply_A(p, v), ro.apply_A(d, v)) <= MATVEC_TOL
 
 
+@pytest.mark.parametrize("shape", [(101, 20, 256), (29, 16, 128), (3, 8, 384), (57, 64, 512), (2000, 6, 512)])
+def test_fused_sigma_shapes_match_oracle(shape):
+    """Shapes the fused moments+redistribution kernel takes (n_freq = 128 CN, two moments):
+    partial M blocks, an angle count off the 16-unroll, a single space point, CN = 1..4."""
+    ns, na, nf = shape
+    p = configs.slab_problem(2, n_space=ns, n_angles=na, n_freq=nf)
+    d = oracle_desc(p)
+    v = np.random.default_rng(ns + nf).standard_normal(p.n_total)
+    assert rel_l2(P.apply_A(p, v), ro.apply_A(d, v)) <= MATVEC_TOL
+
+
+def test_fused_sigma_equals_unfused_pair(monkeypatch):
+    """cfg2 full size: the fused kernel and the K2a + K2b pair agree to rounding."""
+    p = configs.slab_problem(2)
+    v = np.random.default_rng(5).standard_normal(p.n_total)
+    y_fused = P.apply_A(p, v)
+    monkeypatch.setenv("RTK_SIGMA_UNFUSED", "1")
+    y_pair = P.apply_A(p, v)
+    assert rel_l2(y_fused, y_pair) <= 1e-14
+
+
 def test_reduced_cfg2_gmres_history_prefix_matches_oracle():
     """cfg2 construction at N_z = 300, 16 mu, 64 nu: first 60 history entries within 1e-9
     (the sharp GMRES parity check), solution within 1e-7."""
