@@ -289,6 +289,19 @@ def run_b200(args):
                   "frac_hbm": sweep_bytes / kms[2] / 1e6 / hbm},
     }
     if kms[1] < 0:
+        # the unfused pair (K2a moments, K2b DMMA GEMM) on the same input, for the per-kernel roofline
+        os.environ["RTK_SIGMA_UNFUSED"] = "1"
+        kun = np.zeros(3)
+        for _ in range(kreps):
+            _native.check(lib.rtk_profile_apply_A(h.h, _device.ptr(x), _device.ptr(y), n, sptr, buf))
+            kun += np.array(list(buf), dtype=float)
+        kun /= kreps
+        del os.environ["RTK_SIGMA_UNFUSED"]
+        kernels["unfused_pair"] = {
+            "moments": {"ms": kun[0], "bytes": moments_bytes, "achieved_gbs": moments_bytes / kun[0] / 1e6,
+                        "frac_hbm": moments_bytes / kun[0] / 1e6 / hbm},
+            "redistribute": {"ms": kun[1], "flops": r_flops, "achieved_tflops": r_flops / kun[1] / 1e9,
+                             "frac_fp64": r_flops / kun[1] / 1e9 / fp64_peak}}
         # K2a + K2b ran as ONE kernel (sigma_fused_kernel): x streamed once while the DMMA
         # contraction runs; it is bound by both HBM (x) and the FP64 pipe (R contraction + the
         # 2 n_mom flops per x element of the moment reduction), so both fractions are given
