@@ -92,7 +92,7 @@ struct PassArgs {
 
 // KB = compile-time bucket >= kc: all KB loads of an element are issued back to back
 // (predicated off beyond kc), so each thread keeps KB independent requests in flight.
-template <int MODE, int KB>
+template <int MODE, int KB, int VEC>
 __global__ void __launch_bounds__(kRedThreads) cgs_pass_kernel(PassArgs P) {
     constexpr int NACC = (MODE == MODE_UPDATE_NORM) ? 1 : KB;
     __shared__ double coef[KMAX];
@@ -103,7 +103,38 @@ __global__ void __launch_bounds__(kRedThreads) cgs_pass_kernel(PassArgs P) {
     for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
 
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < P.n; e += stride) {
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (VEC == 2) {
+        // element pairs: 16-byte loads halve the load instructions per byte (all operands 16-byte aligned)
+        const int64_t n2 = P.n >> 1;
+        for (int64_t e = t0; e < n2; e += stride) {
+            double2 vv[KB];
+#pragma unroll
+            for (int k = 0; k < KB; ++k)
+                vv[k] = (k < P.kc) ? __ldg(reinterpret_cast<const double2*>(P.v[k]) + e) : make_double2(0.0, 0.0);
+            double2 we = reinterpret_cast<double2*>(P.w)[e];
+            if (MODE != MODE_DOT) {
+#pragma unroll
+                for (int k = 0; k < KB; ++k) {
+                    we.x = fma(-coef[k], vv[k].x, we.x);
+                    we.y = fma(-coef[k], vv[k].y, we.y);
+                }
+                reinterpret_cast<double2*>(P.w)[e] = we;
+            }
+            if (MODE == MODE_UPDATE_NORM) {
+                acc[0] = fma(we.x, we.x, acc[0]);
+                acc[0] = fma(we.y, we.y, acc[0]);
+            } else if (MODE != MODE_UPDATE) {
+#pragma unroll
+                for (int k = 0; k < KB; ++k) {
+                    acc[k] = fma(vv[k].x, we.x, acc[k]);
+                    acc[k] = fma(vv[k].y, we.y, acc[k]);
+                }
+            }
+        }
+    }
+    // scalar elements: everything (VEC == 1) or the odd tail element (VEC == 2)
+    for (int64_t e = (VEC == 2 ? (P.n & ~int64_t(1)) + t0 : t0); e < P.n; e += stride) {
         double vv[KB];
 #pragma unroll
         for (int k = 0; k < KB; ++k) vv[k] = (k < P.kc) ? __ldg(P.v[k] + e) : 0.0;
@@ -296,11 +327,18 @@ class Engine {
 
     template <int KB>
     void launch_pass(int mode, int blocks, const PassArgs& P) {
+        bool aligned = (reinterpret_cast<uintptr_t>(P.w) & 15) == 0;
+        for (int k = 0; k < P.kc; ++k) aligned = aligned && (reinterpret_cast<uintptr_t>(P.v[k]) & 15) == 0;
+        if (aligned) launch_pass_v<KB, 2>(mode, blocks, P);
+        else launch_pass_v<KB, 1>(mode, blocks, P);
+    }
+    template <int KB, int VEC>
+    void launch_pass_v(int mode, int blocks, const PassArgs& P) {
         switch (mode) {
-            case MODE_DOT: cgs_pass_kernel<MODE_DOT, KB><<<blocks, kRedThreads, 0, s_>>>(P); break;
-            case MODE_UPDATE_DOT: cgs_pass_kernel<MODE_UPDATE_DOT, KB><<<blocks, kRedThreads, 0, s_>>>(P); break;
-            case MODE_UPDATE_NORM: cgs_pass_kernel<MODE_UPDATE_NORM, KB><<<blocks, kRedThreads, 0, s_>>>(P); break;
-            default: cgs_pass_kernel<MODE_UPDATE, KB><<<blocks, kRedThreads, 0, s_>>>(P); break;
+            case MODE_DOT: cgs_pass_kernel<MODE_DOT, KB, VEC><<<blocks, kRedThreads, 0, s_>>>(P); break;
+            case MODE_UPDATE_DOT: cgs_pass_kernel<MODE_UPDATE_DOT, KB, VEC><<<blocks, kRedThreads, 0, s_>>>(P); break;
+            case MODE_UPDATE_NORM: cgs_pass_kernel<MODE_UPDATE_NORM, KB, VEC><<<blocks, kRedThreads, 0, s_>>>(P); break;
+            default: cgs_pass_kernel<MODE_UPDATE, KB, VEC><<<blocks, kRedThreads, 0, s_>>>(P); break;
         }
     }
 
@@ -418,16 +456,28 @@ struct Basis {
     cudaStream_t s = nullptr;
     explicit Basis(cudaStream_t st) : s(st) {}
     ~Basis() {
-        for (double* p : v)
+        for (double* p : slabs)
             if (p) cudaFreeAsync(p, s);
     }
-    int ensure(size_t count, int64_t n) {
+    std::vector<double*> slabs;   // allocations; vectors are carved from them
+    int ensure(size_t count, int64_t n, size_t hint = 0) {
+        // grow in slabs of several vectors (pool growth per 16 MB vector is slow for long
+        // unrestarted solves); `hint` = the cycle length, so a restarted cycle is one slab
+        const size_t pitch = (static_cast<size_t>(n) + 31) / 32 * 32;   // 256-byte aligned vectors
         while (v.size() < count) {
+            size_t want = hint > v.size() ? hint - v.size() : 0;
+            want = std::max(want, count - v.size());
+            want = std::max<size_t>(want, std::min<size_t>(64, std::max<size_t>(1, v.size())));
             double* p = nullptr;
-            if (pool_alloc(&p, static_cast<size_t>(n), s) != RTK_OK)
-                return set_error(RTK_ERESOURCE, "Krylov basis does not fit in device memory (" +
-                                                    std::to_string(v.size()) + " vectors allocated)");
-            v.push_back(p);
+            while (pool_alloc(&p, pitch * want, s) != RTK_OK) {
+                cudaGetLastError();
+                if (want <= count - v.size())
+                    return set_error(RTK_ERESOURCE, "Krylov basis does not fit in device memory (" +
+                                                        std::to_string(v.size()) + " vectors allocated)");
+                want = std::max(count - v.size(), want / 2);
+            }
+            slabs.push_back(p);
+            for (size_t i = 0; i < want; ++i) v.push_back(p + i * pitch);
         }
         return RTK_OK;
     }
@@ -512,7 +562,8 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
             finish(total > 1 ? total : 1, true, false, beta / b_norm);
             return RTK_OK;
         }
-        if ((rc = V.ensure(1, n))) return rc;
+        const size_t hint = static_cast<size_t>(std::min(cycle + 1, 64));
+        if ((rc = V.ensure(1, n, hint))) return rc;
         if ((rc = E.scale(r.p, V.v[0], n, beta))) return rc;
         std::vector<std::vector<double>> h_cols;
         std::vector<double> cs, sn, g{beta};
@@ -525,7 +576,7 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
             if ((rc = E.cgs2(V.v, j + 1, w.p, n, col.data()))) return rc;
             breakdown = col[j + 1] < 1e-14 * b_norm;
             if (!breakdown) {
-                if ((rc = V.ensure(j + 2, n))) return rc;
+                if ((rc = V.ensure(j + 2, n, hint))) return rc;
                 if ((rc = E.scale(w.p, V.v[j + 1], n, col[j + 1]))) return rc;
             }
             // Givens (R/krylov.py:109-122), host scalars
