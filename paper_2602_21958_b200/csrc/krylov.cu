@@ -25,6 +25,7 @@ namespace {
 constexpr int kRedThreads = 256;
 constexpr int kMaxRedBlocks = 592;   // 4 x 148 SMs
 constexpr int KMAX = 32;             // basis vectors handled per pass (restart <= 31 runs fully fused)
+constexpr int kLookahead = 3;        // Arnoldi iterations the device may run ahead of the host
 
 enum PassMode { MODE_DOT = 0, MODE_UPDATE_DOT = 1, MODE_UPDATE_NORM = 2, MODE_UPDATE = 3 };
 
@@ -34,11 +35,28 @@ struct Workspace {
     double* dev_scalars = nullptr;   // device-side coefficient / result scratch
     double* pinned = nullptr;        // host pinned scratch
     int dev_cap = 0, pin_cap = 0;
+    double* look_dev = nullptr;      // GMRES look-ahead column slots (device / pinned host)
+    double* look_pin = nullptr;
+    int look_cap = 0;
     ~Workspace() {
         if (partials) cudaFree(partials);
         if (counter) cudaFree(counter);
         if (dev_scalars) cudaFree(dev_scalars);
         if (pinned) cudaFreeHost(pinned);
+        if (look_dev) cudaFree(look_dev);
+        if (look_pin) cudaFreeHost(look_pin);
+    }
+    int reserve_look(int count) {
+        if (count <= look_cap) return RTK_OK;
+        if (look_dev) cudaFree(look_dev);
+        if (look_pin) cudaFreeHost(look_pin);
+        look_dev = nullptr;
+        look_pin = nullptr;
+        look_cap = 0;
+        RTK_CUDA_TRY(cudaMalloc(&look_dev, sizeof(double) * count * 2));
+        RTK_CUDA_TRY(cudaMallocHost(&look_pin, sizeof(double) * count * 2));
+        look_cap = count * 2;
+        return RTK_OK;
     }
     int init() {
         RTK_CUDA_TRY(cudaMalloc(&partials, sizeof(double) * KMAX * kMaxRedBlocks));
@@ -359,41 +377,38 @@ class Engine {
         return rc;
     }
 
-    // CGS2 Arnoldi step: w <- w - V h, h = h1 + h2 returned in col[0..j], col[j+1] = ||w||.
-    // Only one device->host transfer (the column) per step.
-    int cgs2(const std::vector<double*>& V, int jp1, double* w, int64_t n, double* col) {
+    // Asynchronous CGS2 step: h1 -> slot[0, jp1), h2 -> slot[jp1, 2 jp1), ||w||^2 -> slot[2 jp1];
+    // nothing crosses to the host here (the caller copies the slot back when it needs it).
+    int cgs2_enqueue(const std::vector<double*>& V, int jp1, double* w, int64_t n, double* slot) {
         int rc;
-        if ((rc = wsp_->reserve_scalars(2 * jp1 + 1))) return rc;
-        double* h1 = wsp_->dev_scalars;
-        double* h2 = wsp_->dev_scalars + jp1;
-        double* nrm = wsp_->dev_scalars + 2 * jp1;
+        double* h1 = slot;
+        double* h2 = slot + jp1;
+        double* nrm = slot + 2 * jp1;
         if (jp1 <= KMAX) {
-            // pass 1: h1 = V^T w ; pass 2: w -= V h1, h2 = V^T w ; pass 3: w -= V h2, ||w||^2
             if ((rc = pass(MODE_DOT, V.data(), jp1, nullptr, w, n, h1))) return rc;
             if ((rc = pass(MODE_UPDATE_DOT, V.data(), jp1, h1, w, n, h2))) return rc;
-            if ((rc = pass(MODE_UPDATE_NORM, V.data(), jp1, h2, w, n, nrm))) return rc;
-        } else {
-            // long bases: chunked dot / update sweeps, still device-resident
-            for (int k0 = 0; k0 < jp1; k0 += KMAX)
-                if ((rc = pass(MODE_DOT, V.data() + k0, std::min(KMAX, jp1 - k0), nullptr, w, n, h1 + k0))) return rc;
-            for (int k0 = 0; k0 < jp1; k0 += KMAX)
-                if ((rc = pass(MODE_UPDATE, V.data() + k0, std::min(KMAX, jp1 - k0), h1 + k0, w, n, nullptr))) return rc;
-            for (int k0 = 0; k0 < jp1; k0 += KMAX)
-                if ((rc = pass(MODE_DOT, V.data() + k0, std::min(KMAX, jp1 - k0), nullptr, w, n, h2 + k0))) return rc;
-            for (int k0 = 0; k0 < jp1; k0 += KMAX) {
-                const int kc = std::min(KMAX, jp1 - k0);
-                const bool last = k0 + kc >= jp1;
-                if ((rc = pass(last ? MODE_UPDATE_NORM : MODE_UPDATE, V.data() + k0, kc, h2 + k0, w, n,
-                               last ? nrm : nullptr)))
-                    return rc;
-            }
+            return pass(MODE_UPDATE_NORM, V.data(), jp1, h2, w, n, nrm);
         }
-        if ((rc = wsp_->reserve_pinned(2 * jp1 + 1))) return rc;
-        RTK_CUDA_TRY(cudaMemcpyAsync(wsp_->pinned, wsp_->dev_scalars, sizeof(double) * (2 * jp1 + 1),
-                                     cudaMemcpyDeviceToHost, s_));
-        RTK_CUDA_TRY(cudaStreamSynchronize(s_));
-        for (int i = 0; i < jp1; ++i) col[i] = wsp_->pinned[i] + wsp_->pinned[jp1 + i];
-        col[jp1] = std::sqrt(wsp_->pinned[2 * jp1]);
+        for (int k0 = 0; k0 < jp1; k0 += KMAX)
+            if ((rc = pass(MODE_DOT, V.data() + k0, std::min(KMAX, jp1 - k0), nullptr, w, n, h1 + k0))) return rc;
+        for (int k0 = 0; k0 < jp1; k0 += KMAX)
+            if ((rc = pass(MODE_UPDATE, V.data() + k0, std::min(KMAX, jp1 - k0), h1 + k0, w, n, nullptr))) return rc;
+        for (int k0 = 0; k0 < jp1; k0 += KMAX)
+            if ((rc = pass(MODE_DOT, V.data() + k0, std::min(KMAX, jp1 - k0), nullptr, w, n, h2 + k0))) return rc;
+        for (int k0 = 0; k0 < jp1; k0 += KMAX) {
+            const int kc = std::min(KMAX, jp1 - k0);
+            const bool last = k0 + kc >= jp1;
+            if ((rc = pass(last ? MODE_UPDATE_NORM : MODE_UPDATE, V.data() + k0, kc, h2 + k0, w, n,
+                           last ? nrm : nullptr)))
+                return rc;
+        }
+        return RTK_OK;
+    }
+
+    // y = x / sqrt(*norm2_dev)  (the norm stays on the device)
+    int scale_dev(const double* x, double* y, int64_t n, const double* norm2_dev) {
+        scale_kernel<<<elem_blocks(n), 256, 0, s_>>>(x, y, n, 1.0, norm2_dev);
+        RTK_LAUNCH_CHECK("scale_kernel");
         return RTK_OK;
     }
 
@@ -526,6 +541,15 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
         if (r) return r;
         return RTK_OK;
     };
+    cudaEvent_t look_ev[kLookahead];
+    for (auto& e : look_ev) RTK_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    struct EvGuard {
+        cudaEvent_t* e;
+        ~EvGuard() {
+            for (int q = 0; q < kLookahead; ++q) cudaEventDestroy(e[q]);
+        }
+    } ev_guard{look_ev};
+    int spec_matvecs = 0;   // look-ahead matvecs whose iterations were discarded (not reported)
     const double tol = cfg->rel_tol;
     double b_norm;
     if ((rc = E.norm(b, n, &b_norm))) return rc;
@@ -551,7 +575,7 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
         rep->converged = conv ? 1 : 0;
         rep->breakdown = brk ? 1 : 0;
         rep->true_residual = tr;
-        rep->matvecs = matvecs;
+        rep->matvecs = matvecs - spec_matvecs;
         hist.flush(rep);
     };
     while (total < cfg->max_iter) {
@@ -569,16 +593,39 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
         std::vector<double> cs, sn, g{beta};
         bool breakdown = false;
         const int steps = std::min(cycle, cfg->max_iter - total);
+        // Arnoldi look-ahead: the device runs up to kLookahead iterations ahead of the host's
+        // Givens / convergence bookkeeping (the next basis vector only needs ||w||, which stays
+        // on the device), so the GPU never idles on the per-iteration column read-back.  Work
+        // enqueued past a stopping iteration is discarded; results are those of the
+        // sequential loop (same kernels, same operands, same order).
+        const int slot_sz = 2 * (steps + 1) + 1;
+        if ((rc = E.wsp_->reserve_look(kLookahead * slot_sz))) return rc;
+        double* dslots = E.wsp_->look_dev;
+        double* pslots = E.wsp_->look_pin;
+        int next = 0;
         int j = 0;
         while (j < steps) {
-            if ((rc = A(V.v[j], w.p))) return rc;
-            col.assign(j + 2, 0.0);
-            if ((rc = E.cgs2(V.v, j + 1, w.p, n, col.data()))) return rc;
-            breakdown = col[j + 1] < 1e-14 * b_norm;
-            if (!breakdown) {
-                if ((rc = V.ensure(j + 2, n, hint))) return rc;
-                if ((rc = E.scale(w.p, V.v[j + 1], n, col[j + 1]))) return rc;
+            while (next < steps && next - j < kLookahead) {
+                const int q = next % kLookahead;
+                double* dslot = dslots + static_cast<size_t>(q) * slot_sz;
+                if ((rc = A(V.v[next], w.p))) return rc;
+                if ((rc = E.cgs2_enqueue(V.v, next + 1, w.p, n, dslot))) return rc;
+                if ((rc = V.ensure(next + 2, n, hint))) return rc;
+                if ((rc = E.scale_dev(w.p, V.v[next + 1], n, dslot + 2 * (next + 1)))) return rc;
+                RTK_CUDA_TRY(cudaMemcpyAsync(pslots + static_cast<size_t>(q) * slot_sz, dslot,
+                                             sizeof(double) * (2 * (next + 1) + 1), cudaMemcpyDeviceToHost, s));
+                RTK_CUDA_TRY(cudaEventRecord(look_ev[q], s));
+                ++next;
             }
+            {
+                const int q = j % kLookahead;
+                RTK_CUDA_TRY(cudaEventSynchronize(look_ev[q]));
+                const double* hs = pslots + static_cast<size_t>(q) * slot_sz;
+                col.assign(j + 2, 0.0);
+                for (int i = 0; i <= j; ++i) col[i] = hs[i] + hs[j + 1 + i];
+                col[j + 1] = std::sqrt(hs[2 * (j + 1)]);
+            }
+            breakdown = col[j + 1] < 1e-14 * b_norm;
             // Givens (R/krylov.py:109-122), host scalars
             for (int i = 0; i < j; ++i) {
                 const double tmp = cs[i] * col[i] + sn[i] * col[i + 1];
@@ -599,6 +646,7 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
             const double rel = std::fabs(g[j]) / b_norm;
             hist.push(rel);
             if (rel <= tol || breakdown) {   // R/krylov.py:129-147
+                spec_matvecs = next - j;     // look-ahead iterations not (yet) consumed
                 solve_upper(h_cols, g, j, y);
                 if ((rc = E.combine(V.v, y, x, cand.p, n))) return rc;
                 if ((rc = A(cand.p, w.p))) return rc;
@@ -619,6 +667,7 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
                     finish(total, false, true, true_rel);
                     return RTK_OK;
                 }
+                spec_matvecs = 0;            // continuing: the look-ahead iterations will be consumed
             }
         }
         // cycle exhausted: x += V y ; r = b - A x   (R/krylov.py:149-152)

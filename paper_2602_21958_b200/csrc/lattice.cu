@@ -744,7 +744,10 @@ template <int FS, int SRC, int NM>
 static int launch_mom_steps(const Problem& p, const LatArgs& A, bool with_inflow, double* mom, cudaStream_t s) {
     const unsigned pblocks = static_cast<unsigned>((A.nxy * p.fp + 255) / 256);
     constexpr int F = 2;   // F = 4 measured slower (176 registers, 1 block/SM; cfg5 854 vs 487 ms)
-    const unsigned sblocks = static_cast<unsigned>((A.nxy * ((p.fp + F - 1) / F) + 255) / 256);
+    // 64-thread blocks: a layer step has only nxy * fp / F threads (cfg4: 65,536), so small
+    // blocks spread them evenly over the SMs (256-thread blocks left 40 SMs half occupied)
+    const int mb = getenv("RTK_LAT_BLOCK") ? atoi(getenv("RTK_LAT_BLOCK")) : 64;
+    const unsigned sblocks = static_cast<unsigned>((A.nxy * ((p.fp + F - 1) / F) + mb - 1) / mb);
     double* a = p.lat_state[0];
     double* b = p.lat_state[1];
     for (int t = 0; t < A.nz; ++t) {
@@ -754,7 +757,7 @@ static int launch_mom_steps(const Problem& p, const LatArgs& A, bool with_inflow
             lattice_splane_kernel<SRC, NM><<<pblocks, 256, 0, s>>>(A, t, cur, nxt, t == 0 ? 1 : 0, p.fp);
             RTK_LAUNCH_CHECK("lattice_splane_kernel");
         }
-        lattice_mom_group_kernel<FS, NM, F><<<sblocks, 256, 0, s>>>(A, t, a, b, mom, with_inflow ? 1 : 0, p.fp, cur,
+        lattice_mom_group_kernel<FS, NM, F><<<sblocks, mb, 0, s>>>(A, t, a, b, mom, with_inflow ? 1 : 0, p.fp, cur,
                                                                     nxt);
         RTK_LAUNCH_CHECK("lattice_mom_group_kernel");
         double* tmp = a;
