@@ -744,9 +744,9 @@ template <int FS, int SRC, int NM>
 static int launch_mom_steps(const Problem& p, const LatArgs& A, bool with_inflow, double* mom, cudaStream_t s) {
     const unsigned pblocks = static_cast<unsigned>((A.nxy * p.fp + 255) / 256);
     constexpr int F = 2;   // F = 4 measured slower (176 registers, 1 block/SM; cfg5 854 vs 487 ms)
-    // 64-thread blocks: a layer step has only nxy * fp / F threads (cfg4: 65,536), so small
+    // 128-thread blocks: a layer step has only nxy * fp / F threads (cfg4: 65,536), so small
     // blocks spread them evenly over the SMs (256-thread blocks left 40 SMs half occupied)
-    const int mb = getenv("RTK_LAT_BLOCK") ? atoi(getenv("RTK_LAT_BLOCK")) : 64;
+    const int mb = getenv("RTK_LAT_BLOCK") ? atoi(getenv("RTK_LAT_BLOCK")) : 128;
     const unsigned sblocks = static_cast<unsigned>((A.nxy * ((p.fp + F - 1) / F) + mb - 1) / mb);
     double* a = p.lat_state[0];
     double* b = p.lat_state[1];
