@@ -284,6 +284,48 @@ __global__ void expand_kernel(const double* __restrict__ gmom, const double* __r
     out[t] = s;
 }
 
+// Same expansion, one thread per (node i, frequency f) looping over the directions: the
+// n_mom source moments are loaded once, Y comes from shared memory, and the writes of a
+// direction are contiguous in f (no 64-bit index divisions per element).
+template <int NM>
+__global__ void __launch_bounds__(256) expand_nodes_kernel(const double* __restrict__ gmom, const double* __restrict__ yb,
+                                                           const double* __restrict__ gray,
+                                                           const double* __restrict__ thermal, double* __restrict__ out,
+                                                           int64_t n_space, int n_angles, int n_freq, int fp) {
+    extern __shared__ double s_yb[];   // [NM][n_angles]
+    for (int t = threadIdx.x; t < NM * n_angles; t += blockDim.x) s_yb[t] = yb[t];
+    __syncthreads();
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= n_space * n_freq) return;
+    const int64_t i = t / n_freq;
+    const int f = static_cast<int>(t - i * n_freq);
+    double g[NM];
+#pragma unroll
+    for (int k = 0; k < NM; ++k) g[k] = __ldg(gmom + (i * NM + k) * fp + f);
+    const int64_t n_rays = static_cast<int64_t>(n_angles) * n_freq;
+    const int64_t base = i * n_rays + f;
+    for (int a = 0; a < n_angles; ++a) {
+        double v = 0.0;
+#pragma unroll
+        for (int k = 0; k < NM; ++k) v = fma(s_yb[k * n_angles + a], g[k], v);
+        const int64_t idx = base + static_cast<int64_t>(a) * n_freq;
+        if (gray) v *= __ldg(gray + idx);
+        if (thermal) v += __ldg(thermal + idx);
+        __stcs(out + idx, v);
+    }
+}
+
+template <int NM>
+int launch_expand_nodes(const Problem& p, const double* thermal, double* out, cudaStream_t s) {
+    const int64_t work = p.n_space * p.n_freq;
+    const unsigned blocks = static_cast<unsigned>((work + 255) / 256);
+    const size_t smem = sizeof(double) * NM * p.n_angles;
+    expand_nodes_kernel<NM><<<blocks, 256, smem, s>>>(p.gmom, p.yb, p.gamma_per_ray ? p.gamma : nullptr, thermal, out,
+                                                      p.n_space, p.n_angles, p.n_freq, p.fp);
+    RTK_LAUNCH_CHECK("expand_nodes_kernel");
+    return RTK_OK;
+}
+
 template <int NM>
 int launch_moments_t(const Problem& p, const double* x, cudaStream_t s, int64_t i0 = 0, int64_t i1 = -1) {
     if (i1 < 0) i1 = p.n_space;
@@ -371,6 +413,19 @@ int launch_redistribute(const Problem& p, cudaStream_t s) {
 }
 
 int launch_expand_source(const Problem& p, const double* thermal, double* out, cudaStream_t s) {
+    if (p.n_mom * p.n_angles <= 6144) {   // Y table fits the default shared-memory window
+        switch (p.n_mom) {
+            case 1: return launch_expand_nodes<1>(p, thermal, out, s);
+            case 2: return launch_expand_nodes<2>(p, thermal, out, s);
+            case 3: return launch_expand_nodes<3>(p, thermal, out, s);
+            case 4: return launch_expand_nodes<4>(p, thermal, out, s);
+            case 5: return launch_expand_nodes<5>(p, thermal, out, s);
+            case 6: return launch_expand_nodes<6>(p, thermal, out, s);
+            case 7: return launch_expand_nodes<7>(p, thermal, out, s);
+            case 8: return launch_expand_nodes<8>(p, thermal, out, s);
+            default: break;
+        }
+    }
     const int64_t n_int = p.n_space * p.n_rays;   // intensity-layout length (n_total differs in the moment layout)
     const unsigned blocks = static_cast<unsigned>((n_int + 255) / 256);
     expand_kernel<<<blocks, 256, 0, s>>>(p.gmom, p.yb, p.gamma_per_ray ? p.gamma : nullptr, thermal, out, n_int,
