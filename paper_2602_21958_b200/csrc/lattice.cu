@@ -202,20 +202,29 @@ __device__ __forceinline__ void advance_line_smem4(const LatDir& D, const Shift*
     }
 }
 
-// Intensity layout, small layers (nxy <= ~1500, e.g. the 2D slab): one CTA per
-// (direction, 4-frequency chunk), one thread per line handling the 4 frequencies;
-// the two source and opacity planes the lines cross are staged in shared memory once
-// per layer (ring of two), so every trilinear T_CR sample reads smem.
+// Intensity layout, small layers (nxy <= ~1000, e.g. the 2D slab): one CTA per
+// (direction, 4-frequency chunk), one thread per line handling the 4 frequencies.
+// The source / opacity planes the lines cross and the x plane of the y = x - v gather
+// are staged in shared memory by cp.async two layer steps ahead (rings of 3 and 2),
+// so the global-memory latency of the plane loads overlaps the line march.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src));
+}
+
 template <int FS, int SRC, int OUT>
 __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A, int with_inflow) {
     extern __shared__ __align__(16) double sm[];
     const int nxy = static_cast<int>(A.nxy);
+    constexpr bool XM = (OUT == OUT_X_MINUS);
     double* lines = sm;                         // [nxy][kFC]
-    double* splane = lines + nxy * kFC;         // [2][nxy][kFC]
-    double* cplane = splane + 2 * nxy * kFC;    // [2][nxy]
+    double* splane = lines + nxy * kFC;         // [3][nxy][kFC]
+    double* cplane = splane + 3 * nxy * kFC;    // [3][nxy]
+    double* xplane = cplane + 3 * nxy;          // [2][nxy][kFC]   (XM only)
     const int nfc = (A.n_freq + kFC - 1) / kFC;
     const int a = blockIdx.x / nfc;
     const int f0 = (blockIdx.x % nfc) * kFC;
+    const int nq = min(kFC, A.n_freq - f0);     // valid frequencies of this chunk
     const LatDir D = A.dirs[a];
     double phi[kFC], inflow[kFC];
 #pragma unroll
@@ -226,48 +235,73 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
         const double* in = D.down ? A.inflow_top : A.inflow_bottom;
         inflow[q] = (with_inflow && fv && in) ? in[f] : 0.0;
     }
-    auto load_planes = [&](int k, int ring) {
+    auto layer_of = [&](int t) { return D.down ? t : A.nz - 1 - t; };
+    // source + opacity planes of layer k into ring slot r (asynchronous)
+    auto issue_planes = [&](int k, int r) {
         const int64_t base = static_cast<int64_t>(k) * A.nxy;
-        double* sp = splane + ring * nxy * kFC;
-        double* cp = cplane + ring * nxy;
+        double* sp = splane + r * nxy * kFC;
+        double* cp = cplane + r * nxy;
         for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) {
-            const int c = e / kFC, q = e - c * kFC, f = f0 + q;
-            double v = 0.0;
-            if (f < A.n_freq) {
-                if (SRC == LSRC_VEC) v = __ldg(A.src + ((base + c) * A.n_dirs + a) * A.n_freq + f);
-                else v = __ldg(A.src + (base + c) * A.n_freq + f);
+            const int c = e / kFC, q = e - c * kFC;
+            if (q < nq) {
+                if (SRC == LSRC_VEC) cp_async8(sp + e, A.src + ((base + c) * A.n_dirs + a) * A.n_freq + f0 + q);
+                else cp_async8(sp + e, A.src + (base + c) * A.n_freq + f0 + q);
+            } else {
+                sp[e] = 0.0;
             }
-            sp[e] = v;
         }
-        for (int c = threadIdx.x; c < nxy; c += blockDim.x) cp[c] = __ldg(A.chi + base + c);
+        for (int c = threadIdx.x; c < nxy; c += blockDim.x) cp_async8(cp + c, A.chi + base + c);
     };
+    auto issue_x = [&](int k, int r) {
+        if (!XM) return;
+        const int64_t base = static_cast<int64_t>(k) * A.nxy;
+        double* xp = xplane + r * nxy * kFC;
+        for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) {
+            const int c = e / kFC, q = e - c * kFC;
+            if (q < nq) cp_async8(xp + e, A.x + ((base + c) * A.n_dirs + a) * A.n_freq + f0 + q);
+        }
+    };
+    auto commit = []() { asm volatile("cp.async.commit_group;\n" ::); };
     for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) lines[e] = inflow[e % kFC];
-    load_planes(D.down ? 0 : A.nz - 1, 0);
+    // prologue: group 0 = planes(t=0) + x(t=0); group 1 = planes(t=1) + x(t=1)
+    issue_planes(layer_of(0), 0);
+    issue_x(layer_of(0), 0);
+    commit();
+    if (A.nz > 1) {
+        issue_planes(layer_of(1), 1);
+        issue_x(layer_of(1), 1);
+    }
+    commit();
     for (int t = 0; t < A.nz; ++t) {
-        const int k = D.down ? t : A.nz - 1 - t;
+        const int k = layer_of(t);
+        // groups committed so far: t + 2 (steps 0..t+1); step t needs groups 0..t+1 (planes t and
+        // t+1, x of t): all but none may stay pending
+        asm volatile("cp.async.wait_group 0;\n" ::);
         __syncthreads();
+        // prefetch for step t+1: planes of layer t+2 into the slot last used at step t-1, x of t+1
+        if (t + 2 < A.nz) issue_planes(layer_of(t + 2), (t + 2) % 3);
+        if (t + 1 < A.nz && t > 0) issue_x(layer_of(t + 1), (t + 1) & 1);
+        commit();
         // T_RC gather: one thread per (node, frequency) for coalesced y writes
         const Shift gsh = A.gat_shift[a * A.nz + t];
+        const double* xp = xplane + (t & 1) * nxy * kFC;
         for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) {
-            const int c = e / kFC, q = e - c * kFC, f = f0 + q;
+            const int c = e / kFC, q = e - c * kFC;
             const int j = c / A.nx, i = c - j * A.nx;
             const Stencil st = stencil_at(i, j, gsh, A.nx, A.ny);
             const double v = st.w00 * lines[st.c00 * kFC + q] + st.w10 * lines[st.c10 * kFC + q] +
                              st.w01 * lines[st.c01 * kFC + q] + st.w11 * lines[st.c11 * kFC + q];
-            if (f < A.n_freq) {
-                const int64_t idx = ((static_cast<int64_t>(k) * A.nxy + c) * A.n_dirs + a) * A.n_freq + f;
-                A.y[idx] = (OUT == OUT_X_MINUS) ? A.x[idx] - v : v;
+            if (q < nq) {
+                const int64_t idx = ((static_cast<int64_t>(k) * A.nxy + c) * A.n_dirs + a) * A.n_freq + f0 + q;
+                A.y[idx] = XM ? xp[e] - v : v;
             }
         }
         if (t == A.nz - 1) break;
-        const int k2 = D.down ? k + 1 : k - 1;
-        load_planes(k2, (t + 1) & 1);
-        __syncthreads();
-        const int cur = t & 1, nxt = (t + 1) & 1;
-        const double* Sa = splane + cur * nxy * kFC;
-        const double* Sb = splane + nxt * nxy * kFC;
-        const double* ca = cplane + cur * nxy;
-        const double* cb = cplane + nxt * nxy;
+        __syncthreads();   // the gather read `lines` before the march overwrites them
+        const double* Sa = splane + (t % 3) * nxy * kFC;
+        const double* Sb = splane + ((t + 1) % 3) * nxy * kFC;
+        const double* ca = cplane + (t % 3) * nxy;
+        const double* cb = cplane + ((t + 1) % 3) * nxy;
         for (int c = threadIdx.x; c < nxy; c += blockDim.x) {
             const int ly = c / A.nx, lx = c - ly * A.nx;
             double acc[kFC];
@@ -696,7 +730,7 @@ static LatArgs lat_args(const Problem& p, const double* src, const double* x, do
 
 template <int FS, int SRC, int OUT>
 static int launch_int(const Problem& p, const LatArgs& A, int with_inflow, cudaStream_t s) {
-    const size_t smem_planes = sizeof(double) * A.nxy * (3 * kFC + 2);
+    const size_t smem_planes = sizeof(double) * A.nxy * (kFC + 3 * kFC + 3 + 2 * kFC);
     if (smem_planes <= 160 * 1024 && !getenv_flag("RTK_LATTICE_NO_SMEM")) {
         auto kern = lattice_int_smem_kernel<FS, SRC, OUT>;
         if (smem_planes > 48 * 1024 &&
