@@ -147,24 +147,36 @@ __device__ __forceinline__ double advance_line(const LatDir& D, const Shift* __r
 // Shared-memory variant of advance_line for kFC frequencies at once: the geometry
 // (shift, stencil, trilinear opacity, dt) is computed once per line and sub-node and
 // reused for the kFC frequencies of the chunk.  Planes: chi [nxy], S [nxy][kFC].
-template <int FS>
+// DT: dt of sub-segment m comes from the precomputed table (dtl = entry of (direction,
+// step, line), stride nxy; prefetched one sub-node ahead) instead of the opacity planes.
+template <int FS, bool DT>
 __device__ __forceinline__ void advance_line_smem4(const LatDir& D, const Shift* __restrict__ sub,
                                                    double (&acc)[kFC], int lx, int ly, int t, int nx, int ny,
                                                    const double* chi_a, const double* chi_b,
-                                                   const double* Sa, const double* Sb, const double (&phi)[kFC]) {
+                                                   const double* Sa, const double* Sb, const double (&phi)[kFC],
+                                                   const double* __restrict__ dtl, int nxy) {
     double prev_s[kFC], prev_c = 0.0;
 #pragma unroll
     for (int q = 0; q < kFC; ++q) prev_s[q] = 0.0;
+    double dt_next = DT ? __ldg(dtl) : 0.0;
     for (int m = 0; m <= D.n_sub; ++m) {
         const double wz = static_cast<double>(m) / D.n_sub;
         const Shift sh = sub[m];   // warp-uniform, precomputed at setup (same arithmetic as shift_of)
         const Stencil st = stencil_at(lx, ly, sh, nx, ny);
-        const double ca = st.w00 * chi_a[st.c00] + st.w10 * chi_a[st.c10] + st.w01 * chi_a[st.c01] +
-                          st.w11 * chi_a[st.c11];
-        const double cb = st.w00 * chi_b[st.c00] + st.w10 * chi_b[st.c10] + st.w01 * chi_b[st.c01] +
-                          st.w11 * chi_b[st.c11];
-        const double c_m = (1 - wz) * ca + wz * cb;
-        const double dt = D.sub_len * (prev_c + c_m) * 0.5;
+        double dt = 0.0, c_m = 0.0;
+        if (DT) {
+            if (m > 0) {
+                dt = dt_next;
+                if (m < D.n_sub) dt_next = __ldg(dtl + static_cast<int64_t>(m) * nxy);
+            }
+        } else {
+            const double ca = st.w00 * chi_a[st.c00] + st.w10 * chi_a[st.c10] + st.w01 * chi_a[st.c01] +
+                              st.w11 * chi_a[st.c11];
+            const double cb = st.w00 * chi_b[st.c00] + st.w10 * chi_b[st.c10] + st.w01 * chi_b[st.c01] +
+                              st.w11 * chi_b[st.c11];
+            c_m = (1 - wz) * ca + wz * cb;
+            dt = D.sub_len * (prev_c + c_m) * 0.5;
+        }
         const double2* a00 = reinterpret_cast<const double2*>(Sa + st.c00 * kFC);
         const double2* a10 = reinterpret_cast<const double2*>(Sa + st.c10 * kFC);
         const double2* a01 = reinterpret_cast<const double2*>(Sa + st.c01 * kFC);
@@ -212,15 +224,16 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
                  "l"(src));
 }
 
-template <int FS, int SRC, int OUT>
-__global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A, int with_inflow) {
+template <int FS, int SRC, int OUT, bool DT>
+__global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A, int with_inflow, int max_sub) {
     extern __shared__ __align__(16) double sm[];
     const int nxy = static_cast<int>(A.nxy);
     constexpr bool XM = (OUT == OUT_X_MINUS);
     double* lines = sm;                         // [nxy][kFC]
     double* splane = lines + nxy * kFC;         // [3][nxy][kFC]
-    double* cplane = splane + 3 * nxy * kFC;    // [3][nxy]
+    double* cplane = splane + 3 * nxy * kFC;    // [3][nxy]         (opacity; unused with DT)
     double* xplane = cplane + 3 * nxy;          // [2][nxy][kFC]   (XM only)
+    Shift* shs = reinterpret_cast<Shift*>(xplane + 2 * nxy * kFC);   // [max_sub + 1] shifts of the step
     const int nfc = (A.n_freq + kFC - 1) / kFC;
     const int a = blockIdx.x / nfc;
     const int f0 = (blockIdx.x % nfc) * kFC;
@@ -250,7 +263,8 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
                 sp[e] = 0.0;
             }
         }
-        for (int c = threadIdx.x; c < nxy; c += blockDim.x) cp_async8(cp + c, A.chi + base + c);
+        if (!DT)
+            for (int c = threadIdx.x; c < nxy; c += blockDim.x) cp_async8(cp + c, A.chi + base + c);
     };
     auto issue_x = [&](int k, int r) {
         if (!XM) return;
@@ -297,7 +311,8 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
             }
         }
         if (t == A.nz - 1) break;
-        __syncthreads();   // the gather read `lines` before the march overwrites them
+        for (int m = threadIdx.x; m <= D.n_sub; m += blockDim.x) shs[m] = A.sub_shift[D.shift_off + t * (D.n_sub + 1) + m];
+        __syncthreads();   // the gather read `lines` before the march overwrites them; shifts staged
         const double* Sa = splane + (t % 3) * nxy * kFC;
         const double* Sb = splane + ((t + 1) % 3) * nxy * kFC;
         const double* ca = cplane + (t % 3) * nxy;
@@ -307,8 +322,9 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
             double acc[kFC];
 #pragma unroll
             for (int q = 0; q < kFC; ++q) acc[q] = lines[c * kFC + q];
-            advance_line_smem4<FS>(D, A.sub_shift + D.shift_off + t * (D.n_sub + 1), acc, lx, ly, t, A.nx, A.ny, ca,
-                                   cb, Sa, Sb, phi);
+            advance_line_smem4<FS, DT>(D, shs, acc, lx, ly, t, A.nx, A.ny, ca, cb, Sa, Sb, phi,
+                                       DT ? A.dtab + D.dtab_off + static_cast<int64_t>(t) * D.n_sub * A.nxy + c : nullptr,
+                                       nxy);
 #pragma unroll
             for (int q = 0; q < kFC; ++q) lines[c * kFC + q] = acc[q];
         }
@@ -691,9 +707,18 @@ int setup_lattice(Problem& p, const rtk_lattice_desc* d) {
     }
     RTK_CUDA_TRY(cudaMalloc(&p.lat_dirs, sizeof(LatDir) * dirs.size()));
     RTK_CUDA_TRY(cudaMemcpy(p.lat_dirs, dirs.data(), sizeof(LatDir) * dirs.size(), cudaMemcpyHostToDevice));
-    if (d->layout == RTK_LAYOUT_MOMENTS) {
-        // frequency-independent sub-segment optical paths, streamed by the moment-layout sweep
+    p.lat_max_sub = 0;
+    for (const auto& D : dirs) p.lat_max_sub = std::max(p.lat_max_sub, D.n_sub);
+    const bool small_layers = sizeof(double) * nxy * (10 * kFC + 3) <= 160 * 1024;
+    if (d->layout == RTK_LAYOUT_MOMENTS || small_layers) {
+        // frequency-independent sub-segment optical paths, streamed by the moment-layout sweep and
+        // by the shared-memory intensity kernel (optional there: without it the opacity is sampled)
         cudaError_t e = cudaMalloc(&p.lat_dtab, sizeof(double) * std::max<int64_t>(1, dtab_count));
+        if (e != cudaSuccess && d->layout != RTK_LAYOUT_MOMENTS) {
+            cudaGetLastError();
+            p.lat_dtab = nullptr;
+            return RTK_OK;
+        }
         if (e != cudaSuccess) return cuda_status(e, "lattice dt table");
         dim3 grid(static_cast<unsigned>((nxy * (d->nz - 1) + 255) / 256), d->n_dirs);
         lattice_dtab_kernel<<<grid, 256>>>(p.lat_dirs, reinterpret_cast<const Shift*>(p.lat_sub_shift), p.lat_chi,
@@ -730,15 +755,17 @@ static LatArgs lat_args(const Problem& p, const double* src, const double* x, do
 
 template <int FS, int SRC, int OUT>
 static int launch_int(const Problem& p, const LatArgs& A, int with_inflow, cudaStream_t s) {
-    const size_t smem_planes = sizeof(double) * A.nxy * (kFC + 3 * kFC + 3 + 2 * kFC);
+    const size_t smem_planes = sizeof(double) * A.nxy * (kFC + 3 * kFC + 3 + 2 * kFC) +
+                               sizeof(Shift) * (p.lat_max_sub + 1);
     if (smem_planes <= 160 * 1024 && !getenv_flag("RTK_LATTICE_NO_SMEM")) {
-        auto kern = lattice_int_smem_kernel<FS, SRC, OUT>;
+        const bool dt = A.dtab != nullptr && !getenv_flag("RTK_LATTICE_NO_DTAB");
+        auto kern = dt ? lattice_int_smem_kernel<FS, SRC, OUT, true> : lattice_int_smem_kernel<FS, SRC, OUT, false>;
         if (smem_planes > 48 * 1024 &&
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_planes)) !=
                 cudaSuccess)
             return set_error(RTK_ERESOURCE, "lattice planes do not fit in shared memory");
         const int nfc = (A.n_freq + kFC - 1) / kFC;
-        kern<<<A.n_dirs * nfc, kIntThreads, smem_planes, s>>>(A, with_inflow);
+        kern<<<A.n_dirs * nfc, kIntThreads, smem_planes, s>>>(A, with_inflow, p.lat_max_sub);
         RTK_LAUNCH_CHECK("lattice_int_smem_kernel");
         return RTK_OK;
     }

@@ -107,7 +107,8 @@ struct Problem {
     CUtensorMap mom_gmap, tma_dtmap_mom;
     void* lat_sub_shift = nullptr;               // Shift table (lattice.cu), sub-nodes
     void* lat_gat_shift = nullptr;               // Shift table, T_RC gathers
-    double* lat_dtab = nullptr;                  // [dir][t][m][line] sub-segment optical paths (moment layout)
+    double* lat_dtab = nullptr;                  // [dir][t][m][line] sub-segment optical paths
+    int lat_max_sub = 0;                         // largest sub-segment count over the directions
     // overlap of the HBM-bound moment reduction with the FP64 redistribution GEMM (slab apply_A)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chunk[8] = {};
