@@ -26,6 +26,8 @@ from paper_2602_21958_b200.krylov import SolveConfig, SolveReport, bicgstab, gmr
 from paper_2602_21958_b200.redistribution import gaussian_profile, prd_matrix
 from paper_2602_21958_b200.lattice import (LatticeProblem, dipole_harmonics, lattice_apply_A, lattice_build_rhs,
                                            lattice_problem, product_quadrature)
+from paper_2602_21958_b200.spectrum import SpectrumReport, TrendSummary, clustering_trend, compute_spectrum
+from paper_2602_21958_b200 import presets
 
 __all__ = [
     "DENSE_CAP_DEFAULT", "CoverageError", "ResourceLimitError",
@@ -38,6 +40,7 @@ __all__ = [
     "DeviceOperator", "RTProblem", "apply_A", "apply_A_batch", "build_rhs", "intensity_from_moments", "materialize_A", "operator", "source_function",
     "spectral_radius_estimate",
     "SolveConfig", "SolveReport", "bicgstab", "gmres", "solve_system",
+    "SpectrumReport", "TrendSummary", "clustering_trend", "compute_spectrum", "presets",
     "gaussian_profile", "prd_matrix",
     "LatticeProblem", "dipole_harmonics", "lattice_apply_A", "lattice_build_rhs", "lattice_problem",
     "product_quadrature",

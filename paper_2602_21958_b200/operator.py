@@ -193,10 +193,12 @@ def materialize_A(problem: RTProblem, dense_cap: int = DENSE_CAP_DEFAULT) -> np.
     if n > dense_cap:
         raise ResourceLimitError(f"dense operator of size {n} exceeds cap {dense_cap}")
     torch = _device.require_cuda()
-    out = np.empty((n, n))
-    e = torch.zeros(n, dtype=torch.float64, device="cuda")
-    for j in range(n):
-        e.zero_()
-        e[j] = 1.0
-        out[:, j] = apply_A(problem, e).cpu().numpy()
-    return out
+    h = problem.device()
+    lib = _native.lib()
+    s = _device.stream_ptr()
+    eye = torch.eye(n, dtype=torch.float64, device="cuda")      # row j = e_j
+    cols = torch.empty((n, n), dtype=torch.float64, device="cuda")   # row j = A e_j
+    row = 8 * n
+    for j in range(n):   # stream-ordered, no host round trip per column
+        _native.check(lib.rtk_apply_A(h.h, eye.data_ptr() + j * row, cols.data_ptr() + j * row, n, s))
+    return cols.t().contiguous().cpu().numpy()
