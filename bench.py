@@ -349,7 +349,27 @@ def run_b200(args):
         t0 = time.perf_counter()
         P.apply_A_batch(problem, xs, ys)
         el_b = time.perf_counter() - t0
+        # ceiling: the same bytes moved H2D and D2H at once with no compute (pinned buffers)
+        d_tmp = torch.empty_like(x)
+        s_a, s_b = torch.cuda.Stream(), torch.cuda.Stream()
+
+        def copies():
+            with torch.cuda.stream(s_a):
+                d_tmp.copy_(hx[0], non_blocking=True)
+            with torch.cuda.stream(s_b):
+                hy[0].copy_(y, non_blocking=True)
+
+        copies()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(4):
+            copies()
+        torch.cuda.synchronize()
+        ceiling = 4 / (time.perf_counter() - t0)
+        del d_tmp
         e2e = {"value": world * k_e2e / el_b, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+               "copy_ceiling": world * ceiling,
+               "copy_ceiling_note": "H2D + D2H of the same bytes at once, no compute: the PCIe bound of this metric",
                "path": "paper_2602_21958_b200.apply_A_batch -> rtk_apply_A_host_batch (pinned host buffers; "
                        "H2D of step k+1 overlaps D2H of step k)",
                "value_one_call_per_step": world * k_e2e / el_seq,
