@@ -485,7 +485,7 @@ __global__ void lattice_dtab_kernel(const LatDir* __restrict__ dirs, const Shift
 // Directions are processed hemisphere by hemisphere so only NM x F moment accumulators
 // are live; layer t gets the down part, layer nz-1-t the up part.
 template <int FS, int NM, int F>
-__global__ void __launch_bounds__(256) lattice_mom_group_kernel(LatArgs A, int t, const double* __restrict__ st_in,
+__global__ void __launch_bounds__(128, 5) lattice_mom_group_kernel(LatArgs A, int t, const double* __restrict__ st_in,
                                                                  double* __restrict__ st_out, double* __restrict__ mom,
                                                                  int with_inflow, int fp,
                                                                  const double* __restrict__ plane_cur,
@@ -518,11 +518,14 @@ __global__ void __launch_bounds__(256) lattice_mom_group_kernel(LatArgs A, int t
     const int g2 = f0 >> 1;               // first double2 of the group within a line
     for (int hemi = 0; hemi < 2; ++hemi) {       // 0: down (layer t), 1: up (layer nz-1-t)
         const int k = hemi == 0 ? t : A.nz - 1 - t;
-        double mo[NM][F];
+        // moment accumulators live in shared memory ([l][q][thread], conflict-free) to keep
+        // registers for the loads in flight (occupancy)
+        extern __shared__ double mo_s[];
+        auto mo = [&](int l, int q) -> double& { return mo_s[(l * F + q) * blockDim.x + threadIdx.x]; };
 #pragma unroll
         for (int l = 0; l < NM; ++l)
 #pragma unroll
-            for (int q = 0; q < F; ++q) mo[l][q] = 0.0;
+            for (int q = 0; q < F; ++q) mo(l, q) = 0.0;
         for (int a = 0; a < A.n_dirs; ++a) {
             const LatDir& D = A.dirs[a];
             if ((D.down != 0) != (hemi == 0)) continue;
@@ -549,7 +552,7 @@ __global__ void __launch_bounds__(256) lattice_mom_group_kernel(LatArgs A, int t
             for (int l = 0; l < NM; ++l) {
                 const double w = D.wy[l];
 #pragma unroll
-                for (int q = 0; q < F; ++q) mo[l][q] = fma(w, v[q], mo[l][q]);
+                for (int q = 0; q < F; ++q) mo(l, q) = fma(w, v[q], mo(l, q));
             }
             if (t < A.nz - 1) {
                 const int k2 = hemi == 0 ? k + 1 : k - 1;
@@ -598,7 +601,7 @@ __global__ void __launch_bounds__(256) lattice_mom_group_kernel(LatArgs A, int t
 #pragma unroll
             for (int q = 0; q < F; ++q) {
                 if (f0 + q >= fp) continue;
-                const double val = fv[q] ? mo[l][q] : 0.0;
+                const double val = fv[q] ? mo(l, q) : 0.0;
                 double* o = out + static_cast<int64_t>(l) * fp + q;
                 *o = first ? val : *o + val;
             }
@@ -818,8 +821,8 @@ static int launch_mom_steps(const Problem& p, const LatArgs& A, bool with_inflow
             lattice_splane_kernel<SRC, NM><<<pblocks, 256, 0, s>>>(A, t, cur, nxt, t == 0 ? 1 : 0, p.fp);
             RTK_LAUNCH_CHECK("lattice_splane_kernel");
         }
-        lattice_mom_group_kernel<FS, NM, F><<<sblocks, mb, 0, s>>>(A, t, a, b, mom, with_inflow ? 1 : 0, p.fp, cur,
-                                                                    nxt);
+        lattice_mom_group_kernel<FS, NM, F><<<sblocks, mb, sizeof(double) * NM * F * mb, s>>>(
+            A, t, a, b, mom, with_inflow ? 1 : 0, p.fp, cur, nxt);
         RTK_LAUNCH_CHECK("lattice_mom_group_kernel");
         double* tmp = a;
         a = b;
