@@ -7,11 +7,13 @@
 //   G[i,k,f] = c_k gamma[i,f] sum_g R[f,g] w_g m[i,k,g]  (DMMA, K = n_freq)
 //
 // Work decomposition (n_mom = 2, n_freq = 128 * CN, CN = 1..4):
-// * a thread-block CLUSTER of CN CTAs owns an M block of SP <= 31 space points
-//   (GEMM rows 2 SP <= 62 of a 64-row = 8 m8-tile block; SP is chosen per problem
-//   so the blocks split evenly over the co-resident clusters) and the whole
-//   frequency range; CTA rank r computes output columns [128 r, 128 r + 128);
-// * K (= source frequency g) is walked in KT = 16 steps of BK = 8 CN columns.  In
+// * a thread-block CLUSTER of CN CTAs owns an M block of SP space points (GEMM rows
+//   2 SP of an 8 MT-row block; SP is chosen per problem so the blocks split evenly
+//   over the co-resident clusters) and the whole frequency range; CTA rank r
+//   computes output columns [BN r, BN r + BN).  Two shapes: BN = 128 with up to 31
+//   points (default), and BN = 256 with up to 16 points (clusters half as large,
+//   opt-in: measured slower);
+// * K (= source frequency g) is walked in KT = BN / 8 steps of BK = 8 CN columns.  In
 //   each step CTA r reduces ITS 8 columns of x for the SP points: a producer lane
 //   streams x[SP points][16 directions][8 columns] boxes with TMA into a ring (no
 //   register staging), 8 reducer warps sum the directions into the 64 x 8 moment
@@ -38,20 +40,11 @@ namespace {
 namespace fused {
 
 constexpr int NM = 2;
-constexpr int SPMAX = 31;              // space points per M block (runtime SP <= SPMAX)
-constexpr int ROWS = 64;               // 8 m8 tiles; rows >= 2 SP are computed but never stored
-constexpr int MT = ROWS / 8;
-constexpr int BN = 128;                // output columns per CTA
 constexpr int KS = 8;                  // source columns reduced per CTA per K step
-constexpr int KT = 16;                 // K steps (n_freq = 128 CN, BK = 8 CN)
 constexpr int PA = KS;                 // A slice row pitch; columns XOR-swizzled by 4 on rows with bit 1 set
-constexpr int SLICE = ROWS * PA;       // doubles per A slice (4 KB)
 constexpr int AC = 16;                 // directions per x box
-constexpr int XBOX = KS * AC * SPMAX;  // doubles per x ring slot (a box holds KS * AC * SP)
-constexpr int XS = 4;                  // x ring stages
-constexpr int AS = 2;                  // A ring stages
-constexpr int BS = 2;                  // R^T tile ring stages
-constexpr int MMA_WARPS = 8, RED_WARPS = 8;
+// 16 warps = 4 per SM sub-partition, so the register cap is 128 (17 warps would cap it at 96)
+constexpr int MMA_WARPS = 8, RED_WARPS = 7;
 constexpr int THREADS = 32 * (MMA_WARPS + RED_WARPS + 1);   // + producer warp (lane 0: x, lane 1: R^T)
 constexpr int RED0 = 32 * MMA_WARPS;   // first reducer thread
 constexpr int XPROD = 32 * (MMA_WARPS + RED_WARPS);
@@ -59,11 +52,26 @@ constexpr int BPROD = XPROD + 1;
 constexpr int MAX_ANGLES = 256;
 constexpr size_t kSmemLimit = 232448;
 
-template <int CN>
+// Variant: CN CTAs per cluster, MT m8 tiles of GEMM rows (2 SP <= 8 MT), NT n8 tiles per
+// MMA warp (BN = 64 NT output columns per CTA).  (CN, 8, 2): 31 points x 128 columns;
+// (CN, 4, 4): 16 points x 256 columns -- half the cluster size for the same N_nu, so
+// clusters of 2 tile every GPC (all 148 SMs) where clusters of 4 leave 16 SMs idle.
+template <int CN, int MT_, int NT_>
 struct Cfg {
+    static constexpr int MT = MT_, NT = NT_;
+    static constexpr int ROWS = 8 * MT;                      // rows >= 2 SP are computed but never stored
+    static constexpr int SPMAX = MT == 8 ? 31 : 4 * MT;      // space points per M block (runtime SP <= SPMAX)
+    static constexpr int NSP = (SPMAX + RED_WARPS - 1) / RED_WARPS;   // points per reducer warp
+    static constexpr int BN = 8 * NT * MMA_WARPS;            // output columns per CTA
+    static constexpr int KT = BN / KS;                       // K steps (n_freq = BN CN, BK = KS CN)
+    static constexpr int SLICE = ROWS * PA;                  // doubles per A slice
+    static constexpr int XBOX = KS * AC * SPMAX;             // doubles per x ring slot
+    static constexpr int XS = MT == 8 ? 4 : 6;               // x ring stages
+    static constexpr int AS = MT == 8 ? 2 : 4;               // A ring stages
+    static constexpr int BS = MT == 8 ? 2 : 3;               // R^T tile ring stages
     static constexpr int BK = KS * CN;
     static constexpr size_t a_elems = static_cast<size_t>(CN) * SLICE;   // one A stage
-    static constexpr size_t b_elems = static_cast<size_t>(BK) * BN;      // one R^T stage (8 swizzled boxes)
+    static constexpr size_t b_elems = static_cast<size_t>(BK) * BN;      // one R^T stage (BN / 16 swizzled boxes)
     static size_t smem_bytes(int n_apad) {
         return 1024 /* alignment slack */ +
                sizeof(double) * (BS * b_elems + static_cast<size_t>(XS) * XBOX + AS * a_elems +
@@ -95,21 +103,22 @@ __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
     asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
-__device__ __forceinline__ void red_bar() { asm volatile("bar.sync 2, 256;\n" ::: "memory"); }
+__device__ __forceinline__ void red_bar() { asm volatile("bar.sync 2, %0;\n" ::"n"(32 * RED_WARPS) : "memory"); }
 __device__ __forceinline__ void mma(double (&c)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c[0]), "+d"(c[1])
                  : "d"(a), "d"(b));
 }
 
-template <int CN>
+template <int CN, int MT_, int NT_>
 __global__ void __launch_bounds__(THREADS, 1)
     sigma_fused_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap rmap,
                        const double* __restrict__ wy, const double* __restrict__ gamma,
                        const double* __restrict__ coeffs, double* __restrict__ G, int n_space, int n_angles, int fp,
                        int gamma_mode, int SP) {
-    using C = Cfg<CN>;
-    constexpr int BK = C::BK;
+    using C = Cfg<CN, MT_, NT_>;
+    constexpr int BK = C::BK, MT = C::MT, NT = C::NT, BN = C::BN, KT = C::KT, SLICE = C::SLICE, XBOX = C::XBOX;
+    constexpr int XS = C::XS, AS = C::AS, BS = C::BS, NSP = C::NSP;
     const int n_freq = BN * CN;
     const int n_chunks = (n_angles + AC - 1) / AC;
     const int n_apad = n_chunks * AC;
@@ -186,13 +195,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         // ---------------- reducers: x boxes -> 64 x 8 moment slice -> cluster A stages ----------------
         const int rw = warp - MMA_WARPS;
         const int aq = lane >> 3, f = lane & 7;
-        const int nsp = (SP - rw + 7) / 8;            // local points rw, rw + 8, rw + 16, rw + 24 below SP
+        const int nsp = (SP - rw + RED_WARPS - 1) / RED_WARPS;   // local points rw, rw + RED_WARPS, ... below SP
         int it = 0;
         for (int n = 0; n < total; ++n) {
             const int buf = n % AS;
-            double acc[4][NM];
+            double acc[NSP][NM];
 #pragma unroll
-            for (int s = 0; s < 4; ++s) acc[s][0] = acc[s][1] = 0.0;
+            for (int s = 0; s < NSP; ++s) acc[s][0] = acc[s][1] = 0.0;
             for (int c = 0; c < n_chunks; ++c, ++it) {
                 const int st = it % XS;
                 mbar_wait(&x_full[st], (it / XS) & 1);
@@ -204,9 +213,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                     const int a = aq + 4 * t;
                     const double wa = w0[a], wb = w1[a];
 #pragma unroll
-                    for (int s = 0; s < 4; ++s) {
+                    for (int s = 0; s < NSP; ++s) {
                         if (s < nsp) {
-                            const double v = xb[((rw + 8 * s) * AC + a) * KS + f];
+                            const double v = xb[((rw + RED_WARPS * s) * AC + a) * KS + f];
                             acc[s][0] = fma(wa, v, acc[s][0]);
                             acc[s][1] = fma(wb, v, acc[s][1]);
                         }
@@ -216,7 +225,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (lane == 0) mbar_arrive(&x_empty[st]);
             }
 #pragma unroll
-            for (int s = 0; s < 4; ++s)
+            for (int s = 0; s < NSP; ++s)
 #pragma unroll
                 for (int k = 0; k < NM; ++k) {
                     acc[s][k] += __shfl_xor_sync(0xffffffffu, acc[s][k], 8);
@@ -230,9 +239,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             double* slice = As + buf * C::a_elems + rank * SLICE;
             if (aq == 0) {
 #pragma unroll
-                for (int s = 0; s < 4; ++s)
+                for (int s = 0; s < NSP; ++s)
                     if (s < nsp) {
-                        const int r = 2 * (rw + 8 * s);     // rows r, r + 1 share the swizzle (bit 1)
+                        const int r = 2 * (rw + RED_WARPS * s);   // rows r, r + 1 share the swizzle (bit 1)
                         const int cs = f ^ (((r >> 1) & 1) << 2);
                         slice[r * PA + cs] = acc[s][0];
                         slice[(r + 1) * PA + cs] = acc[s][1];
@@ -254,40 +263,41 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         if (tid == RED0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     } else if (warp < MMA_WARPS) {
-        // ---------------- MMA warps: G tile (64 x 128) += A (64 x BK) * R^T tile (BK x 128) ----------------
+        // ---------------- MMA warps: G tile (ROWS x BN) += A (ROWS x BK) * R^T tile (BK x BN) ----------------
         const int g = lane >> 2, q = lane & 3;
-        const int col_w = warp * 16;                  // = swizzled box `warp` of the R^T stage
+        const int col_w = warp * 8 * NT;              // = swizzled boxes warp NT/2 .. of the R^T stage
         const int sw = ((g >> 1) & 1) << 2;           // A-slice column swizzle of rows 8 i + g
         // fragment offsets for the two kk % 8 phases (0, 4): A slice column and swizzled R^T chunk
         const int aoff0 = q ^ sw, aoff1 = (4 + q) ^ sw;
         const int boff00 = ((g >> 1) ^ q) << 1, boff01 = ((4 + (g >> 1)) ^ q) << 1;
         const int boff10 = ((g >> 1) ^ (4 + q)) << 1, boff11 = ((4 + (g >> 1)) ^ (4 + q)) << 1;
-        double acc[MT][2][2];
+        double acc[MT][NT][2];
 #pragma unroll
         for (int i = 0; i < MT; ++i)
 #pragma unroll
-            for (int jn = 0; jn < 2; ++jn) acc[i][jn][0] = acc[i][jn][1] = 0.0;
+            for (int jn = 0; jn < NT; ++jn) acc[i][jn][0] = acc[i][jn][1] = 0.0;
         for (int n = 0; n < total; ++n) {
             const int j = n % KT, bst = n % BS, buf = n % AS;
             mbar_wait(&b_full[bst], (n / BS) & 1);
             mbar_wait(&a_full[buf], (n / AS) & 1);
             const double* abuf = As + buf * C::a_elems + g * PA;
-            const double* bbox = Bs + bst * C::b_elems + warp * 16 * BK + q * 16 + (g & 1);
+            const double* bbox = Bs + bst * C::b_elems + warp * (NT / 2) * 16 * BK + q * 16 + (g & 1);
 #pragma unroll
             for (int kk = 0; kk < BK; kk += 4) {
                 // R^T row kk + q of the box, 128-byte swizzle on (kk + q) % 8 = (kk & 4) + q
                 const bool hi = (kk & 4) != 0;
                 const double* as = abuf + (kk / KS) * SLICE + (hi ? aoff1 : aoff0);
                 const double* br = bbox + kk * 16;
-                double af[MT], bf[2];
+                double af[MT], bf[NT];
 #pragma unroll
                 for (int i = 0; i < MT; ++i) af[i] = as[i * 8 * PA];
-                bf[0] = br[hi ? boff10 : boff00];
-                bf[1] = br[hi ? boff11 : boff01];
+#pragma unroll
+                for (int jn = 0; jn < NT; ++jn)   // n8 tile jn: box jn / 2, chunk half jn % 2
+                    bf[jn] = br[(jn >> 1) * 16 * BK + ((jn & 1) ? (hi ? boff11 : boff01) : (hi ? boff10 : boff00))];
 #pragma unroll
                 for (int i = 0; i < MT; ++i)
 #pragma unroll
-                    for (int jn = 0; jn < 2; ++jn) mma(acc[i][jn], af[i], bf[jn]);
+                    for (int jn = 0; jn < NT; ++jn) mma(acc[i][jn], af[i], bf[jn]);
             }
             __syncwarp();
             if (lane == 0) {
@@ -301,14 +311,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                 // loads of a group are in flight together
 #pragma unroll
                 for (int i0 = 0; i0 < MT; i0 += 2) {
-                    double2 gm[2][2];
+                    double2 gm[2][NT];
 #pragma unroll
                     for (int di = 0; di < 2; ++di) {
                         const int r = (i0 + di) * 8 + g;
                         const int sp = blk * SP + (r >> 1);
                         const bool ok = gamma_mode && (r >> 1) < SP && sp < n_space;
 #pragma unroll
-                        for (int jn = 0; jn < 2; ++jn) {
+                        for (int jn = 0; jn < NT; ++jn) {
                             const int col = static_cast<int>(rank) * BN + col_w + jn * 8 + 2 * q;
                             gm[di][jn] = ok ? __ldg(reinterpret_cast<const double2*>(
                                                   gamma + static_cast<int64_t>(sp) * n_freq + col))
@@ -323,14 +333,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                         if ((r >> 1) < SP && sp < n_space) {
                             const double ck = coeffs[k];
 #pragma unroll
-                            for (int jn = 0; jn < 2; ++jn) {
+                            for (int jn = 0; jn < NT; ++jn) {
                                 const int col = static_cast<int>(rank) * BN + col_w + jn * 8 + 2 * q;
                                 *reinterpret_cast<double2*>(G + (static_cast<int64_t>(sp) * NM + k) * fp + col) =
                                     make_double2(ck * acc[i][jn][0] * gm[di][jn].x, ck * acc[i][jn][1] * gm[di][jn].y);
                             }
                         }
 #pragma unroll
-                        for (int jn = 0; jn < 2; ++jn) acc[i][jn][0] = acc[i][jn][1] = 0.0;
+                        for (int jn = 0; jn < NT; ++jn) acc[i][jn][0] = acc[i][jn][1] = 0.0;
                     }
                 }
             }
@@ -340,15 +350,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     cluster_sync_all();   // no CTA leaves while peers may still copy into / signal its shared memory
 }
 
-template <int CN>
+template <int CN, int MT, int NT>
 int launch_t(const Problem& p, const double* x, cudaStream_t s) {
+    using C = Cfg<CN, MT, NT>;
+    auto kernel = sigma_fused_kernel<CN, MT, NT>;
     const int n_apad = (p.n_angles + AC - 1) / AC * AC;
-    const size_t smem = Cfg<CN>::smem_bytes(n_apad);
+    const size_t smem = C::smem_bytes(n_apad);
     if (smem > kSmemLimit) return -1;
     static int max_clusters = -1;   // per instantiation
     static size_t configured_smem = 0;
     if (configured_smem != smem) {
-        RTK_CUDA_TRY(cudaFuncSetAttribute(sigma_fused_kernel<CN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        RTK_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(smem)));
         cudaLaunchConfig_t qc = {};
         cudaLaunchAttribute qa[1];
@@ -362,18 +374,19 @@ int launch_t(const Problem& p, const double* x, cudaStream_t s) {
         qc.attrs = qa;
         qc.numAttrs = 1;
         int nc = 0;
-        if (cudaOccupancyMaxActiveClusters(&nc, sigma_fused_kernel<CN>, &qc) != cudaSuccess || nc <= 0) {
+        if (cudaOccupancyMaxActiveClusters(&nc, kernel, &qc) != cudaSuccess || nc <= 0) {
             cudaGetLastError();
             return -1;
         }
         max_clusters = nc;
         configured_smem = smem;
-        if (getenv_flag("RTK_DEBUG")) std::fprintf(stderr, "sigma_fused<%d>: %d co-resident clusters\n", CN, nc);
+        if (getenv_flag("RTK_DEBUG"))
+            std::fprintf(stderr, "sigma_fused<%d,%d,%d>: %d co-resident clusters\n", CN, MT, NT, nc);
     }
     // block size: the fewest rounds over the co-resident clusters, then the smallest SP
     // that keeps that round count (balanced blocks), then as few clusters as possible
-    const int64_t rounds = (p.n_space + static_cast<int64_t>(SPMAX) * max_clusters - 1) /
-                           (static_cast<int64_t>(SPMAX) * max_clusters);
+    const int64_t rounds = (p.n_space + static_cast<int64_t>(C::SPMAX) * max_clusters - 1) /
+                           (static_cast<int64_t>(C::SPMAX) * max_clusters);
     const int sp = static_cast<int>((p.n_space + rounds * max_clusters - 1) / (rounds * max_clusters));
     const int nblk = static_cast<int>((p.n_space + sp - 1) / sp);
     const int ncl = static_cast<int>((nblk + rounds - 1) / rounds);
@@ -385,7 +398,7 @@ int launch_t(const Problem& p, const double* x, cudaStream_t s) {
         const uint32_t box[3] = {KS, AC, static_cast<uint32_t>(sp)};
         if (!encode_f64_map(&xmap, x, 3, dims, strides, box)) return -1;
         const uint64_t rd[2] = {static_cast<uint64_t>(p.fp), static_cast<uint64_t>(p.n_freq)};
-        const uint32_t rb[2] = {16, static_cast<uint32_t>(Cfg<CN>::BK)};
+        const uint32_t rb[2] = {16, static_cast<uint32_t>(C::BK)};
         if (!encode_f64_map_sw128(&rmap, p.rwt, rd, sizeof(double) * p.fp, rb)) return -1;
     }
     cudaLaunchConfig_t cfg = {};
@@ -400,7 +413,7 @@ int launch_t(const Problem& p, const double* x, cudaStream_t s) {
     cfg.stream = s;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    RTK_CUDA_TRY(cudaLaunchKernelEx(&cfg, sigma_fused_kernel<CN>, xmap, rmap, static_cast<const double*>(p.wy),
+    RTK_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, xmap, rmap, static_cast<const double*>(p.wy),
                                     static_cast<const double*>(p.gamma), static_cast<const double*>(p.coeffs), p.gmom,
                                     static_cast<int>(p.n_space), p.n_angles, p.fp, p.gamma_per_ray ? 0 : 1, sp));
     RTK_LAUNCH_CHECK("sigma_fused_kernel");
@@ -413,15 +426,25 @@ int launch_t(const Problem& p, const double* x, cudaStream_t s) {
 // -1: shape not covered (caller runs the unfused moments + redistribution pair)
 int launch_sigma_fused(const Problem& p, const double* x, cudaStream_t s) {
     if (p.kind != KIND_SLAB && p.kind != KIND_LATTICE) return -1;
-    if (p.n_mom != fused::NM || p.n_freq % fused::BN != 0 || p.fp != p.n_freq) return -1;
+    if (p.n_mom != fused::NM || p.n_freq % 128 != 0 || p.fp != p.n_freq) return -1;
     if (p.n_angles > fused::MAX_ANGLES || p.n_space > (1 << 30)) return -1;
     if (reinterpret_cast<uintptr_t>(x) % 16 != 0) return -1;
     if (getenv_flag("RTK_SIGMA_UNFUSED")) return -1;
-    switch (p.n_freq / fused::BN) {
-        case 1: return fused::launch_t<1>(p, x, s);
-        case 2: return fused::launch_t<2>(p, x, s);
-        case 3: return fused::launch_t<3>(p, x, s);
-        case 4: return fused::launch_t<4>(p, x, s);
+    // 128-column CTAs (clusters of N_nu / 128).  The 256-column shape (clusters of N_nu / 256,
+    // which tile all 148 SMs) measured slower on cfg2 (166 vs 146 us: twice the K steps per
+    // block, each with a cluster hand-off), so it is opt-in (RTK_SIGMA_BN256=1).
+    if (p.n_freq % 256 == 0 && getenv_flag("RTK_SIGMA_BN256")) {
+        switch (p.n_freq / 256) {
+            case 1: return fused::launch_t<1, 4, 4>(p, x, s);
+            case 2: return fused::launch_t<2, 4, 4>(p, x, s);
+            default: break;
+        }
+    }
+    switch (p.n_freq / 128) {
+        case 1: return fused::launch_t<1, 8, 2>(p, x, s);
+        case 2: return fused::launch_t<2, 8, 2>(p, x, s);
+        case 3: return fused::launch_t<3, 8, 2>(p, x, s);
+        case 4: return fused::launch_t<4, 8, 2>(p, x, s);
         default: return -1;
     }
 }

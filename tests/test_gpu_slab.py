@@ -170,6 +170,17 @@ def test_fused_sigma_shapes_match_oracle(shape):
     assert rel_l2(P.apply_A(p, v), ro.apply_A(d, v)) <= MATVEC_TOL
 
 
+@pytest.mark.parametrize("shape", [(101, 20, 256), (2000, 64, 512)])
+def test_fused_sigma_bn256_shape_matches_oracle(shape, monkeypatch):
+    """The opt-in 256-column cluster shape of the fused kernel (RTK_SIGMA_BN256=1)."""
+    monkeypatch.setenv("RTK_SIGMA_BN256", "1")
+    ns, na, nf = shape
+    p = configs.slab_problem(2, n_space=ns, n_angles=na, n_freq=nf)
+    d = oracle_desc(p)
+    v = np.random.default_rng(ns).standard_normal(p.n_total)
+    assert rel_l2(P.apply_A(p, v), ro.apply_A(d, v)) <= MATVEC_TOL
+
+
 def test_fused_sigma_equals_unfused_pair(monkeypatch):
     """cfg2 full size: the fused kernel and the K2a + K2b pair agree to rounding."""
     p = configs.slab_problem(2)
