@@ -113,6 +113,7 @@ struct Problem {
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chunk[8] = {};
     CUtensorMap tma_gmap, tma_dtmap;
+    CUtensorMap tma_gmap4, tma_dtmap4;          // U = 4 boxes (exp-linear weight-warp sweep)
     ~Problem();
 };
 

@@ -484,7 +484,8 @@ int launch_tma_el(const Problem& p, const double* x, double* y, cudaStream_t s) 
         }
         configured = smem;
     }
-    kern<<<p.tma_n_ctas, kElThreads, smem, s>>>(xmap, p.tma_gmap, p.tma_dtmap, A);
+    kern<<<p.tma_n_ctas, kElThreads, smem, s>>>(xmap, U == 4 ? p.tma_gmap4 : p.tma_gmap,
+                                                U == 4 ? p.tma_dtmap4 : p.tma_dtmap, A);
     RTK_LAUNCH_CHECK("sweep1d_tma_el_kernel");
     return RTK_OK;
 }
@@ -496,7 +497,8 @@ template <int FS, int NM>
 int launch_tma_t(const Problem& p, const double* x, double* y, cudaStream_t s) {
     if (FS == RTK_FS_EXP_LINEAR && p.tma_u == 8 && !getenv_flag("RTK_TMA_EL_SINGLE")) {
         // the G tensor map's box height is tma_u * n_mom rows: the weight-warp kernel uses the same U
-        const int rc = launch_tma_el<NM, 8, 2>(p, x, y, s);
+        const int rc = getenv_flag("RTK_TMA_EL_U8") ? launch_tma_el<NM, 8, 2>(p, x, y, s)
+                                                    : launch_tma_el<NM, 4, 4>(p, x, y, s);
         if (rc != -1) return rc;
     }
     if (p.tma_u == 8) return launch_tma_us<FS, NM, 8, 4>(p, x, y, s);
@@ -606,6 +608,12 @@ int setup_tma(Problem& p) {
     const uint32_t db[1] = {static_cast<uint32_t>(p.tma_u + 2)};
     if (!encode_f64_map(&p.tma_gmap, p.gmom, 2, gd, gs, gb)) return RTK_OK;
     if (!encode_f64_map(&p.tma_dtmap, p.dtpad, 1, dd, nullptr, db)) return RTK_OK;
+    {
+        const uint32_t gb4[2] = {static_cast<uint32_t>(p.tma_gw), static_cast<uint32_t>(4 * p.n_mom)};
+        const uint32_t db4[1] = {6};
+        if (!encode_f64_map(&p.tma_gmap4, p.gmom, 2, gd, gs, gb4)) return RTK_OK;
+        if (!encode_f64_map(&p.tma_dtmap4, p.dtpad, 1, dd, nullptr, db4)) return RTK_OK;
+    }
     RTK_CUDA_TRY(cudaMalloc(&p.tma_ctas, sizeof(TmaCta) * ctas.size()));
     RTK_CUDA_TRY(cudaMemcpy(p.tma_ctas, ctas.data(), sizeof(TmaCta) * ctas.size(), cudaMemcpyHostToDevice));
     p.tma_n_ctas = static_cast<int>(ctas.size());
