@@ -73,6 +73,84 @@ __device__ __forceinline__ ExpLin exp_linear_weights(double d) {
     return w;
 }
 
+// exp(-d) for d >= 0 without the library call's special-case handling: d log2(e) =
+// k + f, exp(-d) = 2^-k e^r with r = k ln2 - d in [-ln2/2, ln2/2] (Cody-Waite split of
+// ln2), e^r by its degree-13 Taylor polynomial (remainder < 4e-19), 2^-k from the
+// exponent field.  Within 2 ulp of exp(); 0 below the normal range (d > 708).
+__device__ __forceinline__ double exp_neg_fast(double d) {
+    if (d > 708.0) return 0.0;
+    const double k = rint(d * 1.4426950408889634);
+    double r = fma(k, 6.93147180369123816490e-01, -d);
+    r = fma(k, 1.90821492927058770002e-10, r);
+    double p = 1.0 / 6227020800.0;
+    p = fma(p, r, 1.0 / 479001600.0);
+    p = fma(p, r, 1.0 / 39916800.0);
+    p = fma(p, r, 1.0 / 3628800.0);
+    p = fma(p, r, 1.0 / 362880.0);
+    p = fma(p, r, 1.0 / 40320.0);
+    p = fma(p, r, 1.0 / 5040.0);
+    p = fma(p, r, 1.0 / 720.0);
+    p = fma(p, r, 1.0 / 120.0);
+    p = fma(p, r, 1.0 / 24.0);
+    p = fma(p, r, 1.0 / 6.0);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = fma(p, r, 1.0);
+    const long long ebits = static_cast<long long>(1023 - static_cast<int>(k)) << 52;
+    return p * __longlong_as_double(ebits);
+}
+
+// 1/x by the hardware approximation and two Newton steps (within 1 ulp)
+__device__ __forceinline__ double rcp_fast(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
+// Weight-warp versions of the exponential weights (sweep_tma.cu): same formulas with
+// exp_neg_fast and reciprocal multiplications; agree with the reference formulas to a
+// few ulp (the parity tests bound the matvec at 1e-11).
+__device__ __forceinline__ ExpLin exp_linear_weights_fast(double d) {
+    ExpLin w;
+    double e0;
+    if (d < RTK_EXP_SERIES_THRESHOLD) {
+        w.wc = d * e1_over_d2(d);
+        e0 = d - d * w.wc;
+        w.att = 1.0 - e0;
+    } else {
+        w.att = exp_neg_fast(d);
+        e0 = 1.0 - w.att;
+        w.wc = (d - e0) * rcp_fast(d);
+    }
+    w.wu = e0 - w.wc;
+    return w;
+}
+
+__device__ __forceinline__ ExpPar exp_parabolic_weights_fast(double du, double dd) {
+    ExpPar w;
+    double e0, e1, e2;
+    if (du < RTK_EXP_SERIES_THRESHOLD) {
+        e1 = du * du * e1_over_d2(du);
+        e2 = du * du * du * e2_over_d3(du);
+        e0 = du - e1;
+        w.att = 1.0 - e0;
+    } else {
+        w.att = exp_neg_fast(du);
+        e0 = 1.0 - w.att;
+        e1 = du - e0;
+        e2 = du * du - 2.0 * e1;
+    }
+    const double s = du + dd;
+    const double r = rcp_fast(du * dd * s);
+    w.wu = e0 + (e2 - (dd + 2.0 * du) * e1) * (dd * r);
+    w.wc = (s * e1 - e2) * (s * r);
+    w.wd = (e2 - du * e1) * (du * r);
+    return w;
+}
+
 // Parabolic (Kunasz-Auer) weights through upwind u, current c, downwind d nodes.
 __device__ __forceinline__ ExpPar exp_parabolic_weights(double du, double dd) {
     ExpPar w;

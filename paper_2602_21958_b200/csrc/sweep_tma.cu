@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(kElThreads, 2) sweep1d_tma_el_kernel(const __g
 #pragma unroll
             for (int e = wt; e < U * kRaysPerCta; e += 32 * kElWeightWarps) {
                 const int u = e / kRaysPerCta, r = e - u * kRaysPerCta;
-                const ExpLin w = exp_linear_weights(phis[r] * dts[dt_off + u] * imus[r]);
+                const ExpLin w = exp_linear_weights_fast(phis[r] * dts[dt_off + u] * imus[r]);
                 W[(u * 3 + 0) * kRaysPerCta + r] = w.att;
                 W[(u * 3 + 1) * kRaysPerCta + r] = w.wu;
                 W[(u * 3 + 2) * kRaysPerCta + r] = w.wc;
@@ -546,7 +546,8 @@ __global__ void __launch_bounds__(kElThreads, 2) sweep1d_tma_ep_kernel(const __g
                 // segments into this node and into the previous node of the march
                 const int i_in = down ? row - 1 : row, i_prev = down ? row - 2 : row + 1;
                 const int k_in = min(max(i_in - b, 0), U + 1), k_prev = min(max(i_prev - b, 0), U + 1);
-                const ExpPar w = exp_parabolic_weights(phis[r] * dts[k_prev] * imus[r], phis[r] * dts[k_in] * imus[r]);
+                const ExpPar w =
+                    exp_parabolic_weights_fast(phis[r] * dts[k_prev] * imus[r], phis[r] * dts[k_in] * imus[r]);
                 W[(u * 4 + 0) * kRaysPerCta + r] = w.att;
                 W[(u * 4 + 1) * kRaysPerCta + r] = w.wu;
                 W[(u * 4 + 2) * kRaysPerCta + r] = w.wc;
