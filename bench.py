@@ -381,6 +381,8 @@ def run_b200(args):
         extra["gmres"] = gmres_timings(torch)
         extra["gmres_cfg2_moment_layout"] = gmres_cfg2_moments(torch)
         extra["krylov_cfg2"] = krylov_cfg2(torch, problem, ms_per_step, hbm)
+    if rank == 0 and not args.no_gmres:
+        extra["formal_solvers_cfg2"] = formal_solver_timings(torch, lib, hbm)
     if rank == 0 and not args.no_lattice:
         extra["lattice"] = lattice_timings(torch)
     cpu = None
@@ -481,6 +483,44 @@ def krylov_cfg2(torch, problem, matvec_ms, hbm):
             "orth_s": orth_s, "orth_algorithmic_bytes": orth_bytes,
             "orth_achieved_gbs": orth_bytes / orth_s / 1e9 if orth_s > 0 else None,
             "orth_frac_hbm": orth_bytes / orth_s / 1e9 / hbm if orth_s > 0 else None}
+
+
+def formal_solver_timings(torch, lib, hbm):
+    """cfg2 matvec with the exponential integrators (the north star's formal solver; the
+    headline uses the reference's implicit Euler): matvec rate and the sweep's HBM fraction."""
+    from paper_2602_21958_b200 import configs
+
+    out = {}
+    for fs in ("exp_linear", "exp_parabolic"):
+        p = configs.slab_problem(2, formal_solver=fs)
+        n = p.n_total
+        h = p.device()
+        x = torch.randn(n, dtype=torch.float64, device="cuda")
+        y = torch.empty_like(x)
+        sptr = _device.stream_ptr()
+        for _ in range(3):
+            _native.check(lib.rtk_apply_A(h.h, _device.ptr(x), _device.ptr(y), n, sptr))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10
+        e0.record()
+        for _ in range(reps):
+            _native.check(lib.rtk_apply_A(h.h, _device.ptr(x), _device.ptr(y), n, sptr))
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        buf = (ctypes.c_float * 3)()
+        sweep_ms = 0.0
+        for _ in range(5):
+            _native.check(lib.rtk_profile_apply_A(h.h, _device.ptr(x), _device.ptr(y), n, sptr, buf))
+            sweep_ms += buf[2] / 5
+        g = p.grid
+        sweep_bytes = 16 * n + 8 * 2 * g.n_freq * g.n_space + 8 * g.n_space
+        out[fs] = {"matvecs_per_s": 1e3 / ms, "ms_per_matvec": ms, "sweep_ms": sweep_ms,
+                   "sweep_gbs": sweep_bytes / sweep_ms / 1e6, "sweep_frac_hbm": sweep_bytes / sweep_ms / 1e6 / hbm,
+                   "kernel": "sweep1d_tma_el_kernel / sweep1d_tma_ep_kernel (weight warps + chain warps)"}
+        del p, x, y
+        torch.cuda.empty_cache()
+    return out
 
 
 def lattice_timings(torch):
