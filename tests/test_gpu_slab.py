@@ -191,6 +191,17 @@ def test_fused_sigma_equals_unfused_pair(monkeypatch):
     assert rel_l2(y_fused, y_pair) <= 1e-14
 
 
+@pytest.mark.parametrize("ns", [2, 3, 5, 9])
+@pytest.mark.parametrize("fs", ["ie", "exp_linear", "exp_parabolic"])
+def test_few_depth_points_match_oracle(ns, fs):
+    """Slabs shorter than one pipeline stage (and a first/last stage edge in one): the TMA
+    sweeps' boundary handling and the exp-parabolic closing step."""
+    p = configs.slab_problem(1, formal_solver=fs, n_space=ns, n_angles=8, n_freq=128)
+    d = oracle_desc(p)
+    v = np.random.default_rng(ns).standard_normal(p.n_total)
+    assert rel_l2(P.apply_A(p, v), ro.apply_A(d, v)) <= MATVEC_TOL
+
+
 def test_reduced_cfg2_gmres_history_prefix_matches_oracle():
     """cfg2 construction at N_z = 300, 16 mu, 64 nu: first 60 history entries within 1e-9
     (the sharp GMRES parity check), solution within 1e-7."""
