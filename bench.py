@@ -64,6 +64,23 @@ def dist_setup(backend):
     return world, rank, local
 
 
+def ncu_raw(path):
+    """The `raw:` metrics line of a committed ncu summary (profiles/), as a dict, or {}."""
+    try:
+        with open(path) as fh:
+            for line in fh:
+                if "raw:" in line:
+                    out = {}
+                    for part in line.split("raw:")[1].split(","):
+                        if "=" in part:
+                            k, v = part.strip().split("=", 1)
+                            out[k] = v
+                    return out
+    except OSError:
+        pass
+    return {}
+
+
 def ncu_traffic(path=os.path.join(ROOT, "profiles", "r01_ncu_sweep_tma_v3.txt")):
     """dram__bytes_read.sum + dram__bytes_write.sum of the sweep kernel from the committed
     `ncu --set full` capture (profiles/), bytes per launch, or None."""
@@ -551,6 +568,13 @@ def lattice_timings(torch):
         dof = p.n_space * p.n_dirs * p.n_freq
         out[f"cfg{cfg}"] = {"layout": kw["layout"], "unknowns": p.n_total, "dof": dof, "ms_per_matvec": ms,
                             "matvecs_per_s": 1e3 / ms, "gdof_per_s": dof / ms / 1e6}
+        # the multi-D sweeps are bound by the FP64 pipe / latency, not HBM -- report the
+        # transfer kernel's FP64-pipe utilisation from the committed ncu capture of this config
+        raw = ncu_raw(os.path.join(ROOT, "profiles", f"r01_ncu_lattice_cfg{cfg}.txt"))
+        key = "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"
+        if key in raw:
+            out[f"cfg{cfg}"]["transfer_kernel_fp64_pipe_frac"] = float(raw[key].rstrip("%")) / 100
+            out[f"cfg{cfg}"]["fp64_source"] = f"profiles/r01_ncu_lattice_cfg{cfg}.txt (ncu --set full, one launch)"
         del p, x
         torch.cuda.empty_cache()
     return out
