@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gmres", action="store_true")
     ap.add_argument("--no-lattice", action="store_true")
+    ap.add_argument("--mode", choices=["replicas", "sharded"], default="replicas",
+                    help="N > 1: independent cfg2 matvecs per GPU (weak scaling, default) or ONE cfg2 matvec "
+                         "sharded by direction with an NCCL all-reduce of the moments (strong scaling)")
     return ap.parse_args()
 
 
@@ -237,6 +240,56 @@ def run_reference(args):
                                        f"R/operator.py:48-53 + R/_kernels.py:70-88), OpenMP {threads} threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def run_sharded(args):
+    """--mode sharded: one cfg2 matvec per step, directions split over the ranks
+    (paper_2602_21958_b200.sharding), one NCCL all-reduce of the 16 MB moment array per matvec."""
+    import torch
+
+    world, rank, local = dist_setup("nccl")
+    torch.cuda.set_device(local)
+    from paper_2602_21958_b200 import _native, configs
+    from paper_2602_21958_b200.sharding import ShardedOperator
+
+    problem = configs.slab_problem(CFG, formal_solver=args.formal_solver)
+    op = ShardedOperator(problem, rank=rank, world=world)
+    gen = torch.Generator(device="cuda").manual_seed(1234)
+    x = torch.randn(problem.n_total, dtype=torch.float64, device="cuda", generator=gen)
+    x_local = op.local_slice(x).contiguous()
+    del x
+    for _ in range(max(args.warmup, 3)):
+        op(x_local)
+    torch.cuda.synchronize()
+    torch.distributed.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = _native.launch_count()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        op(x_local)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = _native.launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    torch.distributed.barrier()
+    clk = clocks.stop()
+    ms_max, _ = aggregate(ms, args.steps, world, "cuda")
+    value = args.steps / (ms_max / 1e3)   # whole-job matvecs/s: every step is ONE global matvec
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; BASELINE cfg2 shapes)",
+                "config": workload_config({"formal_solver": args.formal_solver,
+                                           "parallelism": f"direction-sharded x{world} (NCCL all-reduce of moments)"}),
+                "gdof_per_s": value * problem.n_total / 1e9, "gpu_launches": launches, "clocks": clk,
+                "e2e": None, "mode": "sharded"}
+        print(json.dumps(line), flush=True)
+    torch.distributed.barrier()
+    torch.distributed.destroy_process_group()
 
 
 def run_b200(args):
@@ -584,6 +637,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.mode == "sharded" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        run_sharded(args)
     else:
         run_b200(args)
 

@@ -148,6 +148,14 @@ int rtk_apply_A_host_batch(rtk_problem* p, const double* const* x_host, double* 
  * I_dev are intensity-layout vectors of n_intensity = n_space * n_rays entries. */
 int rtk_intensity_from_moments(rtk_problem* p, const double* u_dev, const double* thermal_dev, double* I_dev,
                                int64_t n_intensity, void* stream);
+/* Direction sharding: a rank holds a problem built on ITS directions and the
+ * matching slice of x.  rtk_partial_moments writes m[i][k][f] = sum_{a in this problem}
+ * w_a Y_k(a) x[i,a,f] (n_m = n_space * n_moments * n_freq); after the moments of all ranks
+ * are summed (one all-reduce), rtk_apply_A_with_moments returns y = x - Lambda Sigma x for
+ * this problem's rays with Sigma built from the summed m.  Slab, intensity layout. */
+int rtk_partial_moments(rtk_problem* p, const double* x_dev, double* m_dev, int64_t n_m, void* stream);
+int rtk_apply_A_with_moments(rtk_problem* p, const double* x_dev, const double* m_dev, int64_t n_m, double* y_dev,
+                             int64_t n, void* stream);
 /* s = Sigma x -- apply_scattering, R/scattering.py:126-148. */
 int rtk_apply_sigma(rtk_problem* p, const double* x_dev, double* s_dev, int64_t n, void* stream);
 /* y = Lambda s (homogeneous part) -- apply_transfer, R/transfer.py:134-141. */

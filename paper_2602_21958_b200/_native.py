@@ -86,6 +86,8 @@ SIGNATURES = [
     ("rtk_apply_A_host_batch", ctypes.c_int, [_P, _P, _P, _I32, _I64]),
     ("rtk_profile_apply_A", ctypes.c_int, [_P, _P, _P, _I64, _P, ctypes.POINTER(ctypes.c_float)]),
     ("rtk_intensity_from_moments", ctypes.c_int, [_P, _P, _P, _P, _I64, _P]),
+    ("rtk_partial_moments", ctypes.c_int, [_P, _P, _P, _I64, _P]),
+    ("rtk_apply_A_with_moments", ctypes.c_int, [_P, _P, _P, _I64, _P, _I64, _P]),
     ("rtk_apply_sigma", ctypes.c_int, [_P, _P, _P, _I64, _P]),
     ("rtk_apply_lambda", ctypes.c_int, [_P, _P, _P, _I64, _P]),
     ("rtk_boundary", ctypes.c_int, [_P, _P, _I64, _P]),

@@ -437,6 +437,40 @@ int rtk_intensity_from_moments(rtk_problem* p, const double* u, const double* th
     return rc;
 }
 
+static int check_shard(const rtk_problem* p, int64_t n_m) {
+    if (!p) return set_error(RTK_EINVAL, "null problem handle");
+    const Problem& q = p->impl;
+    if (q.kind != rtk::KIND_SLAB || q.layout != rtk::LAYOUT_INTENSITY)
+        return set_error(RTK_EINVAL, "direction sharding needs a slab problem in the intensity layout");
+    if (n_m != q.n_space * q.n_mom * q.n_freq)
+        return set_error(RTK_EINVAL, "moment array must hold n_space * n_moments * n_freq values");
+    return RTK_OK;
+}
+
+int rtk_partial_moments(rtk_problem* p, const double* x, double* m, int64_t n_m, void* stream) {
+    int rc = check_shard(p, n_m);
+    if (rc) return rc;
+    const Problem& q = p->impl;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if ((rc = rtk::launch_moments(q, x, s))) return rc;   // -> q.mom, row pitch fp
+    RTK_CUDA_TRY(cudaMemcpy2DAsync(m, sizeof(double) * q.n_freq, q.mom, sizeof(double) * q.fp,
+                                   sizeof(double) * q.n_freq, q.n_space * q.n_mom, cudaMemcpyDeviceToDevice, s));
+    return RTK_OK;
+}
+
+int rtk_apply_A_with_moments(rtk_problem* p, const double* x, const double* m, int64_t n_m, double* y, int64_t n,
+                             void* stream) {
+    int rc = check_shard(p, n_m);
+    if (rc) return rc;
+    if ((rc = check_n(p, n))) return rc;
+    Problem& q = p->impl;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    RTK_CUDA_TRY(cudaMemcpy2DAsync(q.mom, sizeof(double) * q.fp, m, sizeof(double) * q.n_freq,
+                                   sizeof(double) * q.n_freq, q.n_space * q.n_mom, cudaMemcpyDeviceToDevice, s));
+    if ((rc = rtk::launch_redistribute(q, s))) return rc;   // G from the summed moments
+    return rtk::sweep_apply(q, x, y, s);
+}
+
 int rtk_apply_sigma(rtk_problem* p, const double* x, double* s_out, int64_t n, void* stream) {
     int rc = check_n(p, n);
     if (rc) return rc;

@@ -1,0 +1,117 @@
+"""Direction-sharded (I - Lambda Sigma) for several GPUs.
+
+Lambda is independent per (direction, frequency) and Sigma couples
+the directions only through the angular moments, so the operator
+shards by direction with ONE exchange per matvec: every rank holds all of space
+x all frequencies x its block of directions, computes the partial moments of
+its slice of x, the partial moments are summed across ranks (one all-reduce of
+n_space x n_mom x N_nu values: 16 MB at cfg2), and each rank redistributes the
+summed moments (replicated DMMA GEMM) and sweeps its own rays.
+
+    op = ShardedOperator(problem)              # inside torch.distributed, NCCL on GPUs
+    y_local = op(x_local)                      # x_local = op.local_slice(x)
+
+The local pieces run through the C ABI (rtk_partial_moments /
+rtk_apply_A_with_moments); the exchange is torch.distributed.all_reduce.
+`ops_factory` / `all_reduce` are injectable so the host logic is testable on
+CPU ranks (tests/test_sharding.py, gloo).  Slab problems, intensity layout.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2602_21958_b200 import _device, _native
+from paper_2602_21958_b200.grid import Grid
+from paper_2602_21958_b200.operator import RTProblem
+from paper_2602_21958_b200.scattering import ScatteringOperator, separable_form
+from paper_2602_21958_b200.transfer import build_transfer
+
+
+def angle_block(n_angles: int, rank: int, world: int) -> np.ndarray:
+    """Directions of `rank`: a contiguous, balanced block of the angle index range."""
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world of size {world}")
+    if world > n_angles:
+        raise ValueError(f"cannot shard {n_angles} directions over {world} ranks")
+    lo = (n_angles * rank) // world
+    hi = (n_angles * (rank + 1)) // world
+    return np.arange(lo, hi)
+
+
+def shard_problem(problem: RTProblem, rank: int, world: int):
+    """(local problem on this rank's directions, their global indices).  The local grid keeps
+    the global quadrature weights, so partial moments add up to the global ones."""
+    if problem.layout != "intensity":
+        raise ValueError("direction sharding needs the intensity layout")
+    g = problem.grid
+    sel = angle_block(g.n_angles, rank, world)
+    grid = Grid(g.t_nodes, g.mu_nodes[sel], g.angular_weights[sel], g.nu_nodes, g.frequency_weights, g.profile)
+    rays = (sel[:, None] * g.n_freq + np.arange(g.n_freq)[None, :]).reshape(-1)
+    gamma = np.ascontiguousarray(np.asarray(problem.scattering.gamma_table).reshape(g.n_space, g.n_rays)[:, rays])
+    scat = ScatteringOperator(grid, problem.scattering.kernel, gamma)
+    tr = build_transfer(grid, 0.0, 0.0, formal_solver=problem.transfer.formal_solver)
+    tr.inflow = np.asarray(problem.transfer.inflow)[rays]
+    thermal = np.asarray(problem.thermal).reshape(g.n_space, g.n_rays)[:, rays].reshape(-1)
+    desc = dict(problem.descriptor)
+    desc.update({"shard": f"{rank}/{world}", "angles": [int(sel[0]), int(sel[-1]) + 1]})
+    return RTProblem(grid, tr, scat, thermal=thermal, descriptor=desc), sel
+
+
+class NativeShardOps:
+    """The device halves of a sharded matvec on this rank's local problem."""
+
+    def __init__(self, local: RTProblem):
+        self.local = local
+        self.n = local.n_total
+        g = local.grid
+        self.n_m = g.n_space * separable_form(local.scattering.kernel, g)[0].shape[0] * g.n_freq
+
+    def partial_moments(self, x):
+        h = self.local.device()
+        m = _device.empty(self.n_m)
+        _native.check(_native.lib().rtk_partial_moments(h.h, _device.ptr(x), _device.ptr(m), self.n_m,
+                                                        _device.stream_ptr()))
+        return m
+
+    def apply_with_moments(self, x, m):
+        h = self.local.device()
+        y = _device.empty(self.n)
+        _native.check(_native.lib().rtk_apply_A_with_moments(h.h, _device.ptr(x), _device.ptr(m), self.n_m,
+                                                             _device.ptr(y), self.n, _device.stream_ptr()))
+        return y
+
+
+def _dist_all_reduce(t, group=None):
+    import torch.distributed as dist
+
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+class ShardedOperator:
+    """y_local = (I - Lambda Sigma) x restricted to this rank's rays (see module docstring)."""
+
+    def __init__(self, problem: RTProblem, rank: int = None, world: int = None, group=None,
+                 ops_factory=NativeShardOps, all_reduce=None):
+        if rank is None or world is None:
+            import torch.distributed as dist
+
+            rank = dist.get_rank(group) if rank is None else rank
+            world = dist.get_world_size(group) if world is None else world
+        self.problem = problem
+        self.rank, self.world = rank, world
+        self.local, self.angles = shard_problem(problem, rank, world)
+        self.ops = ops_factory(self.local)
+        self._all_reduce = all_reduce or (lambda t: _dist_all_reduce(t, group))
+
+    def local_slice(self, x):
+        """This rank's part of a global space-major vector (n_space x local directions x N_nu)."""
+        g = self.problem.grid
+        a0, a1 = int(self.angles[0]), int(self.angles[-1]) + 1
+        return x.reshape(g.n_space, g.n_angles, g.n_freq)[:, a0:a1, :].reshape(-1)
+
+    def __call__(self, x_local):
+        m = self.ops.partial_moments(x_local)
+        m = self._all_reduce(m)
+        return self.ops.apply_with_moments(x_local, m)

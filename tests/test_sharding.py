@@ -1,0 +1,114 @@
+"""Direction-sharded operator: host logic on CPU ranks (gloo, world_size 2) with the oracle
+standing in for the device halves, and the setup split (local problems) without a GPU.
+
+The device halves (rtk_partial_moments / rtk_apply_A_with_moments) are checked on the GPU
+in tests/test_gpu_sharding.py.
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+class OracleShardOps:
+    """Oracle restatement of the two device halves (test infrastructure only)."""
+
+    def __init__(self, local):
+        from oracle import rt_oracle as ro
+
+        self.ro = ro
+        self.d = ro.desc_from_problem(local)
+
+    def partial_moments(self, x):
+        import torch
+
+        d = self.d
+        cube = np.asarray(x, dtype=float).reshape(d.n_space, d.n_angles, d.n_freq)
+        return torch.from_numpy(np.einsum("saf,ka->skf", cube, d.ybasis * d.ang_w[None, :]).reshape(-1).copy())
+
+    def apply_with_moments(self, x, m):
+        d = self.d
+        m = np.asarray(m, dtype=float).reshape(d.n_space, -1, d.n_freq)
+        M = np.einsum("fg,skg->skf", d.R * d.freq_w[None, :], m)
+        S = np.einsum("ka,skf->saf", d.coeffs[:, None] * d.ybasis, M)
+        S = (d.gamma * S.reshape(d.n_space, d.n_rays)).ravel()
+        return np.asarray(x, dtype=float) - self.ro.apply_transfer(d, S)
+
+
+def _problem():
+    sys.path.insert(0, ROOT)
+    from paper_2602_21958_b200 import configs
+
+    return configs.slab_problem(1, n_space=12, n_angles=8, n_freq=7)
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from paper_2602_21958_b200.sharding import ShardedOperator
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    p = _problem()
+    x = np.random.default_rng(3).standard_normal(p.n_total)
+    op = ShardedOperator(p, ops_factory=OracleShardOps)
+    y_local = op(op.local_slice(x))
+    q.put((rank, op.angles.tolist(), np.asarray(y_local).tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+def test_two_ranks_reassemble_the_full_operator():
+    from oracle import rt_oracle as ro
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + os.getpid() % 1000
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    out = sorted(q.get(timeout=150) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=30)
+    assert all(pr.exitcode == 0 for pr in procs)
+    p = _problem()
+    g = p.grid
+    x = np.random.default_rng(3).standard_normal(p.n_total)
+    ref = ro.apply_A(ro.desc_from_problem(p), x).reshape(g.n_space, g.n_angles, g.n_freq)
+    y = np.empty_like(ref)
+    for _, angles, y_local in out:
+        y[:, angles, :] = np.asarray(y_local).reshape(g.n_space, len(angles), g.n_freq)
+    assert [a for _, ang, _ in out for a in ang] == list(range(g.n_angles))
+    assert np.linalg.norm(y - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+def test_angle_blocks_partition_the_directions():
+    from paper_2602_21958_b200.sharding import angle_block
+
+    for n, world in ((8, 2), (64, 8), (7, 3), (16, 16)):
+        blocks = [angle_block(n, r, world) for r in range(world)]
+        assert np.array_equal(np.concatenate(blocks), np.arange(n))
+        assert max(b.size for b in blocks) - min(b.size for b in blocks) <= 1
+    with pytest.raises(ValueError):
+        angle_block(4, 0, 8)
+
+
+def test_local_problems_carry_the_global_weights_and_rays():
+    from paper_2602_21958_b200.sharding import shard_problem
+
+    p = _problem()
+    g = p.grid
+    for rank in range(2):
+        loc, sel = shard_problem(p, rank, 2)
+        np.testing.assert_array_equal(loc.grid.mu_nodes, g.mu_nodes[sel])
+        np.testing.assert_array_equal(loc.grid.angular_weights, g.angular_weights[sel])
+        gam = np.asarray(p.scattering.gamma_table).reshape(g.n_space, g.n_angles, g.n_freq)[:, sel, :]
+        np.testing.assert_array_equal(loc.scattering.gamma_table.reshape(gam.shape), gam)
+        np.testing.assert_array_equal(loc.transfer.inflow,
+                                      np.asarray(p.transfer.inflow).reshape(g.n_angles, g.n_freq)[sel].reshape(-1))
