@@ -132,6 +132,31 @@ __global__ void __launch_bounds__(kGemmThreads) redistribute_kernel(const double
     }
 }
 
+// Few rows (cfg1-sized problems: M = 200): one thread per output, the K-length dot from
+// L1-cached operands.  The tiled kernel would launch only ceil(M / 64) CTAs.
+__global__ void __launch_bounds__(256) redistribute_small_kernel(const double* __restrict__ A,
+                                                                 const double* __restrict__ B, double* __restrict__ C,
+                                                                 const double* __restrict__ gamma,
+                                                                 const double* __restrict__ coeffs, int64_t M, int N,
+                                                                 int K, int n_mom, int epi, int ld, int ldc,
+                                                                 const double* __restrict__ U, int ldu) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= M * N) return;
+    const int64_t r = t / N;
+    const int c = static_cast<int>(t - r * N);
+    const double* a = A + r * ld;
+    double acc0 = 0.0, acc1 = 0.0;
+    int g = 0;
+    for (; g + 2 <= K; g += 2) {
+        acc0 = fma(__ldg(a + g), __ldg(B + static_cast<int64_t>(g) * ld + c), acc0);
+        acc1 = fma(__ldg(a + g + 1), __ldg(B + static_cast<int64_t>(g + 1) * ld + c), acc1);
+    }
+    if (g < K) acc0 = fma(__ldg(a + g), __ldg(B + static_cast<int64_t>(g) * ld + c), acc0);
+    const double acc = acc0 + acc1;
+    const int64_t i = r / n_mom;
+    C[r * ldc + c] = epilogue(epi, acc, coeffs[r - i * n_mom], gamma, i * N + c, U, r * ldu + c);
+}
+
 // ---- K2b on the FP64 tensor pipe: mma.sync m8n8k4 f64 (DMMA) -------------------
 // tcgen05 has no f64 kind on sm_100a, so FP64 tensor work is the warp-level
 // DMMA path.  CTA tile 64 (rows c) x 128 (cols f), K staged 16 at a time in a
@@ -392,6 +417,13 @@ int launch_redistribute_ex(const Problem& p, const double* A, double* C, int ldc
         dmma::redistribute_dmma_kernel<2><<<grid, dmma::THREADS, dmma::kSmem, s>>>(
             A, p.rwt, C, gamma, p.coeffs, M, p.n_freq, p.n_freq, p.n_mom, epi, p.fp, ldc, U, ldu);
         RTK_LAUNCH_CHECK("redistribute_dmma_kernel");
+        return RTK_OK;
+    }
+    if (M * p.n_freq <= (int64_t(1) << 18)) {
+        const unsigned blocks = static_cast<unsigned>((M * p.n_freq + 255) / 256);
+        redistribute_small_kernel<<<blocks, 256, 0, s>>>(A, p.rwt, C, gamma, p.coeffs, M, p.n_freq, p.n_freq,
+                                                         p.n_mom, epi, p.fp, ldc, U, ldu);
+        RTK_LAUNCH_CHECK("redistribute_small_kernel");
         return RTK_OK;
     }
     dim3 grid(static_cast<unsigned>((M + BM - 1) / BM), (p.n_freq + BN - 1) / BN);
