@@ -145,14 +145,11 @@ __global__ void __launch_bounds__(256) redistribute_small_kernel(const double* _
     const int64_t r = t / N;
     const int c = static_cast<int>(t - r * N);
     const double* a = A + r * ld;
-    double acc0 = 0.0, acc1 = 0.0;
-    int g = 0;
-    for (; g + 2 <= K; g += 2) {
-        acc0 = fma(__ldg(a + g), __ldg(B + static_cast<int64_t>(g) * ld + c), acc0);
-        acc1 = fma(__ldg(a + g + 1), __ldg(B + static_cast<int64_t>(g + 1) * ld + c), acc1);
-    }
-    if (g < K) acc0 = fma(__ldg(a + g), __ldg(B + static_cast<int64_t>(g) * ld + c), acc0);
-    const double acc = acc0 + acc1;
+    // one accumulator in ascending g: the tiled kernel's summation order, so results are identical
+    // (restarted GMRES on the slow CRD cases is sensitive to the last bit)
+    double acc = 0.0;
+#pragma unroll 4
+    for (int g = 0; g < K; ++g) acc = fma(__ldg(a + g), __ldg(B + static_cast<int64_t>(g) * ld + c), acc);
     const int64_t i = r / n_mom;
     C[r * ldc + c] = epilogue(epi, acc, coeffs[r - i * n_mom], gamma, i * N + c, U, r * ldu + c);
 }
