@@ -524,6 +524,26 @@ struct History {
     }
 };
 
+// One restart cycle of Arnoldi (matvec, CGS2, next basis vector, column read-back) captured
+// as a CUDA graph and replayed every cycle: a cycle's pointers never change (fixed basis
+// slab, w, per-iteration column slots), and for small problems the launch overhead of the
+// ~10 kernels per iteration dominates the GPU work (cfg1: 65 us per iteration).
+struct CycleGraph {
+    cudaStream_t gs = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<cudaEvent_t> evs;     // evs[j]: column j is in its pinned slot
+    cudaEvent_t start = nullptr, done = nullptr;
+    bool ready = false, failed = false;
+    int64_t launches = 0;             // kernels per replay (counted during the capture)
+    ~CycleGraph() {
+        if (exec) cudaGraphExecDestroy(exec);
+        for (auto e : evs) cudaEventDestroy(e);
+        if (start) cudaEventDestroy(start);
+        if (done) cudaEventDestroy(done);
+        if (gs) cudaStreamDestroy(gs);
+    }
+};
+
 int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, double* x, const rtk_solve_cfg* cfg,
                rtk_solve_report* rep, double* hist_out, int hist_cap, cudaStream_t s) {
     if (!cfg || !rep || !b || !x) return set_error(RTK_EINVAL, "null argument");
@@ -570,6 +590,13 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
     const int cycle = cfg->restart > 0 ? cfg->restart : cfg->max_iter;
     Basis V(s);
     std::vector<double> col, y;
+    // graph replay of whole cycles: the library's own matvec only (a user callback may
+    // synchronise), restarted GMRES with short cycles, small vectors (launch-bound regime)
+    // (capturing + instantiating costs ~1 ms, so only solves allowed several cycles use it)
+    const bool graph_ok = apply == rtk_problem_matvec && cfg->restart > 0 && cycle <= 64 && n <= (int64_t(1) << 23) &&
+                          cfg->max_iter >= 3 * cycle && !getenv_flag("RTK_GMRES_NO_GRAPH");
+    CycleGraph G;
+    const int slot_max = 2 * (cycle + 1) + 1;
     auto finish = [&](int iters, bool conv, bool brk, double tr) {
         rep->iterations = iters;
         rep->converged = conv ? 1 : 0;
@@ -598,14 +625,62 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
         // on the device), so the GPU never idles on the per-iteration column read-back.  Work
         // enqueued past a stopping iteration is discarded; results are those of the
         // sequential loop (same kernels, same operands, same order).
-        const int slot_sz = 2 * (steps + 1) + 1;
-        if ((rc = E.wsp_->reserve_look(kLookahead * slot_sz))) return rc;
+        const bool use_graph = graph_ok && !G.failed && steps == cycle;
+        // slots: graph mode keeps one per iteration of the cycle (fixed size, captured pointers)
+        const int slot_sz = use_graph ? slot_max : 2 * (steps + 1) + 1;
+        if ((rc = E.wsp_->reserve_look(std::max(kLookahead, graph_ok ? cycle : 0) * slot_max))) return rc;
         double* dslots = E.wsp_->look_dev;
         double* pslots = E.wsp_->look_pin;
         int next = 0;
+        if (use_graph && !G.ready) {
+            if ((rc = V.ensure(cycle + 1, n, hint))) return rc;
+            RTK_CUDA_TRY(cudaStreamCreateWithFlags(&G.gs, cudaStreamNonBlocking));
+            RTK_CUDA_TRY(cudaEventCreateWithFlags(&G.start, cudaEventDisableTiming));
+            RTK_CUDA_TRY(cudaEventCreateWithFlags(&G.done, cudaEventDisableTiming));
+            G.evs.resize(cycle, nullptr);
+            for (auto& e : G.evs) RTK_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            // the first matvec of a problem may configure kernels (attributes, occupancy queries):
+            // do it outside the capture, on scratch
+            RTK_CUDA_TRY(cudaStreamSynchronize(s));
+            if ((rc = apply(ctx, V.v[0], cand.p, n, G.gs))) return rc;
+            RTK_CUDA_TRY(cudaStreamSynchronize(G.gs));
+            Engine Eg(G.gs);
+            if ((rc = Eg.init())) return rc;
+            cudaGraph_t graph = nullptr;
+            const int64_t l0 = rtk_kernel_launch_count();
+            bool ok = cudaStreamBeginCapture(G.gs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+            for (int jj = 0; ok && jj < cycle; ++jj) {
+                double* dslot = dslots + static_cast<size_t>(jj) * slot_max;
+                ok = apply(ctx, V.v[jj], w.p, n, G.gs) == RTK_OK &&
+                     Eg.cgs2_enqueue(V.v, jj + 1, w.p, n, dslot) == RTK_OK &&
+                     Eg.scale_dev(w.p, V.v[jj + 1], n, dslot + 2 * (jj + 1)) == RTK_OK &&
+                     cudaMemcpyAsync(pslots + static_cast<size_t>(jj) * slot_max, dslot,
+                                     sizeof(double) * (2 * (jj + 1) + 1), cudaMemcpyDeviceToHost, G.gs) == cudaSuccess &&
+                     cudaEventRecordWithFlags(G.evs[jj], G.gs, cudaEventRecordExternal) == cudaSuccess;
+            }
+            const cudaError_t ec = cudaStreamEndCapture(G.gs, &graph);
+            ok = ok && ec == cudaSuccess && graph != nullptr &&
+                 cudaGraphInstantiate(&G.exec, graph, 0) == cudaSuccess;
+            if (graph) cudaGraphDestroy(graph);
+            cudaGetLastError();
+            G.launches = rtk_kernel_launch_count() - l0;
+            count_launch(static_cast<int>(-G.launches));   // captured, not launched
+            G.ready = ok;
+            G.failed = !ok;
+        }
+        const bool graph_cycle = use_graph && G.ready;
+        if (graph_cycle) {
+            RTK_CUDA_TRY(cudaEventRecord(G.start, s));
+            RTK_CUDA_TRY(cudaStreamWaitEvent(G.gs, G.start, 0));
+            RTK_CUDA_TRY(cudaGraphLaunch(G.exec, G.gs));
+            RTK_CUDA_TRY(cudaEventRecord(G.done, G.gs));
+            RTK_CUDA_TRY(cudaStreamWaitEvent(s, G.done, 0));   // later work on s sees the whole cycle
+            count_launch(static_cast<int>(G.launches));
+            next = steps;
+        }
         int j = 0;
         while (j < steps) {
-            while (next < steps && next - j < kLookahead) {
+            while (!graph_cycle && next < steps && next - j < kLookahead) {
                 const int q = next % kLookahead;
                 double* dslot = dslots + static_cast<size_t>(q) * slot_sz;
                 if ((rc = A(V.v[next], w.p))) return rc;
@@ -618,8 +693,9 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
                 ++next;
             }
             {
-                const int q = j % kLookahead;
-                RTK_CUDA_TRY(cudaEventSynchronize(look_ev[q]));
+                const int q = graph_cycle ? j : j % kLookahead;
+                RTK_CUDA_TRY(cudaEventSynchronize(graph_cycle ? G.evs[j] : look_ev[q]));
+                if (graph_cycle) ++matvecs;   // the replayed matvec of iteration j is consumed
                 const double* hs = pslots + static_cast<size_t>(q) * slot_sz;
                 col.assign(j + 2, 0.0);
                 for (int i = 0; i <= j; ++i) col[i] = hs[i] + hs[j + 1 + i];
@@ -646,7 +722,7 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
             const double rel = std::fabs(g[j]) / b_norm;
             hist.push(rel);
             if (rel <= tol || breakdown) {   // R/krylov.py:129-147
-                spec_matvecs = next - j;     // look-ahead iterations not (yet) consumed
+                spec_matvecs = graph_cycle ? 0 : next - j;   // look-ahead iterations not (yet) consumed
                 solve_upper(h_cols, g, j, y);
                 if ((rc = E.combine(V.v, y, x, cand.p, n))) return rc;
                 if ((rc = A(cand.p, w.p))) return rc;
