@@ -200,9 +200,19 @@ __global__ void __launch_bounds__(kRedThreads) cgs_pass_kernel(PassArgs P) {
     if (is_last) {
         __threadfence();
         if (threadIdx.x < nk) {
+            // L2 loads (.cg: past the non-coherent L1) issued ahead of the in-order sum
             double s = 0.0;
-            const volatile double* pp = P.partials + threadIdx.x * kMaxRedBlocks;
-            for (unsigned b = 0; b < gridDim.x; ++b) s += pp[b];
+            const double* pp = P.partials + threadIdx.x * kMaxRedBlocks;
+            const unsigned nb = gridDim.x;
+            unsigned b = 0;
+            for (; b + 8 <= nb; b += 8) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = __ldcg(pp + b + u);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) s += v[u];
+            }
+            for (; b < nb; ++b) s += __ldcg(pp + b);
             P.out[threadIdx.x] = s;
         }
         if (threadIdx.x == 0) *P.counter = 0u;

@@ -132,26 +132,40 @@ __global__ void __launch_bounds__(kGemmThreads) redistribute_kernel(const double
     }
 }
 
-// Few rows (cfg1-sized problems: M = 200): one thread per output, the K-length dot from
-// L1-cached operands.  The tiled kernel would launch only ceil(M / 64) CTAs.
+// Few rows (cfg1-sized problems: M = 200): a block stages the whole K x N B operand and its
+// rows of A in shared memory with one round of coalesced loads, then each thread forms one
+// output from shared memory.  (The tiled kernel would launch ceil(M / 64) CTAs.)
+constexpr int kSmallRows = 8;
 __global__ void __launch_bounds__(256) redistribute_small_kernel(const double* __restrict__ A,
                                                                  const double* __restrict__ B, double* __restrict__ C,
                                                                  const double* __restrict__ gamma,
                                                                  const double* __restrict__ coeffs, int64_t M, int N,
                                                                  int K, int n_mom, int epi, int ld, int ldc,
                                                                  const double* __restrict__ U, int ldu) {
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= M * N) return;
-    const int64_t r = t / N;
-    const int c = static_cast<int>(t - r * N);
-    const double* a = A + r * ld;
-    // one accumulator in ascending g: the tiled kernel's summation order, so results are identical
-    // (restarted GMRES on the slow CRD cases is sensitive to the last bit)
-    double acc = 0.0;
-#pragma unroll 4
-    for (int g = 0; g < K; ++g) acc = fma(__ldg(a + g), __ldg(B + static_cast<int64_t>(g) * ld + c), acc);
-    const int64_t i = r / n_mom;
-    C[r * ldc + c] = epilogue(epi, acc, coeffs[r - i * n_mom], gamma, i * N + c, U, r * ldu + c);
+    extern __shared__ double sm_small[];
+    double* Bs = sm_small;                 // [K][N]
+    double* As = sm_small + K * N;         // [kSmallRows][K]
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kSmallRows;
+    const int rows = static_cast<int>(M - r0 < kSmallRows ? M - r0 : kSmallRows);
+    for (int t = threadIdx.x; t < K * N; t += blockDim.x) {
+        const int g = t / N, c = t - g * N;
+        Bs[t] = __ldg(B + static_cast<int64_t>(g) * ld + c);
+    }
+    for (int t = threadIdx.x; t < rows * K; t += blockDim.x) {
+        const int rr = t / K, g = t - rr * K;
+        As[t] = __ldg(A + (r0 + rr) * ld + g);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < rows * N; t += blockDim.x) {
+        const int rr = t / N, c = t - rr * N;
+        // one accumulator in ascending g: the tiled kernel's summation order, so results are
+        // identical (restarted GMRES on the slow CRD cases is sensitive to the last bit)
+        double acc = 0.0;
+        for (int g = 0; g < K; ++g) acc = fma(As[rr * K + g], Bs[g * N + c], acc);
+        const int64_t r = r0 + rr;
+        const int64_t i = r / n_mom;
+        C[r * ldc + c] = epilogue(epi, acc, coeffs[r - i * n_mom], gamma, i * N + c, U, r * ldu + c);
+    }
 }
 
 // ---- K2b on the FP64 tensor pipe: mma.sync m8n8k4 f64 (DMMA) -------------------
@@ -417,9 +431,10 @@ int launch_redistribute_ex(const Problem& p, const double* A, double* C, int ldc
         return RTK_OK;
     }
     if (M * p.n_freq <= (int64_t(1) << 18)) {
-        const unsigned blocks = static_cast<unsigned>((M * p.n_freq + 255) / 256);
-        redistribute_small_kernel<<<blocks, 256, 0, s>>>(A, p.rwt, C, gamma, p.coeffs, M, p.n_freq, p.n_freq,
-                                                         p.n_mom, epi, p.fp, ldc, U, ldu);
+        const unsigned blocks = static_cast<unsigned>((M + kSmallRows - 1) / kSmallRows);
+        const size_t smem = sizeof(double) * (static_cast<size_t>(p.n_freq) * p.n_freq + kSmallRows * p.n_freq);
+        redistribute_small_kernel<<<blocks, 256, smem, s>>>(A, p.rwt, C, gamma, p.coeffs, M, p.n_freq, p.n_freq,
+                                                            p.n_mom, epi, p.fp, ldc, U, ldu);
         RTK_LAUNCH_CHECK("redistribute_small_kernel");
         return RTK_OK;
     }
