@@ -558,7 +558,7 @@ def krylov_cfg2(torch, problem, matvec_ms, hbm):
 def formal_solver_timings(torch, lib, hbm):
     """cfg2 matvec with the exponential integrators (the north star's formal solver; the
     headline uses the reference's implicit Euler): matvec rate and the sweep's HBM fraction."""
-    from paper_2602_21958_b200 import configs
+    from paper_2602_21958_b200 import _device, _native, configs
 
     out = {}
     for fs in ("exp_linear", "exp_parabolic"):
