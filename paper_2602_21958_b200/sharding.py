@@ -115,3 +115,94 @@ class ShardedOperator:
         m = self.ops.partial_moments(x_local)
         m = self._all_reduce(m)
         return self.ops.apply_with_moments(x_local, m)
+
+
+def sharded_gmres(op: ShardedOperator, b_local, rel_tol: float = 1e-12, max_iter: int = 1000, restart: int = None):
+    """GMRES on direction-sharded vectors (R/krylov.py:56-158 control flow: x0 = 0, Givens least
+    squares, restart, breakdown below 1e-14 ||b||, 10 rel_tol true-residual guard).  Every rank
+    holds its slice of the Krylov vectors; the dots are local products plus one all-reduce, so
+    all ranks see the same scalars and take the same decisions.  Arnoldi is CGS2 (as the native
+    solver).  Returns (x_local, iterations, converged, residual history, true residual)."""
+    import torch
+
+    def gdot(u, v):
+        t = torch.dot(u, v).reshape(1)
+        return float(op._all_reduce(t)[0])
+
+    def gnorm(u):
+        return gdot(u, u) ** 0.5
+
+    b = b_local
+    b_norm = gnorm(b)
+    hist = []
+    if b_norm == 0.0:
+        return torch.zeros_like(b), 0, True, [0.0], 0.0
+    x = torch.zeros_like(b)
+    r = b.clone()
+    total = 0
+    cycle = restart if restart is not None else max_iter
+    while total < max_iter:
+        beta = gnorm(r)
+        if beta / b_norm <= rel_tol:
+            hist.append(beta / b_norm)
+            return x, max(total, 1), True, hist, beta / b_norm
+        V = [r / beta]
+        h_cols, cs, sn, g = [], [], [], [beta]
+        breakdown = False
+        steps = min(cycle, max_iter - total)
+        j = 0
+        while j < steps:
+            w = op(V[j])
+            Vm = torch.stack(V)                                        # (j+1, n_local)
+            h1 = op._all_reduce(Vm @ w)
+            w = w - Vm.t() @ h1
+            h2 = op._all_reduce(Vm @ w)
+            w = w - Vm.t() @ h2
+            col = (h1 + h2).tolist()
+            col.append(gnorm(w))
+            breakdown = col[j + 1] < 1e-14 * b_norm
+            if not breakdown:
+                V.append(w / col[j + 1])
+            for i in range(j):
+                tmp = cs[i] * col[i] + sn[i] * col[i + 1]
+                col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1]
+                col[i] = tmp
+            denom = (col[j] ** 2 + col[j + 1] ** 2) ** 0.5
+            cj = col[j] / denom if denom else 1.0
+            sj = col[j + 1] / denom if denom else 0.0
+            cs.append(cj)
+            sn.append(sj)
+            col[j] = denom
+            h_cols.append(col[: j + 1])
+            g.append(-sj * g[j])
+            g[j] = cj * g[j]
+            total += 1
+            j += 1
+            rel = abs(g[j]) / b_norm
+            hist.append(rel)
+            if rel <= rel_tol or breakdown:
+                y = _solve_upper(h_cols, g[:j])
+                cand = x + sum(yi * vi for yi, vi in zip(y, V))
+                true_rel = gnorm(b - op(cand)) / b_norm
+                if true_rel <= 10.0 * rel_tol:
+                    if breakdown:
+                        hist[-1] = true_rel
+                    return cand, total, True, hist, true_rel
+                if breakdown:
+                    return cand, total, False, hist, true_rel
+        y = _solve_upper(h_cols, g[:j])
+        x = x + sum(yi * vi for yi, vi in zip(y, V))
+        r = b - op(x)
+    return x, total, False, hist, gnorm(r) / b_norm
+
+
+def _solve_upper(h_cols, g):
+    """Back substitution on the rotated Hessenberg columns (R/krylov.py:161-170)."""
+    m = len(g)
+    y = [0.0] * m
+    for i in range(m - 1, -1, -1):
+        s = g[i]
+        for k in range(i + 1, m):
+            s -= h_cols[k][i] * y[k]
+        y[i] = s / h_cols[i][i]
+    return y
