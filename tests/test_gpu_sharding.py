@@ -34,3 +34,18 @@ def test_sharded_matvec_equals_full_operator(world, shape):
     assert rel_l2(y.cpu().numpy(), full.cpu().numpy()) <= 1e-12
     if ns <= 300:
         assert rel_l2(y.cpu().numpy(), ro.apply_A(ro.desc_from_problem(p), x.cpu().numpy())) <= 1e-11
+
+
+def test_sharded_gmres_single_rank_matches_native_gmres():
+    """sharded_gmres with the native device halves (one rank, identity all-reduce) reproduces the
+    native GMRES: iterations +-1, history prefix, solution 1e-7."""
+    from paper_2602_21958_b200.sharding import sharded_gmres
+
+    p = configs.slab_problem(1)
+    op = ShardedOperator(p, rank=0, world=1, all_reduce=lambda t: t)
+    b = P.build_rhs(p, device=True)
+    x, its, conv, hist, _ = sharded_gmres(op, b, rel_tol=1e-8, max_iter=300)
+    rep = P.gmres(p, b, P.SolveConfig(rel_tol=1e-8, max_iter=300))
+    assert conv and rep.converged and abs(its - rep.iterations) <= 1
+    np.testing.assert_allclose(hist[:30], rep.residual_history[:30], rtol=1e-9)
+    assert rel_l2(x.cpu().numpy(), rep.solution.cpu().numpy()) <= 1e-7
