@@ -101,6 +101,7 @@ struct LatArgs {
     const double* inflow_bottom;
     int nx, ny, nz, n_dirs, n_freq, n_mom;
     int64_t nxy;
+    int total_sub;            // sum over directions of (n_sub + 1): one step's sub-node shifts
 };
 
 enum LatSrc { LSRC_VEC = 0, LSRC_ISO = 1, LSRC_U = 2 };
@@ -484,6 +485,12 @@ __global__ void lattice_dtab_kernel(const LatDir* __restrict__ dirs, const Shift
 // thread = (line c, frequency group q of F): f = F q .. F q + F - 1 (the tail may be padding).
 // Directions are processed hemisphere by hemisphere so only NM x F moment accumulators
 // are live; layer t gets the down part, layer nz-1-t the up part.
+struct StepDir {
+    int down, n_sub, sub_pref;
+    long long dtab;        // this step's first dt-table entry of the direction
+    double wy[8];
+};
+
 template <int FS, int NM, int F>
 __global__ void __launch_bounds__(128, 5) lattice_mom_group_kernel(LatArgs A, int t, const double* __restrict__ st_in,
                                                                  double* __restrict__ st_out, double* __restrict__ mom,
@@ -492,6 +499,38 @@ __global__ void __launch_bounds__(128, 5) lattice_mom_group_kernel(LatArgs A, in
                                                                  const double* __restrict__ plane_next) {
     const int ng = (fp + F - 1) / F;       // groups per line
     const int hp = fp >> 1;                // double2 per line in the [dir][line][fp] planes
+    // this step's direction metadata and shifts, staged once per CTA in shared memory (the
+    // per-direction / per-sub-node lookups are warp-uniform and sat on the load-latency chain)
+    extern __shared__ double mo_s[];       // [NM][F][blockDim] accumulators, then the tables
+    StepDir* sdir = reinterpret_cast<StepDir*>(mo_s + NM * F * blockDim.x);
+    Shift* sgat = reinterpret_cast<Shift*>(sdir + A.n_dirs);
+    Shift* ssub = sgat + A.n_dirs;
+    for (int a = threadIdx.x; a < A.n_dirs; a += blockDim.x) {
+        const LatDir& D = A.dirs[a];
+        StepDir sd;
+        sd.down = D.down;
+        sd.n_sub = D.n_sub;
+        sd.sub_pref = D.sub_pref;
+        sd.dtab = D.dtab_off + static_cast<int64_t>(t) * D.n_sub * A.nxy;
+#pragma unroll
+        for (int l = 0; l < NM; ++l) sd.wy[l] = D.wy[l];
+        sdir[a] = sd;
+        sgat[a] = A.gat_shift[a * A.nz + t];
+    }
+    if (t < A.nz - 1) {
+        for (int e = threadIdx.x; e < A.total_sub; e += blockDim.x) {
+            // entry e belongs to the direction whose prefix range holds it
+            int lo = 0, hi = A.n_dirs - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (A.dirs[mid].sub_pref <= e) lo = mid;
+                else hi = mid - 1;
+            }
+            const LatDir& D = A.dirs[lo];
+            ssub[e] = A.sub_shift[D.shift_off + t * (D.n_sub + 1) + (e - D.sub_pref)];
+        }
+    }
+    __syncthreads();
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (tid >= A.nxy * ng) return;
     const int c = static_cast<int>(tid / ng);
@@ -520,14 +559,13 @@ __global__ void __launch_bounds__(128, 5) lattice_mom_group_kernel(LatArgs A, in
         const int k = hemi == 0 ? t : A.nz - 1 - t;
         // moment accumulators live in shared memory ([l][q][thread], conflict-free) to keep
         // registers for the loads in flight (occupancy)
-        extern __shared__ double mo_s[];
         auto mo = [&](int l, int q) -> double& { return mo_s[(l * F + q) * blockDim.x + threadIdx.x]; };
 #pragma unroll
         for (int l = 0; l < NM; ++l)
 #pragma unroll
             for (int q = 0; q < F; ++q) mo(l, q) = 0.0;
         for (int a = 0; a < A.n_dirs; ++a) {
-            const LatDir& D = A.dirs[a];
+            const StepDir& D = sdir[a];
             if ((D.down != 0) != (hemi == 0)) continue;
             const double2* sa = sin2 + a * plane2 + g2;
             double v[F];
@@ -535,7 +573,7 @@ __global__ void __launch_bounds__(128, 5) lattice_mom_group_kernel(LatArgs A, in
 #pragma unroll
                 for (int q = 0; q < F; ++q) v[q] = hemi == 0 ? in_top[q] : in_bot[q];
             } else {
-                const Stencil st = stencil_at(i, j, A.gat_shift[a * A.nz + t], A.nx, A.ny);
+                const Stencil st = stencil_at(i, j, sgat[a], A.nx, A.ny);
 #pragma unroll
                 for (int h = 0; h < F / 2; ++h) {
                     if (!full_group && g2 + h >= hp) {
@@ -567,13 +605,12 @@ __global__ void __launch_bounds__(128, 5) lattice_mom_group_kernel(LatArgs A, in
                     acc[2 * h] = s2.x;
                     acc[2 * h + 1] = s2.y;
                 }
-                const LatDir Dl = D;
+                LatDir Dl;
+                Dl.n_sub = D.n_sub;
                 if (full_group) {
-                    advance_lineF<FS, F, true>(Dl, A.sub_shift + Dl.shift_off + t * (Dl.n_sub + 1), acc, i, j, t,
-                                               A.nx, A.ny, nullptr, nullptr, pc2 + a * plane2 + g2,
-                                               pn2 + a * plane2 + g2, hp, phi,
-                                               A.dtab + Dl.dtab_off + static_cast<int64_t>(t) * Dl.n_sub * A.nxy + c,
-                                               A.nxy);
+                    advance_lineF<FS, F, true>(Dl, ssub + D.sub_pref, acc, i, j, t, A.nx, A.ny, nullptr, nullptr,
+                                               pc2 + a * plane2 + g2, pn2 + a * plane2 + g2, hp, phi,
+                                               A.dtab + D.dtab + c, A.nxy);
 #pragma unroll
                     for (int h = 0; h < F / 2; ++h)
                         sout2[a * plane2 + static_cast<int64_t>(c) * hp + g2 + h] = make_double2(acc[2 * h], acc[2 * h + 1]);
@@ -582,11 +619,9 @@ __global__ void __launch_bounds__(128, 5) lattice_mom_group_kernel(LatArgs A, in
                     for (int h = 0; h < F / 2 && g2 + h < hp; ++h) {
                         double ap[2] = {acc[2 * h], acc[2 * h + 1]};
                         const double pp[2] = {phi[2 * h], phi[2 * h + 1]};
-                        advance_lineF<FS, 2, true>(Dl, A.sub_shift + Dl.shift_off + t * (Dl.n_sub + 1), ap, i, j, t,
-                                                   A.nx, A.ny, nullptr, nullptr, pc2 + a * plane2 + g2 + h,
-                                                   pn2 + a * plane2 + g2 + h, hp, pp,
-                                                   A.dtab + Dl.dtab_off + static_cast<int64_t>(t) * Dl.n_sub * A.nxy + c,
-                                                   A.nxy);
+                        advance_lineF<FS, 2, true>(Dl, ssub + D.sub_pref, ap, i, j, t, A.nx, A.ny, nullptr, nullptr,
+                                                   pc2 + a * plane2 + g2 + h, pn2 + a * plane2 + g2 + h, hp, pp,
+                                                   A.dtab + D.dtab + c, A.nxy);
                         sout2[a * plane2 + static_cast<int64_t>(c) * hp + g2 + h] = make_double2(ap[0], ap[1]);
                     }
                 }
@@ -687,6 +722,12 @@ int setup_lattice(Problem& p, const rtk_lattice_desc* d) {
     }
     // warp-uniform interpolation shifts, tabulated once (same arithmetic as the device's shift_of)
     std::vector<Shift> sub, gat(static_cast<size_t>(d->n_dirs) * d->nz);
+    p.lat_total_sub = 0;
+    for (int a = 0; a < d->n_dirs; ++a) {
+        LatDir& D = dirs[a];
+        D.sub_pref = p.lat_total_sub;
+        p.lat_total_sub += D.n_sub + 1;
+    }
     for (int a = 0; a < d->n_dirs; ++a) {
         LatDir& D = dirs[a];
         D.shift_off = static_cast<int>(sub.size());
@@ -738,6 +779,7 @@ static LatArgs lat_args(const Problem& p, const double* src, const double* x, do
     A.sub_shift = reinterpret_cast<const Shift*>(p.lat_sub_shift);
     A.gat_shift = reinterpret_cast<const Shift*>(p.lat_gat_shift);
     A.dtab = p.lat_dtab;
+    A.total_sub = p.lat_total_sub;
     A.chi = p.lat_chi;
     A.phi = p.phi;
     A.src = src;
@@ -811,6 +853,11 @@ static int launch_mom_steps(const Problem& p, const LatArgs& A, bool with_inflow
     // 128-thread blocks: a layer step has only nxy * fp / F threads (cfg4: 65,536), so small
     // blocks spread them evenly over the SMs (256-thread blocks left 40 SMs half occupied)
     const int mb = getenv("RTK_LAT_BLOCK") ? atoi(getenv("RTK_LAT_BLOCK")) : 128;
+    const size_t mom_smem = sizeof(double) * NM * F * mb + sizeof(StepDir) * A.n_dirs +
+                            sizeof(Shift) * (A.n_dirs + A.total_sub);
+    if (mom_smem > 48 * 1024)
+        RTK_CUDA_TRY(cudaFuncSetAttribute(lattice_mom_group_kernel<FS, NM, F>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(mom_smem)));
     const unsigned sblocks = static_cast<unsigned>((A.nxy * ((p.fp + F - 1) / F) + mb - 1) / mb);
     double* a = p.lat_state[0];
     double* b = p.lat_state[1];
@@ -821,7 +868,7 @@ static int launch_mom_steps(const Problem& p, const LatArgs& A, bool with_inflow
             lattice_splane_kernel<SRC, NM><<<pblocks, 256, 0, s>>>(A, t, cur, nxt, t == 0 ? 1 : 0, p.fp);
             RTK_LAUNCH_CHECK("lattice_splane_kernel");
         }
-        lattice_mom_group_kernel<FS, NM, F><<<sblocks, mb, sizeof(double) * NM * F * mb, s>>>(
+        lattice_mom_group_kernel<FS, NM, F><<<sblocks, mb, mom_smem, s>>>(
             A, t, a, b, mom, with_inflow ? 1 : 0, p.fp, cur, nxt);
         RTK_LAUNCH_CHECK("lattice_mom_group_kernel");
         double* tmp = a;

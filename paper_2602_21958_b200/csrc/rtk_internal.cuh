@@ -58,6 +58,7 @@ struct LatDir {
     int n_sub;        // sub-segments per layer step
     int shift_off;    // first entry of this direction in the sub-node shift table
     long long dtab_off;   // first entry of this direction in the dt table (moment layout)
+    int sub_pref;     // sum of (n_sub + 1) over the preceding directions (one step's shift block)
     double sx, sy;    // horizontal cells moved per layer step
     double sub_len;   // path length of one sub-segment
     double wy[8];     // w_a Y_l(a)   (moment accumulation)
@@ -109,6 +110,7 @@ struct Problem {
     void* lat_gat_shift = nullptr;               // Shift table, T_RC gathers
     double* lat_dtab = nullptr;                  // [dir][t][m][line] sub-segment optical paths
     int lat_max_sub = 0;                         // largest sub-segment count over the directions
+    int lat_total_sub = 0;                       // sum over directions of (n_sub + 1)
     // overlap of the HBM-bound moment reduction with the FP64 redistribution GEMM (slab apply_A)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chunk[8] = {};
