@@ -151,6 +151,117 @@ __device__ __forceinline__ ExpPar exp_parabolic_weights_fast(double du, double d
     return w;
 }
 
+// Branch-free exponential moments for the weight warps of the ring sweep
+// (sweep_tma.cu).  With d ln2-range-reduced, d = k ln2 + r, |r| <= ln2/2, and z = -r:
+//   V(z) = sum_{m>=0} z^m / (m+3)!   (degree 11: truncation < 3e-18 relative on |z| <= 0.347)
+//   T(z) = (e^z - 1 - z) / z^2 = 1/2 + z V(z),   e^z - 1 = z + z^2 T(z)
+// k = 0 (d < ln2/2): e0 = d - d^2 T, e1 = d^2 T, e2 = 2 d^3 V  (no cancellation: these are
+//                    the series of e_k, as the d < 0.05 branch of the reference formulas);
+// k > 0:             att = 2^-k e^-r, e0 = 1 - att, e1 = d - e0, e2 = d^2 - 2 e1 (the closed forms).
+// Both paths are evaluated and selected, so a warp never diverges: every lane costs the
+// same ~30 FP64 instructions and the compiler can interleave several weights per thread.
+// Agrees with exp_linear_weights / exp_parabolic_weights to a few ulp (the parity tests
+// bound the matvec at 1e-11 against the oracle's formulas).
+struct ExpMom {
+    double att, e0, e1, e2, t;   // t = e1 / d^2 on the k = 0 path
+    bool small;
+};
+
+template <bool E2>
+__device__ __forceinline__ ExpMom exp_moments_bf(double d) {
+    const double dc = fmin(d, 708.0);
+    // k = rint(dc log2 e) by the 1.5 * 2^52 shifter (k is the low word of kb), no FRND / F2I
+    const double kb = fma(dc, 1.4426950408889634, 6755399441055744.0);
+    const double kf = kb - 6755399441055744.0;
+    const int k = __double2loint(kb);
+    double r = fma(kf, -6.93147180369123816490e-01, dc);
+    r = fma(kf, -1.90821492927058770002e-10, r);
+    const double z = -r;
+    double v = 1.0 / 87178291200.0;   // 1/14!
+    v = fma(v, z, 1.0 / 6227020800.0);
+    v = fma(v, z, 1.0 / 479001600.0);
+    v = fma(v, z, 1.0 / 39916800.0);
+    v = fma(v, z, 1.0 / 3628800.0);
+    v = fma(v, z, 1.0 / 362880.0);
+    v = fma(v, z, 1.0 / 40320.0);
+    v = fma(v, z, 1.0 / 5040.0);
+    v = fma(v, z, 1.0 / 720.0);
+    v = fma(v, z, 1.0 / 120.0);
+    v = fma(v, z, 1.0 / 24.0);
+    v = fma(v, z, 1.0 / 6.0);
+    const double t = fma(z, v, 0.5);
+    const double z2 = z * z;
+    const double em1 = fma(z2, t, z);
+    // 2^-k (exactly 1 for k = 0, so att = 1 + em1 there); 0 beyond the normal range
+    const double scale = d > 708.0 ? 0.0 : __hiloint2double((1023 - k) << 20, 0);
+    ExpMom m;
+    m.small = k == 0;
+    m.t = t;
+    m.att = scale * (1.0 + em1);
+    m.e0 = m.small ? -em1 : 1.0 - m.att;
+    m.e1 = m.small ? z2 * t : d - m.e0;
+    if (E2) m.e2 = m.small ? 2.0 * (z2 * d) * v : fma(d, d, -2.0 * m.e1);
+    return m;
+}
+
+// rint / F2I variant of exp_moments_bf.  Measured at cfg2 (same arithmetic, different
+// schedule): exp-linear sweep 267 us with this one vs 352 us with the shifter; the
+// exp-parabolic sweep is faster with the shifter (349 vs 357 us).
+template <bool E2>
+__device__ __forceinline__ ExpMom exp_moments_bf_rint(double d) {
+    const double dc = fmin(d, 708.0);
+    const double kf = rint(dc * 1.4426950408889634);
+    double r = fma(kf, -6.93147180369123816490e-01, dc);
+    r = fma(kf, -1.90821492927058770002e-10, r);
+    const double z = -r;
+    double v = 1.0 / 87178291200.0;   // 1/14!
+    v = fma(v, z, 1.0 / 6227020800.0);
+    v = fma(v, z, 1.0 / 479001600.0);
+    v = fma(v, z, 1.0 / 39916800.0);
+    v = fma(v, z, 1.0 / 3628800.0);
+    v = fma(v, z, 1.0 / 362880.0);
+    v = fma(v, z, 1.0 / 40320.0);
+    v = fma(v, z, 1.0 / 5040.0);
+    v = fma(v, z, 1.0 / 720.0);
+    v = fma(v, z, 1.0 / 120.0);
+    v = fma(v, z, 1.0 / 24.0);
+    v = fma(v, z, 1.0 / 6.0);
+    const double t = fma(z, v, 0.5);
+    const double z2 = z * z;
+    const double em1 = fma(z2, t, z);
+    const long long ebits = static_cast<long long>(1023 - static_cast<int>(kf)) << 52;
+    const double att_big = d > 708.0 ? 0.0 : __longlong_as_double(ebits) * (1.0 + em1);
+    ExpMom m;
+    m.small = kf == 0.0;
+    m.t = t;
+    m.att = m.small ? 1.0 + em1 : att_big;
+    m.e0 = m.small ? -em1 : 1.0 - att_big;
+    m.e1 = m.small ? z2 * t : d - m.e0;
+    if (E2) m.e2 = m.small ? 2.0 * (z2 * d) * v : fma(d, d, -2.0 * m.e1);
+    return m;
+}
+
+__device__ __forceinline__ ExpLin exp_linear_weights_bf(double d) {
+    const ExpMom m = exp_moments_bf_rint<false>(d);
+    ExpLin w;
+    w.att = m.att;
+    w.wc = m.small ? d * m.t : m.e1 * rcp_fast(d);
+    w.wu = m.e0 - w.wc;
+    return w;
+}
+
+__device__ __forceinline__ ExpPar exp_parabolic_weights_bf(double du, double dd) {
+    const ExpMom m = exp_moments_bf<true>(du);
+    ExpPar w;
+    w.att = m.att;
+    const double s = du + dd;
+    const double r = rcp_fast(du * dd * s);
+    w.wu = m.e0 + (m.e2 - (dd + 2.0 * du) * m.e1) * (dd * r);
+    w.wc = (s * m.e1 - m.e2) * (s * r);
+    w.wd = (m.e2 - du * m.e1) * (du * r);
+    return w;
+}
+
 // Parabolic (Kunasz-Auer) weights through upwind u, current c, downwind d nodes.
 __device__ __forceinline__ ExpPar exp_parabolic_weights(double du, double dd) {
     ExpPar w;

@@ -126,11 +126,24 @@ struct ConsumerCtx {
 
 // U march steps of one stage.  DOWN: box row u = step uu (ascending i); up: u = U-1-uu.
 // CHECK: first/last stage (node 0 has no segment; rows beyond the slab are skipped).
+// Exponential solvers: the stage's weights are computed first, branch-free
+// (exp_linear_weights_bf), so the U weight evaluations are independent instruction
+// streams the scheduler interleaves; the recursion then runs over them.
 template <int FS, int NM, int U, bool DOWN, bool CHECK>
 __device__ __forceinline__ void consume(const ConsumerCtx<NM>& c, SweepState& st, const double* __restrict__ xs,
                                         const double* __restrict__ gs, const double* __restrict__ dts, int q,
                                         int64_t n, int64_t step) {
     const double* gcol = gs + c.gcol;
+    double w0[U], w1[U], w2[U];
+    if (FS != RTK_FS_IE) {
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) {
+            const ExpLin w = exp_linear_weights_bf(c.phi_f * dts[DOWN ? uu : U - 1 - uu] * c.inv_mu);
+            w0[uu] = w.att;
+            w1[uu] = w.wu;
+            w2[uu] = w.wc;
+        }
+    }
 #pragma unroll
     for (int uu = 0; uu < U; ++uu) {
         const int j = q * U + uu;
@@ -141,13 +154,12 @@ __device__ __forceinline__ void consume(const ConsumerCtx<NM>& c, SweepState& st
 #pragma unroll
         for (int k = 0; k < NM; ++k) sv = fma(c.yk[k], gcol[(u * NM + k) * c.gw], sv);
         if (!CHECK || j > 0) {
-            const double d = c.phi_f * dts[u] * c.inv_mu;
             if (FS == RTK_FS_IE) {
+                const double d = c.phi_f * dts[u] * c.inv_mu;
                 const double r = rcp_nr(1.0 + d);
                 st.acc = fma(st.acc, r, (d * sv) * r);
             } else {
-                const ExpLin w = exp_linear_weights(d);
-                st.acc = fma(st.acc, w.att, w.wu * st.s_prev + w.wc * sv);
+                st.acc = fma(st.acc, w0[uu], w1[uu] * st.s_prev + w2[uu] * sv);
             }
         }
         st.s_prev = sv;
@@ -168,6 +180,19 @@ __device__ __forceinline__ void consume_par(const ConsumerCtx<NM>& c, ParState& 
                                             const double* __restrict__ gs, const double* __restrict__ dts, int q,
                                             int64_t n, int64_t step) {
     const double* gcol = gs + c.gcol;
+    // optical depths of the segments into each step's node, then the stage's weights
+    // (update at step uu uses the segments into nodes j-1 and j)
+    double din[U], w0[U], w1[U], w2[U], w3[U];
+#pragma unroll
+    for (int uu = 0; uu < U; ++uu) din[uu] = c.phi_f * dts[DOWN ? uu : U - 1 - uu] * c.inv_mu;
+#pragma unroll
+    for (int uu = 0; uu < U; ++uu) {
+        const ExpPar w = exp_parabolic_weights_bf(uu == 0 ? st.d_m2 : din[uu - 1], din[uu]);
+        w0[uu] = w.att;
+        w1[uu] = w.wu;
+        w2[uu] = w.wc;
+        w3[uu] = w.wd;
+    }
 #pragma unroll
     for (int uu = 0; uu < U; ++uu) {
         const int j = q * U + uu;
@@ -184,16 +209,14 @@ __device__ __forceinline__ void consume_par(const ConsumerCtx<NM>& c, ParState& 
             st.x_m1 = xv;
             continue;
         }
-        const double d_m1 = c.phi_f * dts[u] * c.inv_mu;   // segment j-1 -> j
         if (!(CHECK && j == 1)) {
-            const ExpPar w = exp_parabolic_weights(st.d_m2, d_m1);
-            st.acc = fma(st.acc, w.att, w.wu * st.s_m2 + w.wc * st.s_m1 + w.wd * sv);
+            st.acc = fma(st.acc, w0[uu], w1[uu] * st.s_m2 + w2[uu] * st.s_m1 + w3[uu] * sv);
             if (c.valid) *st.yp = st.x_m1 - st.acc;
             st.yp += step;
         }
         st.s_m2 = st.s_m1;
         st.s_m1 = sv;
-        st.d_m2 = d_m1;
+        st.d_m2 = din[uu];
         st.x_m1 = xv;
     }
 }
@@ -311,12 +334,14 @@ __global__ void __launch_bounds__(kTmaThreads) sweep1d_tma_kernel(const __grid_c
 }
 
 // ---------------------------------------------------------------------------
-// Exp-linear variant: the exponential weights of a (ray, step) do not depend on the
-// recursion, so 8 extra "weight" warps compute them for the whole stage (U steps x 128
-// rays) into shared memory while the 4 chain warps run the recursion on the previous
-// stage.  The ray count (32,768 = 7 warps per SM at cfg2) otherwise caps the FP64
-// latency hiding of the transcendental path.  Same weights (exp_linear_weights), same
-// recursion order, so results equal the single-pass kernel's.
+// Weight-warp variants (RTK_TMA_W_OLD=1; the default for the exponential solvers is
+// sweep1d_tma_kernel with branch-free weights, see consume()).  8 extra "weight" warps
+// compute the two-branch weights for the whole stage (U steps x 128 rays) into shared
+// memory while the 4 chain warps run the recursion on the previous stage.  Measured at
+// cfg2 (profiles/r01_ncu_sweep_exp.txt): exp-linear 342 us, exp-parabolic 529 us, bound
+// by the L1/shared-memory traffic of the weight hand-off (96 B per element, twice the
+// single-pass kernel's) and by weight warps of unequal cost (the exp branch) gating the
+// chain; the single-pass kernel with branch-free weights takes 267 / 349 us.
 constexpr int kElWeightWarps = 8;
 constexpr int kElThreads = kTmaThreads + 32 * kElWeightWarps;
 
@@ -698,6 +723,7 @@ int launch_tma_us(const Problem& p, const double* x, double* y, cudaStream_t s);
 
 template <int FS, int NM>
 int launch_tma_t(const Problem& p, const double* x, double* y, cudaStream_t s) {
+    if (FS != RTK_FS_IE && p.tma_u == 8 && !getenv_flag("RTK_TMA_W_OLD")) return launch_tma_us<FS, NM, 8, 4>(p, x, y, s);
     if (FS == RTK_FS_EXP_PARABOLIC && p.tma_u == 8 && !getenv_flag("RTK_TMA_EL_SINGLE")) {
         const int rc = launch_tma_ep<NM, 4, 3>(p, x, y, s);
         if (rc != -1) return rc;

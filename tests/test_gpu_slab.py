@@ -148,6 +148,24 @@ def test_cp_async_fallback_sweep_matches_tma_sweep(fs, monkeypatch):
     assert rel_l2(y_gen, y_tma) <= 1e-14
 
 
+@pytest.mark.parametrize("fs", ["exp_linear", "exp_parabolic"])
+@pytest.mark.parametrize("shape", [(2000, 64, 512), (37, 8, 256), (6, 4, 128)])
+def test_branch_free_weight_sweep_matches_weight_warp_sweep(fs, shape, monkeypatch):
+    """The default exponential sweep (branch-free weights inside the TMA sweep) and the
+    weight-warp kernels (RTK_TMA_W_OLD=1, two-branch weights) agree to a few ulp per
+    weight (the two-branch closed form loses up to ~40 ulp in w_c just above its 0.05
+    switch, so the bound is 1e-13), and the default path matches the oracle."""
+    ns, na, nf = shape
+    p = configs.slab_problem(2, formal_solver=fs, n_space=ns, n_angles=na, n_freq=nf)
+    v = np.random.default_rng(ns + 1).standard_normal(p.n_total)
+    y_new = P.apply_A(p, v)
+    monkeypatch.setenv("RTK_TMA_W_OLD", "1")
+    y_old = P.apply_A(p, v)
+    assert rel_l2(y_new, y_old) <= 1e-13
+    if ns < 2000:
+        assert rel_l2(y_new, ro.apply_A(oracle_desc(p), v)) <= MATVEC_TOL
+
+
 @pytest.mark.parametrize("shape", [(37, 6, 5), (64, 12, 130), (50, 4, 257), (9, 2, 1)])
 def test_odd_shapes_match_oracle(shape):
     """Ragged shapes: odd N_nu (TMA pitch padding), N_nu > 128 with a partial tile, mono (N_nu = 1)."""
