@@ -88,6 +88,16 @@ typedef struct rtk_slab_desc {
  * For lattice problems rtk_build_rhs takes thermal as [n_space][n_freq]
  * (isotropic thermal source).
  */
+/* Characteristics of a lattice problem (TRIP chooses by ray inclination):
+ * LONG   lines of the lattice family carry their values through all layers (T_RC to nodes);
+ * SHORT  each layer step restarts at the upwind point of every node (bilinear from the
+ *        previous layer's nodes) and integrates to the node with the same sub-segments;
+ * HYBRID SHORT for steep directions (upwind point in the adjacent cell, n_sub = 1), LONG
+ *        for grazing ones. */
+#define RTK_CHAR_LONG 0
+#define RTK_CHAR_SHORT 1
+#define RTK_CHAR_HYBRID 2
+
 typedef struct rtk_lattice_desc {
     int32_t nx, ny, nz;
     int32_t n_dirs;
@@ -107,6 +117,7 @@ typedef struct rtk_lattice_desc {
     const double* chi;            /* [n_space] frequency-integrated opacity at nodes */
     const double* inflow_top;     /* [n_freq] incident on omega_z < 0 rays at k = 0, or NULL (0) */
     const double* inflow_bottom;  /* [n_freq] incident on omega_z > 0 rays at k = nz-1, or NULL (0) */
+    int32_t characteristics;      /* RTK_CHAR_*: long (lattice family), short, or hybrid by inclination */
 } rtk_lattice_desc;
 
 const char* rtk_last_error_message(void);

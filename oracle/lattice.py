@@ -24,6 +24,18 @@ implements:
   exp-linear extension, on dtau = phi_f dt;
 * line values at a layer go back to the nodes of that layer by bilinear
   interpolation from the four surrounding lines (T_RC, rows sum to one).
+
+Characteristics (TRIP chooses short or long
+characteristics by ray inclination):
+* "long" (default): the lattice family above;
+* "short": every layer step restarts each direction's lines at the nodes: the
+  characteristic through node c of layer t+1 starts at its upwind point c - (sx, sy)
+  on layer t with the bilinear interpolate of layer t's node values there, and is
+  integrated with the same n_sub sub-segments / T_CR sampling up to the node; no T_RC
+  (the line ends on the node);
+* "hybrid": short characteristics for steep directions (max(|sx|, |sy|) <= 1: the
+  upwind point lies in the adjacent cell), long ones for grazing directions.
+Vertical (integer-shift) directions give identical results in all three.
 """
 
 from __future__ import annotations
@@ -57,6 +69,7 @@ class LatticeDesc:
     inflow_bottom: np.ndarray
     thermal: np.ndarray      # (n_space, n_freq) isotropic thermal source
     formal_solver: str = "ie"
+    characteristics: str = "long"   # "long" | "short" | "hybrid"
 
     @property
     def n_space(self):
@@ -84,6 +97,17 @@ def direction_geometry(d: LatticeDesc, a: int):
     n_sub = max(1, int(math.ceil(max(abs(sx), abs(sy)) - 1e-12)))
     length = d.dz / abs(oz)          # 3D path length per layer (the slab is y-invariant, not 2D-transport)
     return down, sx, sy, n_sub, length / n_sub
+
+
+def uses_short_characteristics(d: LatticeDesc, a: int) -> bool:
+    """Short characteristics for direction a under d.characteristics."""
+    if d.characteristics == "short":
+        return True
+    if d.characteristics == "hybrid":
+        return direction_geometry(d, a)[3] == 1
+    if d.characteristics != "long":
+        raise ValueError(f"characteristics must be 'long', 'short' or 'hybrid', not {d.characteristics!r}")
+    return False
 
 
 def _bilinear_sample(field_layer, X, Y):
@@ -117,6 +141,7 @@ def lattice_transfer(d: LatticeDesc, S: np.ndarray, with_boundary: bool = False,
     gi, gj = lx.copy(), ly.copy()           # grid columns, same enumeration as lines
     for a in range(na):
         down, sx, sy, n_sub, sub_len = direction_geometry(d, a)
+        short = uses_short_characteristics(d, a)
         if with_boundary:
             inflow = d.inflow_top if down else d.inflow_bottom
             state = np.tile(np.asarray(inflow, dtype=float), (nx * ny, 1))
@@ -124,21 +149,32 @@ def lattice_transfer(d: LatticeDesc, S: np.ndarray, with_boundary: bool = False,
             state = np.zeros((nx * ny, nf))
         for t in range(nz):
             k = t if down else nz - 1 - t
-            # T_RC: node (i, j) from the four lines around it at this layer
-            u = gi - t * sx
-            v = gj - t * sy
-            grid_vals = _bilinear_sample(state.reshape(ny, nx, nf), u, v)
+            if short:
+                # lines end on the nodes: node values are the line values
+                grid_vals = state
+            else:
+                # T_RC: node (i, j) from the four lines around it at this layer
+                u = gi - t * sx
+                v = gj - t * sy
+                grid_vals = _bilinear_sample(state.reshape(ny, nx, nf), u, v)
             out[k].reshape(ny * nx, na, nf)[:, a, :] = grid_vals
             if t == nz - 1:
                 break
             k2 = k + 1 if down else k - 1
             Sa = S4[k, :, :, a, :]
             Sb = S4[k2, :, :, a, :]
+            if short:
+                # restart at the upwind point of each node of layer k2, from layer k's nodes
+                state = _bilinear_sample(state.reshape(ny, nx, nf), gi - sx, gj - sy)
             prev_S = prev_chi = None
             for m in range(n_sub + 1):
-                tt = t + m / n_sub
-                X = lx + tt * sx
-                Y = ly + tt * sy
+                if short:
+                    X = gi + (m / n_sub - 1.0) * sx
+                    Y = gj + (m / n_sub - 1.0) * sy
+                else:
+                    tt = t + m / n_sub
+                    X = lx + tt * sx
+                    Y = ly + tt * sy
                 wz = m / n_sub
                 s_m = (1 - wz) * _bilinear_sample(Sa, X, Y) + wz * _bilinear_sample(Sb, X, Y)
                 c_m = (1 - wz) * _bilinear_sample(chi3[k], X, Y) + wz * _bilinear_sample(chi3[k2], X, Y)
@@ -208,7 +244,8 @@ def desc_from_lattice_problem(p) -> LatticeDesc:
                        ybasis=np.asarray(p.ybasis), coeffs=np.asarray(p.coeffs), R=np.asarray(p.R),
                        gamma=np.asarray(p.gamma), chi=np.asarray(p.chi), inflow_top=np.asarray(p.inflow_top),
                        inflow_bottom=np.asarray(p.inflow_bottom), thermal=np.asarray(p.thermal),
-                       formal_solver=p.formal_solver)
+                       formal_solver=p.formal_solver,
+                       characteristics=getattr(p, "characteristics", "long"))
 
 
 def apply_A(d: LatticeDesc, layout: str, x):

@@ -243,6 +243,9 @@ int rtk_problem_create_lattice(const rtk_lattice_desc* d, rtk_problem** out) {
     if (d->layout != RTK_LAYOUT_INTENSITY && d->layout != RTK_LAYOUT_MOMENTS)
         return set_error(RTK_EINVAL, "unknown layout");
     if (!(d->dx > 0 && d->dy > 0 && d->dz > 0)) return set_error(RTK_EINVAL, "spacings must be positive");
+    if (d->characteristics != RTK_CHAR_LONG && d->characteristics != RTK_CHAR_SHORT &&
+        d->characteristics != RTK_CHAR_HYBRID)
+        return set_error(RTK_EINVAL, "characteristics must be RTK_CHAR_LONG, _SHORT or _HYBRID");
     if (!d->omega || !d->dir_w || !d->phi || !d->freq_w || !d->ybasis || !d->coeffs || !d->redistribution ||
         !d->gamma || !d->chi)
         return set_error(RTK_EINVAL, "missing description array");

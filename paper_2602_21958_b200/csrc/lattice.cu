@@ -86,6 +86,16 @@ __device__ __forceinline__ Stencil stencil_at(int lx, int ly, const Shift& sh, i
     return s;
 }
 
+// SC restart: value at the upwind point c - s of node c, bilinear from a [nxy][stride] plane
+__device__ __forceinline__ Shift restart_shift(const LatDir& D) {
+    Shift sh;
+    sh.bx = D.rbx;
+    sh.by = D.rby;
+    sh.ax = D.rax;
+    sh.ay = D.ray;
+    return sh;
+}
+
 struct LatArgs {
     const LatDir* dirs;
     const Shift* sub_shift;   // [dir: shift_off + t * (n_sub + 1) + m] sub-node shifts
@@ -234,7 +244,8 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
     double* splane = lines + nxy * kFC;         // [3][nxy][kFC]
     double* cplane = splane + 3 * nxy * kFC;    // [3][nxy]         (opacity; unused with DT)
     double* xplane = cplane + 3 * nxy;          // [2][nxy][kFC]   (XM only)
-    Shift* shs = reinterpret_cast<Shift*>(xplane + 2 * nxy * kFC);   // [max_sub + 1] shifts of the step
+    double* seeds = xplane + 2 * nxy * kFC;     // [nxy][kFC] SC restart values
+    Shift* shs = reinterpret_cast<Shift*>(seeds + nxy * kFC);   // [max_sub + 1] shifts of the step
     const int nfc = (A.n_freq + kFC - 1) / kFC;
     const int a = blockIdx.x / nfc;
     const int f0 = (blockIdx.x % nfc) * kFC;
@@ -313,7 +324,19 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
         }
         if (t == A.nz - 1) break;
         for (int m = threadIdx.x; m <= D.n_sub; m += blockDim.x) shs[m] = A.sub_shift[D.shift_off + t * (D.n_sub + 1) + m];
+        if (D.sc) {
+            // short characteristics: every line restarts at its node's upwind point on this layer
+            const Shift rsh = restart_shift(D);
+            for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) {
+                const int c = e / kFC, q = e - c * kFC;
+                const int j = c / A.nx, i = c - j * A.nx;
+                const Stencil st = stencil_at(i, j, rsh, A.nx, A.ny);
+                seeds[e] = st.w00 * lines[st.c00 * kFC + q] + st.w10 * lines[st.c10 * kFC + q] +
+                           st.w01 * lines[st.c01 * kFC + q] + st.w11 * lines[st.c11 * kFC + q];
+            }
+        }
         __syncthreads();   // the gather read `lines` before the march overwrites them; shifts staged
+        const double* start = D.sc ? seeds : lines;
         const double* Sa = splane + (t % 3) * nxy * kFC;
         const double* Sb = splane + ((t + 1) % 3) * nxy * kFC;
         const double* ca = cplane + (t % 3) * nxy;
@@ -322,7 +345,7 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
             const int ly = c / A.nx, lx = c - ly * A.nx;
             double acc[kFC];
 #pragma unroll
-            for (int q = 0; q < kFC; ++q) acc[q] = lines[c * kFC + q];
+            for (int q = 0; q < kFC; ++q) acc[q] = start[c * kFC + q];
             advance_line_smem4<FS, DT>(D, shs, acc, lx, ly, t, A.nx, A.ny, ca, cb, Sa, Sb, phi,
                                        DT ? A.dtab + D.dtab_off + static_cast<int64_t>(t) * D.n_sub * A.nxy + c : nullptr,
                                        nxy);
@@ -379,7 +402,7 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_kernel(LatArgs A, int
         const double* chi_b = A.chi + static_cast<int64_t>(k2) * A.nxy;
         for (int c = slot; c < A.nxy; c += slots) {
             const int ly = c / A.nx, lx = c - ly * A.nx;
-            double acc = lines[c * kFC + fq];
+            double acc = lines[c * kFC + fq];   // long characteristics only (SC: smem kernel)
             if (fvalid)
                 acc = advance_line<FS>(D, A.sub_shift + D.shift_off + t * (D.n_sub + 1), acc, lx, ly, t, A.nx, A.ny,
                                        chi_a, chi_b, Sa, Sb, ss, phi_f);
@@ -486,7 +509,7 @@ __global__ void lattice_dtab_kernel(const LatDir* __restrict__ dirs, const Shift
 // Directions are processed hemisphere by hemisphere so only NM x F moment accumulators
 // are live; layer t gets the down part, layer nz-1-t the up part.
 struct StepDir {
-    int down, n_sub, sub_pref;
+    int down, n_sub, sub_pref, sc;
     long long dtab;        // this step's first dt-table entry of the direction
     double wy[8];
 };
@@ -504,14 +527,17 @@ __global__ void __launch_bounds__(128, 5) lattice_mom_group_kernel(LatArgs A, in
     extern __shared__ double mo_s[];       // [NM][F][blockDim] accumulators, then the tables
     StepDir* sdir = reinterpret_cast<StepDir*>(mo_s + NM * F * blockDim.x);
     Shift* sgat = reinterpret_cast<Shift*>(sdir + A.n_dirs);
-    Shift* ssub = sgat + A.n_dirs;
+    Shift* srst = sgat + A.n_dirs;          // SC restart shifts
+    Shift* ssub = srst + A.n_dirs;
     for (int a = threadIdx.x; a < A.n_dirs; a += blockDim.x) {
         const LatDir& D = A.dirs[a];
         StepDir sd;
         sd.down = D.down;
         sd.n_sub = D.n_sub;
         sd.sub_pref = D.sub_pref;
+        sd.sc = D.sc;
         sd.dtab = D.dtab_off + static_cast<int64_t>(t) * D.n_sub * A.nxy;
+        srst[a] = restart_shift(D);
 #pragma unroll
         for (int l = 0; l < NM; ++l) sd.wy[l] = D.wy[l];
         sdir[a] = sd;
@@ -595,15 +621,32 @@ __global__ void __launch_bounds__(128, 5) lattice_mom_group_kernel(LatArgs A, in
             if (t < A.nz - 1) {
                 const int k2 = hemi == 0 ? k + 1 : k - 1;
                 double acc[F];
+                if (D.sc && t > 0) {
+                    // short characteristics: restart at the upwind point of node c (bilinear
+                    // from the previous step's node values = line values)
+                    const Stencil rs = stencil_at(i, j, srst[a], A.nx, A.ny);
 #pragma unroll
-                for (int h = 0; h < F / 2; ++h) {
-                    double2 s2;
-                    if (t == 0) s2 = hemi == 0 ? make_double2(in_top[2 * h], in_top[2 * h + 1])
-                                                : make_double2(in_bot[2 * h], in_bot[2 * h + 1]);
-                    else s2 = (!full_group && g2 + h >= hp) ? make_double2(0.0, 0.0)
-                                                            : sa[static_cast<int64_t>(c) * hp + h];
-                    acc[2 * h] = s2.x;
-                    acc[2 * h + 1] = s2.y;
+                    for (int h = 0; h < F / 2; ++h) {
+                        if (!full_group && g2 + h >= hp) {
+                            acc[2 * h] = acc[2 * h + 1] = 0.0;
+                            continue;
+                        }
+                        const double2 s00 = sa[rs.c00 * hp + h], s10 = sa[rs.c10 * hp + h];
+                        const double2 s01 = sa[rs.c01 * hp + h], s11 = sa[rs.c11 * hp + h];
+                        acc[2 * h] = rs.w00 * s00.x + rs.w10 * s10.x + rs.w01 * s01.x + rs.w11 * s11.x;
+                        acc[2 * h + 1] = rs.w00 * s00.y + rs.w10 * s10.y + rs.w01 * s01.y + rs.w11 * s11.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int h = 0; h < F / 2; ++h) {
+                        double2 s2;
+                        if (t == 0) s2 = hemi == 0 ? make_double2(in_top[2 * h], in_top[2 * h + 1])
+                                                    : make_double2(in_bot[2 * h], in_bot[2 * h + 1]);
+                        else s2 = (!full_group && g2 + h >= hp) ? make_double2(0.0, 0.0)
+                                                                : sa[static_cast<int64_t>(c) * hp + h];
+                        acc[2 * h] = s2.x;
+                        acc[2 * h + 1] = s2.y;
+                    }
                 }
                 LatDir Dl;
                 Dl.n_sub = D.n_sub;
@@ -714,6 +757,12 @@ int setup_lattice(Problem& p, const rtk_lattice_desc* d) {
         D.sy = d->ny > 1 ? oy * d->dz / (std::fabs(oz) * d->dy) : 0.0;
         D.n_sub = std::max(1, static_cast<int>(std::ceil(std::max(std::fabs(D.sx), std::fabs(D.sy)) - 1e-12)));
         D.sub_len = d->dz / std::fabs(oz) / D.n_sub;
+        D.sc = d->characteristics == RTK_CHAR_SHORT || (d->characteristics == RTK_CHAR_HYBRID && D.n_sub == 1);
+        const Shift rs = shift_of(-D.sx, -D.sy, d->nx, d->ny);
+        D.rbx = rs.bx;
+        D.rby = rs.by;
+        D.rax = rs.ax;
+        D.ray = rs.ay;
         for (int l = 0; l < 8; ++l) {
             const bool in = l < d->n_moments;
             D.wy[l] = in ? d->dir_w[a] * d->ybasis[l * d->n_dirs + a] : 0.0;
@@ -731,12 +780,17 @@ int setup_lattice(Problem& p, const rtk_lattice_desc* d) {
     for (int a = 0; a < d->n_dirs; ++a) {
         LatDir& D = dirs[a];
         D.shift_off = static_cast<int>(sub.size());
+        // LC: line c sits at c + (t + m / n_sub) s; SC: the characteristic ending on node c
+        // starts at c - s, sub-node m at c + (m / n_sub - 1) s, and node values are the line
+        // values (identity gather)
         for (int t = 0; t < d->nz - 1; ++t)
             for (int m = 0; m <= D.n_sub; ++m) {
-                const double tt = t + static_cast<double>(m) / D.n_sub;
+                const double tt = D.sc ? static_cast<double>(m) / D.n_sub - 1.0 : t + static_cast<double>(m) / D.n_sub;
                 sub.push_back(shift_of(tt * D.sx, tt * D.sy, d->nx, d->ny));
             }
-        for (int t = 0; t < d->nz; ++t) gat[static_cast<size_t>(a) * d->nz + t] = shift_of(-t * D.sx, -t * D.sy, d->nx, d->ny);
+        for (int t = 0; t < d->nz; ++t)
+            gat[static_cast<size_t>(a) * d->nz + t] = D.sc ? shift_of(0.0, 0.0, d->nx, d->ny)
+                                                           : shift_of(-t * D.sx, -t * D.sy, d->nx, d->ny);
     }
     if (sub.empty()) sub.push_back(Shift{});
     RTK_CUDA_TRY(cudaMalloc(&p.lat_sub_shift, sizeof(Shift) * sub.size()));
@@ -752,7 +806,11 @@ int setup_lattice(Problem& p, const rtk_lattice_desc* d) {
     RTK_CUDA_TRY(cudaMalloc(&p.lat_dirs, sizeof(LatDir) * dirs.size()));
     RTK_CUDA_TRY(cudaMemcpy(p.lat_dirs, dirs.data(), sizeof(LatDir) * dirs.size(), cudaMemcpyHostToDevice));
     p.lat_max_sub = 0;
-    for (const auto& D : dirs) p.lat_max_sub = std::max(p.lat_max_sub, D.n_sub);
+    p.lat_any_sc = false;
+    for (const auto& D : dirs) {
+        p.lat_max_sub = std::max(p.lat_max_sub, D.n_sub);
+        p.lat_any_sc = p.lat_any_sc || D.sc;
+    }
     const bool small_layers = sizeof(double) * nxy * (10 * kFC + 3) <= 160 * 1024;
     if (d->layout == RTK_LAYOUT_MOMENTS || small_layers) {
         // frequency-independent sub-segment optical paths, streamed by the moment-layout sweep and
@@ -800,7 +858,7 @@ static LatArgs lat_args(const Problem& p, const double* src, const double* x, do
 
 template <int FS, int SRC, int OUT>
 static int launch_int(const Problem& p, const LatArgs& A, int with_inflow, cudaStream_t s) {
-    const size_t smem_planes = sizeof(double) * A.nxy * (kFC + 3 * kFC + 3 + 2 * kFC) +
+    const size_t smem_planes = sizeof(double) * A.nxy * (kFC + 3 * kFC + 3 + 2 * kFC + kFC) +
                                sizeof(Shift) * (p.lat_max_sub + 1);
     if (smem_planes <= 160 * 1024 && !getenv_flag("RTK_LATTICE_NO_SMEM")) {
         const bool dt = A.dtab != nullptr && !getenv_flag("RTK_LATTICE_NO_DTAB");
@@ -814,6 +872,9 @@ static int launch_int(const Problem& p, const LatArgs& A, int with_inflow, cudaS
         RTK_LAUNCH_CHECK("lattice_int_smem_kernel");
         return RTK_OK;
     }
+    if (p.lat_any_sc)
+        return set_error(RTK_ERESOURCE, "short characteristics in the intensity layout need the shared-memory kernel "
+                                        "(small layers); use the moment layout");
     const size_t smem = sizeof(double) * A.nxy * kFC;
     auto kern = lattice_int_kernel<FS, SRC, OUT>;
     if (smem > 48 * 1024) {
@@ -854,7 +915,7 @@ static int launch_mom_steps(const Problem& p, const LatArgs& A, bool with_inflow
     // blocks spread them evenly over the SMs (256-thread blocks left 40 SMs half occupied)
     const int mb = getenv("RTK_LAT_BLOCK") ? atoi(getenv("RTK_LAT_BLOCK")) : 128;
     const size_t mom_smem = sizeof(double) * NM * F * mb + sizeof(StepDir) * A.n_dirs +
-                            sizeof(Shift) * (A.n_dirs + A.total_sub);
+                            sizeof(Shift) * (2 * A.n_dirs + A.total_sub);
     if (mom_smem > 48 * 1024)
         RTK_CUDA_TRY(cudaFuncSetAttribute(lattice_mom_group_kernel<FS, NM, F>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(mom_smem)));

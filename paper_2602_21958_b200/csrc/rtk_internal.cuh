@@ -63,6 +63,9 @@ struct LatDir {
     double sub_len;   // path length of one sub-segment
     double wy[8];     // w_a Y_l(a)   (moment accumulation)
     double cy[8];     // c_l Y_l(a)   (source expansion)
+    int sc;           // short characteristics: lines restart at each node's upwind point every step
+    int rbx, rby;     // SC restart gather: integer part of (-sx, -sy) mod (nx, ny) ...
+    double rax, ray;  // ... and its fractional part (same arithmetic as shift_of)
 };
 
 enum ProblemKind { KIND_SLAB = 1, KIND_LATTICE = 2 };
@@ -110,6 +113,7 @@ struct Problem {
     void* lat_gat_shift = nullptr;               // Shift table, T_RC gathers
     double* lat_dtab = nullptr;                  // [dir][t][m][line] sub-segment optical paths
     int lat_max_sub = 0;                         // largest sub-segment count over the directions
+    bool lat_any_sc = false;   // some direction uses short characteristics
     int lat_total_sub = 0;                       // sum over directions of (n_sub + 1)
     // overlap of the HBM-bound moment reduction with the FP64 redistribution GEMM (slab apply_A)
     cudaStream_t aux = nullptr;

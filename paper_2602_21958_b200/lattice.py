@@ -37,7 +37,10 @@ class LatticeDesc(ctypes.Structure):
                 ("dx", ctypes.c_double), ("dy", ctypes.c_double), ("dz", ctypes.c_double)] + \
                [(n, _native.c_double_p) for n in ("omega", "dir_w", "phi", "freq_w", "ybasis", "coeffs",
                                                    "redistribution", "gamma", "chi", "inflow_top",
-                                                   "inflow_bottom")]
+                                                   "inflow_bottom")] + \
+               [("characteristics", ctypes.c_int32)]
+
+CHARACTERISTICS = {"long": 0, "short": 1, "hybrid": 2}
 
 
 def product_quadrature(n_polar: int, n_azimuth: int):
@@ -104,6 +107,7 @@ class LatticeProblem:
     inflow_bottom: np.ndarray
     layout: str = "intensity"
     formal_solver: str = "ie"
+    characteristics: str = "long"   # "long" | "short" | "hybrid" (short for steep, long for grazing directions)
     dx: float = 1.0
     dy: float = 1.0
     dz: float = 1.0
@@ -151,6 +155,9 @@ class _LatticeHandle:
             raise ValueError("lattice problems support the 'ie' and 'exp_linear' formal solvers")
         d.formal_solver = _native.FS_CODES[p.formal_solver]
         d.layout = LAYOUTS[p.layout]
+        if p.characteristics not in CHARACTERISTICS:
+            raise ValueError(f"characteristics must be one of {sorted(CHARACTERISTICS)}, not {p.characteristics!r}")
+        d.characteristics = CHARACTERISTICS[p.characteristics]
         d.dx, d.dy, d.dz = p.dx, p.dy, p.dz
         for name, key in (("omega", "omega"), ("dir_w", "dir_w"), ("phi", "phi"), ("freq_w", "freq_w"),
                           ("ybasis", "ybasis"), ("coeffs", "coeffs"), ("redistribution", "R"), ("gamma", "gamma"),
@@ -178,7 +185,8 @@ class _LatticeHandle:
 def lattice_problem(nx: int, ny: int, nz: int, n_polar: int, n_azimuth: int, n_freq: int, x_max: float = 5.0,
                     eps: float = 1e-4, sigma: float = 0.5, corr_len: float = 8.0, seed: int = 0,
                     layout: str = "intensity", formal_solver: str = "ie", coherence: float = 0.5,
-                    bottom_inflow: float = 1.0, t_range=(1e-4, 1e4)) -> LatticeProblem:
+                    bottom_inflow: float = 1.0, t_range=(1e-4, 1e4),
+                    characteristics: str = "long") -> LatticeProblem:
     """Seeded lattice problem: log-normal opacity on an exponential stratification, dipole x PRD
     scattering with gamma = (1 - eps) / (4 pi phi), thermal eps B (B = 1), zero incident
     intensity at the top and B at the bottom."""
@@ -198,7 +206,7 @@ def lattice_problem(nx: int, ny: int, nz: int, n_polar: int, n_azimuth: int, n_f
     return LatticeProblem(nx=nx, ny=ny, nz=nz, omega=omega, dir_w=w, nu=nu, freq_w=fw, phi=phi, ybasis=Y,
                           coeffs=c, R=R, gamma=gamma, chi=chi, thermal=thermal, inflow_top=np.zeros(n_freq),
                           inflow_bottom=np.full(n_freq, bottom_inflow), layout=layout, formal_solver=formal_solver,
-                          descriptor=dict(eps=eps, sigma=sigma, corr_len=corr_len, seed=seed, coherence=coherence))
+                          characteristics=characteristics, descriptor=dict(eps=eps, sigma=sigma, corr_len=corr_len, seed=seed, coherence=coherence))
 
 
 def lattice_apply_A(problem: LatticeProblem, v):

@@ -32,6 +32,34 @@ def test_lattice_matvec_matches_oracle(case, layout, fs):
     assert rel_l2(P.build_rhs(p), OL.build_rhs(d, layout)) <= MATVEC_TOL
 
 
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("layout", ["intensity", "moments"])
+@pytest.mark.parametrize("chars", ["short", "hybrid"])
+@pytest.mark.parametrize("fs", ["ie", "exp_linear"])
+def test_short_and_hybrid_characteristics_match_oracle(case, layout, chars, fs):
+    """Short characteristics (restart at each node's upwind point every layer step) and the
+    hybrid (short for steep, long for grazing directions) against the oracle."""
+    nx, ny, nz, npol, naz, nf = case
+    p = L.lattice_problem(nx, ny, nz, npol, naz, nf, corr_len=2.0, seed=13, layout=layout, formal_solver=fs,
+                          characteristics=chars)
+    d = OL.desc_from_lattice_problem(p)
+    assert d.characteristics == chars
+    v = np.random.default_rng(nx + nz).standard_normal(p.n_total)
+    assert rel_l2(P.apply_A(p, v), OL.apply_A(d, layout, v)) <= MATVEC_TOL
+    assert rel_l2(P.build_rhs(p), OL.build_rhs(d, layout)) <= MATVEC_TOL
+
+
+def test_hybrid_characteristics_gmres_matches_oracle():
+    p = L.lattice_problem(8, 6, 8, 8, 8, 4, corr_len=2.0, seed=7, layout="moments", characteristics="hybrid")
+    d = OL.desc_from_lattice_problem(p)
+    b = OL.build_rhs(d, "moments")
+    ref = ro.gmres(lambda v: OL.apply_A(d, "moments", v), b, rel_tol=1e-8, max_iter=500)
+    rep = P.gmres(p, b, P.SolveConfig(rel_tol=1e-8, max_iter=500))
+    assert rep.converged and ref.converged
+    assert abs(rep.iterations - ref.iterations) <= 1
+    assert rel_l2(rep.solution, ref.solution) <= 1e-7
+
+
 @pytest.mark.parametrize("layout", ["intensity", "moments"])
 def test_lattice_gmres_matches_oracle(layout):
     p = L.lattice_problem(8, 1, 10, 8, 8, 5, corr_len=2.0, seed=5, layout=layout)

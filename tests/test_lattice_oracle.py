@@ -114,3 +114,74 @@ def test_stratification_and_field():
     rho = L.lognormal_field((16, 16, 16), 0.5, 4.0, 1)
     g = (np.log(rho) + 0.125) / 0.5
     assert abs(g.std() - 1) < 1e-12 and abs(g.mean()) < 1e-12
+
+
+# ---------------- short / hybrid characteristics ----------------
+
+def _desc(p, characteristics):
+    d = OL.desc_from_lattice_problem(p)
+    d.characteristics = characteristics
+    return d
+
+
+@pytest.mark.parametrize("solver", ["ie", "exp_linear"])
+def test_short_characteristics_equal_long_on_integer_shift_directions(solver):
+    """Vertical and sx = 1 directions: the upwind point of every node is a node, so the
+    SC restart is a selection and SC, LC and hybrid coincide."""
+    p = tiny(nx=5, nz=8, nf=3, formal_solver=solver)
+    s = math.sqrt(0.5)
+    p.omega = np.array([[0.0, 0.0, -1.0], [0.0, 0.0, 1.0], [s, 0.0, -s], [-s, 0.0, s]])
+    p.dir_w = np.full(4, math.pi)
+    p.ybasis = L.dipole_harmonics(p.omega)
+    rng = np.random.default_rng(1)
+    S = rng.standard_normal((p.n_space, 4, p.n_freq))
+    lc = OL.lattice_transfer(_desc(p, "long"), S)
+    for mode in ("short", "hybrid"):
+        np.testing.assert_allclose(OL.lattice_transfer(_desc(p, mode), S), lc, rtol=1e-13, atol=1e-15)
+
+
+@pytest.mark.parametrize("solver", ["ie", "exp_linear"])
+def test_short_characteristics_equal_long_for_horizontally_uniform_fields(solver):
+    """Horizontally uniform opacity and source: bilinear interpolation is exact, so SC = LC
+    for every direction, including grazing ones with several sub-segments per layer."""
+    p = tiny(nx=6, ny=4, nz=7, n_polar=8, n_az=6, nf=3, formal_solver=solver)
+    chi = p.chi.reshape(p.nz, p.ny, p.nx)
+    p.chi = np.repeat(chi[:, :1, :1], p.ny, 1).repeat(p.nx, 2).reshape(-1)
+    rng = np.random.default_rng(2)
+    S = np.repeat(rng.standard_normal((p.nz, 1, 1, p.n_dirs, p.n_freq)), p.ny, 1).repeat(p.nx, 2)
+    S = S.reshape(p.n_space, p.n_dirs, p.n_freq)
+    lc = OL.lattice_transfer(_desc(p, "long"), S, with_boundary=True)
+    sc = OL.lattice_transfer(_desc(p, "short"), S, with_boundary=True)
+    np.testing.assert_allclose(sc, lc, rtol=1e-12, atol=1e-14)
+
+
+def test_hybrid_takes_short_for_steep_and_long_for_grazing_directions():
+    p = tiny(nx=6, ny=5, nz=6, n_polar=8, n_az=6, nf=3)
+    rng = np.random.default_rng(3)
+    S = rng.standard_normal((p.n_space, p.n_dirs, p.n_freq))
+    outs = {m: OL.lattice_transfer(_desc(p, m), S) for m in ("long", "short", "hybrid")}
+    d = _desc(p, "hybrid")
+    steep = [OL.direction_geometry(d, a)[3] == 1 for a in range(p.n_dirs)]
+    assert any(steep) and not all(steep)
+    for a in range(p.n_dirs):
+        ref = outs["short"] if steep[a] else outs["long"]
+        np.testing.assert_array_equal(outs["hybrid"][:, a, :], ref[:, a, :])
+    # on a heterogeneous field the two characteristics are different discretisations
+    assert np.abs(outs["short"] - outs["long"]).max() > 1e-6
+
+
+def test_short_characteristics_constant_source_relaxes_to_source():
+    """A constant source with matching inflow is a fixed point of the exact transfer; the SC
+    restart (rows of the bilinear stencil sum to one) keeps it one to rounding."""
+    p = tiny(nx=5, ny=3, nz=6, n_polar=8, n_az=4, nf=3, formal_solver="exp_linear")
+    p.inflow_top = np.full(p.n_freq, 0.7)
+    p.inflow_bottom = np.full(p.n_freq, 0.7)
+    S = np.full((p.n_space, p.n_dirs, p.n_freq), 0.7)
+    out = OL.lattice_transfer(_desc(p, "short"), S, with_boundary=True)
+    np.testing.assert_allclose(out, 0.7, rtol=1e-13)
+
+
+def test_characteristics_validation():
+    p = tiny()
+    with pytest.raises(ValueError):
+        OL.lattice_transfer(_desc(p, "medium"), np.zeros((p.n_space, p.n_dirs, p.n_freq)))
