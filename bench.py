@@ -587,7 +587,7 @@ def formal_solver_timings(torch, lib, hbm):
         sweep_bytes = 16 * n + 8 * 2 * g.n_freq * g.n_space + 8 * g.n_space
         out[fs] = {"matvecs_per_s": 1e3 / ms, "ms_per_matvec": ms, "sweep_ms": sweep_ms,
                    "sweep_gbs": sweep_bytes / sweep_ms / 1e6, "sweep_frac_hbm": sweep_bytes / sweep_ms / 1e6 / hbm,
-                   "kernel": "sweep1d_tma_el_kernel / sweep1d_tma_ep_kernel (weight warps + chain warps)"}
+                   "kernel": "sweep1d_tma_kernel<EXP_*> (branch-free range-reduced weights in the chain warps)"}
         del p, x, y
         torch.cuda.empty_cache()
     return out
@@ -605,22 +605,35 @@ def lattice_timings(torch):
             5: dict(nx=128, ny=128, nz=128, n_polar=8, n_azimuth=12, n_freq=41, corr_len=16.0, eps=1e-5,
                     layout="moments")}
     out = {}
-    for cfg, kw in cfgs.items():
-        p = L.lattice_problem(seed=21958 + cfg, **kw)
+
+    def time_matvec(p):
         x = torch.randn(p.n_total, dtype=torch.float64, device="cuda")
         P.apply_A(p, x)
         torch.cuda.synchronize()
-        reps = 2 if cfg == 5 else 4
+        reps = 2 if p.nz >= 128 else 4
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(reps):
             P.apply_A(p, x)
         e1.record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / reps
+        return e0.elapsed_time(e1) / reps
+
+    for cfg, kw in cfgs.items():
+        p = L.lattice_problem(seed=21958 + cfg, **kw)
+        ms = time_matvec(p)
         dof = p.n_space * p.n_dirs * p.n_freq
-        out[f"cfg{cfg}"] = {"layout": kw["layout"], "unknowns": p.n_total, "dof": dof, "ms_per_matvec": ms,
-                            "matvecs_per_s": 1e3 / ms, "gdof_per_s": dof / ms / 1e6}
+        n_total = p.n_total
+        del p
+        torch.cuda.empty_cache()
+        # hybrid characteristics (short for steep, long for grazing directions; TRIP)
+        ph = L.lattice_problem(seed=21958 + cfg, characteristics="hybrid", **kw)
+        ms_h = time_matvec(ph)
+        del ph
+        torch.cuda.empty_cache()
+        out[f"cfg{cfg}"] = {"layout": kw["layout"], "unknowns": n_total, "dof": dof, "ms_per_matvec": ms,
+                            "matvecs_per_s": 1e3 / ms, "gdof_per_s": dof / ms / 1e6,
+                            "hybrid_characteristics": {"ms_per_matvec": ms_h, "gdof_per_s": dof / ms_h / 1e6}}
         # the multi-D sweeps are bound by the FP64 pipe / latency, not HBM -- report the
         # transfer kernel's FP64-pipe utilisation from the committed ncu capture of this config
         raw = ncu_raw(os.path.join(ROOT, "profiles", f"r01_ncu_lattice_cfg{cfg}.txt"))
@@ -628,8 +641,6 @@ def lattice_timings(torch):
         if key in raw:
             out[f"cfg{cfg}"]["transfer_kernel_fp64_pipe_frac"] = float(raw[key].rstrip("%")) / 100
             out[f"cfg{cfg}"]["fp64_source"] = f"profiles/r01_ncu_lattice_cfg{cfg}.txt (ncu --set full, one launch)"
-        del p, x
-        torch.cuda.empty_cache()
     return out
 
 

@@ -160,7 +160,9 @@ __device__ __forceinline__ double advance_line(const LatDir& D, const Shift* __r
 // reused for the kFC frequencies of the chunk.  Planes: chi [nxy], S [nxy][kFC].
 // DT: dt of sub-segment m comes from the precomputed table (dtl = entry of (direction,
 // step, line), stride nxy; prefetched one sub-node ahead) instead of the opacity planes.
-template <int FS, bool DT>
+// PLANAR (ny = 1, the 2D slab): sy = 0, so the stencil's second row has weight exactly 0
+// and only two corners per layer are read (half the shared-memory traffic; same result).
+template <int FS, bool DT, bool PLANAR>
 __device__ __forceinline__ void advance_line_smem4(const LatDir& D, const Shift* __restrict__ sub,
                                                    double (&acc)[kFC], int lx, int ly, int t, int nx, int ny,
                                                    const double* chi_a, const double* chi_b,
@@ -181,10 +183,12 @@ __device__ __forceinline__ void advance_line_smem4(const LatDir& D, const Shift*
                 if (m < D.n_sub) dt_next = __ldg(dtl + static_cast<int64_t>(m) * nxy);
             }
         } else {
-            const double ca = st.w00 * chi_a[st.c00] + st.w10 * chi_a[st.c10] + st.w01 * chi_a[st.c01] +
-                              st.w11 * chi_a[st.c11];
-            const double cb = st.w00 * chi_b[st.c00] + st.w10 * chi_b[st.c10] + st.w01 * chi_b[st.c01] +
-                              st.w11 * chi_b[st.c11];
+            const double ca = PLANAR ? st.w00 * chi_a[st.c00] + st.w10 * chi_a[st.c10]
+                                     : st.w00 * chi_a[st.c00] + st.w10 * chi_a[st.c10] + st.w01 * chi_a[st.c01] +
+                                           st.w11 * chi_a[st.c11];
+            const double cb = PLANAR ? st.w00 * chi_b[st.c00] + st.w10 * chi_b[st.c10]
+                                     : st.w00 * chi_b[st.c00] + st.w10 * chi_b[st.c10] + st.w01 * chi_b[st.c01] +
+                                           st.w11 * chi_b[st.c11];
             c_m = (1 - wz) * ca + wz * cb;
             dt = D.sub_len * (prev_c + c_m) * 0.5;
         }
@@ -198,13 +202,18 @@ __device__ __forceinline__ void advance_line_smem4(const LatDir& D, const Shift*
         const double2* b11 = reinterpret_cast<const double2*>(Sb + st.c11 * kFC);
 #pragma unroll
         for (int h = 0; h < kFC / 2; ++h) {
-            const double2 p00 = a00[h], p10 = a10[h], p01 = a01[h], p11 = a11[h];
-            const double2 q00 = b00[h], q10 = b10[h], q01 = b01[h], q11 = b11[h];
+            const double2 p00 = a00[h], p10 = a10[h], q00 = b00[h], q10 = b10[h];
             double s2[2];
-            s2[0] = (1 - wz) * (st.w00 * p00.x + st.w10 * p10.x + st.w01 * p01.x + st.w11 * p11.x) +
-                    wz * (st.w00 * q00.x + st.w10 * q10.x + st.w01 * q01.x + st.w11 * q11.x);
-            s2[1] = (1 - wz) * (st.w00 * p00.y + st.w10 * p10.y + st.w01 * p01.y + st.w11 * p11.y) +
-                    wz * (st.w00 * q00.y + st.w10 * q10.y + st.w01 * q01.y + st.w11 * q11.y);
+            if (PLANAR) {
+                s2[0] = (1 - wz) * (st.w00 * p00.x + st.w10 * p10.x) + wz * (st.w00 * q00.x + st.w10 * q10.x);
+                s2[1] = (1 - wz) * (st.w00 * p00.y + st.w10 * p10.y) + wz * (st.w00 * q00.y + st.w10 * q10.y);
+            } else {
+                const double2 p01 = a01[h], p11 = a11[h], q01 = b01[h], q11 = b11[h];
+                s2[0] = (1 - wz) * (st.w00 * p00.x + st.w10 * p10.x + st.w01 * p01.x + st.w11 * p11.x) +
+                        wz * (st.w00 * q00.x + st.w10 * q10.x + st.w01 * q01.x + st.w11 * q11.x);
+                s2[1] = (1 - wz) * (st.w00 * p00.y + st.w10 * p10.y + st.w01 * p01.y + st.w11 * p11.y) +
+                        wz * (st.w00 * q00.y + st.w10 * q10.y + st.w01 * q01.y + st.w11 * q11.y);
+            }
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int q = 2 * h + e;
@@ -235,7 +244,7 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
                  "l"(src));
 }
 
-template <int FS, int SRC, int OUT, bool DT>
+template <int FS, int SRC, int OUT, bool DT, bool PLANAR>
 __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A, int with_inflow, int max_sub) {
     extern __shared__ __align__(16) double sm[];
     const int nxy = static_cast<int>(A.nxy);
@@ -346,7 +355,7 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
             double acc[kFC];
 #pragma unroll
             for (int q = 0; q < kFC; ++q) acc[q] = start[c * kFC + q];
-            advance_line_smem4<FS, DT>(D, shs, acc, lx, ly, t, A.nx, A.ny, ca, cb, Sa, Sb, phi,
+            advance_line_smem4<FS, DT, PLANAR>(D, shs, acc, lx, ly, t, A.nx, A.ny, ca, cb, Sa, Sb, phi,
                                        DT ? A.dtab + D.dtab_off + static_cast<int64_t>(t) * D.n_sub * A.nxy + c : nullptr,
                                        nxy);
 #pragma unroll
@@ -514,8 +523,14 @@ struct StepDir {
     double wy[8];
 };
 
-template <int FS, int NM, int F>
-__global__ void __launch_bounds__(128, 5) lattice_mom_group_kernel(LatArgs A, int t, const double* __restrict__ st_in,
+// DG direction groups: the CTA is DG x IPB threads, thread (dgi, item) handles directions
+// a = dgi, dgi + DG, ... of item (line, frequency group) blockIdx.x * IPB + item, and the DG
+// partial moments of an item are summed in shared memory in dgi order (deterministic).  A
+// layer step has only nxy * fp / F items (cfg4: 65,536 = 14 warps per SM); DG = 8 gives the
+// SMs 8x the warps to hide the L2 latency of the gathers with.
+template <int FS, int NM, int F, int DG>
+__global__ void __launch_bounds__(DG == 1 ? 128 : 256, DG == 1 ? 5 : 3)
+    lattice_mom_group_kernel(LatArgs A, int t, const double* __restrict__ st_in,
                                                                  double* __restrict__ st_out, double* __restrict__ mom,
                                                                  int with_inflow, int fp,
                                                                  const double* __restrict__ plane_cur,
@@ -557,9 +572,12 @@ __global__ void __launch_bounds__(128, 5) lattice_mom_group_kernel(LatArgs A, in
         }
     }
     __syncthreads();
-    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (tid >= A.nxy * ng) return;
-    const int c = static_cast<int>(tid / ng);
+    const int ipb = blockDim.x / DG;                 // items per CTA
+    const int dgi = threadIdx.x / ipb;               // direction group of this thread
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * ipb + (threadIdx.x - dgi * ipb);
+    const bool item_ok = tid < A.nxy * ng;
+    if (DG == 1 && !item_ok) return;
+    const int c = item_ok ? static_cast<int>(tid / ng) : 0;
     const int g = static_cast<int>(tid - static_cast<int64_t>(c) * ng);
     const int f0 = F * g;
     const int j = c / A.nx, i = c - j * A.nx;
@@ -590,7 +608,7 @@ __global__ void __launch_bounds__(128, 5) lattice_mom_group_kernel(LatArgs A, in
         for (int l = 0; l < NM; ++l)
 #pragma unroll
             for (int q = 0; q < F; ++q) mo(l, q) = 0.0;
-        for (int a = 0; a < A.n_dirs; ++a) {
+        for (int a = dgi; a < A.n_dirs && item_ok; a += DG) {
             const StepDir& D = sdir[a];
             if ((D.down != 0) != (hemi == 0)) continue;
             const double2* sa = sin2 + a * plane2 + g2;
@@ -669,6 +687,22 @@ __global__ void __launch_bounds__(128, 5) lattice_mom_group_kernel(LatArgs A, in
                     }
                 }
             }
+        }
+        if (DG > 1) {
+            // partial moments of the DG direction groups, summed by group 0 in dgi order
+            __syncthreads();
+            if (dgi == 0 && item_ok) {
+#pragma unroll
+                for (int l = 0; l < NM; ++l)
+#pragma unroll
+                    for (int q = 0; q < F; ++q) {
+                        double sum = mo(l, q);
+                        for (int g2i = 1; g2i < DG; ++g2i) sum += mo_s[(l * F + q) * blockDim.x + threadIdx.x + g2i * ipb];
+                        mo(l, q) = sum;
+                    }
+            }
+            __syncthreads();
+            if (dgi != 0 || !item_ok) continue;
         }
         // step t is the first visit of layers t and nz-1-t iff t < nz-1-t; the middle layer
         // (odd nz) gets both parts in this thread, up added to down
@@ -862,7 +896,11 @@ static int launch_int(const Problem& p, const LatArgs& A, int with_inflow, cudaS
                                sizeof(Shift) * (p.lat_max_sub + 1);
     if (smem_planes <= 160 * 1024 && !getenv_flag("RTK_LATTICE_NO_SMEM")) {
         const bool dt = A.dtab != nullptr && !getenv_flag("RTK_LATTICE_NO_DTAB");
-        auto kern = dt ? lattice_int_smem_kernel<FS, SRC, OUT, true> : lattice_int_smem_kernel<FS, SRC, OUT, false>;
+        const bool planar = A.ny == 1 && !getenv_flag("RTK_LATTICE_NO_PLANAR");
+        auto kern = dt ? (planar ? lattice_int_smem_kernel<FS, SRC, OUT, true, true>
+                                 : lattice_int_smem_kernel<FS, SRC, OUT, true, false>)
+                       : (planar ? lattice_int_smem_kernel<FS, SRC, OUT, false, true>
+                                 : lattice_int_smem_kernel<FS, SRC, OUT, false, false>);
         if (smem_planes > 48 * 1024 &&
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_planes)) !=
                 cudaSuccess)
@@ -907,19 +945,20 @@ int lattice_transfer_intensity(const Problem& p, int src_mode, int out_mode, boo
     return set_error(RTK_EINVAL, "lattice: unsupported source/output mode");
 }
 
-template <int FS, int SRC, int NM>
-static int launch_mom_steps(const Problem& p, const LatArgs& A, bool with_inflow, double* mom, cudaStream_t s) {
+template <int FS, int SRC, int NM, int DG>
+static int launch_mom_steps_dg(const Problem& p, const LatArgs& A, bool with_inflow, double* mom, cudaStream_t s) {
     const unsigned pblocks = static_cast<unsigned>((A.nxy * p.fp + 255) / 256);
     constexpr int F = 2;   // F = 4 measured slower (176 registers, 1 block/SM; cfg5 854 vs 487 ms)
-    // 128-thread blocks: a layer step has only nxy * fp / F threads (cfg4: 65,536), so small
-    // blocks spread them evenly over the SMs (256-thread blocks left 40 SMs half occupied)
-    const int mb = getenv("RTK_LAT_BLOCK") ? atoi(getenv("RTK_LAT_BLOCK")) : 128;
+    // DG = 1: 128-thread blocks spread the nxy * fp / F items of a step evenly over the SMs;
+    // DG > 1: 32 items x DG direction groups per block
+    const int mb = DG == 1 ? 128 : 32 * DG;
+    const int ipb = mb / DG;
     const size_t mom_smem = sizeof(double) * NM * F * mb + sizeof(StepDir) * A.n_dirs +
                             sizeof(Shift) * (2 * A.n_dirs + A.total_sub);
+    auto kern = lattice_mom_group_kernel<FS, NM, F, DG>;
     if (mom_smem > 48 * 1024)
-        RTK_CUDA_TRY(cudaFuncSetAttribute(lattice_mom_group_kernel<FS, NM, F>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(mom_smem)));
-    const unsigned sblocks = static_cast<unsigned>((A.nxy * ((p.fp + F - 1) / F) + mb - 1) / mb);
+        RTK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(mom_smem)));
+    const unsigned sblocks = static_cast<unsigned>((A.nxy * ((p.fp + F - 1) / F) + ipb - 1) / ipb);
     double* a = p.lat_state[0];
     double* b = p.lat_state[1];
     for (int t = 0; t < A.nz; ++t) {
@@ -929,14 +968,24 @@ static int launch_mom_steps(const Problem& p, const LatArgs& A, bool with_inflow
             lattice_splane_kernel<SRC, NM><<<pblocks, 256, 0, s>>>(A, t, cur, nxt, t == 0 ? 1 : 0, p.fp);
             RTK_LAUNCH_CHECK("lattice_splane_kernel");
         }
-        lattice_mom_group_kernel<FS, NM, F><<<sblocks, mb, mom_smem, s>>>(
-            A, t, a, b, mom, with_inflow ? 1 : 0, p.fp, cur, nxt);
+        kern<<<sblocks, mb, mom_smem, s>>>(A, t, a, b, mom, with_inflow ? 1 : 0, p.fp, cur, nxt);
         RTK_LAUNCH_CHECK("lattice_mom_group_kernel");
         double* tmp = a;
         a = b;
         b = tmp;
     }
     return RTK_OK;
+}
+
+template <int FS, int SRC, int NM>
+static int launch_mom_steps(const Problem& p, const LatArgs& A, bool with_inflow, double* mom, cudaStream_t s) {
+    // direction groups only where a step has too few items to fill the SMs: measured cfg4
+    // (65,536 items) 45.0 -> 41.3 ms with DG = 8; cfg5 (344,064 items) is slower with it
+    const int64_t items = A.nxy * ((p.fp + 1) / 2);
+    const int dg = getenv("RTK_LAT_DG") ? atoi(getenv("RTK_LAT_DG")) : (items <= 131072 ? 8 : 1);
+    if (dg == 1) return launch_mom_steps_dg<FS, SRC, NM, 1>(p, A, with_inflow, mom, s);
+    if (dg == 4) return launch_mom_steps_dg<FS, SRC, NM, 4>(p, A, with_inflow, mom, s);
+    return launch_mom_steps_dg<FS, SRC, NM, 8>(p, A, with_inflow, mom, s);
 }
 
 template <int FS, int SRC>
