@@ -103,7 +103,7 @@ typedef struct rtk_lattice_desc {
     int32_t n_dirs;
     int32_t n_freq;
     int32_t n_moments;            /* 1..RTK_MAX_MOMENTS */
-    int32_t formal_solver;        /* RTK_FS_IE or RTK_FS_EXP_LINEAR */
+    int32_t formal_solver;        /* RTK_FS_IE, RTK_FS_EXP_LINEAR or RTK_FS_EXP_PARABOLIC */
     int32_t layout;               /* RTK_LAYOUT_* */
     double dx, dy, dz;
     const double* omega;          /* [n_dirs][3] unit vectors, omega_z != 0 */

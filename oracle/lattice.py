@@ -21,7 +21,11 @@ implements:
   sub-nodes by trilinear interpolation (T_CR): bilinear in the layer, linear
   between the two layers; dt = len * (chi_a + chi_b) / 2 per sub-segment;
 * the recursion per sub-segment is the reference IE (R/_kernels.py:96) or the
-  exp-linear extension, on dtau = phi_f dt;
+  exp-linear extension, on dtau = phi_f dt; exp-parabolic (Kunasz-Auer) updates the
+  point P_j of a line from P_{j-1}, P_j and the downwind P_{j+1}: the next sub-node of
+  the step, or for a step's last point (the crossing of the next layer) the point one
+  sub-segment beyond it, P_n + s / n_sub between the next two layers; the line's last
+  segment (exit layer) uses the linear weights, as in the 1D sweep;
 * line values at a layer go back to the nodes of that layer by bilinear
   interpolation from the four surrounding lines (T_RC, rows sum to one).
 
@@ -45,7 +49,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from oracle.rt_oracle import _linear_weights
+from oracle.rt_oracle import _linear_weights, _parabolic_weights
 
 
 @dataclass
@@ -166,7 +170,9 @@ def lattice_transfer(d: LatticeDesc, S: np.ndarray, with_boundary: bool = False,
             if short:
                 # restart at the upwind point of each node of layer k2, from layer k's nodes
                 state = _bilinear_sample(state.reshape(ny, nx, nf), gi - sx, gj - sy)
-            prev_S = prev_chi = None
+            # sample points of the step: m = 0 .. n_sub (+ the downwind point beyond the step for
+            # exp-parabolic, when a further layer step exists)
+            pts = []
             for m in range(n_sub + 1):
                 if short:
                     X = gi + (m / n_sub - 1.0) * sx
@@ -178,15 +184,33 @@ def lattice_transfer(d: LatticeDesc, S: np.ndarray, with_boundary: bool = False,
                 wz = m / n_sub
                 s_m = (1 - wz) * _bilinear_sample(Sa, X, Y) + wz * _bilinear_sample(Sb, X, Y)
                 c_m = (1 - wz) * _bilinear_sample(chi3[k], X, Y) + wz * _bilinear_sample(chi3[k2], X, Y)
-                if m > 0:
-                    dt = sub_len * (prev_chi + c_m) * 0.5
-                    dtau = d.phi[None, :] * dt[:, None]
-                    if solver == "ie":
-                        state = (state + dtau * s_m) / (1.0 + dtau)
-                    else:
-                        att, wu, wc = _linear_weights(dtau)
-                        state = att * state + wu * prev_S + wc * s_m
-                prev_S, prev_chi = s_m, c_m
+                pts.append((s_m, c_m, X, Y))
+            down_pt = None
+            if solver == "exp_parabolic" and t < nz - 2:
+                k3 = k2 + 1 if down else k2 - 1
+                X = pts[-1][2] + sx / n_sub
+                Y = pts[-1][3] + sy / n_sub
+                wz = 1.0 / n_sub
+                s_x = (1 - wz) * _bilinear_sample(S4[k2, :, :, a, :], X, Y) + wz * _bilinear_sample(
+                    S4[k3, :, :, a, :], X, Y)
+                c_x = (1 - wz) * _bilinear_sample(chi3[k2], X, Y) + wz * _bilinear_sample(chi3[k3], X, Y)
+                down_pt = (s_x, c_x)
+            for m in range(1, n_sub + 1):
+                (prev_S, prev_chi), (s_m, c_m) = pts[m - 1][:2], pts[m][:2]
+                dtau = d.phi[None, :] * (sub_len * (prev_chi + c_m) * 0.5)[:, None]
+                nxt = pts[m + 1][:2] if m < n_sub else down_pt
+                if solver == "ie":
+                    state = (state + dtau * s_m) / (1.0 + dtau)
+                elif solver == "exp_parabolic" and nxt is not None:
+                    s_d, c_d = nxt
+                    dd = d.phi[None, :] * (sub_len * (c_m + c_d) * 0.5)[:, None]
+                    att, wu, wc, wd = _parabolic_weights(dtau, dd)
+                    state = att * state + wu * prev_S + wc * s_m + wd * s_d
+                elif solver in ("exp_linear", "exp_parabolic"):
+                    att, wu, wc = _linear_weights(dtau)
+                    state = att * state + wu * prev_S + wc * s_m
+                else:
+                    raise ValueError(f"unknown formal solver {solver!r}")
     return out.reshape(d.n_space, na, nf)
 
 

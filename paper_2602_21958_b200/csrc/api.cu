@@ -56,9 +56,10 @@ Problem::~Problem() {
     if (dtpad_mom) cudaFree(dtpad_mom);
     if (lat_sub_shift) cudaFree(lat_sub_shift);
     if (lat_gat_shift) cudaFree(lat_gat_shift);
+    if (lat_down_shift) cudaFree(lat_down_shift);
     if (lat_dtab) cudaFree(lat_dtab);
     double* lat[] = {lat_chi, lat_in_top, lat_in_bot, lat_state[0], lat_state[1], lat_src, lat_zero, lat_splane[0],
-                     lat_splane[1]};
+                     lat_splane[1], lat_splane[2]};
     for (double* b : lat)
         if (b) cudaFree(b);
 }
@@ -238,8 +239,9 @@ int rtk_problem_create_lattice(const rtk_lattice_desc* d, rtk_problem** out) {
     if (d->n_dirs < 1 || d->n_freq < 1) return set_error(RTK_EINVAL, "need at least one direction and frequency");
     if (d->n_moments < 1 || d->n_moments > RTK_MAX_MOMENTS)
         return set_error(RTK_EINVAL, "n_moments must be in 1.." + std::to_string(RTK_MAX_MOMENTS));
-    if (d->formal_solver != RTK_FS_IE && d->formal_solver != RTK_FS_EXP_LINEAR)
-        return set_error(RTK_EINVAL, "lattice problems support the IE and exp-linear formal solvers");
+    if (d->formal_solver != RTK_FS_IE && d->formal_solver != RTK_FS_EXP_LINEAR &&
+        d->formal_solver != RTK_FS_EXP_PARABOLIC)
+        return set_error(RTK_EINVAL, "unknown formal solver");
     if (d->layout != RTK_LAYOUT_INTENSITY && d->layout != RTK_LAYOUT_MOMENTS)
         return set_error(RTK_EINVAL, "unknown layout");
     if (!(d->dx > 0 && d->dy > 0 && d->dz > 0)) return set_error(RTK_EINVAL, "spacings must be positive");
@@ -296,6 +298,8 @@ int rtk_problem_create_lattice(const rtk_lattice_desc* d, rtk_problem** out) {
         if (!rc) rc = rtk::upload(&p.lat_state[1], nullptr, plane);
         if (!rc) rc = rtk::upload(&p.lat_splane[0], nullptr, plane);
         if (!rc) rc = rtk::upload(&p.lat_splane[1], nullptr, plane);
+        // exp-parabolic reads the plane after next (downwind point of a step's last sub-node)
+        if (!rc && d->formal_solver == RTK_FS_EXP_PARABOLIC) rc = rtk::upload(&p.lat_splane[2], nullptr, plane);
     }
     if (!rc) rc = rtk::upload(&p.lat_zero, nullptr, static_cast<size_t>(p.n_space) * p.n_freq);
     if (!rc) rc = rtk::setup_lattice(p, d);

@@ -100,6 +100,7 @@ struct LatArgs {
     const LatDir* dirs;
     const Shift* sub_shift;   // [dir: shift_off + t * (n_sub + 1) + m] sub-node shifts
     const Shift* gat_shift;   // [dir * nz + t] T_RC gather shifts
+    const Shift* down_shift;  // [dir * nz + t] exp-parabolic downwind point of step t's last sub-node
     const double* dtab;       // sub-segment optical paths (moment layout), see lattice_dtab_kernel
     const double* chi;      // [n_space]
     const double* phi;      // [n_freq]
@@ -234,6 +235,74 @@ __device__ __forceinline__ void advance_line_smem4(const LatDir& D, const Shift*
     }
 }
 
+// Exp-parabolic (Kunasz-Auer) variant of advance_line_smem4 (oracle/lattice.py): the point
+// P_m of the step is updated from P_{m-1}, P_m and the downwind P_{m+1}; for the step's last
+// point the downwind is one sub-segment beyond the crossing (shift dsh, planes b / c of the
+// next two layers), or, on the line's last step (no plane c), the linear weights are used.
+// Samples are streamed one ahead; dt comes from the opacity planes (same arithmetic as the
+// dt table, so LC results equal the table-driven kernels').
+template <bool PLANAR>
+struct ParSample {
+    double s[kFC];
+    double c;
+};
+
+template <bool PLANAR>
+__device__ __forceinline__ void sample_planes(ParSample<PLANAR>& o, const Stencil& st, double wz,
+                                              const double* chi_a, const double* chi_b, const double* Sa,
+                                              const double* Sb) {
+    const double ca = PLANAR ? st.w00 * chi_a[st.c00] + st.w10 * chi_a[st.c10]
+                             : st.w00 * chi_a[st.c00] + st.w10 * chi_a[st.c10] + st.w01 * chi_a[st.c01] +
+                                   st.w11 * chi_a[st.c11];
+    const double cb = PLANAR ? st.w00 * chi_b[st.c00] + st.w10 * chi_b[st.c10]
+                             : st.w00 * chi_b[st.c00] + st.w10 * chi_b[st.c10] + st.w01 * chi_b[st.c01] +
+                                   st.w11 * chi_b[st.c11];
+    o.c = (1 - wz) * ca + wz * cb;
+#pragma unroll
+    for (int q = 0; q < kFC; ++q) {
+        const double pa = PLANAR ? st.w00 * Sa[st.c00 * kFC + q] + st.w10 * Sa[st.c10 * kFC + q]
+                                 : st.w00 * Sa[st.c00 * kFC + q] + st.w10 * Sa[st.c10 * kFC + q] +
+                                       st.w01 * Sa[st.c01 * kFC + q] + st.w11 * Sa[st.c11 * kFC + q];
+        const double pb = PLANAR ? st.w00 * Sb[st.c00 * kFC + q] + st.w10 * Sb[st.c10 * kFC + q]
+                                 : st.w00 * Sb[st.c00 * kFC + q] + st.w10 * Sb[st.c10 * kFC + q] +
+                                       st.w01 * Sb[st.c01 * kFC + q] + st.w11 * Sb[st.c11 * kFC + q];
+        o.s[q] = (1 - wz) * pa + wz * pb;
+    }
+}
+
+template <bool PLANAR>
+__device__ __forceinline__ void advance_line_smem4_par(const LatDir& D, const Shift* __restrict__ sub, Shift dsh,
+                                                       double (&acc)[kFC], int lx, int ly, int nx, int ny,
+                                                       const double* chi_a, const double* chi_b,
+                                                       const double* chi_c, const double* Sa, const double* Sb,
+                                                       const double* Sc, const double (&phi)[kFC]) {
+    ParSample<PLANAR> prev, cur, nxt;
+    sample_planes<PLANAR>(prev, stencil_at(lx, ly, sub[0], nx, ny), 0.0, chi_a, chi_b, Sa, Sb);
+    sample_planes<PLANAR>(cur, stencil_at(lx, ly, sub[1], nx, ny), 1.0 / D.n_sub, chi_a, chi_b, Sa, Sb);
+    for (int m = 1; m <= D.n_sub; ++m) {
+        const bool down = m < D.n_sub || Sc != nullptr;
+        if (m < D.n_sub)
+            sample_planes<PLANAR>(nxt, stencil_at(lx, ly, sub[m + 1], nx, ny), static_cast<double>(m + 1) / D.n_sub,
+                                  chi_a, chi_b, Sa, Sb);
+        else if (Sc != nullptr)
+            sample_planes<PLANAR>(nxt, stencil_at(lx, ly, dsh, nx, ny), 1.0 / D.n_sub, chi_b, chi_c, Sb, Sc);
+        const double dtu = D.sub_len * (prev.c + cur.c) * 0.5;
+        const double dtd = D.sub_len * (cur.c + nxt.c) * 0.5;
+#pragma unroll
+        for (int q = 0; q < kFC; ++q) {
+            if (down) {
+                const ExpPar w = exp_parabolic_weights_bf(phi[q] * dtu, phi[q] * dtd);
+                acc[q] = fma(acc[q], w.att, w.wu * prev.s[q] + w.wc * cur.s[q] + w.wd * nxt.s[q]);
+            } else {
+                const ExpLin w = exp_linear_weights_bf(phi[q] * dtu);
+                acc[q] = fma(acc[q], w.att, w.wu * prev.s[q] + w.wc * cur.s[q]);
+            }
+        }
+        prev = cur;
+        cur = nxt;
+    }
+}
+
 // Intensity layout, small layers (nxy <= ~1000, e.g. the 2D slab): one CTA per
 // (direction, 4-frequency chunk), one thread per line handling the 4 frequencies.
 // The source / opacity planes the lines cross and the x plane of the y = x - v gather
@@ -250,9 +319,11 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
     const int nxy = static_cast<int>(A.nxy);
     constexpr bool XM = (OUT == OUT_X_MINUS);
     double* lines = sm;                         // [nxy][kFC]
-    double* splane = lines + nxy * kFC;         // [3][nxy][kFC]
-    double* cplane = splane + 3 * nxy * kFC;    // [3][nxy]         (opacity; unused with DT)
-    double* xplane = cplane + 3 * nxy;          // [2][nxy][kFC]   (XM only)
+    constexpr bool PAR = FS == RTK_FS_EXP_PARABOLIC;
+    constexpr int RING = PAR ? 4 : 3;           // source / opacity plane ring (PAR reads layer t + 2)
+    double* splane = lines + nxy * kFC;         // [RING][nxy][kFC]
+    double* cplane = splane + RING * nxy * kFC; // [RING][nxy]      (opacity; unused with DT)
+    double* xplane = cplane + RING * nxy;       // [2][nxy][kFC]   (XM only)
     double* seeds = xplane + 2 * nxy * kFC;     // [nxy][kFC] SC restart values
     Shift* shs = reinterpret_cast<Shift*>(seeds + nxy * kFC);   // [max_sub + 1] shifts of the step
     const int nfc = (A.n_freq + kFC - 1) / kFC;
@@ -307,6 +378,8 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
         issue_x(layer_of(1), 1);
     }
     commit();
+    if (PAR && A.nz > 2) issue_planes(layer_of(2), 2);
+    if (PAR) commit();
     for (int t = 0; t < A.nz; ++t) {
         const int k = layer_of(t);
         // groups committed so far: t + 2 (steps 0..t+1); step t needs groups 0..t+1 (planes t and
@@ -314,7 +387,7 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
         asm volatile("cp.async.wait_group 0;\n" ::);
         __syncthreads();
         // prefetch for step t+1: planes of layer t+2 into the slot last used at step t-1, x of t+1
-        if (t + 2 < A.nz) issue_planes(layer_of(t + 2), (t + 2) % 3);
+        if (t + RING - 1 < A.nz) issue_planes(layer_of(t + RING - 1), (t + RING - 1) % RING);
         if (t + 1 < A.nz && t > 0) issue_x(layer_of(t + 1), (t + 1) & 1);
         commit();
         // T_RC gather: one thread per (node, frequency) for coalesced y writes
@@ -346,15 +419,22 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
         }
         __syncthreads();   // the gather read `lines` before the march overwrites them; shifts staged
         const double* start = D.sc ? seeds : lines;
-        const double* Sa = splane + (t % 3) * nxy * kFC;
-        const double* Sb = splane + ((t + 1) % 3) * nxy * kFC;
-        const double* ca = cplane + (t % 3) * nxy;
-        const double* cb = cplane + ((t + 1) % 3) * nxy;
+        const double* Sa = splane + (t % RING) * nxy * kFC;
+        const double* Sb = splane + ((t + 1) % RING) * nxy * kFC;
+        const double* ca = cplane + (t % RING) * nxy;
+        const double* cb = cplane + ((t + 1) % RING) * nxy;
+        const bool has_c = PAR && t + 2 < A.nz;
+        const double* Sc = has_c ? splane + ((t + 2) % RING) * nxy * kFC : nullptr;
+        const double* cc = has_c ? cplane + ((t + 2) % RING) * nxy : nullptr;
+        const Shift dsh = PAR ? A.down_shift[a * A.nz + t] : Shift{};
         for (int c = threadIdx.x; c < nxy; c += blockDim.x) {
             const int ly = c / A.nx, lx = c - ly * A.nx;
             double acc[kFC];
 #pragma unroll
             for (int q = 0; q < kFC; ++q) acc[q] = start[c * kFC + q];
+            if (PAR)
+                advance_line_smem4_par<PLANAR>(D, shs, dsh, acc, lx, ly, A.nx, A.ny, ca, cb, cc, Sa, Sb, Sc, phi);
+            else
             advance_line_smem4<FS, DT, PLANAR>(D, shs, acc, lx, ly, t, A.nx, A.ny, ca, cb, Sa, Sb, phi,
                                        DT ? A.dtab + D.dtab_off + static_cast<int64_t>(t) * D.n_sub * A.nxy + c : nullptr,
                                        nxy);
@@ -487,6 +567,68 @@ __device__ __forceinline__ void advance_lineF(const LatDir& D, const Shift* __re
     }
 }
 
+// Exp-parabolic advance of a line over one layer step in the moment layout (oracle/lattice.py):
+// point m is updated from m - 1, m and the downwind m + 1; the downwind of the step's last
+// point lies one sub-segment beyond the crossing (shift dsh, planes Sb / Sc of the next two
+// layers, dt from the opacity: chi_a / chi_b / chi_c are the three layers), or the linear
+// weights apply on the line's last step (Sc == nullptr).  Interior dt from the table.
+template <int F>
+__device__ __forceinline__ void sample_s2(double (&out)[F], const Stencil& st, double wz, const double2* __restrict__ Sa,
+                                          const double2* __restrict__ Sb, int64_t ss) {
+#pragma unroll
+    for (int h = 0; h < F / 2; ++h) {
+        const double2 a00 = __ldg(Sa + st.c00 * ss + h), a10 = __ldg(Sa + st.c10 * ss + h);
+        const double2 a01 = __ldg(Sa + st.c01 * ss + h), a11 = __ldg(Sa + st.c11 * ss + h);
+        const double2 b00 = __ldg(Sb + st.c00 * ss + h), b10 = __ldg(Sb + st.c10 * ss + h);
+        const double2 b01 = __ldg(Sb + st.c01 * ss + h), b11 = __ldg(Sb + st.c11 * ss + h);
+        out[2 * h] = (1 - wz) * (st.w00 * a00.x + st.w10 * a10.x + st.w01 * a01.x + st.w11 * a11.x) +
+                     wz * (st.w00 * b00.x + st.w10 * b10.x + st.w01 * b01.x + st.w11 * b11.x);
+        out[2 * h + 1] = (1 - wz) * (st.w00 * a00.y + st.w10 * a10.y + st.w01 * a01.y + st.w11 * a11.y) +
+                         wz * (st.w00 * b00.y + st.w10 * b10.y + st.w01 * b01.y + st.w11 * b11.y);
+    }
+}
+
+template <int F>
+__device__ __forceinline__ void advance_lineF_par(int n_sub, double sub_len, const Shift* __restrict__ sub, Shift dsh,
+                                                  double (&acc)[F], int lx, int ly, int nx, int ny,
+                                                  const double2* __restrict__ Sa, const double2* __restrict__ Sb,
+                                                  const double2* __restrict__ Sc, int64_t ss, const double (&phi)[F],
+                                                  const double* __restrict__ dtab, int64_t nxy,
+                                                  const double* __restrict__ chi_a, const double* __restrict__ chi_b,
+                                                  const double* __restrict__ chi_c) {
+    const double inv_n = 1.0 / n_sub;
+    double sp[F], sc[F], sn[F];
+    sample_s2<F>(sp, stencil_at(lx, ly, sub[0], nx, ny), 0.0, Sa, Sb, ss);
+    sample_s2<F>(sc, stencil_at(lx, ly, sub[1], nx, ny), inv_n, Sa, Sb, ss);
+    double dtu = __ldg(dtab);
+    for (int m = 1; m <= n_sub; ++m) {
+        const bool down = m < n_sub || Sc != nullptr;
+        double dtd = 0.0;
+        if (m < n_sub) {
+            sample_s2<F>(sn, stencil_at(lx, ly, sub[m + 1], nx, ny), static_cast<double>(m + 1) / n_sub, Sa, Sb, ss);
+            dtd = __ldg(dtab + static_cast<int64_t>(m) * nxy);
+        } else if (Sc != nullptr) {
+            const Stencil sx = stencil_at(lx, ly, dsh, nx, ny);
+            sample_s2<F>(sn, sx, inv_n, Sb, Sc, ss);
+            const double cn = chi_at(stencil_at(lx, ly, sub[n_sub], nx, ny), 1.0, chi_a, chi_b);
+            dtd = sub_len * (cn + chi_at(sx, inv_n, chi_b, chi_c)) * 0.5;
+        }
+#pragma unroll
+        for (int q = 0; q < F; ++q) {
+            if (down) {
+                const ExpPar w = exp_parabolic_weights_bf(phi[q] * dtu, phi[q] * dtd);
+                acc[q] = fma(acc[q], w.att, w.wu * sp[q] + w.wc * sc[q] + w.wd * sn[q]);
+            } else {
+                const ExpLin w = exp_linear_weights_bf(phi[q] * dtu);
+                acc[q] = fma(acc[q], w.att, w.wu * sp[q] + w.wc * sc[q]);
+            }
+            sp[q] = sc[q];
+            sc[q] = sn[q];
+        }
+        dtu = dtd;
+    }
+}
+
 // dt table: dtab[D.dtab_off + (t * n_sub + m - 1) * nxy + c] = sub_len (chi(m-1) + chi(m)) / 2,
 // computed with the same expressions as the on-the-fly path.
 __global__ void lattice_dtab_kernel(const LatDir* __restrict__ dirs, const Shift* __restrict__ sub_shift,
@@ -534,7 +676,8 @@ __global__ void __launch_bounds__(DG == 1 ? 128 : 256, DG == 1 ? 5 : 3)
                                                                  double* __restrict__ st_out, double* __restrict__ mom,
                                                                  int with_inflow, int fp,
                                                                  const double* __restrict__ plane_cur,
-                                                                 const double* __restrict__ plane_next) {
+                                                                 const double* __restrict__ plane_next,
+                                                                 const double* __restrict__ plane_nn) {
     const int ng = (fp + F - 1) / F;       // groups per line
     const int hp = fp >> 1;                // double2 per line in the [dir][line][fp] planes
     // this step's direction metadata and shifts, staged once per CTA in shared memory (the
@@ -598,6 +741,7 @@ __global__ void __launch_bounds__(DG == 1 ? 128 : 256, DG == 1 ? 5 : 3)
     double2* sout2 = reinterpret_cast<double2*>(st_out);
     const double2* pc2 = reinterpret_cast<const double2*>(plane_cur);
     const double2* pn2 = reinterpret_cast<const double2*>(plane_next);
+    const double2* pnn2 = reinterpret_cast<const double2*>(plane_nn);   // exp-parabolic, may be null
     const int g2 = f0 >> 1;               // first double2 of the group within a line
     for (int hemi = 0; hemi < 2; ++hemi) {       // 0: down (layer t), 1: up (layer nz-1-t)
         const int k = hemi == 0 ? t : A.nz - 1 - t;
@@ -668,7 +812,31 @@ __global__ void __launch_bounds__(DG == 1 ? 128 : 256, DG == 1 ? 5 : 3)
                 }
                 LatDir Dl;
                 Dl.n_sub = D.n_sub;
-                if (full_group) {
+                constexpr bool PAR = FS == RTK_FS_EXP_PARABOLIC;
+                const int k3 = hemi == 0 ? k2 + 1 : k2 - 1;
+                const Shift dsh = PAR ? A.down_shift[a * A.nz + t] : Shift{};
+                const double* chk = A.chi + static_cast<int64_t>(k) * A.nxy;
+                const double* chk2 = A.chi + static_cast<int64_t>(k2) * A.nxy;
+                const double* chk3 = pnn2 ? A.chi + static_cast<int64_t>(k3) * A.nxy : nullptr;
+                if (PAR && full_group) {
+                    advance_lineF_par<F>(D.n_sub, A.dirs[a].sub_len, ssub + D.sub_pref, dsh, acc, i, j, A.nx, A.ny,
+                                         pc2 + a * plane2 + g2, pn2 + a * plane2 + g2,
+                                         pnn2 ? pnn2 + a * plane2 + g2 : nullptr, hp, phi, A.dtab + D.dtab + c, A.nxy,
+                                         chk, chk2, chk3);
+#pragma unroll
+                    for (int h = 0; h < F / 2; ++h)
+                        sout2[a * plane2 + static_cast<int64_t>(c) * hp + g2 + h] = make_double2(acc[2 * h], acc[2 * h + 1]);
+                } else if (PAR) {
+                    for (int h = 0; h < F / 2 && g2 + h < hp; ++h) {
+                        double ap[2] = {acc[2 * h], acc[2 * h + 1]};
+                        const double pp[2] = {phi[2 * h], phi[2 * h + 1]};
+                        advance_lineF_par<2>(D.n_sub, A.dirs[a].sub_len, ssub + D.sub_pref, dsh, ap, i, j, A.nx, A.ny,
+                                             pc2 + a * plane2 + g2 + h, pn2 + a * plane2 + g2 + h,
+                                             pnn2 ? pnn2 + a * plane2 + g2 + h : nullptr, hp, pp,
+                                             A.dtab + D.dtab + c, A.nxy, chk, chk2, chk3);
+                        sout2[a * plane2 + static_cast<int64_t>(c) * hp + g2 + h] = make_double2(ap[0], ap[1]);
+                    }
+                } else if (full_group) {
                     advance_lineF<FS, F, true>(Dl, ssub + D.sub_pref, acc, i, j, t, A.nx, A.ny, nullptr, nullptr,
                                                pc2 + a * plane2 + g2, pn2 + a * plane2 + g2, hp, phi,
                                                A.dtab + D.dtab + c, A.nxy);
@@ -721,12 +889,14 @@ __global__ void __launch_bounds__(DG == 1 ? 128 : 256, DG == 1 ? 5 : 3)
     }
 }
 
-// Source planes: for every direction a, S_a on the layer it reaches next (down: t+1,
-// up: nz-2-t), and at t = 0 also on its entry layer; S = gamma sum_l c_l Y_l(a) u_l
-// (SRC_U) or the isotropic thermal source (SRC_ISO).  Layout plane[a][c][f].
+// Source planes: for every direction a, S_a on the layers its march visits at offsets
+// o = 0, 1, 2 from step t (down: t + o, up: nz - 1 - t - o) into plane_o, for the offsets in
+// fill_mask (bit o); S = gamma sum_l c_l Y_l(a) u_l (SRC_U) or the isotropic thermal source
+// (SRC_ISO).  Layout plane[a][c][f].  Offset 2 is the exp-parabolic downwind plane.
 template <int SRC, int NM>
-__global__ void __launch_bounds__(256) lattice_splane_kernel(LatArgs A, int t, double* __restrict__ plane_cur,
-                                                              double* __restrict__ plane_next, int fill_cur, int fp) {
+__global__ void __launch_bounds__(256) lattice_splane_kernel(LatArgs A, int t, double* __restrict__ plane0,
+                                                              double* __restrict__ plane1,
+                                                              double* __restrict__ plane2, int fill_mask, int fp) {
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (tid >= A.nxy * fp) return;
     const int64_t c = tid / fp;
@@ -734,18 +904,20 @@ __global__ void __launch_bounds__(256) lattice_splane_kernel(LatArgs A, int t, d
     const bool fvalid = fpad < A.n_freq;
     const int f = fvalid ? fpad : 0;
     const int64_t plane = A.nxy * fp;
-    // layers: [0] down-current, [1] up-current, [2] down-next, [3] up-next
-    const int layers[4] = {t, A.nz - 1 - t, t + 1, A.nz - 2 - t};
-    double uval[4][NM], g[4];
+    double* planes[3] = {plane0, plane1, plane2};
+    // q = 2 o + (0: down, 1: up)
+    double uval[6][NM], g[6];
+    bool use[6];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        if (q < 2 && !fill_cur) {
-            g[q] = 0.0;
+    for (int q = 0; q < 6; ++q) {
+        const int o = q >> 1;
+        const int layer = (q & 1) ? A.nz - 1 - t - o : t + o;
+        use[q] = ((fill_mask >> o) & 1) && layer >= 0 && layer < A.nz;
+        g[q] = 0.0;
 #pragma unroll
-            for (int l = 0; l < NM; ++l) uval[q][l] = 0.0;
-            continue;
-        }
-        const int64_t sidx = static_cast<int64_t>(layers[q]) * A.nxy + c;
+        for (int l = 0; l < NM; ++l) uval[q][l] = 0.0;
+        if (!use[q]) continue;
+        const int64_t sidx = static_cast<int64_t>(layer) * A.nxy + c;
         if (SRC == LSRC_U) {
 #pragma unroll
             for (int l = 0; l < NM; ++l) uval[q][l] = __ldg(A.src + (sidx * NM + l) * A.n_freq + f);
@@ -761,8 +933,8 @@ __global__ void __launch_bounds__(256) lattice_splane_kernel(LatArgs A, int t, d
 #pragma unroll
         for (int l = 0; l < NM; ++l) cy[l] = D.cy[l];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if ((q & 1) != qd || (q < 2 && !fill_cur)) continue;
+        for (int q = 0; q < 6; ++q) {
+            if ((q & 1) != qd || !use[q]) continue;
             double v;
             if (SRC == LSRC_U) {
                 v = 0.0;
@@ -772,8 +944,7 @@ __global__ void __launch_bounds__(256) lattice_splane_kernel(LatArgs A, int t, d
             } else {
                 v = g[q];
             }
-            double* dst = (q < 2) ? plane_cur : plane_next;
-            dst[a * plane + c * fp + fpad] = fvalid ? v : 0.0;
+            planes[q >> 1][a * plane + c * fp + fpad] = fvalid ? v : 0.0;
         }
     }
 }
@@ -804,7 +975,7 @@ int setup_lattice(Problem& p, const rtk_lattice_desc* d) {
         }
     }
     // warp-uniform interpolation shifts, tabulated once (same arithmetic as the device's shift_of)
-    std::vector<Shift> sub, gat(static_cast<size_t>(d->n_dirs) * d->nz);
+    std::vector<Shift> sub, gat(static_cast<size_t>(d->n_dirs) * d->nz), dsh(gat.size());
     p.lat_total_sub = 0;
     for (int a = 0; a < d->n_dirs; ++a) {
         LatDir& D = dirs[a];
@@ -822,15 +993,22 @@ int setup_lattice(Problem& p, const rtk_lattice_desc* d) {
                 const double tt = D.sc ? static_cast<double>(m) / D.n_sub - 1.0 : t + static_cast<double>(m) / D.n_sub;
                 sub.push_back(shift_of(tt * D.sx, tt * D.sy, d->nx, d->ny));
             }
-        for (int t = 0; t < d->nz; ++t)
+        for (int t = 0; t < d->nz; ++t) {
             gat[static_cast<size_t>(a) * d->nz + t] = D.sc ? shift_of(0.0, 0.0, d->nx, d->ny)
                                                            : shift_of(-t * D.sx, -t * D.sy, d->nx, d->ny);
+            // exp-parabolic: one sub-segment beyond the step's last point (LC: the line at
+            // t + 1 + 1/n_sub; SC: the node + s / n_sub)
+            const double td = D.sc ? 1.0 / D.n_sub : t + 1.0 + 1.0 / D.n_sub;
+            dsh[static_cast<size_t>(a) * d->nz + t] = shift_of(td * D.sx, td * D.sy, d->nx, d->ny);
+        }
     }
     if (sub.empty()) sub.push_back(Shift{});
     RTK_CUDA_TRY(cudaMalloc(&p.lat_sub_shift, sizeof(Shift) * sub.size()));
     RTK_CUDA_TRY(cudaMemcpy(p.lat_sub_shift, sub.data(), sizeof(Shift) * sub.size(), cudaMemcpyHostToDevice));
     RTK_CUDA_TRY(cudaMalloc(&p.lat_gat_shift, sizeof(Shift) * gat.size()));
     RTK_CUDA_TRY(cudaMemcpy(p.lat_gat_shift, gat.data(), sizeof(Shift) * gat.size(), cudaMemcpyHostToDevice));
+    RTK_CUDA_TRY(cudaMalloc(&p.lat_down_shift, sizeof(Shift) * dsh.size()));
+    RTK_CUDA_TRY(cudaMemcpy(p.lat_down_shift, dsh.data(), sizeof(Shift) * dsh.size(), cudaMemcpyHostToDevice));
     int64_t dtab_count = 0;
     const int64_t nxy = static_cast<int64_t>(d->nx) * d->ny;
     for (auto& D : dirs) {
@@ -870,6 +1048,7 @@ static LatArgs lat_args(const Problem& p, const double* src, const double* x, do
     A.dirs = p.lat_dirs;
     A.sub_shift = reinterpret_cast<const Shift*>(p.lat_sub_shift);
     A.gat_shift = reinterpret_cast<const Shift*>(p.lat_gat_shift);
+    A.down_shift = reinterpret_cast<const Shift*>(p.lat_down_shift);
     A.dtab = p.lat_dtab;
     A.total_sub = p.lat_total_sub;
     A.chi = p.lat_chi;
@@ -892,10 +1071,15 @@ static LatArgs lat_args(const Problem& p, const double* src, const double* x, do
 
 template <int FS, int SRC, int OUT>
 static int launch_int(const Problem& p, const LatArgs& A, int with_inflow, cudaStream_t s) {
-    const size_t smem_planes = sizeof(double) * A.nxy * (kFC + 3 * kFC + 3 + 2 * kFC + kFC) +
+    constexpr int ring = FS == RTK_FS_EXP_PARABOLIC ? 4 : 3;
+    const size_t smem_planes = sizeof(double) * A.nxy * (kFC + ring * kFC + ring + 2 * kFC + kFC) +
                                sizeof(Shift) * (p.lat_max_sub + 1);
+    if (FS == RTK_FS_EXP_PARABOLIC && (smem_planes > 160 * 1024 || getenv_flag("RTK_LATTICE_NO_SMEM")))
+        return set_error(RTK_ERESOURCE, "exp-parabolic in the intensity layout needs the shared-memory kernel "
+                                        "(small layers); use the moment layout");
     if (smem_planes <= 160 * 1024 && !getenv_flag("RTK_LATTICE_NO_SMEM")) {
-        const bool dt = A.dtab != nullptr && !getenv_flag("RTK_LATTICE_NO_DTAB");
+        // the parabolic march samples the opacity planes (its downwind segment is not in the table)
+        const bool dt = A.dtab != nullptr && !getenv_flag("RTK_LATTICE_NO_DTAB") && FS != RTK_FS_EXP_PARABOLIC;
         const bool planar = A.ny == 1 && !getenv_flag("RTK_LATTICE_NO_PLANAR");
         auto kern = dt ? (planar ? lattice_int_smem_kernel<FS, SRC, OUT, true, true>
                                  : lattice_int_smem_kernel<FS, SRC, OUT, true, false>)
@@ -940,6 +1124,7 @@ int lattice_transfer_intensity(const Problem& p, int src_mode, int out_mode, boo
         if (src_mode == LSRC_ISO && out_mode == OUT_ACC) return launch_int<FS, LSRC_ISO, OUT_ACC>(p, A, wi, s);         \
     } while (0)
     if (p.fs == RTK_FS_IE) RTK_LAT_INT(RTK_FS_IE);
+    else if (p.fs == RTK_FS_EXP_PARABOLIC) RTK_LAT_INT(RTK_FS_EXP_PARABOLIC);
     else RTK_LAT_INT(RTK_FS_EXP_LINEAR);
 #undef RTK_LAT_INT
     return set_error(RTK_EINVAL, "lattice: unsupported source/output mode");
@@ -961,14 +1146,20 @@ static int launch_mom_steps_dg(const Problem& p, const LatArgs& A, bool with_inf
     const unsigned sblocks = static_cast<unsigned>((A.nxy * ((p.fp + F - 1) / F) + ipb - 1) / ipb);
     double* a = p.lat_state[0];
     double* b = p.lat_state[1];
+    constexpr bool PAR = FS == RTK_FS_EXP_PARABOLIC;
+    constexpr int ring = PAR ? 3 : 2;   // source planes: current, next (and after next)
     for (int t = 0; t < A.nz; ++t) {
-        double* cur = p.lat_splane[t & 1];
-        double* nxt = p.lat_splane[(t + 1) & 1];
+        double* cur = p.lat_splane[t % ring];
+        double* nxt = p.lat_splane[(t + 1) % ring];
+        double* nn = PAR ? p.lat_splane[(t + 2) % ring] : nullptr;
         if (t < A.nz - 1) {
-            lattice_splane_kernel<SRC, NM><<<pblocks, 256, 0, s>>>(A, t, cur, nxt, t == 0 ? 1 : 0, p.fp);
+            // step 0 fills every plane of the ring; later steps only the newest one
+            const int mask = PAR ? (t == 0 ? 7 : 4) : (t == 0 ? 3 : 2);
+            lattice_splane_kernel<SRC, NM><<<pblocks, 256, 0, s>>>(A, t, cur, nxt, nn, mask, p.fp);
             RTK_LAUNCH_CHECK("lattice_splane_kernel");
         }
-        kern<<<sblocks, mb, mom_smem, s>>>(A, t, a, b, mom, with_inflow ? 1 : 0, p.fp, cur, nxt);
+        kern<<<sblocks, mb, mom_smem, s>>>(A, t, a, b, mom, with_inflow ? 1 : 0, p.fp, cur, nxt,
+                                           PAR && t + 2 < A.nz ? nn : nullptr);
         RTK_LAUNCH_CHECK("lattice_mom_group_kernel");
         double* tmp = a;
         a = b;
@@ -1010,6 +1201,10 @@ int lattice_transfer_moments(const Problem& p, int src_mode, bool with_inflow, c
     if (p.fs == RTK_FS_IE) {
         if (src_mode == LSRC_U) return dispatch_mom_nm<RTK_FS_IE, LSRC_U>(p, A, with_inflow, mom, s);
         return dispatch_mom_nm<RTK_FS_IE, LSRC_ISO>(p, A, with_inflow, mom, s);
+    }
+    if (p.fs == RTK_FS_EXP_PARABOLIC) {
+        if (src_mode == LSRC_U) return dispatch_mom_nm<RTK_FS_EXP_PARABOLIC, LSRC_U>(p, A, with_inflow, mom, s);
+        return dispatch_mom_nm<RTK_FS_EXP_PARABOLIC, LSRC_ISO>(p, A, with_inflow, mom, s);
     }
     if (src_mode == LSRC_U) return dispatch_mom_nm<RTK_FS_EXP_LINEAR, LSRC_U>(p, A, with_inflow, mom, s);
     return dispatch_mom_nm<RTK_FS_EXP_LINEAR, LSRC_ISO>(p, A, with_inflow, mom, s);

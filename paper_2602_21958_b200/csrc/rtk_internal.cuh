@@ -102,7 +102,7 @@ struct Problem {
     double* lat_state[2] = {nullptr, nullptr};   // [dir][line][freq] line values (moment layout)
     double* lat_src = nullptr;                   // full source vector (intensity layout)
     double* lat_zero = nullptr;                  // [n_space][n_freq] zeros (boundary-only RHS)
-    double* lat_splane[2] = {nullptr, nullptr};  // [dir][line][freq] source planes (moment layout ring)
+    double* lat_splane[3] = {nullptr, nullptr, nullptr};  // [dir][line][freq] source planes (moment layout ring)
     // slab moment layout (sweep_mom.cu)
     MomCta* mom_ctas = nullptr;
     int mom_n_ctas = 0, mom_n_groups = 0;
@@ -111,6 +111,7 @@ struct Problem {
     CUtensorMap mom_gmap, tma_dtmap_mom;
     void* lat_sub_shift = nullptr;               // Shift table (lattice.cu), sub-nodes
     void* lat_gat_shift = nullptr;               // Shift table, T_RC gathers
+    void* lat_down_shift = nullptr;              // Shift table, exp-parabolic downwind points
     double* lat_dtab = nullptr;                  // [dir][t][m][line] sub-segment optical paths
     int lat_max_sub = 0;                         // largest sub-segment count over the directions
     bool lat_any_sc = false;   // some direction uses short characteristics

@@ -151,8 +151,8 @@ class _LatticeHandle:
         d = LatticeDesc()
         d.nx, d.ny, d.nz = p.nx, p.ny, p.nz
         d.n_dirs, d.n_freq, d.n_moments = p.n_dirs, p.n_freq, p.n_mom
-        if p.formal_solver not in ("ie", "exp_linear"):
-            raise ValueError("lattice problems support the 'ie' and 'exp_linear' formal solvers")
+        if p.formal_solver not in ("ie", "exp_linear", "exp_parabolic"):
+            raise ValueError("formal_solver must be 'ie', 'exp_linear' or 'exp_parabolic'")
         d.formal_solver = _native.FS_CODES[p.formal_solver]
         d.layout = LAYOUTS[p.layout]
         if p.characteristics not in CHARACTERISTICS:

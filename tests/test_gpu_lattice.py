@@ -20,7 +20,7 @@ CASES = [  # (nx, ny, nz, n_polar, n_az, n_freq)
 
 @pytest.mark.parametrize("case", CASES)
 @pytest.mark.parametrize("layout", ["intensity", "moments"])
-@pytest.mark.parametrize("fs", ["ie", "exp_linear"])
+@pytest.mark.parametrize("fs", ["ie", "exp_linear", "exp_parabolic"])
 def test_lattice_matvec_matches_oracle(case, layout, fs):
     nx, ny, nz, npol, naz, nf = case
     p = L.lattice_problem(nx, ny, nz, npol, naz, nf, corr_len=2.0, seed=11, layout=layout, formal_solver=fs)
@@ -35,7 +35,7 @@ def test_lattice_matvec_matches_oracle(case, layout, fs):
 @pytest.mark.parametrize("case", CASES)
 @pytest.mark.parametrize("layout", ["intensity", "moments"])
 @pytest.mark.parametrize("chars", ["short", "hybrid"])
-@pytest.mark.parametrize("fs", ["ie", "exp_linear"])
+@pytest.mark.parametrize("fs", ["ie", "exp_linear", "exp_parabolic"])
 def test_short_and_hybrid_characteristics_match_oracle(case, layout, chars, fs):
     """Short characteristics (restart at each node's upwind point every layer step) and the
     hybrid (short for steep, long for grazing directions) against the oracle."""
@@ -115,3 +115,15 @@ def test_full_size_lattice_matvec_matches_oracle(cfg):
     d = OL.desc_from_lattice_problem(p)
     v = np.random.default_rng(cfg).standard_normal(p.n_total)
     assert rel_l2(P.apply_A(p, v), OL.apply_A(d, p.layout, v)) <= MATVEC_TOL
+
+
+def test_exp_parabolic_lattice_gmres_matches_oracle():
+    p = L.lattice_problem(6, 5, 8, 8, 8, 4, corr_len=2.0, seed=9, layout="moments", formal_solver="exp_parabolic",
+                          characteristics="hybrid")
+    d = OL.desc_from_lattice_problem(p)
+    b = OL.build_rhs(d, "moments")
+    ref = ro.gmres(lambda v: OL.apply_A(d, "moments", v), b, rel_tol=1e-8, max_iter=500)
+    rep = P.gmres(p, b, P.SolveConfig(rel_tol=1e-8, max_iter=500))
+    assert rep.converged and ref.converged
+    assert abs(rep.iterations - ref.iterations) <= 1
+    assert rel_l2(rep.solution, ref.solution) <= 1e-7

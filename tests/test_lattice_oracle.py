@@ -37,7 +37,7 @@ def _column_problem(nz=9, nf=4, solver="ie"):
     return p
 
 
-@pytest.mark.parametrize("solver", ["ie", "exp_linear"])
+@pytest.mark.parametrize("solver", ["ie", "exp_linear", "exp_parabolic"])
 def test_vertical_lines_reduce_to_reference_1d_sweep(solver):
     p = _column_problem(solver=solver)
     d = OL.desc_from_lattice_problem(p)
@@ -55,10 +55,12 @@ def test_vertical_lines_reduce_to_reference_1d_sweep(solver):
         np.testing.assert_allclose(out[:, 0, i, 1, :], up, rtol=1e-13, atol=1e-15)
 
 
-def test_integer_shift_direction_is_a_selection():
+@pytest.mark.parametrize("solver", ["ie", "exp_parabolic"])
+def test_integer_shift_direction_is_a_selection(solver):
     """sx = 1: lines hit nodes exactly at every layer, T_RC is a 0/1 selection and the
-    recursion is the 1D sweep along the node diagonal (periodic wrap in x)."""
-    p = tiny(nx=5, nz=6, nf=3)
+    recursion is the 1D sweep along the node diagonal (periodic wrap in x); for
+    exp-parabolic the downwind point of each node is the next node on the diagonal."""
+    p = tiny(nx=5, nz=6, nf=3, formal_solver=solver)
     p.omega = np.array([[1 / math.sqrt(2), 0.0, -1 / math.sqrt(2)]])
     p.dir_w = np.array([4 * math.pi])
     p.ybasis = L.dipole_harmonics(p.omega)
@@ -73,7 +75,7 @@ def test_integer_shift_direction_is_a_selection():
         dt = math.sqrt(2) * 0.5 * (c[1:] + c[:-1])
         dtau = p.phi[:, None] * dt[None, :]
         src = np.array([Sg[k, cols[k]] for k in range(p.nz)]).T
-        ref = ro.sweep_down(dtau, src).T
+        ref = ro.sweep_down(dtau, src, solver=solver).T
         got = np.array([out[k, cols[k]] for k in range(p.nz)])
         np.testing.assert_allclose(got, ref, rtol=1e-13, atol=1e-15)
 
@@ -124,7 +126,7 @@ def _desc(p, characteristics):
     return d
 
 
-@pytest.mark.parametrize("solver", ["ie", "exp_linear"])
+@pytest.mark.parametrize("solver", ["ie", "exp_linear", "exp_parabolic"])
 def test_short_characteristics_equal_long_on_integer_shift_directions(solver):
     """Vertical and sx = 1 directions: the upwind point of every node is a node, so the
     SC restart is a selection and SC, LC and hybrid coincide."""
@@ -140,7 +142,7 @@ def test_short_characteristics_equal_long_on_integer_shift_directions(solver):
         np.testing.assert_allclose(OL.lattice_transfer(_desc(p, mode), S), lc, rtol=1e-13, atol=1e-15)
 
 
-@pytest.mark.parametrize("solver", ["ie", "exp_linear"])
+@pytest.mark.parametrize("solver", ["ie", "exp_linear", "exp_parabolic"])
 def test_short_characteristics_equal_long_for_horizontally_uniform_fields(solver):
     """Horizontally uniform opacity and source: bilinear interpolation is exact, so SC = LC
     for every direction, including grazing ones with several sub-segments per layer."""
@@ -185,3 +187,32 @@ def test_characteristics_validation():
     p = tiny()
     with pytest.raises(ValueError):
         OL.lattice_transfer(_desc(p, "medium"), np.zeros((p.n_space, p.n_dirs, p.n_freq)))
+
+
+def test_exp_parabolic_constant_source_is_a_fixed_point():
+    """Kunasz-Auer weights sum to e0, so a constant source with matching inflow stays
+    constant through every sub-segment, layer crossing and downwind lookup."""
+    for chars in ("long", "short"):
+        p = tiny(nx=5, ny=3, nz=6, n_polar=8, n_az=4, nf=3, formal_solver="exp_parabolic")
+        p.inflow_top = np.full(p.n_freq, 0.3)
+        p.inflow_bottom = np.full(p.n_freq, 0.3)
+        S = np.full((p.n_space, p.n_dirs, p.n_freq), 0.3)
+        out = OL.lattice_transfer(_desc(p, chars), S, with_boundary=True)
+        np.testing.assert_allclose(out, 0.3, rtol=1e-12)
+
+
+def test_exp_parabolic_differs_from_linear_only_through_curvature():
+    """A source linear in depth along vertical lines in a uniform medium: parabolic and
+    linear interpolation agree (both exact); on a random source they differ."""
+    p = _column_problem(nz=9, nf=3, solver="exp_parabolic")
+    p.chi = np.ones_like(p.chi)
+    d_par = OL.desc_from_lattice_problem(p)
+    d_lin = OL.desc_from_lattice_problem(p)
+    d_lin.formal_solver = "exp_linear"
+    z = np.arange(p.nz, dtype=float)
+    S_lin = np.broadcast_to((2.0 + 0.5 * z)[:, None, None, None, None],
+                            (p.nz, p.ny, p.nx, 2, p.n_freq)).reshape(p.n_space, 2, p.n_freq).copy()
+    np.testing.assert_allclose(OL.lattice_transfer(d_par, S_lin), OL.lattice_transfer(d_lin, S_lin),
+                               rtol=1e-12, atol=1e-14)
+    S_rnd = np.random.default_rng(5).standard_normal((p.n_space, 2, p.n_freq))
+    assert np.abs(OL.lattice_transfer(d_par, S_rnd) - OL.lattice_transfer(d_lin, S_rnd)).max() > 1e-6
