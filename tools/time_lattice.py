@@ -17,6 +17,11 @@ def main():
   which = [int(a) for a in sys.argv[1:]] or [3, 4, 5]
   for cfg in which:
     kw = dict(CFGS[cfg])
+    import os
+    if os.environ.get("FS"):
+        kw["formal_solver"] = os.environ["FS"]
+    if os.environ.get("CHARS"):
+        kw["characteristics"] = os.environ["CHARS"]
     t0 = time.time()
     p = L.lattice_problem(seed=21958 + cfg, **kw)
     p.device()
