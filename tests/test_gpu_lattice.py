@@ -100,9 +100,12 @@ def test_lattice_rejects_bad_arguments():
     p = L.lattice_problem(4, 1, 4, 4, 4, 3, corr_len=1.0)
     with pytest.raises(ValueError):
         P.apply_A(p, np.zeros(7))
-    q = L.lattice_problem(4, 1, 4, 4, 4, 3, corr_len=1.0, formal_solver="exp_parabolic")
+    q = L.lattice_problem(4, 1, 4, 4, 4, 3, corr_len=1.0, formal_solver="exp_cubic")
     with pytest.raises(ValueError):
         q.device()
+    r = L.lattice_problem(4, 1, 4, 4, 4, 3, corr_len=1.0, characteristics="medium")
+    with pytest.raises(ValueError):
+        r.device()
 
 
 @pytest.mark.parametrize("cfg", [3, 4])
