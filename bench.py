@@ -634,6 +634,15 @@ def lattice_timings(torch):
         out[f"cfg{cfg}"] = {"layout": kw["layout"], "unknowns": n_total, "dof": dof, "ms_per_matvec": ms,
                             "matvecs_per_s": 1e3 / ms, "gdof_per_s": dof / ms / 1e6,
                             "hybrid_characteristics": {"ms_per_matvec": ms_h, "gdof_per_s": dof / ms_h / 1e6}}
+        if cfg in (3, 4):   # the exponential integrators (cfg5 skipped to keep the default run short)
+            fsd = {}
+            for fs in ("exp_linear", "exp_parabolic"):
+                pf = L.lattice_problem(seed=21958 + cfg, formal_solver=fs, **kw)
+                ms_f = time_matvec(pf)
+                del pf
+                torch.cuda.empty_cache()
+                fsd[fs] = {"ms_per_matvec": ms_f, "gdof_per_s": dof / ms_f / 1e6}
+            out[f"cfg{cfg}"]["formal_solvers"] = fsd
         # the multi-D sweeps are bound by the FP64 pipe / latency, not HBM -- report the
         # transfer kernel's FP64-pipe utilisation from the committed ncu capture of this config
         raw = ncu_raw(os.path.join(ROOT, "profiles", f"r01_ncu_lattice_cfg{cfg}.txt"))
