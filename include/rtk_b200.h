@@ -167,6 +167,17 @@ int rtk_intensity_from_moments(rtk_problem* p, const double* u_dev, const double
 int rtk_partial_moments(rtk_problem* p, const double* x_dev, double* m_dev, int64_t n_m, void* stream);
 int rtk_apply_A_with_moments(rtk_problem* p, const double* x_dev, const double* m_dev, int64_t n_m, double* y_dev,
                              int64_t n, void* stream);
+/* Direction sharding of a LATTICE problem in the moment layout (configs 4-5): every rank
+ * holds the full problem and the full (replicated) unknown u; it transfers only the
+ * directions [a0, a1).  rtk_lattice_partial_moments writes the partial angular moments
+ * m[s][l][f] = sum_{a0 <= a < a1} w_a Y_l(a) (Lambda S(u))(s, a, f) (n_m = n_space *
+ * n_moments * n_freq = n_total); after the moments of all ranks are summed (one
+ * all-reduce), rtk_lattice_apply_with_moments returns y = u - R_w m.  The sum over a
+ * partition of the directions is apply_A (rtk_apply_A) of the whole problem. */
+int rtk_lattice_partial_moments(rtk_problem* p, const double* u_dev, double* m_dev, int64_t n_m, int32_t a0,
+                                int32_t a1, void* stream);
+int rtk_lattice_apply_with_moments(rtk_problem* p, const double* u_dev, const double* m_dev, int64_t n_m,
+                                   double* y_dev, int64_t n, void* stream);
 /* s = Sigma x -- apply_scattering, R/scattering.py:126-148. */
 int rtk_apply_sigma(rtk_problem* p, const double* x_dev, double* s_dev, int64_t n, void* stream);
 /* y = Lambda s (homogeneous part) -- apply_transfer, R/transfer.py:134-141. */

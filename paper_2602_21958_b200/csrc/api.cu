@@ -454,6 +454,41 @@ static int check_shard(const rtk_problem* p, int64_t n_m) {
     return RTK_OK;
 }
 
+static int check_lattice_shard(const rtk_problem* p, int64_t n_m) {
+    if (!p) return set_error(RTK_EINVAL, "null problem handle");
+    const Problem& q = p->impl;
+    if (q.kind != rtk::KIND_LATTICE || q.layout != rtk::LAYOUT_MOMENTS)
+        return set_error(RTK_EINVAL, "lattice direction sharding needs a lattice problem in the moment layout");
+    if (n_m != q.n_space * q.n_mom * q.n_freq)
+        return set_error(RTK_EINVAL, "moment array must hold n_space * n_moments * n_freq values");
+    return RTK_OK;
+}
+
+int rtk_lattice_partial_moments(rtk_problem* p, const double* u, double* m, int64_t n_m, int32_t a0, int32_t a1,
+                                void* stream) {
+    int rc = check_lattice_shard(p, n_m);
+    if (rc) return rc;
+    const Problem& q = p->impl;
+    if (a0 < 0 || a1 > q.n_angles || a0 >= a1) return set_error(RTK_EINVAL, "direction range must satisfy 0 <= a0 < a1 <= n_dirs");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if ((rc = rtk::lattice_transfer_moments(q, 2 /*LSRC_U*/, false, u, q.mom, s, a0, a1))) return rc;
+    RTK_CUDA_TRY(cudaMemcpy2DAsync(m, sizeof(double) * q.n_freq, q.mom, sizeof(double) * q.fp,
+                                   sizeof(double) * q.n_freq, q.n_space * q.n_mom, cudaMemcpyDeviceToDevice, s));
+    return RTK_OK;
+}
+
+int rtk_lattice_apply_with_moments(rtk_problem* p, const double* u, const double* m, int64_t n_m, double* y,
+                                   int64_t n, void* stream) {
+    int rc = check_lattice_shard(p, n_m);
+    if (rc) return rc;
+    if ((rc = check_n(p, n))) return rc;
+    Problem& q = p->impl;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    RTK_CUDA_TRY(cudaMemcpy2DAsync(q.mom, sizeof(double) * q.fp, m, sizeof(double) * q.n_freq,
+                                   sizeof(double) * q.n_freq, q.n_space * q.n_mom, cudaMemcpyDeviceToDevice, s));
+    return rtk::launch_redistribute_ex(q, q.mom, y, q.n_freq, rtk::EPI_SUB, u, q.n_freq, s);
+}
+
 int rtk_partial_moments(rtk_problem* p, const double* x, double* m, int64_t n_m, void* stream) {
     int rc = check_shard(p, n_m);
     if (rc) return rc;

@@ -111,6 +111,7 @@ struct LatArgs {
     const double* inflow_top;     // [n_freq] or null
     const double* inflow_bottom;
     int nx, ny, nz, n_dirs, n_freq, n_mom;
+    int a0, a1;               // direction range of this call (sharded operator); default all
     int64_t nxy;
     int total_sub;            // sum over directions of (n_sub + 1): one step's sub-node shifts
 };
@@ -752,7 +753,7 @@ __global__ void __launch_bounds__(DG == 1 ? 128 : 256, DG == 1 ? 5 : 3)
         for (int l = 0; l < NM; ++l)
 #pragma unroll
             for (int q = 0; q < F; ++q) mo(l, q) = 0.0;
-        for (int a = dgi; a < A.n_dirs && item_ok; a += DG) {
+        for (int a = A.a0 + dgi; a < A.a1 && item_ok; a += DG) {
             const StepDir& D = sdir[a];
             if ((D.down != 0) != (hemi == 0)) continue;
             const double2* sa = sin2 + a * plane2 + g2;
@@ -926,7 +927,7 @@ __global__ void __launch_bounds__(256) lattice_splane_kernel(LatArgs A, int t, d
             g[q] = __ldg(A.src + sidx * A.n_freq + f);
         }
     }
-    for (int a = 0; a < A.n_dirs; ++a) {
+    for (int a = A.a0; a < A.a1; ++a) {
         const LatDir& D = A.dirs[a];
         const int qd = D.down ? 0 : 1;
         double cy[NM];
@@ -1066,6 +1067,8 @@ static LatArgs lat_args(const Problem& p, const double* src, const double* x, do
     A.n_freq = p.n_freq;
     A.n_mom = p.n_mom;
     A.nxy = static_cast<int64_t>(p.lat_nx) * p.lat_ny;
+    A.a0 = 0;
+    A.a1 = p.n_angles;
     return A;
 }
 
@@ -1196,8 +1199,12 @@ static int dispatch_mom_nm(const Problem& p, const LatArgs& A, bool with_inflow,
 
 // moment layout: mom[s][l][f] = sum_a w_a Y_l(a) (Lambda S)(s, a, f); S from u (SRC_U) or thermal (SRC_ISO)
 int lattice_transfer_moments(const Problem& p, int src_mode, bool with_inflow, const double* src, double* mom,
-                             cudaStream_t s) {
+                             cudaStream_t s, int a0, int a1) {
     LatArgs A = lat_args(p, src, nullptr, nullptr);
+    if (a1 >= 0) {   // partial moments over directions [a0, a1) (direction-sharded operator)
+        A.a0 = a0;
+        A.a1 = a1;
+    }
     if (p.fs == RTK_FS_IE) {
         if (src_mode == LSRC_U) return dispatch_mom_nm<RTK_FS_IE, LSRC_U>(p, A, with_inflow, mom, s);
         return dispatch_mom_nm<RTK_FS_IE, LSRC_ISO>(p, A, with_inflow, mom, s);

@@ -150,7 +150,7 @@ int setup_lattice(Problem& p, const rtk_lattice_desc* d);
 int lattice_transfer_intensity(const Problem& p, int src_mode, int out_mode, bool with_inflow, const double* src,
                                const double* x, double* y, cudaStream_t s);
 int lattice_transfer_moments(const Problem& p, int src_mode, bool with_inflow, const double* src, double* mom,
-                             cudaStream_t s);
+                             cudaStream_t s, int a0 = 0, int a1 = -1);
 // sigma.cu GEMM epilogues: C = c_k gamma acc | c_k acc | U - acc | acc
 enum Epilogue { EPI_GAMMA = 0, EPI_COEF = 1, EPI_SUB = 2, EPI_PLAIN = 3 };
 int launch_redistribute_ex(const Problem& p, const double* A, double* C, int ldc, int epi, const double* U, int ldu,

@@ -14,7 +14,8 @@ summed moments (replicated DMMA GEMM) and sweeps its own rays.
 The local pieces run through the C ABI (rtk_partial_moments /
 rtk_apply_A_with_moments); the exchange is torch.distributed.all_reduce.
 `ops_factory` / `all_reduce` are injectable so the host logic is testable on
-CPU ranks (tests/test_sharding.py, gloo).  Slab problems, intensity layout.
+CPU ranks (tests/test_sharding.py, gloo).  Slab problems, intensity layout;
+lattice problems in the moment layout: LatticeShardedOperator below.
 """
 
 from __future__ import annotations
@@ -115,6 +116,93 @@ class ShardedOperator:
         m = self.ops.partial_moments(x_local)
         m = self._all_reduce(m)
         return self.ops.apply_with_moments(x_local, m)
+
+
+# ---------------------------------------------------------------------------
+# Multi-D lattice problems in the moment layout (configs 4-5)
+#
+# The unknown u (redistributed dipole moments, 4.1 GB at cfg5) is REPLICATED on every rank;
+# rank r transfers only its block of directions [a0, a1) and produces partial angular moments;
+# one all-reduce of n_space x n_mom x N_nu values sums them, and every rank finishes
+# y = u - R_w m.  All ranks then hold identical y (the all-reduce delivers the same sum to
+# every rank), so any solver can run redundantly on the replicated vectors -- including the
+# native GMRES through a callable.  Directions are split by transfer cost (sub-segments per
+# layer step), not by count: grazing directions cost several times a steep one.
+
+
+def lattice_direction_cost(problem) -> np.ndarray:
+    """Relative transfer cost of each direction: n_sub + 1 sub-node samples per layer step
+    (the geometry of oracle/lattice.py: n_sub = ceil(max(|sx|, |sy|)))."""
+    om = np.asarray(problem.omega, dtype=float)
+    sx = np.abs(om[:, 0] * problem.dz / (np.abs(om[:, 2]) * problem.dx))
+    sy = np.abs(om[:, 1] * problem.dz / (np.abs(om[:, 2]) * problem.dy)) if problem.ny > 1 else 0.0 * sx
+    n_sub = np.maximum(1, np.ceil(np.maximum(sx, sy) - 1e-12)).astype(int)
+    return n_sub + 1.0
+
+
+def direction_blocks(cost: np.ndarray, world: int):
+    """Contiguous direction ranges [(a0, a1)] with balanced total cost, one per rank."""
+    n = cost.size
+    if world > n:
+        raise ValueError(f"cannot shard {n} directions over {world} ranks")
+    csum = np.concatenate([[0.0], np.cumsum(cost)])
+    bounds = [0]
+    for r in range(1, world):
+        target = csum[-1] * r / world
+        b = int(np.searchsorted(csum, target))
+        b = min(max(b, bounds[-1] + 1), n - (world - r))
+        bounds.append(b)
+    bounds.append(n)
+    return [(bounds[r], bounds[r + 1]) for r in range(world)]
+
+
+class NativeLatticeShardOps:
+    """Device halves of a direction-sharded lattice matvec (rtk_lattice_partial_moments /
+    rtk_lattice_apply_with_moments)."""
+
+    def __init__(self, problem, a0: int, a1: int):
+        self.problem, self.a0, self.a1 = problem, a0, a1
+        self.n = problem.n_total
+
+    def partial_moments(self, u):
+        h = self.problem.device()
+        m = _device.empty(self.n)
+        _native.check(_native.lib().rtk_lattice_partial_moments(h.h, _device.ptr(u), _device.ptr(m), self.n,
+                                                                self.a0, self.a1, _device.stream_ptr()))
+        return m
+
+    def apply_with_moments(self, u, m):
+        h = self.problem.device()
+        y = _device.empty(self.n)
+        _native.check(_native.lib().rtk_lattice_apply_with_moments(h.h, _device.ptr(u), _device.ptr(m), self.n,
+                                                                   _device.ptr(y), self.n, _device.stream_ptr()))
+        return y
+
+
+class LatticeShardedOperator:
+    """y = u - R_w M Lambda S(u) with the directions split over the ranks (see above); u and y
+    are full, replicated vectors."""
+
+    def __init__(self, problem, rank: int = None, world: int = None, group=None,
+                 ops_factory=NativeLatticeShardOps, all_reduce=None):
+        if getattr(problem, "layout", None) != "moments":
+            raise ValueError("lattice direction sharding needs the moment layout")
+        if rank is None or world is None:
+            import torch.distributed as dist
+
+            rank = dist.get_rank(group) if rank is None else rank
+            world = dist.get_world_size(group) if world is None else world
+        self.problem = problem
+        self.rank, self.world = rank, world
+        self.blocks = direction_blocks(lattice_direction_cost(problem), world)
+        self.a0, self.a1 = self.blocks[rank]
+        self.ops = ops_factory(problem, self.a0, self.a1)
+        self._all_reduce = all_reduce or (lambda t: _dist_all_reduce(t, group))
+
+    def __call__(self, u):
+        m = self.ops.partial_moments(u)
+        m = self._all_reduce(m)
+        return self.ops.apply_with_moments(u, m)
 
 
 def sharded_gmres(op: ShardedOperator, b_local, rel_tol: float = 1e-12, max_iter: int = 1000, restart: int = None):
