@@ -256,9 +256,9 @@ __device__ __forceinline__ ExpPar exp_parabolic_weights_bf(double du, double dd)
     w.att = m.att;
     const double s = du + dd;
     const double r = rcp_fast(du * dd * s);
-    w.wu = m.e0 + (m.e2 - (dd + 2.0 * du) * m.e1) * (dd * r);
     w.wc = (s * m.e1 - m.e2) * (s * r);
     w.wd = (m.e2 - du * m.e1) * (du * r);
+    w.wu = (m.e0 - w.wc) - w.wd;   // the three weights sum to e0
     return w;
 }
 
