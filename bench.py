@@ -455,6 +455,8 @@ def run_b200(args):
         extra["formal_solvers_cfg2"] = formal_solver_timings(torch, lib, hbm)
     if rank == 0 and not args.no_lattice:
         extra["lattice"] = lattice_timings(torch)
+        if not args.no_gmres:
+            extra["gmres_lattice"] = lattice_gmres_timings(torch)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -589,6 +591,35 @@ def formal_solver_timings(torch, lib, hbm):
                    "sweep_gbs": sweep_bytes / sweep_ms / 1e6, "sweep_frac_hbm": sweep_bytes / sweep_ms / 1e6 / hbm,
                    "kernel": "sweep1d_tma_kernel<EXP_*> (branch-free range-reduced weights in the chain warps)"}
         del p, x, y
+        torch.cuda.empty_cache()
+    return out
+
+
+def lattice_gmres_timings(torch):
+    """GMRES time-to-1e-8 on the multi-D configurations that reach it within a bench run:
+    cfg4 (moment layout) unrestarted, cfg3 (intensity layout, 2.75 GB vectors) GMRES(40).
+    cfg5 GMRES(20) needs ~10^3 iterations (minutes); see DESIGN.md section 11."""
+    import time
+
+    import paper_2602_21958_b200 as P
+    from paper_2602_21958_b200 import lattice as L
+
+    runs = {4: (dict(nx=64, ny=64, nz=64, n_polar=8, n_azimuth=16, n_freq=31, corr_len=8.0, eps=1e-4,
+                     layout="moments"), None, 600),
+            3: (dict(nx=256, ny=1, nz=256, n_polar=8, n_azimuth=16, n_freq=41, corr_len=16.0, eps=1e-4,
+                     layout="intensity"), 40, 1200)}
+    out = {}
+    for cfg, (kw, restart, its) in runs.items():
+        p = L.lattice_problem(seed=21958 + cfg, **kw)
+        b = P.build_rhs(p, device=True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = P.gmres(p, b, P.SolveConfig(rel_tol=1e-8, max_iter=its, restart=restart))
+        torch.cuda.synchronize()
+        out[f"cfg{cfg}"] = {"restart": restart, "iterations": rep.iterations, "converged": bool(rep.converged),
+                            "time_s": time.perf_counter() - t0, "true_residual": float(rep.true_residual),
+                            "unknowns": p.n_total, "layout": kw["layout"]}
+        del p, b, rep
         torch.cuda.empty_cache()
     return out
 
