@@ -130,3 +130,12 @@ def test_exp_parabolic_lattice_gmres_matches_oracle():
     assert rep.converged and ref.converged
     assert abs(rep.iterations - ref.iterations) <= 1
     assert rel_l2(rep.solution, ref.solution) <= 1e-7
+
+
+def test_lattice_matvec_is_bitwise_reproducible():
+    """The direction-grouped moment kernel sums its partial moments in a fixed order."""
+    import torch
+
+    p = L.lattice_problem(16, 16, 8, 8, 12, 6, corr_len=2.0, seed=2, layout="moments", characteristics="hybrid")
+    u = torch.from_numpy(np.random.default_rng(1).standard_normal(p.n_total)).cuda()
+    np.testing.assert_array_equal(P.apply_A(p, u).cpu().numpy(), P.apply_A(p, u).cpu().numpy())

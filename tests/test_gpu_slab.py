@@ -331,3 +331,22 @@ def test_moment_layout_solve_reproduces_intensity_solve():
     assert rel_l2(I, ri.solution) <= 1e-8
     d = oracle_desc(pm)
     assert rel_l2(I, ro.intensity_from_moments(d, rm.solution)) <= 1e-11
+
+
+def test_matvec_and_gmres_are_bitwise_reproducible():
+    """Fixed-order reductions everywhere (fused sigma cluster hand-off, CGS2 block sums, no
+    atomics): repeated runs give identical bits (run-to-run reproducibility)."""
+    import torch
+
+    p = configs.slab_problem(2)
+    x = torch.from_numpy(np.random.default_rng(11).standard_normal(p.n_total)).cuda()
+    y1 = P.apply_A(p, x).cpu().numpy()
+    y2 = P.apply_A(p, x).cpu().numpy()
+    np.testing.assert_array_equal(y1, y2)
+    q = configs.slab_problem(1)
+    b = P.build_rhs(q)
+    r1 = P.gmres(q, b, P.SolveConfig(rel_tol=1e-8, max_iter=200, restart=30))
+    r2 = P.gmres(q, b, P.SolveConfig(rel_tol=1e-8, max_iter=200, restart=30))
+    assert r1.iterations == r2.iterations
+    np.testing.assert_array_equal(r1.residual_history, r2.residual_history)
+    np.testing.assert_array_equal(r1.solution, r2.solution)
