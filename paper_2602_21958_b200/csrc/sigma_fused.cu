@@ -118,6 +118,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                        int gamma_mode, int SP) {
     using C = Cfg<CN, MT_, NT_>;
     constexpr int BK = C::BK, MT = C::MT, NT = C::NT, BN = C::BN, KT = C::KT, SLICE = C::SLICE, XBOX = C::XBOX;
+    // let the sweep (launched with programmatic stream serialization) start its prologue on
+    // free SMs; it waits (griddepcontrol.wait) for this grid before reading G
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     constexpr int XS = C::XS, AS = C::AS, BS = C::BS, NSP = C::NSP;
     const int n_freq = BN * CN;
     const int n_chunks = (n_angles + AC - 1) / AC;

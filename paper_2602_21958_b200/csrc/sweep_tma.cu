@@ -252,6 +252,9 @@ __global__ void __launch_bounds__(kTmaThreads) sweep1d_tma_kernel(const __grid_c
     if (warp == kConsumerWarps) {
         // ---------------- producer warp ----------------
         if (lane == 0) {
+            // programmatic dependent launch: the prologue above overlapped the tail of the
+            // kernel that produced G; wait for it to complete before streaming G
+            asm volatile("griddepcontrol.wait;\n" ::: "memory");
             prefetch_tensormap(&xmap);
             prefetch_tensormap(&gmap);
             prefetch_tensormap(&dtmap);
@@ -767,7 +770,20 @@ int launch_tma_us(const Problem& p, const double* x, double* y, cudaStream_t s) 
         }
         configured = smem;
     }
-    kern<<<p.tma_n_ctas, kTmaThreads, smem, s>>>(xmap, p.tma_gmap, p.tma_dtmap, A);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = getenv_flag("RTK_NO_PDL") ? 0 : 1;
+    cfg.gridDim = dim3(p.tma_n_ctas);
+    cfg.blockDim = dim3(kTmaThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, xmap, p.tma_gmap, p.tma_dtmap, A) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
     RTK_LAUNCH_CHECK("sweep1d_tma_kernel");
     return RTK_OK;
 }
