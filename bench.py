@@ -84,6 +84,25 @@ def ncu_raw(path):
     return {}
 
 
+def ncu_dmma_pipes(path=os.path.join(ROOT, "profiles", "r01_ncu_dmma_pipes.txt")):
+    """{kernel: DMMA sub-pipe active fraction} from the committed ncu capture, or {}."""
+    out, name = {}, None
+    try:
+        with open(path) as fh:
+            for line in fh:
+                if line.startswith("=="):
+                    name = "sigma_fused_kernel" if "sigma_fused" in line else (
+                        "redistribute_dmma_kernel" if "redistribute_dmma" in line else None)
+                elif name and "dmma_cycles_active" in line:
+                    for part in line.split("raw:")[1].split(","):
+                        k, v = part.strip().split("=")
+                        if "dmma_cycles_active" in k:
+                            out[name] = float(v.rstrip("%")) / 100
+    except OSError:
+        pass
+    return out
+
+
 def ncu_traffic(path=os.path.join(ROOT, "profiles", "r01_ncu_sweep_tma_v3.txt")):
     """dram__bytes_read.sum + dram__bytes_write.sum of the sweep kernel from the committed
     `ncu --set full` capture (profiles/), bytes per launch, or None."""
@@ -372,6 +391,13 @@ def run_b200(args):
                         "frac_hbm": moments_bytes / kun[0] / 1e6 / hbm},
             "redistribute": {"ms": kun[1], "flops": r_flops, "achieved_tflops": r_flops / kun[1] / 1e9,
                              "frac_fp64": r_flops / kun[1] / 1e9 / fp64_peak}}
+        # FP64 tensor (DMMA) pipe utilisation from the committed ncu capture (north star: "FP64
+        # tensor-pipe utilisation (redistribution) taken from ncu")
+        dm = ncu_dmma_pipes()
+        if "redistribute_dmma_kernel" in dm:
+            kernels["unfused_pair"]["redistribute"]["ncu_dmma_pipe_active"] = dm["redistribute_dmma_kernel"]
+        if "sigma_fused_kernel" in dm:
+            kernels.setdefault("sigma_fused_ncu", {})["dmma_pipe_active"] = dm["sigma_fused_kernel"]
         # K2a + K2b ran as ONE kernel (sigma_fused_kernel): x streamed once while the DMMA
         # contraction runs; it is bound by both HBM (x) and the FP64 pipe (R contraction + the
         # 2 n_mom flops per x element of the moment reduction), so both fractions are given
