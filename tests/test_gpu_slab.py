@@ -350,3 +350,36 @@ def test_matvec_and_gmres_are_bitwise_reproducible():
     assert r1.iterations == r2.iterations
     np.testing.assert_array_equal(r1.residual_history, r2.residual_history)
     np.testing.assert_array_equal(r1.solution, r2.solution)
+
+
+def test_random_configurations_match_dense_oracle_and_lu():
+    """Acceptance-criterion-6 pattern (T/test_acceptance.py:188-242) on the device path: 20
+    seeded random small problems (reference presets and the dipole x PRD kernel, all three formal
+    solvers); the dense matrix comes from the CPU oracle, the device matvec must agree to 1e-12
+    and the native GMRES solution with the LU solve to 1e-8."""
+    from paper_2602_21958_b200 import presets
+
+    rng = np.random.default_rng(20260810)
+    for trial in range(20):
+        kind = rng.choice(["mono", "coherent", "crd", "prd"])
+        if kind == "mono":
+            p = presets.build("mono", n_space=int(rng.integers(5, 40)), n_angles=int(rng.choice([4, 8, 12])))
+        elif kind in ("coherent", "crd"):
+            p = presets.build(kind, n_space=int(rng.integers(4, 15)), n_angles=int(rng.choice([4, 8])),
+                              n_freq=int(rng.integers(3, 12)))
+        else:
+            p = configs.slab_problem(1, formal_solver=str(rng.choice(["ie", "exp_linear", "exp_parabolic"])),
+                                     n_space=int(rng.integers(4, 20)), n_angles=int(rng.choice([4, 8])),
+                                     n_freq=int(rng.integers(3, 12)))
+        n = p.n_total
+        if n > 1500:
+            continue
+        d = oracle_desc(p)
+        dense = np.stack([ro.apply_A(d, e) for e in np.eye(n)], axis=1)
+        for _ in range(3):
+            v = rng.standard_normal(n)
+            assert rel_l2(P.apply_A(p, v), dense @ v) <= 1e-12, (trial, kind)
+        b = rng.standard_normal(n)
+        rep = P.gmres(p, b, P.SolveConfig(rel_tol=1e-13, max_iter=n))
+        x = np.linalg.solve(dense, b)
+        assert rel_l2(rep.solution, x) <= 1e-8, (trial, kind, rep.iterations)
