@@ -139,3 +139,20 @@ def test_lattice_matvec_is_bitwise_reproducible():
     p = L.lattice_problem(16, 16, 8, 8, 12, 6, corr_len=2.0, seed=2, layout="moments", characteristics="hybrid")
     u = torch.from_numpy(np.random.default_rng(1).standard_normal(p.n_total)).cuda()
     np.testing.assert_array_equal(P.apply_A(p, u).cpu().numpy(), P.apply_A(p, u).cpu().numpy())
+
+
+@pytest.mark.parametrize("fs", ["ie", "exp_linear", "exp_parabolic"])
+@pytest.mark.parametrize("chars", ["long", "hybrid"])
+def test_thick_limit_lambda_reproduces_the_source(fs, chars):
+    """T/test_multidim.py:115-123 pattern: in an optically thick medium (Delta tau >> 1 per
+    cell) the formal solution of a constant source is the source away from the inflow
+    boundaries; the device transfer (thermal source path of build_rhs, zero inflow) shows it."""
+    p = L.lattice_problem(8, 6, 10, 8, 8, 3, corr_len=2.0, seed=3, layout="intensity", formal_solver=fs,
+                          characteristics=chars, t_range=(1e3, 1e6))
+    p.inflow_bottom = np.zeros(p.n_freq)
+    p.thermal = np.ones_like(p.thermal)
+    I = P.build_rhs(p).reshape(p.nz, p.ny, p.nx, p.n_dirs, p.n_freq)
+    # line centre (the wings, phi ~ 1e-11, stay optically thin)
+    np.testing.assert_allclose(I[2:-2, ..., 1], 1.0, rtol=1e-4)
+    np.testing.assert_allclose(I, OL.build_rhs(OL.desc_from_lattice_problem(p), "intensity").reshape(I.shape),
+                               rtol=1e-11, atol=1e-14)
