@@ -156,3 +156,27 @@ def test_thick_limit_lambda_reproduces_the_source(fs, chars):
     np.testing.assert_allclose(I[2:-2, ..., 1], 1.0, rtol=1e-4)
     np.testing.assert_allclose(I, OL.build_rhs(OL.desc_from_lattice_problem(p), "intensity").reshape(I.shape),
                                rtol=1e-11, atol=1e-14)
+
+
+def test_cfg5_full_size_linearity_and_direction_shards():
+    """BASELINE cfg5 at full size (128^3, 96 directions, 41 nu, moment layout: 516 M unknowns,
+    8.25 G intensity DOF) through size-independent properties: linearity, and two direction
+    shards (rtk_lattice_partial_moments, summed) reassembling the operator."""
+    import torch
+
+    from paper_2602_21958_b200.sharding import LatticeShardedOperator
+    from tools.time_lattice import CFGS
+
+    p = L.lattice_problem(seed=21963, **CFGS[5])
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    u = torch.randn(p.n_total, dtype=torch.float64, device="cuda", generator=gen)
+    w = torch.randn(p.n_total, dtype=torch.float64, device="cuda", generator=gen)
+    au, aw = P.apply_A(p, u), P.apply_A(p, w)
+    comb = P.apply_A(p, 2.0 * u - 0.5 * w)
+    assert float(torch.linalg.vector_norm(comb - (2.0 * au - 0.5 * aw)) / torch.linalg.vector_norm(comb)) <= 1e-13
+    del w, aw, comb
+    ops = [LatticeShardedOperator(p, rank=r, world=2, all_reduce=lambda t: t) for r in range(2)]
+    m = ops[0].ops.partial_moments(u)
+    m += ops[1].ops.partial_moments(u)
+    y = ops[0].ops.apply_with_moments(u, m)
+    assert float(torch.linalg.vector_norm(y - au) / torch.linalg.vector_norm(au)) <= 1e-12
