@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gmres", action="store_true")
     ap.add_argument("--no-lattice", action="store_true")
+    ap.add_argument("--cfg5-gmres", action="store_true",
+                    help="also run cfg5 GMRES(20) to 1e-8 (about 1,550 iterations, ~9 minutes)")
     ap.add_argument("--mode", choices=["replicas", "sharded"], default="replicas",
                     help="N > 1: independent cfg2 matvecs per GPU (weak scaling, default) or ONE cfg2 matvec "
                          "sharded by direction with an NCCL all-reduce of the moments (strong scaling)")
@@ -482,7 +484,7 @@ def run_b200(args):
     if rank == 0 and not args.no_lattice:
         extra["lattice"] = lattice_timings(torch)
         if not args.no_gmres:
-            extra["gmres_lattice"] = lattice_gmres_timings(torch)
+            extra["gmres_lattice"] = lattice_gmres_timings(torch, cfg5=args.cfg5_gmres)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -621,7 +623,7 @@ def formal_solver_timings(torch, lib, hbm):
     return out
 
 
-def lattice_gmres_timings(torch):
+def lattice_gmres_timings(torch, cfg5=False):
     """GMRES time-to-1e-8 on the multi-D configurations that reach it within a bench run:
     cfg4 (moment layout) unrestarted, cfg3 (intensity layout, 2.75 GB vectors) GMRES(40).
     cfg5 GMRES(20) needs ~10^3 iterations (minutes); see DESIGN.md section 11."""
@@ -634,6 +636,9 @@ def lattice_gmres_timings(torch):
                      layout="moments"), None, 600),
             3: (dict(nx=256, ny=1, nz=256, n_polar=8, n_azimuth=16, n_freq=41, corr_len=16.0, eps=1e-4,
                      layout="intensity"), 40, 1200)}
+    if cfg5:
+        runs[5] = (dict(nx=128, ny=128, nz=128, n_polar=8, n_azimuth=12, n_freq=41, corr_len=16.0, eps=1e-5,
+                        layout="moments"), 20, 2500)
     out = {}
     for cfg, (kw, restart, its) in runs.items():
         p = L.lattice_problem(seed=21958 + cfg, **kw)
