@@ -117,3 +117,18 @@ def test_direction_blocks_balance_the_transfer_cost():
         assert max(loads) <= cost.sum() / world + cost.max()
     with pytest.raises(ValueError):
         direction_blocks(cost, p.n_dirs + 1)
+
+
+def test_direction_cost_uses_the_oracle_geometry():
+    """The host-side cost model (n_sub + 1 per direction) is the oracle's sub-segment count,
+    the one the CUDA setup (csrc/lattice.cu: setup_lattice) computes with the same formula."""
+    sys.path.insert(0, ROOT)
+    from oracle import lattice as OL
+    from paper_2602_21958_b200 import lattice as L
+    from paper_2602_21958_b200.sharding import lattice_direction_cost
+
+    for ny in (1, 6):
+        p = L.lattice_problem(7, ny, 5, 8, 12, 3, layout="moments")
+        d = OL.desc_from_lattice_problem(p)
+        n_sub = np.array([OL.direction_geometry(d, a)[3] for a in range(p.n_dirs)])
+        np.testing.assert_array_equal(lattice_direction_cost(p), n_sub + 1)
