@@ -472,6 +472,16 @@ def run_b200(args):
                        "H2D of step k+1 overlaps D2H of step k)",
                "value_one_call_per_step": world * k_e2e / el_seq,
                "one_call_path": "rtk_apply_A_host (H2D + matvec + D2H, synchronous)"}
+        # the drop-in call a reference user makes: apply_A(problem, numpy array), pageable
+        # buffers staged through pinned chunks inside the library
+        import time as _time
+        xv = np.random.default_rng(1).standard_normal(n)
+        P.apply_A(problem, xv)
+        t0 = _time.perf_counter()
+        for _ in range(3):
+            P.apply_A(problem, xv)
+        e2e["drop_in_numpy_apply_A_per_s"] = 3.0 / (_time.perf_counter() - t0)
+        del xv
         del hx, hy, xs, ys
 
     extra = {}

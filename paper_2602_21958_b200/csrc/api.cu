@@ -2,6 +2,10 @@
 // lifetime, operator applications, RHS.  R/ = /root/reference/pkg/src/rtkrylov/.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <thread>
+#include <vector>
+
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -43,6 +47,10 @@ Problem::~Problem() {
     for (double* b : bufs)
         if (b) cudaFree(b);
     if (dir_sign) cudaFree(dir_sign);
+    for (int b = 0; b < 2; ++b) {
+        if (stage[b]) cudaFreeHost(stage[b]);
+        if (stage_ev[b]) cudaEventDestroy(stage_ev[b]);
+    }
     if (aux) cudaStreamDestroy(aux);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
@@ -379,6 +387,83 @@ int rtk_problem_matvec(void* ctx, const double* x, double* y, int64_t n, void* s
     return rtk_apply_A(static_cast<rtk_problem*>(ctx), x, y, n, stream);
 }
 
+namespace {
+bool is_pageable(const void* ptr) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return at.type == cudaMemoryTypeUnregistered;
+}
+
+// host memcpy split over the machine's cores (pageable <-> pinned staging)
+void parallel_copy(void* dst, const void* src, size_t bytes) {
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const size_t per = (bytes / hw + 63) / 64 * 64;
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < hw && t * per < bytes; ++t)
+        pool.emplace_back([=] {
+            const size_t off = t * per;
+            std::memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, std::min(per, bytes - off));
+        });
+    std::memcpy(dst, src, std::min(per, bytes));
+    for (auto& th : pool) th.join();
+}
+}  // namespace
+
+namespace rtk {
+// Pageable user buffers (e.g. a numpy array through the drop-in apply_A): the copies go
+// through two pinned chunks owned by the problem, so the multithreaded host memcpy of one
+// chunk overlaps the DMA of the other (cudaMemcpy from pageable memory would stage through
+// the driver's small bounce buffers one thread at a time: ~6x slower at cfg2).
+int staged_h2d(Problem& q, double* dst_dev, const double* src, int64_t n, cudaStream_t s) {
+    const int64_t chunk = Problem::kStageChunk;
+    for (int64_t i0 = 0, c = 0; i0 < n; i0 += chunk, ++c) {
+        const int b = static_cast<int>(c & 1);
+        const int64_t cnt = std::min(chunk, n - i0);
+        RTK_CUDA_TRY(cudaEventSynchronize(q.stage_ev[b]));   // the DMA out of this chunk is done
+        parallel_copy(q.stage[b], src + i0, sizeof(double) * cnt);
+        RTK_CUDA_TRY(cudaMemcpyAsync(dst_dev + i0, q.stage[b], sizeof(double) * cnt, cudaMemcpyHostToDevice, s));
+        RTK_CUDA_TRY(cudaEventRecord(q.stage_ev[b], s));
+    }
+    return RTK_OK;
+}
+
+int staged_d2h(Problem& q, double* dst, const double* src_dev, int64_t n, cudaStream_t s) {
+    const int64_t chunk = Problem::kStageChunk;
+    const int64_t nch = (n + chunk - 1) / chunk;
+    auto issue = [&](int64_t c) -> int {
+        const int b = static_cast<int>(c & 1);
+        const int64_t i0 = c * chunk, cnt = std::min(chunk, n - i0);
+        RTK_CUDA_TRY(cudaMemcpyAsync(q.stage[b], src_dev + i0, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s));
+        RTK_CUDA_TRY(cudaEventRecord(q.stage_ev[b], s));
+        return RTK_OK;
+    };
+    int rc;
+    if ((rc = issue(0))) return rc;
+    for (int64_t c = 0; c < nch; ++c) {
+        const int b = static_cast<int>(c & 1);
+        RTK_CUDA_TRY(cudaEventSynchronize(q.stage_ev[b]));
+        if (c + 1 < nch && (rc = issue(c + 1))) return rc;   // next chunk's DMA overlaps this memcpy
+        const int64_t i0 = c * chunk, cnt = std::min(chunk, n - i0);
+        parallel_copy(dst + i0, q.stage[b], sizeof(double) * cnt);
+    }
+    return RTK_OK;
+}
+
+int ensure_staging(Problem& q) {
+    for (int b = 0; b < 2; ++b) {
+        if (!q.stage[b]) RTK_CUDA_TRY(cudaMallocHost(&q.stage[b], sizeof(double) * Problem::kStageChunk));
+        if (!q.stage_ev[b]) {
+            RTK_CUDA_TRY(cudaEventCreateWithFlags(&q.stage_ev[b], cudaEventDisableTiming));
+            RTK_CUDA_TRY(cudaEventRecord(q.stage_ev[b], 0));
+        }
+    }
+    return RTK_OK;
+}
+}  // namespace rtk
+
 int rtk_apply_A_host(rtk_problem* p, const double* x_host, double* y_host, int64_t n, void* stream) {
     int rc = check_n(p, n);
     if (rc) return rc;
@@ -386,9 +471,19 @@ int rtk_apply_A_host(rtk_problem* p, const double* x_host, double* y_host, int64
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (!q.host_x) RTK_CUDA_TRY(cudaMalloc(&q.host_x, sizeof(double) * q.n_total));
     if (!q.host_y) RTK_CUDA_TRY(cudaMalloc(&q.host_y, sizeof(double) * q.n_total));
-    RTK_CUDA_TRY(cudaMemcpyAsync(q.host_x, x_host, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    const bool stage_in = is_pageable(x_host), stage_out = is_pageable(y_host);
+    if ((stage_in || stage_out) && (rc = rtk::ensure_staging(q))) return rc;
+    if (stage_in) {
+        if ((rc = rtk::staged_h2d(q, q.host_x, x_host, n, s))) return rc;
+    } else {
+        RTK_CUDA_TRY(cudaMemcpyAsync(q.host_x, x_host, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    }
     if ((rc = rtk::apply_A_dev(q, q.host_x, q.host_y, s))) return rc;
-    RTK_CUDA_TRY(cudaMemcpyAsync(y_host, q.host_y, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    if (stage_out) {
+        if ((rc = rtk::staged_d2h(q, y_host, q.host_y, n, s))) return rc;
+    } else {
+        RTK_CUDA_TRY(cudaMemcpyAsync(y_host, q.host_y, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    }
     RTK_CUDA_TRY(cudaStreamSynchronize(s));
     return RTK_OK;
 }

@@ -88,6 +88,9 @@ struct Problem {
     double *mom = nullptr, *gmom = nullptr;
     double *host_x = nullptr, *host_y = nullptr;   // lazily allocated device staging for *_host calls
     double *host_x2 = nullptr, *host_y2 = nullptr; // second staging pair (batched host calls)
+    static constexpr int64_t kStageChunk = int64_t(1) << 22;   // 32 MB pinned chunks for pageable host buffers
+    double* stage[2] = {nullptr, nullptr};
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};
     cudaStream_t io[2] = {nullptr, nullptr};
     cudaEvent_t io_done[2] = {nullptr, nullptr};
     // TMA sweep path (sweep_tma.cu)
