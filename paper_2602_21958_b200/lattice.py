@@ -213,6 +213,15 @@ def lattice_apply_A(problem: LatticeProblem, v):
     """y = v - Lambda Sigma v (intensity layout) or u - R_w M Lambda S(u) (moment layout)."""
     n = problem.n_total
     h = problem.device()
+    if not _device.is_tensor(v):
+        # host arrays go through the library's staged host path (pinned chunks, overlapped copies)
+        arr = np.ascontiguousarray(np.asarray(v, dtype=float).reshape(-1))
+        if arr.size != n:
+            raise ValueError(f"expected length {n}, got {arr.size}")
+        out = np.empty(n)
+        _native.check(_native.lib().rtk_apply_A_host(h.h, _device.dptr(arr), _device.dptr(out), n,
+                                                     _device.stream_ptr()))
+        return out
     x, kind = _device.to_device(v, n)
     y = _device.empty(n)
     _native.check(_native.lib().rtk_apply_A(h.h, _device.ptr(x), _device.ptr(y), n, _device.stream_ptr()))
