@@ -328,7 +328,6 @@ class Engine {
         wsp_ = &thread_workspace(&rc);
         return rc;
     }
-    cudaStream_t stream() const { return s_; }
 
     // results (dots or norm^2) land in out_dev[0 .. k)
     int pass(int mode, const double* const* V, int k, const double* coef_dev, double* w, int64_t n, double* out_dev) {
