@@ -596,7 +596,7 @@ __device__ __forceinline__ void advance_lineF_par(int n_sub, double sub_len, con
                                                   const double2* __restrict__ Sc, int64_t ss, const double (&phi)[F],
                                                   const double* __restrict__ dtab, int64_t nxy,
                                                   const double* __restrict__ chi_a, const double* __restrict__ chi_b,
-                                                  const double* __restrict__ chi_c) {
+                                                  const double* __restrict__ chi_c, bool dt_next_tab) {
     const double inv_n = 1.0 / n_sub;
     double sp[F], sc[F], sn[F];
     sample_s2<F>(sp, stencil_at(lx, ly, sub[0], nx, ny), 0.0, Sa, Sb, ss);
@@ -611,8 +611,14 @@ __device__ __forceinline__ void advance_lineF_par(int n_sub, double sub_len, con
         } else if (Sc != nullptr) {
             const Stencil sx = stencil_at(lx, ly, dsh, nx, ny);
             sample_s2<F>(sn, sx, inv_n, Sb, Sc, ss);
-            const double cn = chi_at(stencil_at(lx, ly, sub[n_sub], nx, ny), 1.0, chi_a, chi_b);
-            dtd = sub_len * (cn + chi_at(sx, inv_n, chi_b, chi_c)) * 0.5;
+            if (dt_next_tab) {
+                // LC: the downwind segment is the line's first sub-segment of step t + 1, whose
+                // table entry follows this step's last (same shifts, same arithmetic)
+                dtd = __ldg(dtab + static_cast<int64_t>(n_sub) * nxy);
+            } else {
+                const double cn = chi_at(stencil_at(lx, ly, sub[n_sub], nx, ny), 1.0, chi_a, chi_b);
+                dtd = sub_len * (cn + chi_at(sx, inv_n, chi_b, chi_c)) * 0.5;
+            }
         }
 #pragma unroll
         for (int q = 0; q < F; ++q) {
@@ -823,7 +829,7 @@ __global__ void __launch_bounds__(DG == 1 ? 128 : 256, DG == 1 ? 5 : 3)
                     advance_lineF_par<F>(D.n_sub, A.dirs[a].sub_len, ssub + D.sub_pref, dsh, acc, i, j, A.nx, A.ny,
                                          pc2 + a * plane2 + g2, pn2 + a * plane2 + g2,
                                          pnn2 ? pnn2 + a * plane2 + g2 : nullptr, hp, phi, A.dtab + D.dtab + c, A.nxy,
-                                         chk, chk2, chk3);
+                                         chk, chk2, chk3, !D.sc);
 #pragma unroll
                     for (int h = 0; h < F / 2; ++h)
                         sout2[a * plane2 + static_cast<int64_t>(c) * hp + g2 + h] = make_double2(acc[2 * h], acc[2 * h + 1]);
@@ -834,7 +840,7 @@ __global__ void __launch_bounds__(DG == 1 ? 128 : 256, DG == 1 ? 5 : 3)
                         advance_lineF_par<2>(D.n_sub, A.dirs[a].sub_len, ssub + D.sub_pref, dsh, ap, i, j, A.nx, A.ny,
                                              pc2 + a * plane2 + g2 + h, pn2 + a * plane2 + g2 + h,
                                              pnn2 ? pnn2 + a * plane2 + g2 + h : nullptr, hp, pp,
-                                             A.dtab + D.dtab + c, A.nxy, chk, chk2, chk3);
+                                             A.dtab + D.dtab + c, A.nxy, chk, chk2, chk3, !D.sc);
                         sout2[a * plane2 + static_cast<int64_t>(c) * hp + g2 + h] = make_double2(ap[0], ap[1]);
                     }
                 } else if (full_group) {
