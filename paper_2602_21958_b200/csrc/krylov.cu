@@ -25,6 +25,7 @@ namespace {
 constexpr int kRedThreads = 256;
 constexpr int kMaxRedBlocks = 592;   // 4 x 148 SMs
 constexpr int KMAX = 32;             // basis vectors handled per pass (restart <= 31 runs fully fused)
+constexpr int kFinChunk = 64;        // block partials staged per round trip by the last block
 constexpr int kLookahead = 3;        // Arnoldi iterations the device may run ahead of the host
 
 enum PassMode { MODE_DOT = 0, MODE_UPDATE_DOT = 1, MODE_UPDATE_NORM = 2, MODE_UPDATE = 3 };
@@ -199,22 +200,25 @@ __global__ void __launch_bounds__(kRedThreads) cgs_pass_kernel(PassArgs P) {
     __syncthreads();
     if (is_last) {
         __threadfence();
-        if (threadIdx.x < nk) {
-            // L2 loads (.cg: past the non-coherent L1) issued ahead of the in-order sum
-            double s = 0.0;
-            const double* pp = P.partials + threadIdx.x * kMaxRedBlocks;
-            const unsigned nb = gridDim.x;
-            unsigned b = 0;
-            for (; b + 8 <= nb; b += 8) {
-                double v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = __ldcg(pp + b + u);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) s += v[u];
+        // the partials are staged in shared memory 64 blocks at a time by the whole block (one
+        // L2 round trip per chunk instead of one per 8 blocks), then thread k sums row k in
+        // block-index order: the same sequential sum, so results do not depend on the staging
+        __shared__ double fin[KMAX][kFinChunk + 1];
+        const unsigned nb = gridDim.x;
+        double total = 0.0;
+        for (unsigned b0 = 0; b0 < nb; b0 += kFinChunk) {
+            const unsigned cnt = min(static_cast<unsigned>(kFinChunk), nb - b0);
+#pragma unroll 8
+            for (int e = threadIdx.x; e < nk * kFinChunk; e += kRedThreads) {
+                const int k = e / kFinChunk, bb = e - k * kFinChunk;
+                if (bb < static_cast<int>(cnt)) fin[k][bb] = __ldcg(P.partials + k * kMaxRedBlocks + b0 + bb);
             }
-            for (; b < nb; ++b) s += __ldcg(pp + b);
-            P.out[threadIdx.x] = s;
+            __syncthreads();
+            if (threadIdx.x < nk)
+                for (unsigned bb = 0; bb < cnt; ++bb) total += fin[threadIdx.x][bb];
+            __syncthreads();
         }
+        if (threadIdx.x < nk) P.out[threadIdx.x] = total;
         if (threadIdx.x == 0) *P.counter = 0u;
     }
 }
