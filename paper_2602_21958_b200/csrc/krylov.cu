@@ -543,6 +543,8 @@ struct History {
 // ~10 kernels per iteration dominates the GPU work (cfg1: 65 us per iteration).
 struct CycleGraph {
     cudaStream_t gs = nullptr;
+    cudaStream_t side = nullptr;      // column read-backs, forked off the Arnoldi chain
+    cudaEvent_t fork = nullptr, join = nullptr;
     cudaGraphExec_t exec = nullptr;
     std::vector<cudaEvent_t> evs;     // evs[j]: column j is in its pinned slot
     cudaEvent_t start = nullptr, done = nullptr;
@@ -553,6 +555,9 @@ struct CycleGraph {
         for (auto e : evs) cudaEventDestroy(e);
         if (start) cudaEventDestroy(start);
         if (done) cudaEventDestroy(done);
+        if (fork) cudaEventDestroy(fork);
+        if (join) cudaEventDestroy(join);
+        if (side) cudaStreamDestroy(side);
         if (gs) cudaStreamDestroy(gs);
     }
 };
@@ -650,6 +655,9 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
             RTK_CUDA_TRY(cudaStreamCreateWithFlags(&G.gs, cudaStreamNonBlocking));
             RTK_CUDA_TRY(cudaEventCreateWithFlags(&G.start, cudaEventDisableTiming));
             RTK_CUDA_TRY(cudaEventCreateWithFlags(&G.done, cudaEventDisableTiming));
+            RTK_CUDA_TRY(cudaStreamCreateWithFlags(&G.side, cudaStreamNonBlocking));
+            RTK_CUDA_TRY(cudaEventCreateWithFlags(&G.fork, cudaEventDisableTiming));
+            RTK_CUDA_TRY(cudaEventCreateWithFlags(&G.join, cudaEventDisableTiming));
             G.evs.resize(cycle, nullptr);
             for (auto& e : G.evs) RTK_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             // the first matvec of a problem may configure kernels (attributes, occupancy queries):
@@ -664,13 +672,22 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
             bool ok = cudaStreamBeginCapture(G.gs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
             for (int jj = 0; ok && jj < cycle; ++jj) {
                 double* dslot = dslots + static_cast<size_t>(jj) * slot_max;
+                // the column's read-back (copy + external event) branches off after the CGS2
+                // passes, so the next matvec does not wait for the device-to-host copy
                 ok = apply(ctx, V.v[jj], w.p, n, G.gs) == RTK_OK &&
                      Eg.cgs2_enqueue(V.v, jj + 1, w.p, n, dslot) == RTK_OK &&
-                     Eg.scale_dev(w.p, V.v[jj + 1], n, dslot + 2 * (jj + 1)) == RTK_OK &&
+                     cudaEventRecord(G.fork, G.gs) == cudaSuccess &&
+                     cudaStreamWaitEvent(G.side, G.fork, 0) == cudaSuccess &&
                      cudaMemcpyAsync(pslots + static_cast<size_t>(jj) * slot_max, dslot,
-                                     sizeof(double) * (2 * (jj + 1) + 1), cudaMemcpyDeviceToHost, G.gs) == cudaSuccess &&
-                     cudaEventRecordWithFlags(G.evs[jj], G.gs, cudaEventRecordExternal) == cudaSuccess;
+                                     sizeof(double) * (2 * (jj + 1) + 1), cudaMemcpyDeviceToHost, G.side) == cudaSuccess &&
+                     cudaEventRecordWithFlags(G.evs[jj], G.side, cudaEventRecordExternal) == cudaSuccess &&
+                     Eg.scale_dev(w.p, V.v[jj + 1], n, dslot + 2 * (jj + 1)) == RTK_OK;
             }
+            // join the read-back branch (also when the capture failed part-way: the side stream
+            // must leave capture mode with the origin stream)
+            const bool joined = cudaEventRecord(G.join, G.side) == cudaSuccess &&
+                                cudaStreamWaitEvent(G.gs, G.join, 0) == cudaSuccess;
+            ok = ok && joined;
             const cudaError_t ec = cudaStreamEndCapture(G.gs, &graph);
             ok = ok && ec == cudaSuccess && graph != nullptr &&
                  cudaGraphInstantiate(&G.exec, graph, 0) == cudaSuccess;
