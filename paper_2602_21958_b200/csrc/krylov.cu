@@ -587,6 +587,23 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
             for (int q = 0; q < kLookahead; ++q) cudaEventDestroy(e[q]);
         }
     } ev_guard{look_ev};
+    // column read-backs run on a side stream forked after the CGS2 passes, so the next
+    // matvec on s does not queue behind the device-to-host copy; slot q is rewritten only
+    // after the host consumed its previous column (look-ahead window), and the side stream
+    // is drained before returning
+    struct SideStream {
+        cudaStream_t st = nullptr;
+        cudaEvent_t fork = nullptr;
+        ~SideStream() {
+            if (st) {
+                cudaStreamSynchronize(st);
+                cudaStreamDestroy(st);
+            }
+            if (fork) cudaEventDestroy(fork);
+        }
+    } side;
+    RTK_CUDA_TRY(cudaStreamCreateWithFlags(&side.st, cudaStreamNonBlocking));
+    RTK_CUDA_TRY(cudaEventCreateWithFlags(&side.fork, cudaEventDisableTiming));
     int spec_matvecs = 0;   // look-ahead matvecs whose iterations were discarded (not reported)
     const double tol = cfg->rel_tol;
     double b_norm;
@@ -715,11 +732,13 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
                 double* dslot = dslots + static_cast<size_t>(q) * slot_sz;
                 if ((rc = A(V.v[next], w.p))) return rc;
                 if ((rc = E.cgs2_enqueue(V.v, next + 1, w.p, n, dslot))) return rc;
+                RTK_CUDA_TRY(cudaEventRecord(side.fork, s));
+                RTK_CUDA_TRY(cudaStreamWaitEvent(side.st, side.fork, 0));
+                RTK_CUDA_TRY(cudaMemcpyAsync(pslots + static_cast<size_t>(q) * slot_sz, dslot,
+                                             sizeof(double) * (2 * (next + 1) + 1), cudaMemcpyDeviceToHost, side.st));
+                RTK_CUDA_TRY(cudaEventRecord(look_ev[q], side.st));
                 if ((rc = V.ensure(next + 2, n, hint))) return rc;
                 if ((rc = E.scale_dev(w.p, V.v[next + 1], n, dslot + 2 * (next + 1)))) return rc;
-                RTK_CUDA_TRY(cudaMemcpyAsync(pslots + static_cast<size_t>(q) * slot_sz, dslot,
-                                             sizeof(double) * (2 * (next + 1) + 1), cudaMemcpyDeviceToHost, s));
-                RTK_CUDA_TRY(cudaEventRecord(look_ev[q], s));
                 ++next;
             }
             {
