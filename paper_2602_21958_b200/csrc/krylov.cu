@@ -91,6 +91,28 @@ int red_blocks(int64_t n, int kb = 4) {
     return static_cast<int>(b);
 }
 
+__device__ __forceinline__ void pdl_prologue() {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+// launch with programmatic stream serialization (the kernel starts with pdl_prologue);
+// RTK_NO_PDL=1 launches plainly
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), int blocks, int threads, cudaStream_t s, Args... args) {
+    static const bool off = getenv_flag("RTK_NO_PDL");
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(threads);
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = off ? 0 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -114,6 +136,9 @@ struct PassArgs {
 template <int MODE, int KB, int VEC>
 __global__ void __launch_bounds__(kRedThreads) cgs_pass_kernel(PassArgs P) {
     constexpr int NACC = (MODE == MODE_UPDATE_NORM) ? 1 : KB;
+    // programmatic dependent launch: this grid may start while its predecessor drains; wait
+    // for the predecessor's completion before any global access, and let the next pass launch
+    pdl_prologue();
     __shared__ double coef[KMAX];
     if (threadIdx.x < KMAX) coef[threadIdx.x] = (MODE != MODE_DOT && threadIdx.x < P.kc) ? P.coef[threadIdx.x] : 0.0;
     __syncthreads();
@@ -226,6 +251,7 @@ __global__ void __launch_bounds__(kRedThreads) cgs_pass_kernel(PassArgs P) {
 // y = a * x  (a read from device: 1/sqrt(norm2) or a host scalar)
 __global__ void scale_kernel(const double* __restrict__ x, double* __restrict__ y, int64_t n, double a,
                              const double* __restrict__ norm2) {
+    pdl_prologue();
     const double s = norm2 ? sqrt(*norm2) : a;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride) y[e] = x[e] / s;
@@ -348,28 +374,26 @@ class Engine {
         const int kb = k <= 4 ? 4 : (k <= 8 ? 8 : (k <= 16 ? 16 : 32));
         const char* ov = std::getenv("RTK_PASS_BLOCKS");   // tuning hook: fixed block count for every pass
         const int blocks = ov ? std::max(1, std::min(kMaxRedBlocks, std::atoi(ov))) : red_blocks(n, kb);
-        if (k <= 4) launch_pass<4>(mode, blocks, P);
-        else if (k <= 8) launch_pass<8>(mode, blocks, P);
-        else if (k <= 16) launch_pass<16>(mode, blocks, P);
-        else launch_pass<32>(mode, blocks, P);
+        RTK_CUDA_TRY(k <= 4 ? launch_pass<4>(mode, blocks, P)
+                            : k <= 8 ? launch_pass<8>(mode, blocks, P)
+                                     : k <= 16 ? launch_pass<16>(mode, blocks, P) : launch_pass<32>(mode, blocks, P));
         RTK_LAUNCH_CHECK("cgs_pass_kernel");
         return RTK_OK;
     }
 
     template <int KB>
-    void launch_pass(int mode, int blocks, const PassArgs& P) {
+    cudaError_t launch_pass(int mode, int blocks, const PassArgs& P) {
         bool aligned = (reinterpret_cast<uintptr_t>(P.w) & 15) == 0;
         for (int k = 0; k < P.kc; ++k) aligned = aligned && (reinterpret_cast<uintptr_t>(P.v[k]) & 15) == 0;
-        if (aligned) launch_pass_v<KB, 2>(mode, blocks, P);
-        else launch_pass_v<KB, 1>(mode, blocks, P);
+        return aligned ? launch_pass_v<KB, 2>(mode, blocks, P) : launch_pass_v<KB, 1>(mode, blocks, P);
     }
     template <int KB, int VEC>
-    void launch_pass_v(int mode, int blocks, const PassArgs& P) {
+    cudaError_t launch_pass_v(int mode, int blocks, const PassArgs& P) {
         switch (mode) {
-            case MODE_DOT: cgs_pass_kernel<MODE_DOT, KB, VEC><<<blocks, kRedThreads, 0, s_>>>(P); break;
-            case MODE_UPDATE_DOT: cgs_pass_kernel<MODE_UPDATE_DOT, KB, VEC><<<blocks, kRedThreads, 0, s_>>>(P); break;
-            case MODE_UPDATE_NORM: cgs_pass_kernel<MODE_UPDATE_NORM, KB, VEC><<<blocks, kRedThreads, 0, s_>>>(P); break;
-            default: cgs_pass_kernel<MODE_UPDATE, KB, VEC><<<blocks, kRedThreads, 0, s_>>>(P); break;
+            case MODE_DOT: return launch_pdl(cgs_pass_kernel<MODE_DOT, KB, VEC>, blocks, kRedThreads, s_, P);
+            case MODE_UPDATE_DOT: return launch_pdl(cgs_pass_kernel<MODE_UPDATE_DOT, KB, VEC>, blocks, kRedThreads, s_, P);
+            case MODE_UPDATE_NORM: return launch_pdl(cgs_pass_kernel<MODE_UPDATE_NORM, KB, VEC>, blocks, kRedThreads, s_, P);
+            default: return launch_pdl(cgs_pass_kernel<MODE_UPDATE, KB, VEC>, blocks, kRedThreads, s_, P);
         }
     }
 
@@ -420,13 +444,13 @@ class Engine {
 
     // y = x / sqrt(*norm2_dev)  (the norm stays on the device)
     int scale_dev(const double* x, double* y, int64_t n, const double* norm2_dev) {
-        scale_kernel<<<elem_blocks(n), 256, 0, s_>>>(x, y, n, 1.0, norm2_dev);
+        RTK_CUDA_TRY(launch_pdl(scale_kernel, elem_blocks(n), 256, s_, x, y, n, 1.0, norm2_dev));
         RTK_LAUNCH_CHECK("scale_kernel");
         return RTK_OK;
     }
 
     int scale(const double* x, double* y, int64_t n, double a) {
-        scale_kernel<<<elem_blocks(n), 256, 0, s_>>>(x, y, n, a, nullptr);
+        RTK_CUDA_TRY(launch_pdl(scale_kernel, elem_blocks(n), 256, s_, x, y, n, a, static_cast<const double*>(nullptr)));
         RTK_LAUNCH_CHECK("scale_kernel");
         return RTK_OK;
     }
