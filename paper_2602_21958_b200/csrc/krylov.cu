@@ -91,28 +91,6 @@ int red_blocks(int64_t n, int kb = 4) {
     return static_cast<int>(b);
 }
 
-__device__ __forceinline__ void pdl_prologue() {
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-}
-
-// launch with programmatic stream serialization (the kernel starts with pdl_prologue);
-// RTK_NO_PDL=1 launches plainly
-template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kern)(KArgs...), int blocks, int threads, cudaStream_t s, Args... args) {
-    static const bool off = getenv_flag("RTK_NO_PDL");
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.gridDim = dim3(blocks);
-    cfg.blockDim = dim3(threads);
-    cfg.stream = s;
-    cfg.attrs = at;
-    cfg.numAttrs = off ? 0 : 1;
-    return cudaLaunchKernelEx(&cfg, kern, args...);
-}
-
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -390,10 +368,10 @@ class Engine {
     template <int KB, int VEC>
     cudaError_t launch_pass_v(int mode, int blocks, const PassArgs& P) {
         switch (mode) {
-            case MODE_DOT: return launch_pdl(cgs_pass_kernel<MODE_DOT, KB, VEC>, blocks, kRedThreads, s_, P);
-            case MODE_UPDATE_DOT: return launch_pdl(cgs_pass_kernel<MODE_UPDATE_DOT, KB, VEC>, blocks, kRedThreads, s_, P);
-            case MODE_UPDATE_NORM: return launch_pdl(cgs_pass_kernel<MODE_UPDATE_NORM, KB, VEC>, blocks, kRedThreads, s_, P);
-            default: return launch_pdl(cgs_pass_kernel<MODE_UPDATE, KB, VEC>, blocks, kRedThreads, s_, P);
+            case MODE_DOT: return launch_pdl(cgs_pass_kernel<MODE_DOT, KB, VEC>, blocks, kRedThreads, 0, s_, P);
+            case MODE_UPDATE_DOT: return launch_pdl(cgs_pass_kernel<MODE_UPDATE_DOT, KB, VEC>, blocks, kRedThreads, 0, s_, P);
+            case MODE_UPDATE_NORM: return launch_pdl(cgs_pass_kernel<MODE_UPDATE_NORM, KB, VEC>, blocks, kRedThreads, 0, s_, P);
+            default: return launch_pdl(cgs_pass_kernel<MODE_UPDATE, KB, VEC>, blocks, kRedThreads, 0, s_, P);
         }
     }
 
@@ -444,13 +422,13 @@ class Engine {
 
     // y = x / sqrt(*norm2_dev)  (the norm stays on the device)
     int scale_dev(const double* x, double* y, int64_t n, const double* norm2_dev) {
-        RTK_CUDA_TRY(launch_pdl(scale_kernel, elem_blocks(n), 256, s_, x, y, n, 1.0, norm2_dev));
+        RTK_CUDA_TRY(launch_pdl(scale_kernel, elem_blocks(n), 256, 0, s_, x, y, n, 1.0, norm2_dev));
         RTK_LAUNCH_CHECK("scale_kernel");
         return RTK_OK;
     }
 
     int scale(const double* x, double* y, int64_t n, double a) {
-        RTK_CUDA_TRY(launch_pdl(scale_kernel, elem_blocks(n), 256, s_, x, y, n, a, static_cast<const double*>(nullptr)));
+        RTK_CUDA_TRY(launch_pdl(scale_kernel, elem_blocks(n), 256, 0, s_, x, y, n, a, static_cast<const double*>(nullptr)));
         RTK_LAUNCH_CHECK("scale_kernel");
         return RTK_OK;
     }

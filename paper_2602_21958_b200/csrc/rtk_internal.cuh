@@ -164,6 +164,32 @@ int launch_redistribute_range(const Problem& p, int64_t i0, int64_t i1, cudaStre
 int apply_A_dev(Problem& p, const double* x, double* y, cudaStream_t s);
 int sweep_apply(const Problem& p, const double* x, double* y, cudaStream_t s);
 bool getenv_flag(const char* name);
+
+// Programmatic dependent launch (Krylov passes, moment reductions, small redistribution).
+__device__ __forceinline__ void pdl_prologue() {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+// launch with programmatic stream serialization (the kernel starts with pdl_prologue);
+// RTK_NO_PDL=1 launches plainly
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned blocks, int threads, size_t smem, cudaStream_t s,
+                       Args... args) {
+    static const bool off = getenv_flag("RTK_NO_PDL");
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = off ? 0 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 int upload(double** dst, const double* src, size_t count);
 
 }  // namespace rtk

@@ -21,6 +21,7 @@ __global__ void __launch_bounds__(kMomThreads) moments_kernel(const double* __re
                                                               int n_freq, int fp) {
     extern __shared__ double s_wy[];
     for (int t = threadIdx.x; t < NM * n_angles; t += blockDim.x) s_wy[t] = wy[t];
+    pdl_prologue();   // w Y is problem data; x comes from the preceding kernel
     __syncthreads();
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= n_space * n_freq) return;
@@ -67,6 +68,7 @@ __global__ void __launch_bounds__(kMomThreads) moments_pair_kernel(const double*
                                                                    int n_angles, int n_freq, int fp) {
     extern __shared__ double s_wy[];
     for (int t = threadIdx.x; t < NM * n_angles; t += blockDim.x) s_wy[t] = wy[t];
+    pdl_prologue();   // w Y is problem data; x comes from the preceding kernel
     __syncthreads();
     const int hf = n_freq >> 1;
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -201,6 +203,7 @@ __global__ void __launch_bounds__(256) redistribute_small_kernel(const double* _
         const int g = t / N, c = t - g * N;
         Bs[t] = __ldg(B + static_cast<int64_t>(g) * ld + c);
     }
+    pdl_prologue();   // R is problem data; A (the moments) comes from the preceding kernel
     for (int t = threadIdx.x; t < rows * K; t += blockDim.x) {
         const int rr = t / K, g = t - rr * K;
         As[t] = __ldg(A + (r0 + rr) * ld + g);
@@ -428,14 +431,15 @@ int launch_moments_t(const Problem& p, const double* x, cudaStream_t s, int64_t 
     if ((p.n_freq & 1) == 0 && !getenv_flag("RTK_MOMENTS_SCALAR")) {
         const int64_t work = p.n_space * (p.n_freq / 2);
         const unsigned blocks = static_cast<unsigned>((work + kMomThreads - 1) / kMomThreads);
-        moments_pair_kernel<NM><<<blocks, kMomThreads, smem, s>>>(x, p.wy, p.mom, p.n_space, p.n_angles, p.n_freq,
-                                                                  p.fp);
+        RTK_CUDA_TRY(launch_pdl(moments_pair_kernel<NM>, blocks, kMomThreads, smem, s, x, p.wy, p.mom, p.n_space,
+                                p.n_angles, p.n_freq, p.fp));
         RTK_LAUNCH_CHECK("moments_pair_kernel");
         return RTK_OK;
     }
     const int64_t work = p.n_space * p.n_freq;
     const unsigned blocks = static_cast<unsigned>((work + kMomThreads - 1) / kMomThreads);
-    moments_kernel<NM><<<blocks, kMomThreads, smem, s>>>(x, p.wy, p.mom, p.n_space, p.n_angles, p.n_freq, p.fp);
+    RTK_CUDA_TRY(launch_pdl(moments_kernel<NM>, blocks, kMomThreads, smem, s, x, p.wy, p.mom, p.n_space, p.n_angles,
+                            p.n_freq, p.fp));
     RTK_LAUNCH_CHECK("moments_kernel");
     return RTK_OK;
 }
@@ -491,8 +495,8 @@ int launch_redistribute_ex(const Problem& p, const double* A, double* C, int ldc
     if (M * p.n_freq <= (int64_t(1) << 18)) {
         const unsigned blocks = static_cast<unsigned>((M + kSmallRows - 1) / kSmallRows);
         const size_t smem = sizeof(double) * (static_cast<size_t>(p.n_freq) * p.n_freq + kSmallRows * p.n_freq);
-        redistribute_small_kernel<<<blocks, 256, smem, s>>>(A, p.rwt, C, gamma, p.coeffs, M, p.n_freq, p.n_freq,
-                                                            p.n_mom, epi, p.fp, ldc, U, ldu);
+        RTK_CUDA_TRY(launch_pdl(redistribute_small_kernel, blocks, 256, smem, s, A, p.rwt, C, gamma, p.coeffs, M,
+                                p.n_freq, p.n_freq, p.n_mom, epi, p.fp, ldc, U, ldu));
         RTK_LAUNCH_CHECK("redistribute_small_kernel");
         return RTK_OK;
     }
