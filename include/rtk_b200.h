@@ -136,8 +136,15 @@ int rtk_problem_create_slab(const rtk_slab_desc* desc, rtk_problem** out);
 int rtk_problem_create_lattice(const rtk_lattice_desc* desc, rtk_problem** out);
 int rtk_problem_destroy(rtk_problem* p);
 int64_t rtk_problem_n_total(const rtk_problem* p);
-/* Re-upload inflow after a host-side edit (T/test_operator.py:88-110 mutate it). */
-int rtk_problem_set_inflow(rtk_problem* p, const double* inflow_host, int64_t n_rays);
+/* Re-upload inflow after a host-side edit (T/test_operator.py:88-110 mutate it).  Ordered
+ * on `stream` after earlier work there; a no-op when the values are unchanged. */
+int rtk_problem_set_inflow(rtk_problem* p, const double* inflow_host, int64_t n_rays, void* stream);
+/* Kernel-variant selection of one handle (initialised at creation from the RTK_* environment
+ * variables, read once then): "disable_tma", "lattice_dg" (0 auto, 1, 4, 8),
+ * "lattice_no_smem", "lattice_no_dtab", "lattice_no_planar", "moments_scalar",
+ * "sigma_unfused".  Every variant computes the same operator (tests run each one against
+ * the oracle).  No reference counterpart.  Unknown key or value: RTK_EINVAL. */
+int rtk_problem_set_tuning(rtk_problem* p, const char* key, int64_t value);
 
 /* y = x - Lambda(Sigma x)  -- apply_A, R/operator.py:48-53.  x, y device, length n. */
 int rtk_apply_A(rtk_problem* p, const double* x_dev, double* y_dev, int64_t n, void* stream);
@@ -196,12 +203,23 @@ int rtk_source_function(rtk_problem* p, const double* intensity_dev, const doubl
 /* Matvec callback: y = A x on device vectors, on `stream`; returns a status code. */
 typedef int (*rtk_matvec_fn)(void* ctx, const double* x_dev, double* y_dev, int64_t n, void* stream);
 
+/* Arnoldi orthogonalisation of rtk_gmres / rtk_gmres_problem:
+ * REFERENCE  the reference's choice (R/krylov.py:98-104): modified Gram-Schmidt, one sweep,
+ *            or two when reorthogonalize != 0 (MGS / MGS2);
+ * MGS, MGS2  explicitly;
+ * CGS2       classical Gram-Schmidt + one reorthogonalisation, fused into three streaming
+ *            passes over the whole basis (fewest bytes and launches per iteration). */
+#define RTK_ORTH_REFERENCE 0
+#define RTK_ORTH_MGS 1
+#define RTK_ORTH_MGS2 2
+#define RTK_ORTH_CGS2 3
+
 typedef struct rtk_solve_cfg {       /* SolveConfig, R/krylov.py:21-35 */
     double rel_tol;
     int32_t max_iter;
     int32_t restart;                 /* <= 0: no restart (SolveConfig.restart = None) */
-    int32_t reorthogonalize;         /* accepted for API parity; Arnoldi is always CGS2 (two passes) */
-    int32_t reserved;
+    int32_t reorthogonalize;         /* second Gram-Schmidt sweep (SolveConfig.reorthogonalize) */
+    int32_t orthogonalization;       /* RTK_ORTH_*; RTK_ORTH_REFERENCE follows reorthogonalize */
 } rtk_solve_cfg;
 
 typedef struct rtk_solve_report {    /* SolveReport, R/krylov.py:38-46 (solution stays on device) */
@@ -216,9 +234,11 @@ typedef struct rtk_solve_report {    /* SolveReport, R/krylov.py:38-46 (solution
 
 /* Restarted GMRES with the reference's exact control flow (R/krylov.py:56-158):
  * x0 = 0, Givens least squares, recurrence-residual stop, true-residual guard
- * at 10 tol, breakdown at 1e-14 ||b||.  Arnoldi is CGS2 with deterministic
- * device reductions; the Krylov basis stays in HBM.  x_dev receives the
- * solution. */
+ * at 10 tol, breakdown at 1e-14 ||b||.  Arnoldi by cfg->orthogonalization with
+ * deterministic device reductions; the Krylov basis stays in HBM.  x_dev
+ * receives the solution.  A callable `apply` is invoked exactly in the
+ * reference's order (no look-ahead); the library's own rtk_problem_matvec
+ * lets the device run up to three Arnoldi steps ahead of the host. */
 int rtk_gmres(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b_dev, double* x_dev,
               const rtk_solve_cfg* cfg, rtk_solve_report* report,
               double* history_host, int32_t history_cap, void* stream);

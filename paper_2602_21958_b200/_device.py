@@ -122,7 +122,12 @@ class SlabHandle:
 
     def set_inflow(self, inflow: np.ndarray):
         arr = np.ascontiguousarray(inflow, dtype=float)
-        _native.check(self._lib.rtk_problem_set_inflow(self.h, dptr(arr), arr.size))
+        _native.check(self._lib.rtk_problem_set_inflow(self.h, dptr(arr), arr.size, stream_ptr()))
+
+    def set_tuning(self, key: str, value: int):
+        """Select a kernel variant of this handle (rtk_problem_set_tuning); every variant
+        computes the same operator."""
+        _native.check(self._lib.rtk_problem_set_tuning(self.h, key.encode(), int(value)))
 
     def __del__(self):
         h = getattr(self, "h", None)

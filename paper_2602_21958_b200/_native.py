@@ -49,7 +49,7 @@ class SolveCfg(ctypes.Structure):
         ("max_iter", ctypes.c_int32),
         ("restart", ctypes.c_int32),
         ("reorthogonalize", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("orthogonalization", ctypes.c_int32),
     ]
 
 
@@ -80,7 +80,8 @@ SIGNATURES = [
     ("rtk_problem_create_lattice", ctypes.c_int, [_P, ctypes.POINTER(_P)]),
     ("rtk_problem_destroy", ctypes.c_int, [_P]),
     ("rtk_problem_n_total", _I64, [_P]),
-    ("rtk_problem_set_inflow", ctypes.c_int, [_P, _P, _I64]),
+    ("rtk_problem_set_inflow", ctypes.c_int, [_P, _P, _I64, _P]),
+    ("rtk_problem_set_tuning", ctypes.c_int, [_P, ctypes.c_char_p, _I64]),
     ("rtk_apply_A", ctypes.c_int, [_P, _P, _P, _I64, _P]),
     ("rtk_apply_A_host", ctypes.c_int, [_P, _P, _P, _I64, _P]),
     ("rtk_apply_A_host_batch", ctypes.c_int, [_P, _P, _P, _I32, _I64]),

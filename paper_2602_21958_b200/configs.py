@@ -8,8 +8,6 @@ leaves open).  Seeds: numpy default_rng(21958 + cfg).
 
 from __future__ import annotations
 
-import math
-
 import numpy as np
 
 from paper_2602_21958_b200.grid import grid_from_nodes
@@ -91,5 +89,23 @@ def dof(cfg: int) -> int:
     return c["n_space"] * c["n_angles"] * c["n_freq"]
 
 
-def erfc_check():  # pragma: no cover - sanity helper
-    return math.erfc(0.0)
+# Multi-D configurations 3-5 on the periodic lattice: grid, angular set
+# (n_polar x n_azimuth directions), N_nu, opacity correlation length (cells), eps, the unknown
+# layout the configuration is run in (cfg4/5: moment layout -- an intensity vector would be
+# 8-66 GB) and the GMRES restart (BASELINE: 20 for cfg5; None = unrestarted).
+LATTICE_CONFIGS = {
+    3: dict(nx=256, ny=1, nz=256, n_polar=8, n_azimuth=16, n_freq=41, corr_len=16.0, eps=1e-4, layout="intensity"),
+    4: dict(nx=64, ny=64, nz=64, n_polar=8, n_azimuth=16, n_freq=31, corr_len=8.0, eps=1e-4, layout="moments"),
+    5: dict(nx=128, ny=128, nz=128, n_polar=8, n_azimuth=12, n_freq=41, corr_len=16.0, eps=1e-5, layout="moments"),
+}
+LATTICE_RESTART = {3: 40, 4: None, 5: 20}
+
+
+def lattice_config_problem(cfg: int, **overrides):
+    """BASELINE configuration 3, 4 or 5 (seed 21958 + cfg); keyword overrides give reduced
+    parity cases of the same construction (e.g. nx=ny=nz=16, or another layout)."""
+    from paper_2602_21958_b200.lattice import lattice_problem
+
+    kw = dict(LATTICE_CONFIGS[cfg])
+    kw.update(overrides)
+    return lattice_problem(seed=SEED_BASE + cfg, **kw)

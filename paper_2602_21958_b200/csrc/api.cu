@@ -10,8 +10,11 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "rtk_internal.cuh"
@@ -39,6 +42,7 @@ int cuda_status(cudaError_t e, const char* what) {
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 Problem::~Problem() {
+    if (krylov_ws) destroy_krylov_workspace(krylov_ws);
     double* bufs[] = {dt, phi, inv_mu, wy, yb, rwt, gamma, coeffs, inflow, mom, gmom, host_x, host_y, host_x2, host_y2};
     for (auto st : io)
         if (st) cudaStreamDestroy(st);
@@ -51,11 +55,6 @@ Problem::~Problem() {
         if (stage[b]) cudaFreeHost(stage[b]);
         if (stage_ev[b]) cudaEventDestroy(stage_ev[b]);
     }
-    if (aux) cudaStreamDestroy(aux);
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
-    for (auto e : ev_chunk)
-        if (e) cudaEventDestroy(e);
     if (tma_ctas) cudaFree(tma_ctas);
     if (dtpad) cudaFree(dtpad);
     if (lat_dirs) cudaFree(lat_dirs);
@@ -77,6 +76,79 @@ bool getenv_flag(const char* name) {
     return v && v[0] && v[0] != '0';
 }
 
+static int getenv_int(const char* name) {
+    const char* v = std::getenv(name);
+    return v && v[0] ? std::atoi(v) : 0;
+}
+
+Tuning tuning_from_env() {
+    Tuning t;
+    t.disable_tma = getenv_flag("RTK_DISABLE_TMA");
+    t.lat_dg = getenv_int("RTK_LAT_DG");
+    t.lat_no_smem = getenv_flag("RTK_LATTICE_NO_SMEM");
+    t.lat_no_dtab = getenv_flag("RTK_LATTICE_NO_DTAB");
+    t.lat_no_planar = getenv_flag("RTK_LATTICE_NO_PLANAR");
+    t.moments_scalar = getenv_flag("RTK_MOMENTS_SCALAR");
+    t.sigma_unfused = getenv_flag("RTK_SIGMA_UNFUSED");
+    return t;
+}
+
+int tuning_set(Tuning& t, const char* key, int64_t value) {
+    const std::string k = key ? key : "";
+    const int v = static_cast<int>(value);
+    if (k == "disable_tma") t.disable_tma = v;
+    else if (k == "lattice_dg") {
+        if (v != 0 && v != 1 && v != 4 && v != 8) return 1;
+        t.lat_dg = v;
+    } else if (k == "lattice_no_smem") t.lat_no_smem = v;
+    else if (k == "lattice_no_dtab") t.lat_no_dtab = v;
+    else if (k == "lattice_no_planar") t.lat_no_planar = v;
+    else if (k == "moments_scalar") t.moments_scalar = v;
+    else if (k == "sigma_unfused") t.sigma_unfused = v;
+    else return 1;
+    return 0;
+}
+
+bool pdl_enabled() {
+    static const bool on = !getenv_flag("RTK_NO_PDL");
+    return on;
+}
+
+namespace {
+std::mutex g_attr_mu;
+std::map<std::pair<const void*, int>, size_t> g_smem_set;              // (kernel, device) -> bytes set
+std::map<std::pair<const void*, int>, std::map<int, int>> g_dev_cache;   // (kernel, device) -> slot -> value
+}  // namespace
+
+int ensure_smem(const void* func, size_t bytes) {
+    if (bytes <= 48 * 1024) return RTK_OK;
+    int dev = 0;
+    RTK_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    size_t& have = g_smem_set[{func, dev}];
+    if (have >= bytes) return RTK_OK;
+    RTK_CUDA_TRY(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+    have = bytes;
+    return RTK_OK;
+}
+
+int device_cache_get(const void* func, int slot) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto it = g_dev_cache.find({func, dev});
+    if (it == g_dev_cache.end()) return -1;
+    auto jt = it->second.find(slot);
+    return jt == it->second.end() ? -1 : jt->second;
+}
+
+void device_cache_put(const void* func, int slot, int value) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    g_dev_cache[{func, dev}][slot] = value;
+}
+
 int upload(double** dst, const double* src, size_t count) {
     if (count == 0) count = 1;
     RTK_CUDA_TRY(cudaMalloc(dst, count * sizeof(double)));
@@ -85,8 +157,11 @@ int upload(double** dst, const double* src, size_t count) {
     return RTK_OK;
 }
 
+// The TMA sweep where the problem's shape admits it (launch_sweep_tma returns -1 only for
+// shapes it does not cover, decided at setup; a failing TMA launch is an error, never a
+// silent switch to the slower kernel); otherwise, or with tune.disable_tma, the cp.async sweep.
 int sweep_apply(const Problem& p, const double* x, double* y, cudaStream_t s) {
-    if (!getenv_flag("RTK_DISABLE_TMA")) {
+    if (!p.tune.disable_tma) {
         const int rc = launch_sweep_tma(p, x, y, s);
         if (rc != -1) return rc;
     }
@@ -108,29 +183,6 @@ int apply_A_dev(Problem& p, const double* x, double* y, cudaStream_t s) {
         if ((rc = launch_expand_source(p, nullptr, p.lat_src, s))) return rc;
         return lattice_transfer_intensity(p, 0 /*LSRC_VEC*/, OUT_X_MINUS, false, p.lat_src, x, y, s);
     }
-    if (getenv_flag("RTK_OVERLAP") && p.n_space >= 64) {   // opt-in: measured slower on cfg2
-        // Chunked fork/join: moments of chunk c+1 (HBM-bound, user stream) run while the DMMA
-        // GEMM of chunk c (FP64-bound, auxiliary stream) runs; the sweep waits for all chunks.
-        const int NC = getenv_flag("RTK_OVERLAP4") ? 4 : 2;
-        if (!p.aux) {
-            RTK_CUDA_TRY(cudaStreamCreateWithFlags(&p.aux, cudaStreamNonBlocking));
-            RTK_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming));
-            RTK_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming));
-            for (int c = 0; c < NC; ++c) RTK_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_chunk[c], cudaEventDisableTiming));
-        }
-        RTK_CUDA_TRY(cudaEventRecord(p.ev_fork, s));
-        RTK_CUDA_TRY(cudaStreamWaitEvent(p.aux, p.ev_fork, 0));
-        for (int c = 0; c < NC; ++c) {
-            const int64_t i0 = p.n_space * c / NC, i1 = p.n_space * (c + 1) / NC;
-            if ((rc = launch_moments_range(p, x, i0, i1, s))) return rc;
-            RTK_CUDA_TRY(cudaEventRecord(p.ev_chunk[c], s));
-            RTK_CUDA_TRY(cudaStreamWaitEvent(p.aux, p.ev_chunk[c], 0));
-            if ((rc = launch_redistribute_range(p, i0, i1, p.aux))) return rc;
-        }
-        RTK_CUDA_TRY(cudaEventRecord(p.ev_join, p.aux));
-        RTK_CUDA_TRY(cudaStreamWaitEvent(s, p.ev_join, 0));
-        return sweep_apply(p, x, y, s);
-    }
     if ((rc = launch_sigma(p, x, s))) return rc;
     return sweep_apply(p, x, y, s);
 }
@@ -146,6 +198,10 @@ static int check_n(const rtk_problem* p, int64_t n) {
         return set_error(RTK_EINVAL, "expected length " + std::to_string(p->impl.n_total) + ", got " + std::to_string(n));
     return RTK_OK;
 }
+
+namespace rtk {
+Problem* problem_impl(rtk_problem* p) { return p ? &p->impl : nullptr; }
+}  // namespace rtk
 
 extern "C" {
 
@@ -175,6 +231,7 @@ int rtk_problem_create_slab(const rtk_slab_desc* d, rtk_problem** out) {
     rtk_problem* h = new (std::nothrow) rtk_problem();
     if (!h) return set_error(RTK_ERESOURCE, "host allocation failed");
     Problem& p = h->impl;
+    p.tune = rtk::tuning_from_env();
     p.n_space = d->n_space;
     p.n_angles = d->n_angles;
     p.n_freq = d->n_freq;
@@ -224,6 +281,8 @@ int rtk_problem_create_slab(const rtk_slab_desc* d, rtk_problem** out) {
     if (!rc) rc = rtk::upload(&p.gamma, d->gamma, gamma_count);
     if (!rc) rc = rtk::upload(&p.coeffs, d->coeffs, p.n_mom);
     if (!rc) rc = rtk::upload(&p.inflow, d->inflow, p.n_rays);
+    if (d->inflow) p.h_inflow.assign(d->inflow, d->inflow + p.n_rays);
+    else p.h_inflow.assign(static_cast<size_t>(p.n_rays), 0.0);
     if (!rc) rc = rtk::upload(&p.mom, nullptr, mom_count);
     if (!rc) rc = rtk::upload(&p.gmom, nullptr, mom_count);
     if (!rc) {
@@ -264,6 +323,7 @@ int rtk_problem_create_lattice(const rtk_lattice_desc* d, rtk_problem** out) {
     rtk_problem* h = new (std::nothrow) rtk_problem();
     if (!h) return set_error(RTK_ERESOURCE, "host allocation failed");
     Problem& p = h->impl;
+    p.tune = rtk::tuning_from_env();
     p.kind = rtk::KIND_LATTICE;
     p.layout = d->layout;
     p.lat_nx = d->nx;
@@ -326,14 +386,27 @@ int rtk_problem_destroy(rtk_problem* p) {
 
 int64_t rtk_problem_n_total(const rtk_problem* p) { return p ? p->impl.n_total : -1; }
 
-int rtk_problem_set_inflow(rtk_problem* p, const double* inflow_host, int64_t n_rays) {
+int rtk_problem_set_inflow(rtk_problem* p, const double* inflow_host, int64_t n_rays, void* stream) {
     if (!p) return set_error(RTK_EINVAL, "null problem handle");
     if (p->impl.kind == rtk::KIND_LATTICE) return set_error(RTK_EINVAL, "lattice inflow is fixed at creation");
     if (n_rays != p->impl.n_rays) return set_error(RTK_EINVAL, "inflow length must equal n_rays");
-    if (inflow_host)
-        RTK_CUDA_TRY(cudaMemcpy(p->impl.inflow, inflow_host, sizeof(double) * n_rays, cudaMemcpyHostToDevice));
-    else
-        RTK_CUDA_TRY(cudaMemset(p->impl.inflow, 0, sizeof(double) * n_rays));
+    Problem& q = p->impl;
+    std::vector<double> want(static_cast<size_t>(n_rays), 0.0);
+    if (inflow_host) std::memcpy(want.data(), inflow_host, sizeof(double) * n_rays);
+    if (want == q.h_inflow) return RTK_OK;   // unchanged: no upload
+    // stream-ordered after every earlier kernel on `stream` that may still read the old inflow;
+    // the host copy `want` must outlive the transfer, so wait for it before returning
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    RTK_CUDA_TRY(cudaMemcpyAsync(q.inflow, want.data(), sizeof(double) * n_rays, cudaMemcpyHostToDevice, s));
+    RTK_CUDA_TRY(cudaStreamSynchronize(s));
+    q.h_inflow.swap(want);
+    return RTK_OK;
+}
+
+int rtk_problem_set_tuning(rtk_problem* p, const char* key, int64_t value) {
+    if (!p) return set_error(RTK_EINVAL, "null problem handle");
+    if (rtk::tuning_set(p->impl.tune, key, value))
+        return set_error(RTK_EINVAL, std::string("unknown tuning key or value: ") + (key ? key : "(null)"));
     return RTK_OK;
 }
 

@@ -2,11 +2,15 @@
 // reference's exact control flow (R/krylov.py:56-256); the vectors (Krylov
 // basis, iterate, residual) stay in HBM and only scalars cross to the host.
 //
-// Arnoldi uses classical Gram-Schmidt with one reorthogonalisation pass
-// (CGS2), fused into three streaming passes over the basis:
-//   pass 1  h1 = V^T w
-//   pass 2  w <- w - V h1 ;  h2 = V^T w          (same sweep over V)
-//   pass 3  w <- w - V h2 ;  ||w||^2
+// Arnoldi orthogonalisation (rtk_solve_cfg.orthogonalization):
+//  * MGS / MGS2 -- the reference's modified Gram-Schmidt (R/krylov.py:98-104), one
+//    sweep, or two with reorthogonalize=True: one streaming pass per basis vector,
+//    pass i  w <- w - h_{i-1} v_{i-1} ; h_i = v_i . w   (h_{i-1} read on the device);
+//  * CGS2 -- classical Gram-Schmidt with one reorthogonalisation pass, fused into
+//    three streaming passes over the whole basis:
+//      pass 1  h1 = V^T w
+//      pass 2  w <- w - V h1 ;  h2 = V^T w          (same sweep over V)
+//      pass 3  w <- w - V h2 ;  ||w||^2
 // followed by v_{j+1} = w / ||w||.  Every reduction is a fixed-shape
 // two-level tree (warp shuffle -> block -> last-block serial sum over block
 // partials in index order), so results are bitwise reproducible run to run.
@@ -15,6 +19,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <map>
+#include <new>
 #include <vector>
 
 #include "rtk_internal.cuh"
@@ -30,7 +36,9 @@ constexpr int kLookahead = 3;        // Arnoldi iterations the device may run ah
 
 enum PassMode { MODE_DOT = 0, MODE_UPDATE_DOT = 1, MODE_UPDATE_NORM = 2, MODE_UPDATE = 3 };
 
-struct Workspace {
+}  // namespace
+
+struct KrylovWorkspace {
     double* partials = nullptr;      // [KMAX][kMaxRedBlocks]
     unsigned* counter = nullptr;
     double* dev_scalars = nullptr;   // device-side coefficient / result scratch
@@ -39,7 +47,8 @@ struct Workspace {
     double* look_dev = nullptr;      // GMRES look-ahead column slots (device / pinned host)
     double* look_pin = nullptr;
     int look_cap = 0;
-    ~Workspace() {
+    int device = -1;                 // the device the buffers live on
+    ~KrylovWorkspace() {
         if (partials) cudaFree(partials);
         if (counter) cudaFree(counter);
         if (dev_scalars) cudaFree(dev_scalars);
@@ -60,6 +69,7 @@ struct Workspace {
         return RTK_OK;
     }
     int init() {
+        RTK_CUDA_TRY(cudaGetDevice(&device));
         RTK_CUDA_TRY(cudaMalloc(&partials, sizeof(double) * KMAX * kMaxRedBlocks));
         RTK_CUDA_TRY(cudaMalloc(&counter, sizeof(unsigned)));
         RTK_CUDA_TRY(cudaMemset(counter, 0, sizeof(unsigned)));
@@ -82,6 +92,10 @@ struct Workspace {
     }
 };
 
+void destroy_krylov_workspace(KrylovWorkspace* w) { delete w; }
+
+namespace {
+
 // one full wave: 148 SMs x resident blocks of the pass kernel for this bucket size
 int red_blocks(int64_t n, int kb = 4) {
     const int per_sm = kb <= 8 ? 4 : (kb <= 16 ? 2 : 1);
@@ -95,6 +109,61 @@ __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
+}
+
+// Fixed-order reduction of nk per-thread accumulators over the grid: warp shuffle ->
+// block (warp order) -> block partials; the last block to arrive sums the partials in
+// block-index order and writes out[0..nk).  Bitwise reproducible for a given grid size.
+template <int NACC>
+__device__ __forceinline__ void block_reduce_finish(const double* acc, int nk, double* partials, unsigned* counter,
+                                                    double* out) {
+    __shared__ double red[kRedThreads / 32][KMAX];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) {
+        if (k < nk) {
+            const double s = warp_sum(acc[k]);
+            if (lane == 0) red[warp][k] = s;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < nk) {
+        double s = 0.0;
+        for (int w = 0; w < kRedThreads / 32; ++w) s += red[w][threadIdx.x];
+        partials[threadIdx.x * kMaxRedBlocks + blockIdx.x] = s;
+    }
+    // last block to finish sums the block partials in index order
+    __shared__ bool is_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned ticket = atomicAdd(counter, 1u);
+        is_last = (ticket == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (is_last) {
+        __threadfence();
+        // the partials are staged in shared memory 64 blocks at a time by the whole block (one
+        // L2 round trip per chunk instead of one per 8 blocks), then thread k sums row k in
+        // block-index order: the same sequential sum, so results do not depend on the staging
+        __shared__ double fin[KMAX][kFinChunk + 1];
+        const unsigned nb = gridDim.x;
+        double total = 0.0;
+        for (unsigned b0 = 0; b0 < nb; b0 += kFinChunk) {
+            const unsigned cnt = min(static_cast<unsigned>(kFinChunk), nb - b0);
+#pragma unroll 8
+            for (int e = threadIdx.x; e < nk * kFinChunk; e += kRedThreads) {
+                const int k = e / kFinChunk, bb = e - k * kFinChunk;
+                if (bb < static_cast<int>(cnt)) fin[k][bb] = __ldcg(partials + k * kMaxRedBlocks + b0 + bb);
+            }
+            __syncthreads();
+            if (threadIdx.x < nk)
+                for (unsigned bb = 0; bb < cnt; ++bb) total += fin[threadIdx.x][bb];
+            __syncthreads();
+        }
+        if (threadIdx.x < nk) out[threadIdx.x] = total;
+        if (threadIdx.x == 0) *counter = 0u;
+    }
 }
 
 struct PassArgs {
@@ -174,65 +243,75 @@ __global__ void __launch_bounds__(kRedThreads) cgs_pass_kernel(PassArgs P) {
         }
     }
     if (MODE == MODE_UPDATE) return;
+    block_reduce_finish<NACC>(acc, (MODE == MODE_UPDATE_NORM) ? 1 : P.kc, P.partials, P.counter, P.out);
+}
 
-    // block reduction of each accumulator, fixed order
-    __shared__ double red[kRedThreads / 32][KMAX];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nk = (MODE == MODE_UPDATE_NORM) ? 1 : P.kc;
-#pragma unroll
-    for (int k = 0; k < NACC; ++k) {
-        if (k < nk) {
-            const double s = warp_sum(acc[k]);
-            if (lane == 0) red[warp][k] = s;
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x < nk) {
-        double s = 0.0;
-        for (int w = 0; w < kRedThreads / 32; ++w) s += red[w][threadIdx.x];
-        P.partials[threadIdx.x * kMaxRedBlocks + blockIdx.x] = s;
-    }
-    // last block to finish sums the block partials in index order
-    __shared__ bool is_last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned ticket = atomicAdd(P.counter, 1u);
-        is_last = (ticket == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (is_last) {
-        __threadfence();
-        // the partials are staged in shared memory 64 blocks at a time by the whole block (one
-        // L2 round trip per chunk instead of one per 8 blocks), then thread k sums row k in
-        // block-index order: the same sequential sum, so results do not depend on the staging
-        __shared__ double fin[KMAX][kFinChunk + 1];
-        const unsigned nb = gridDim.x;
-        double total = 0.0;
-        for (unsigned b0 = 0; b0 < nb; b0 += kFinChunk) {
-            const unsigned cnt = min(static_cast<unsigned>(kFinChunk), nb - b0);
-#pragma unroll 8
-            for (int e = threadIdx.x; e < nk * kFinChunk; e += kRedThreads) {
-                const int k = e / kFinChunk, bb = e - k * kFinChunk;
-                if (bb < static_cast<int>(cnt)) fin[k][bb] = __ldcg(P.partials + k * kMaxRedBlocks + b0 + bb);
+// One modified Gram-Schmidt step (R/krylov.py:98-104, one basis vector per pass):
+//   MGS_DOT          out = d . w                         (first vector of a sweep)
+//   MGS_UPDATE_DOT   w <- w - (*coef) u ;  out = d . w   (finish v_{i-1}, start v_i)
+//   MGS_UPDATE_NORM  w <- w - (*coef) u ;  out = ||w||^2 (last vector)
+// The coefficient is the previous pass's result, read on the device (no host round trip).
+enum MgsMode { MGS_DOT = 0, MGS_UPDATE_DOT = 1, MGS_UPDATE_NORM = 2 };
+struct MgsArgs {
+    const double* u;       // vector to subtract (update modes)
+    const double* coef;    // its coefficient, device
+    const double* d;       // vector to dot with (dot modes)
+    double* w;
+    int64_t n;
+    double* partials;
+    unsigned* counter;
+    double* out;
+};
+
+template <int MODE, int VEC>
+__global__ void __launch_bounds__(kRedThreads) mgs_pass_kernel(MgsArgs P) {
+    pdl_prologue();
+    const double c = (MODE == MGS_DOT) ? 0.0 : *P.coef;
+    double acc[1] = {0.0};
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (VEC == 2) {
+        const int64_t n2 = P.n >> 1;
+        for (int64_t e = t0; e < n2; e += stride) {
+            double2 we = reinterpret_cast<double2*>(P.w)[e];
+            if (MODE != MGS_DOT) {
+                const double2 uu = __ldg(reinterpret_cast<const double2*>(P.u) + e);
+                we.x = fma(-c, uu.x, we.x);
+                we.y = fma(-c, uu.y, we.y);
+                reinterpret_cast<double2*>(P.w)[e] = we;
             }
-            __syncthreads();
-            if (threadIdx.x < nk)
-                for (unsigned bb = 0; bb < cnt; ++bb) total += fin[threadIdx.x][bb];
-            __syncthreads();
+            if (MODE == MGS_UPDATE_NORM) {
+                acc[0] = fma(we.x, we.x, acc[0]);
+                acc[0] = fma(we.y, we.y, acc[0]);
+            } else {
+                const double2 dd = __ldg(reinterpret_cast<const double2*>(P.d) + e);
+                acc[0] = fma(dd.x, we.x, acc[0]);
+                acc[0] = fma(dd.y, we.y, acc[0]);
+            }
         }
-        if (threadIdx.x < nk) P.out[threadIdx.x] = total;
-        if (threadIdx.x == 0) *P.counter = 0u;
     }
+    for (int64_t e = (VEC == 2 ? (P.n & ~int64_t(1)) + t0 : t0); e < P.n; e += stride) {
+        double we = P.w[e];
+        if (MODE != MGS_DOT) {
+            we = fma(-c, __ldg(P.u + e), we);
+            P.w[e] = we;
+        }
+        acc[0] = (MODE == MGS_UPDATE_NORM) ? fma(we, we, acc[0]) : fma(__ldg(P.d + e), we, acc[0]);
+    }
+    block_reduce_finish<1>(acc, 1, P.partials, P.counter, P.out);
 }
 
 // y = a * x  (a read from device: 1/sqrt(norm2) or a host scalar)
 __global__ void scale_kernel(const double* __restrict__ x, double* __restrict__ y, int64_t n, double a,
                              const double* __restrict__ norm2) {
     pdl_prologue();
+    // an exactly zero norm (Arnoldi breakdown) gives a zero vector instead of 0/0 = NaN: a
+    // look-ahead iteration enqueued past a breakdown then runs on finite data
     const double s = norm2 ? sqrt(*norm2) : a;
+    const double r = s != 0.0 ? 1.0 / s : 0.0;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride) y[e] = x[e] / s;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride)
+        y[e] = s != 0.0 ? x[e] / s : x[e] * r;
 }
 
 // out = base + sum_k y_k V_k  (the reference's _combine, R/krylov.py:173-177, added to x)
@@ -315,27 +394,55 @@ int pool_alloc(double** p, size_t count, cudaStream_t s) {
     return RTK_OK;
 }
 
-// One reduction workspace per host thread, reused across solves (its allocation
-// -- cudaMallocHost in particular -- costs milliseconds).
-Workspace& thread_workspace(int* rc) {
-    thread_local Workspace ws;
-    thread_local bool ready = false;
-    *rc = RTK_OK;
-    if (!ready) {
-        *rc = ws.init();
-        ready = (*rc == RTK_OK);
+// Reduction scratch (block partials, counter, column slots, pinned staging) reused across
+// solves -- its allocation, cudaMallocHost in particular, costs milliseconds.  A solve on a
+// problem handle uses the handle's own workspace (created on the handle's first solve);
+// callable solves and the exported BLAS-1 use one per (host thread, device).  Either way the
+// buffers belong to the device that is current when they are created and are rebuilt if
+// the same owner is later used on another device.
+int bind_workspace(KrylovWorkspace*& slot, KrylovWorkspace** out) {
+    int dev = 0;
+    RTK_CUDA_TRY(cudaGetDevice(&dev));
+    if (slot && slot->device != dev) {
+        delete slot;
+        slot = nullptr;
     }
-    return ws;
+    if (!slot) {
+        auto* w = new (std::nothrow) KrylovWorkspace();
+        if (!w) return set_error(RTK_ERESOURCE, "host allocation failed (Krylov workspace)");
+        if (int rc = w->init()) {
+            delete w;
+            return rc;
+        }
+        slot = w;
+    }
+    *out = slot;
+    return RTK_OK;
+}
+
+int acquire_workspace(Problem* owner, KrylovWorkspace** out) {
+    if (owner) return bind_workspace(owner->krylov_ws, out);
+    struct PerDevice {
+        std::map<int, KrylovWorkspace*> by_dev;
+        ~PerDevice() {
+            for (auto& kv : by_dev) delete kv.second;
+        }
+    };
+    thread_local PerDevice tl;
+    int dev = 0;
+    RTK_CUDA_TRY(cudaGetDevice(&dev));
+    return bind_workspace(tl.by_dev[dev], out);
+}
+
+bool graphs_enabled() {
+    static const bool on = !getenv_flag("RTK_GMRES_NO_GRAPH");   // A/B switch, read once per process
+    return on;
 }
 
 class Engine {
    public:
-    Engine(cudaStream_t s) : s_(s) {}
-    int init() {
-        int rc;
-        wsp_ = &thread_workspace(&rc);
-        return rc;
-    }
+    explicit Engine(cudaStream_t s, Problem* owner = nullptr) : s_(s), owner_(owner) {}
+    int init() { return acquire_workspace(owner_, &wsp_); }
 
     // results (dots or norm^2) land in out_dev[0 .. k)
     int pass(int mode, const double* const* V, int k, const double* coef_dev, double* w, int64_t n, double* out_dev) {
@@ -350,8 +457,7 @@ class Engine {
         P.counter = wsp_->counter;
         P.out = out_dev;
         const int kb = k <= 4 ? 4 : (k <= 8 ? 8 : (k <= 16 ? 16 : 32));
-        const char* ov = std::getenv("RTK_PASS_BLOCKS");   // tuning hook: fixed block count for every pass
-        const int blocks = ov ? std::max(1, std::min(kMaxRedBlocks, std::atoi(ov))) : red_blocks(n, kb);
+        const int blocks = red_blocks(n, kb);
         RTK_CUDA_TRY(k <= 4 ? launch_pass<4>(mode, blocks, P)
                             : k <= 8 ? launch_pass<8>(mode, blocks, P)
                                      : k <= 16 ? launch_pass<16>(mode, blocks, P) : launch_pass<32>(mode, blocks, P));
@@ -420,6 +526,60 @@ class Engine {
         return RTK_OK;
     }
 
+    int mgs_pass(int mode, const double* u, const double* coef, const double* d, double* w, int64_t n, double* out) {
+        MgsArgs P;
+        P.u = u;
+        P.coef = coef;
+        P.d = d;
+        P.w = w;
+        P.n = n;
+        P.partials = wsp_->partials;
+        P.counter = wsp_->counter;
+        P.out = out;
+        bool aligned = (reinterpret_cast<uintptr_t>(w) & 15) == 0;
+        if (u) aligned = aligned && (reinterpret_cast<uintptr_t>(u) & 15) == 0;
+        if (d) aligned = aligned && (reinterpret_cast<uintptr_t>(d) & 15) == 0;
+        const int blocks = red_blocks(n, 4);
+        cudaError_t e;
+        if (aligned) {
+            e = mode == MGS_DOT ? launch_pdl(mgs_pass_kernel<MGS_DOT, 2>, blocks, kRedThreads, 0, s_, P)
+                : mode == MGS_UPDATE_DOT ? launch_pdl(mgs_pass_kernel<MGS_UPDATE_DOT, 2>, blocks, kRedThreads, 0, s_, P)
+                                         : launch_pdl(mgs_pass_kernel<MGS_UPDATE_NORM, 2>, blocks, kRedThreads, 0, s_, P);
+        } else {
+            e = mode == MGS_DOT ? launch_pdl(mgs_pass_kernel<MGS_DOT, 1>, blocks, kRedThreads, 0, s_, P)
+                : mode == MGS_UPDATE_DOT ? launch_pdl(mgs_pass_kernel<MGS_UPDATE_DOT, 1>, blocks, kRedThreads, 0, s_, P)
+                                         : launch_pdl(mgs_pass_kernel<MGS_UPDATE_NORM, 1>, blocks, kRedThreads, 0, s_, P);
+        }
+        RTK_CUDA_TRY(e);
+        RTK_LAUNCH_CHECK("mgs_pass_kernel");
+        return RTK_OK;
+    }
+
+    // Modified Gram-Schmidt, one sweep (sweeps = 1) or two (reorthogonalize, sweeps = 2), the
+    // reference's loop order (R/krylov.py:98-104): h1 -> slot[0, jp1), h2 -> slot[jp1, 2 jp1)
+    // (second sweep only), ||w||^2 -> slot[2 jp1].
+    int mgs_enqueue(const std::vector<double*>& V, int jp1, double* w, int64_t n, double* slot, int sweeps) {
+        int rc;
+        const double* prev_u = nullptr;
+        const double* prev_c = nullptr;
+        for (int sw = 0; sw < sweeps; ++sw) {
+            double* h = slot + sw * jp1;
+            for (int i = 0; i < jp1; ++i) {
+                const int mode = prev_u ? MGS_UPDATE_DOT : MGS_DOT;
+                if ((rc = mgs_pass(mode, prev_u, prev_c, V[i], w, n, h + i))) return rc;
+                prev_u = V[i];
+                prev_c = h + i;
+            }
+        }
+        return mgs_pass(MGS_UPDATE_NORM, prev_u, prev_c, nullptr, w, n, slot + 2 * jp1);
+    }
+
+    // Arnoldi orthogonalisation of w against V[0, jp1) by the configured method
+    int orth_enqueue(int orth, const std::vector<double*>& V, int jp1, double* w, int64_t n, double* slot) {
+        if (orth == RTK_ORTH_CGS2) return cgs2_enqueue(V, jp1, w, n, slot);
+        return mgs_enqueue(V, jp1, w, n, slot, orth == RTK_ORTH_MGS2 ? 2 : 1);
+    }
+
     // y = x / sqrt(*norm2_dev)  (the norm stays on the device)
     int scale_dev(const double* x, double* y, int64_t n, const double* norm2_dev) {
         RTK_CUDA_TRY(launch_pdl(scale_kernel, elem_blocks(n), 256, 0, s_, x, y, n, 1.0, norm2_dev));
@@ -463,10 +623,11 @@ class Engine {
         return RTK_OK;
     }
 
-    Workspace* wsp_ = nullptr;
+    KrylovWorkspace* wsp_ = nullptr;
 
    private:
     cudaStream_t s_;
+    Problem* owner_;
 };
 
 struct DevBuf {
@@ -564,14 +725,30 @@ struct CycleGraph {
     }
 };
 
+int resolve_orth(const rtk_solve_cfg* cfg, int* orth) {
+    switch (cfg->orthogonalization) {
+        case RTK_ORTH_REFERENCE: *orth = cfg->reorthogonalize ? RTK_ORTH_MGS2 : RTK_ORTH_MGS; return RTK_OK;
+        case RTK_ORTH_MGS:
+        case RTK_ORTH_MGS2:
+        case RTK_ORTH_CGS2: *orth = cfg->orthogonalization; return RTK_OK;
+        default: return set_error(RTK_EINVAL, "unknown orthogonalization");
+    }
+}
+
 int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, double* x, const rtk_solve_cfg* cfg,
-               rtk_solve_report* rep, double* hist_out, int hist_cap, cudaStream_t s) {
+               rtk_solve_report* rep, double* hist_out, int hist_cap, cudaStream_t s, Problem* owner) {
     if (!cfg || !rep || !b || !x) return set_error(RTK_EINVAL, "null argument");
     if (!(cfg->rel_tol > 0)) return set_error(RTK_EINVAL, "rel_tol must be positive");
     if (cfg->max_iter < 1) return set_error(RTK_EINVAL, "max_iter must be >= 1");
+    int orth;
+    if (int e = resolve_orth(cfg, &orth)) return e;
+    const bool two_sweeps = orth != RTK_ORTH_MGS;   // h = h1 + h2
+    // Look-ahead only for the library's own matvec: a user callable sees exactly the
+    // reference's sequence of calls (no speculative applications past a stop or breakdown).
+    const int window = apply == rtk_problem_matvec ? kLookahead : 1;
     *rep = rtk_solve_report{};
     History hist{hist_out, hist_cap};
-    Engine E(s);
+    Engine E(s, owner);
     int rc;
     if ((rc = E.init())) return rc;
     int matvecs = 0;
@@ -631,7 +808,7 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
     // synchronise), restarted GMRES with short cycles, small vectors (launch-bound regime)
     // (capturing + instantiating costs ~1 ms, so only solves allowed several cycles use it)
     const bool graph_ok = apply == rtk_problem_matvec && cfg->restart > 0 && cycle <= 64 && n <= (int64_t(1) << 23) &&
-                          cfg->max_iter >= 3 * cycle && !getenv_flag("RTK_GMRES_NO_GRAPH");
+                          cfg->max_iter >= 3 * cycle && graphs_enabled();
     CycleGraph G;
     const int slot_max = 2 * (cycle + 1) + 1;
     auto finish = [&](int iters, bool conv, bool brk, double tr) {
@@ -684,7 +861,7 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
             RTK_CUDA_TRY(cudaStreamSynchronize(s));
             if ((rc = apply(ctx, V.v[0], cand.p, n, G.gs))) return rc;
             RTK_CUDA_TRY(cudaStreamSynchronize(G.gs));
-            Engine Eg(G.gs);
+            Engine Eg(G.gs, owner);
             if ((rc = Eg.init())) return rc;
             cudaGraph_t graph = nullptr;
             const int64_t l0 = rtk_kernel_launch_count();
@@ -694,7 +871,7 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
                 // the column's read-back (copy + external event) branches off after the CGS2
                 // passes, so the next matvec does not wait for the device-to-host copy
                 ok = apply(ctx, V.v[jj], w.p, n, G.gs) == RTK_OK &&
-                     Eg.cgs2_enqueue(V.v, jj + 1, w.p, n, dslot) == RTK_OK &&
+                     Eg.orth_enqueue(orth, V.v, jj + 1, w.p, n, dslot) == RTK_OK &&
                      cudaEventRecord(G.fork, G.gs) == cudaSuccess &&
                      cudaStreamWaitEvent(G.side, G.fork, 0) == cudaSuccess &&
                      cudaMemcpyAsync(pslots + static_cast<size_t>(jj) * slot_max, dslot,
@@ -729,11 +906,11 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
         }
         int j = 0;
         while (j < steps) {
-            while (!graph_cycle && next < steps && next - j < kLookahead) {
+            while (!graph_cycle && next < steps && next - j < window) {
                 const int q = next % kLookahead;
                 double* dslot = dslots + static_cast<size_t>(q) * slot_sz;
                 if ((rc = A(V.v[next], w.p))) return rc;
-                if ((rc = E.cgs2_enqueue(V.v, next + 1, w.p, n, dslot))) return rc;
+                if ((rc = E.orth_enqueue(orth, V.v, next + 1, w.p, n, dslot))) return rc;
                 RTK_CUDA_TRY(cudaEventRecord(side.fork, s));
                 RTK_CUDA_TRY(cudaStreamWaitEvent(side.st, side.fork, 0));
                 RTK_CUDA_TRY(cudaMemcpyAsync(pslots + static_cast<size_t>(q) * slot_sz, dslot,
@@ -749,7 +926,7 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
                 if (graph_cycle) ++matvecs;   // the replayed matvec of iteration j is consumed
                 const double* hs = pslots + static_cast<size_t>(q) * slot_sz;
                 col.assign(j + 2, 0.0);
-                for (int i = 0; i <= j; ++i) col[i] = hs[i] + hs[j + 1 + i];
+                for (int i = 0; i <= j; ++i) col[i] = two_sweeps ? hs[i] + hs[j + 1 + i] : hs[i];
                 col[j + 1] = std::sqrt(hs[2 * (j + 1)]);
             }
             breakdown = col[j + 1] < 1e-14 * b_norm;
@@ -811,14 +988,14 @@ int gmres_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, doubl
 }
 
 int bicgstab_impl(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, double* x, const rtk_solve_cfg* cfg,
-                  rtk_solve_report* rep, double* hist_out, int hist_cap, cudaStream_t s) {
+                  rtk_solve_report* rep, double* hist_out, int hist_cap, cudaStream_t s, Problem* owner) {
     // R/krylov.py:180-256
     if (!cfg || !rep || !b || !x) return set_error(RTK_EINVAL, "null argument");
     if (!(cfg->rel_tol > 0)) return set_error(RTK_EINVAL, "rel_tol must be positive");
     if (cfg->max_iter < 1) return set_error(RTK_EINVAL, "max_iter must be >= 1");
     *rep = rtk_solve_report{};
     History hist{hist_out, hist_cap};
-    Engine E(s);
+    Engine E(s, owner);
     int rc;
     if ((rc = E.init())) return rc;
     int matvecs = 0;
@@ -935,20 +1112,21 @@ extern "C" {
 int rtk_gmres(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, double* x, const rtk_solve_cfg* cfg,
               rtk_solve_report* rep, double* hist, int32_t cap, void* stream) {
     if (!apply) return rtk::set_error(RTK_EINVAL, "null matvec");
-    return rtk::gmres_impl(apply, ctx, n, b, x, cfg, rep, hist, cap, static_cast<cudaStream_t>(stream));
+    return rtk::gmres_impl(apply, ctx, n, b, x, cfg, rep, hist, cap, static_cast<cudaStream_t>(stream), nullptr);
 }
 
 int rtk_gmres_problem(rtk_problem* p, const double* b, double* x, const rtk_solve_cfg* cfg, rtk_solve_report* rep,
                       double* hist, int32_t cap, void* stream) {
     if (!p) return rtk::set_error(RTK_EINVAL, "null problem handle");
     return rtk::gmres_impl(rtk_problem_matvec, p, rtk_problem_n_total(p), b, x, cfg, rep, hist, cap,
-                           static_cast<cudaStream_t>(stream));
+                           static_cast<cudaStream_t>(stream), rtk::problem_impl(p));
 }
 
 int rtk_bicgstab(rtk_matvec_fn apply, void* ctx, int64_t n, const double* b, double* x, const rtk_solve_cfg* cfg,
                  rtk_solve_report* rep, double* hist, int32_t cap, void* stream) {
     if (!apply) return rtk::set_error(RTK_EINVAL, "null matvec");
-    return rtk::bicgstab_impl(apply, ctx, n, b, x, cfg, rep, hist, cap, static_cast<cudaStream_t>(stream));
+    return rtk::bicgstab_impl(apply, ctx, n, b, x, cfg, rep, hist, cap, static_cast<cudaStream_t>(stream),
+                              apply == rtk_problem_matvec ? rtk::problem_impl(static_cast<rtk_problem*>(ctx)) : nullptr);
 }
 
 int rtk_dot(const double* x, const double* y, int64_t n, double* out_host, void* stream) {

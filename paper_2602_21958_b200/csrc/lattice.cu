@@ -1083,21 +1083,18 @@ static int launch_int(const Problem& p, const LatArgs& A, int with_inflow, cudaS
     constexpr int ring = FS == RTK_FS_EXP_PARABOLIC ? 4 : 3;
     const size_t smem_planes = sizeof(double) * A.nxy * (kFC + ring * kFC + ring + 2 * kFC + kFC) +
                                sizeof(Shift) * (p.lat_max_sub + 1);
-    if (FS == RTK_FS_EXP_PARABOLIC && (smem_planes > 160 * 1024 || getenv_flag("RTK_LATTICE_NO_SMEM")))
+    if (FS == RTK_FS_EXP_PARABOLIC && (smem_planes > 160 * 1024 || p.tune.lat_no_smem))
         return set_error(RTK_ERESOURCE, "exp-parabolic in the intensity layout needs the shared-memory kernel "
                                         "(small layers); use the moment layout");
-    if (smem_planes <= 160 * 1024 && !getenv_flag("RTK_LATTICE_NO_SMEM")) {
+    if (smem_planes <= 160 * 1024 && !p.tune.lat_no_smem) {
         // the parabolic march samples the opacity planes (its downwind segment is not in the table)
-        const bool dt = A.dtab != nullptr && !getenv_flag("RTK_LATTICE_NO_DTAB") && FS != RTK_FS_EXP_PARABOLIC;
-        const bool planar = A.ny == 1 && !getenv_flag("RTK_LATTICE_NO_PLANAR");
+        const bool dt = A.dtab != nullptr && !p.tune.lat_no_dtab && FS != RTK_FS_EXP_PARABOLIC;
+        const bool planar = A.ny == 1 && !p.tune.lat_no_planar;
         auto kern = dt ? (planar ? lattice_int_smem_kernel<FS, SRC, OUT, true, true>
                                  : lattice_int_smem_kernel<FS, SRC, OUT, true, false>)
                        : (planar ? lattice_int_smem_kernel<FS, SRC, OUT, false, true>
                                  : lattice_int_smem_kernel<FS, SRC, OUT, false, false>);
-        if (smem_planes > 48 * 1024 &&
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_planes)) !=
-                cudaSuccess)
-            return set_error(RTK_ERESOURCE, "lattice planes do not fit in shared memory");
+        if (int rc = ensure_smem_for(kern, smem_planes)) return rc;
         const int nfc = (A.n_freq + kFC - 1) / kFC;
         kern<<<A.n_dirs * nfc, kIntThreads, smem_planes, s>>>(A, with_inflow, p.lat_max_sub);
         RTK_LAUNCH_CHECK("lattice_int_smem_kernel");
@@ -1108,11 +1105,7 @@ static int launch_int(const Problem& p, const LatArgs& A, int with_inflow, cudaS
                                         "(small layers); use the moment layout");
     const size_t smem = sizeof(double) * A.nxy * kFC;
     auto kern = lattice_int_kernel<FS, SRC, OUT>;
-    if (smem > 48 * 1024) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
-            cudaSuccess)
-            return set_error(RTK_ERESOURCE, "lattice line plane does not fit in shared memory");
-    }
+    if (int rc = ensure_smem_for(kern, smem)) return rc;
     const int nfc = (A.n_freq + kFC - 1) / kFC;
     kern<<<A.n_dirs * nfc, kIntThreads, smem, s>>>(A, with_inflow);
     RTK_LAUNCH_CHECK("lattice_int_kernel");
@@ -1150,8 +1143,7 @@ static int launch_mom_steps_dg(const Problem& p, const LatArgs& A, bool with_inf
     const size_t mom_smem = sizeof(double) * NM * F * mb + sizeof(StepDir) * A.n_dirs +
                             sizeof(Shift) * (2 * A.n_dirs + A.total_sub);
     auto kern = lattice_mom_group_kernel<FS, NM, F, DG>;
-    if (mom_smem > 48 * 1024)
-        RTK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(mom_smem)));
+    if (int rc = ensure_smem_for(kern, mom_smem)) return rc;
     const unsigned sblocks = static_cast<unsigned>((A.nxy * ((p.fp + F - 1) / F) + ipb - 1) / ipb);
     double* a = p.lat_state[0];
     double* b = p.lat_state[1];
@@ -1182,7 +1174,7 @@ static int launch_mom_steps(const Problem& p, const LatArgs& A, bool with_inflow
     // direction groups only where a step has too few items to fill the SMs: measured cfg4
     // (65,536 items) 45.0 -> 41.3 ms with DG = 8; cfg5 (344,064 items) is slower with it
     const int64_t items = A.nxy * ((p.fp + 1) / 2);
-    const int dg = getenv("RTK_LAT_DG") ? atoi(getenv("RTK_LAT_DG")) : (items <= 131072 ? 8 : 1);
+    const int dg = p.tune.lat_dg ? p.tune.lat_dg : (items <= 131072 ? 8 : 1);
     if (dg == 1) return launch_mom_steps_dg<FS, SRC, NM, 1>(p, A, with_inflow, mom, s);
     if (dg == 4) return launch_mom_steps_dg<FS, SRC, NM, 4>(p, A, with_inflow, mom, s);
     return launch_mom_steps_dg<FS, SRC, NM, 8>(p, A, with_inflow, mom, s);

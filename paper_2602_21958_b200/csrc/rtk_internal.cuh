@@ -69,19 +69,53 @@ struct LatDir {
 };
 
 enum ProblemKind { KIND_SLAB = 1, KIND_LATTICE = 2 };
+
+// Per-problem kernel-selection switches.  Initialised ONCE when the problem is created
+// (tuning_from_env: the RTK_* variables, for A/B measurements) and overridable per handle
+// through rtk_problem_set_tuning (tests select each shipped kernel variant this way).
+// Launchers read only this struct, never the environment.
+struct Tuning {
+    int disable_tma = 0;      // "disable_tma"      RTK_DISABLE_TMA: 1D sweeps take the cp.async kernel (sweep1d.cu)
+    int lat_dg = 0;           // "lattice_dg"       RTK_LAT_DG: direction groups of the lattice moment kernel (0 auto, 1/4/8)
+    int lat_no_smem = 0;      // "lattice_no_smem"  RTK_LATTICE_NO_SMEM: intensity layout without the shared-memory kernel
+    int lat_no_dtab = 0;      // "lattice_no_dtab"  RTK_LATTICE_NO_DTAB: sample opacity instead of the dt table
+    int lat_no_planar = 0;    // "lattice_no_planar" RTK_LATTICE_NO_PLANAR: 2D slabs through the 3D sampling path
+    int moments_scalar = 0;   // "moments_scalar"   RTK_MOMENTS_SCALAR: 8-byte moment kernel instead of the pair kernel
+    int sigma_unfused = 0;    // "sigma_unfused"    RTK_SIGMA_UNFUSED: K2a + K2b instead of the fused Sigma kernel
+};
+Tuning tuning_from_env();
+// 0 ok, 1 unknown key
+int tuning_set(Tuning& t, const char* key, int64_t value);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-DEVICE attribute: this records
+// the largest size set per (kernel, current device) and sets it when a launch needs more.
+// Returns RTK_OK or a CUDA status (with the error message set).
+int ensure_smem(const void* func, size_t bytes);
+template <typename F>
+int ensure_smem_for(F* func, size_t bytes) {
+    return ensure_smem(reinterpret_cast<const void*>(func), bytes);
+}
+// per-(kernel, device) cached integer (e.g. co-resident clusters of a launch shape); -1 if unset
+int device_cache_get(const void* func, int slot);
+void device_cache_put(const void* func, int slot, int value);
 enum Layout { LAYOUT_INTENSITY = 0, LAYOUT_MOMENTS = 1 };
 
 struct MomCta {
     int a0, nd, down, f0, group;   // 1D moment-layout sweep: directions [a0, a0+nd), 16-frequency tile at f0
 };
 
+struct KrylovWorkspace;   // krylov.cu
+
 struct Problem {
     int kind = KIND_SLAB;
+    Tuning tune;
+    KrylovWorkspace* krylov_ws = nullptr;   // reduction scratch of solves on this handle (owned)
     int layout = LAYOUT_INTENSITY;
     int64_t n_space = 0;
     int n_angles = 0, n_freq = 0, n_mom = 0, fs = 0, gamma_per_ray = 0, fp = 0;
     int64_t n_rays = 0, n_total = 0;
     std::vector<double> h_mu, h_coeffs;
+    std::vector<double> h_inflow;   // host copy of the uploaded inflow (set_inflow skips unchanged uploads)
     double *dt = nullptr, *phi = nullptr, *inv_mu = nullptr, *wy = nullptr, *yb = nullptr;
     double *rwt = nullptr, *gamma = nullptr, *coeffs = nullptr, *inflow = nullptr;
     int* dir_sign = nullptr;     // [n_angles] -1 down (mu<0), +1 up
@@ -119,11 +153,7 @@ struct Problem {
     int lat_max_sub = 0;                         // largest sub-segment count over the directions
     bool lat_any_sc = false;   // some direction uses short characteristics
     int lat_total_sub = 0;                       // sum over directions of (n_sub + 1)
-    // overlap of the HBM-bound moment reduction with the FP64 redistribution GEMM (slab apply_A)
-    cudaStream_t aux = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chunk[8] = {};
     CUtensorMap tma_gmap, tma_dtmap;
-    CUtensorMap tma_gmap4, tma_dtmap4;          // U = 4 boxes (exp-linear weight-warp sweep)
     ~Problem();
 };
 
@@ -158,9 +188,9 @@ int lattice_transfer_moments(const Problem& p, int src_mode, bool with_inflow, c
 enum Epilogue { EPI_GAMMA = 0, EPI_COEF = 1, EPI_SUB = 2, EPI_PLAIN = 3 };
 int launch_redistribute_ex(const Problem& p, const double* A, double* C, int ldc, int epi, const double* U, int ldu,
                            cudaStream_t s, int64_t nodes = -1, const double* gamma = nullptr);
-int launch_moments_range(const Problem& p, const double* x, int64_t i0, int64_t i1, cudaStream_t s);
-int launch_redistribute_range(const Problem& p, int64_t i0, int64_t i1, cudaStream_t s);
 // krylov.cu
+void destroy_krylov_workspace(KrylovWorkspace* w);
+Problem* problem_impl(rtk_problem* p);
 int apply_A_dev(Problem& p, const double* x, double* y, cudaStream_t s);
 int sweep_apply(const Problem& p, const double* x, double* y, cudaStream_t s);
 bool getenv_flag(const char* name);
@@ -171,12 +201,15 @@ __device__ __forceinline__ void pdl_prologue() {
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
-// launch with programmatic stream serialization (the kernel starts with pdl_prologue);
-// RTK_NO_PDL=1 launches plainly
+// Programmatic dependent launch on (default); RTK_NO_PDL=1 (read once per process, an A/B
+// measurement switch) launches plainly.
+bool pdl_enabled();
+
+// launch with programmatic stream serialization (the kernel starts with pdl_prologue)
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned blocks, int threads, size_t smem, cudaStream_t s,
                        Args... args) {
-    static const bool off = getenv_flag("RTK_NO_PDL");
+    const bool off = !pdl_enabled();
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -416,19 +416,9 @@ int launch_expand_nodes(const Problem& p, const double* thermal, double* out, cu
 }
 
 template <int NM>
-int launch_moments_t(const Problem& p, const double* x, cudaStream_t s, int64_t i0 = 0, int64_t i1 = -1) {
-    if (i1 < 0) i1 = p.n_space;
-    if (i0 != 0 || i1 != p.n_space) {   // row range [i0, i1): offset the pointers, same kernel
-        const int64_t rows = i1 - i0;
-        const unsigned blocks = static_cast<unsigned>((rows * p.n_freq + kMomThreads - 1) / kMomThreads);
-        const size_t smem = sizeof(double) * NM * p.n_angles;
-        moments_kernel<NM><<<blocks, kMomThreads, smem, s>>>(x + i0 * p.n_rays, p.wy, p.mom + i0 * NM * p.fp, rows,
-                                                             p.n_angles, p.n_freq, p.fp);
-        RTK_LAUNCH_CHECK("moments_kernel");
-        return RTK_OK;
-    }
+int launch_moments_t(const Problem& p, const double* x, cudaStream_t s) {
     const size_t smem = sizeof(double) * NM * p.n_angles;
-    if ((p.n_freq & 1) == 0 && !getenv_flag("RTK_MOMENTS_SCALAR")) {
+    if ((p.n_freq & 1) == 0 && !p.tune.moments_scalar) {
         const int64_t work = p.n_space * (p.n_freq / 2);
         const unsigned blocks = static_cast<unsigned>((work + kMomThreads - 1) / kMomThreads);
         RTK_CUDA_TRY(launch_pdl(moments_pair_kernel<NM>, blocks, kMomThreads, smem, s, x, p.wy, p.mom, p.n_space,
@@ -445,20 +435,6 @@ int launch_moments_t(const Problem& p, const double* x, cudaStream_t s, int64_t 
 }
 
 }  // namespace
-
-int launch_moments_range(const Problem& p, const double* x, int64_t i0, int64_t i1, cudaStream_t s) {
-    switch (p.n_mom) {
-        case 1: return launch_moments_t<1>(p, x, s, i0, i1);
-        case 2: return launch_moments_t<2>(p, x, s, i0, i1);
-        case 3: return launch_moments_t<3>(p, x, s, i0, i1);
-        case 4: return launch_moments_t<4>(p, x, s, i0, i1);
-        case 5: return launch_moments_t<5>(p, x, s, i0, i1);
-        case 6: return launch_moments_t<6>(p, x, s, i0, i1);
-        case 7: return launch_moments_t<7>(p, x, s, i0, i1);
-        case 8: return launch_moments_t<8>(p, x, s, i0, i1);
-        default: return set_error(RTK_EINVAL, "moments: unsupported number of moments");
-    }
-}
 
 int launch_moments(const Problem& p, const double* x, cudaStream_t s) {
     switch (p.n_mom) {
@@ -479,12 +455,7 @@ int launch_redistribute_ex(const Problem& p, const double* A, double* C, int ldc
     const int64_t M = (nodes < 0 ? p.n_space : nodes) * p.n_mom;
     if (!gamma) gamma = p.gamma;
     if (p.n_freq >= 64) {
-        static bool configured = false;
-        if (!configured) {
-            cudaFuncSetAttribute(dmma::redistribute_dmma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(dmma::kSmem));
-            configured = true;
-        }
+        if (int rc = ensure_smem_for(dmma::redistribute_dmma_kernel<2>, dmma::kSmem)) return rc;
         dim3 grid(static_cast<unsigned>((M + dmma::BM - 1) / dmma::BM), (p.n_freq + dmma::BN - 1) / dmma::BN);
         // pitch fp is even: 16-byte copies always legal; pad column/row entries are zero
         dmma::redistribute_dmma_kernel<2><<<grid, dmma::THREADS, dmma::kSmem, s>>>(
@@ -505,13 +476,6 @@ int launch_redistribute_ex(const Problem& p, const double* A, double* C, int ldc
                                                       epi, p.fp, ldc, U, ldu);
     RTK_LAUNCH_CHECK("redistribute_kernel");
     return RTK_OK;
-}
-
-int launch_redistribute_range(const Problem& p, int64_t i0, int64_t i1, cudaStream_t s) {
-    // rows of space nodes [i0, i1): offset A, C and gamma; the kernels index rows relative to the chunk
-    return launch_redistribute_ex(p, p.mom + i0 * p.n_mom * p.fp, p.gmom + i0 * p.n_mom * p.fp, p.fp,
-                                  p.gamma_per_ray ? EPI_COEF : EPI_GAMMA, nullptr, 0, s, i1 - i0,
-                                  p.gamma + i0 * (p.gamma_per_ray ? p.n_rays : p.n_freq));
 }
 
 int launch_redistribute(const Problem& p, cudaStream_t s) {

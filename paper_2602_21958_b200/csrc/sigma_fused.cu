@@ -360,11 +360,11 @@ int launch_t(const Problem& p, const double* x, cudaStream_t s) {
     const int n_apad = (p.n_angles + AC - 1) / AC * AC;
     const size_t smem = C::smem_bytes(n_apad);
     if (smem > kSmemLimit) return -1;
-    static int max_clusters = -1;   // per instantiation
-    static size_t configured_smem = 0;
-    if (configured_smem != smem) {
-        RTK_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(smem)));
+    // co-resident clusters of this instantiation at this smem size, per device
+    const int cache_slot = static_cast<int>(smem);
+    int max_clusters = device_cache_get(reinterpret_cast<const void*>(kernel), cache_slot);
+    if (max_clusters <= 0) {
+        if (int rc = ensure_smem_for(kernel, smem)) return rc;
         cudaLaunchConfig_t qc = {};
         cudaLaunchAttribute qa[1];
         qa[0].id = cudaLaunchAttributeClusterDimension;
@@ -377,14 +377,10 @@ int launch_t(const Problem& p, const double* x, cudaStream_t s) {
         qc.attrs = qa;
         qc.numAttrs = 1;
         int nc = 0;
-        if (cudaOccupancyMaxActiveClusters(&nc, kernel, &qc) != cudaSuccess || nc <= 0) {
-            cudaGetLastError();
-            return -1;
-        }
+        RTK_CUDA_TRY(cudaOccupancyMaxActiveClusters(&nc, kernel, &qc));
+        if (nc <= 0) return -1;   // this cluster shape cannot be resident on the device
         max_clusters = nc;
-        configured_smem = smem;
-        if (getenv_flag("RTK_DEBUG"))
-            std::fprintf(stderr, "sigma_fused<%d,%d,%d>: %d co-resident clusters\n", CN, MT, NT, nc);
+        device_cache_put(reinterpret_cast<const void*>(kernel), cache_slot, nc);
     }
     // block size: the fewest rounds over the co-resident clusters, then the smallest SP
     // that keeps that round count (balanced blocks), then as few clusters as possible
@@ -399,10 +395,11 @@ int launch_t(const Problem& p, const double* x, cudaStream_t s) {
                                   static_cast<uint64_t>(p.n_space)};
         const uint64_t strides[2] = {sizeof(double) * p.n_freq, sizeof(double) * p.n_rays};
         const uint32_t box[3] = {KS, AC, static_cast<uint32_t>(sp)};
-        if (!encode_f64_map(&xmap, x, 3, dims, strides, box)) return -1;
+        if (!encode_f64_map(&xmap, x, 3, dims, strides, box)) return set_error(RTK_ECUDA, "sigma: x tensor map");
         const uint64_t rd[2] = {static_cast<uint64_t>(p.fp), static_cast<uint64_t>(p.n_freq)};
         const uint32_t rb[2] = {16, static_cast<uint32_t>(C::BK)};
-        if (!encode_f64_map_sw128(&rmap, p.rwt, rd, sizeof(double) * p.fp, rb)) return -1;
+        if (!encode_f64_map_sw128(&rmap, p.rwt, rd, sizeof(double) * p.fp, rb))
+            return set_error(RTK_ECUDA, "sigma: R tensor map");
     }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
@@ -432,17 +429,10 @@ int launch_sigma_fused(const Problem& p, const double* x, cudaStream_t s) {
     if (p.n_mom != fused::NM || p.n_freq % 128 != 0 || p.fp != p.n_freq) return -1;
     if (p.n_angles > fused::MAX_ANGLES || p.n_space > (1 << 30)) return -1;
     if (reinterpret_cast<uintptr_t>(x) % 16 != 0) return -1;
-    if (getenv_flag("RTK_SIGMA_UNFUSED")) return -1;
-    // 128-column CTAs (clusters of N_nu / 128).  The 256-column shape (clusters of N_nu / 256,
-    // which tile all 148 SMs) measured slower on cfg2 (166 vs 146 us: twice the K steps per
-    // block, each with a cluster hand-off), so it is opt-in (RTK_SIGMA_BN256=1).
-    if (p.n_freq % 256 == 0 && getenv_flag("RTK_SIGMA_BN256")) {
-        switch (p.n_freq / 256) {
-            case 1: return fused::launch_t<1, 4, 4>(p, x, s);
-            case 2: return fused::launch_t<2, 4, 4>(p, x, s);
-            default: break;
-        }
-    }
+    if (p.tune.sigma_unfused) return -1;
+    // 128-column CTAs (clusters of N_nu / 128).  A 256-column shape (clusters of N_nu / 256,
+    // tiling all 148 SMs) measured slower on cfg2 (166 vs 146 us: twice the K steps per
+    // block, each with a cluster hand-off) and was removed.
     switch (p.n_freq / 128) {
         case 1: return fused::launch_t<1, 8, 2>(p, x, s);
         case 2: return fused::launch_t<2, 8, 2>(p, x, s);

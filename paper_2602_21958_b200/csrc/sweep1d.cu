@@ -153,11 +153,7 @@ int launch_t(const SweepArgs& A, cudaStream_t s) {
     constexpr int NS = Slots<SRC, NM>::kCount;
     const size_t smem = static_cast<size_t>(D) * NS * kThreads * sizeof(double);
     auto kern = sweep1d_kernel<FS, NM, SRC, OUT, D>;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        configured = true;
-    }
+    if (int rc = ensure_smem_for(kern, smem)) return rc;
     const unsigned blocks = static_cast<unsigned>((A.n_rays + kThreads - 1) / kThreads);
     kern<<<blocks, kThreads, smem, s>>>(A);
     RTK_LAUNCH_CHECK("sweep1d_kernel");

@@ -208,13 +208,7 @@ int launch_mom_t(const Problem& p, cudaStream_t s) {
     A.fp = p.fp;
     const size_t smem = 128 + 2 * MLayout<NM>::kRed * 8 + kMS * MLayout<NM>::kStage;
     auto kern = sweep1d_mom_kernel<FS, NM>;
-    static size_t configured = 0;
-    if (configured < smem) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
-            cudaSuccess)
-            return set_error(RTK_ERESOURCE, "moment sweep shared memory");
-        configured = smem;
-    }
+    if (int rc = ensure_smem_for(kern, smem)) return rc;
     kern<<<p.mom_n_ctas, kMThreads, smem, s>>>(p.mom_gmap, p.tma_dtmap_mom, A);
     RTK_LAUNCH_CHECK("sweep1d_mom_kernel");
     return RTK_OK;

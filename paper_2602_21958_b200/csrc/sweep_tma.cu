@@ -336,407 +336,11 @@ __global__ void __launch_bounds__(kTmaThreads) sweep1d_tma_kernel(const __grid_c
     }
 }
 
-// ---------------------------------------------------------------------------
-// Weight-warp variants (RTK_TMA_W_OLD=1; the default for the exponential solvers is
-// sweep1d_tma_kernel with branch-free weights, see consume()).  8 extra "weight" warps
-// compute the two-branch weights for the whole stage (U steps x 128 rays) into shared
-// memory while the 4 chain warps run the recursion on the previous stage.  Measured at
-// cfg2 (profiles/r01_ncu_sweep_exp.txt): exp-linear 342 us, exp-parabolic 529 us, bound
-// by the L1/shared-memory traffic of the weight hand-off (96 B per element, twice the
-// single-pass kernel's) and by weight warps of unequal cost (the exp branch) gating the
-// chain; the single-pass kernel with branch-free weights takes 267 / 349 us.
-constexpr int kElWeightWarps = 8;
-constexpr int kElThreads = kTmaThreads + 32 * kElWeightWarps;
-
-template <int NM, int U>
-struct ElLayout {
-    static constexpr int kW = U * 3 * kRaysPerCta * 8;   // [u][att, wu, wc][ray]
-    __host__ __device__ static int stage_bytes(int gw) { return Layout<NM, U>::stage_bytes(gw) + kW; }
-};
-
-template <int NM, int U, int S>
-__global__ void __launch_bounds__(kElThreads, 2) sweep1d_tma_el_kernel(const __grid_constant__ CUtensorMap xmap,
-                                                                       const __grid_constant__ CUtensorMap gmap,
-                                                                       const __grid_constant__ CUtensorMap dtmap,
-                                                                       TmaArgs A) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-    uint64_t* empty = full + S;
-    uint64_t* wready = empty + S;
-    double* phis = reinterpret_cast<double*>(smem + 256);          // [kRaysPerCta]
-    double* imus = phis + kRaysPerCta;
-    unsigned char* stages = smem + 256 + 2 * kRaysPerCta * 8;
-    const int gbytes = Layout<NM, U>::g_bytes(A.gw);
-    const int tma_bytes = Layout<NM, U>::stage_bytes(A.gw);
-    const int sbytes = ElLayout<NM, U>::stage_bytes(A.gw);
-
-    const TmaCta cta = A.ctas[blockIdx.x];
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31;
-    const int64_t n = A.n_space;
-    const int Q = static_cast<int>((n + U - 1) / U);
-    const bool down = cta.down != 0;
-
-    if (tid == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumerWarps);
-            mbar_init(&wready[s], kElWeightWarps);
-        }
-        fence_mbar_init();
-    }
-    if (tid < kRaysPerCta) {
-        const bool v = tid < cta.nr;
-        const int64_t ray = cta.ray0 + tid;
-        const int a = v ? static_cast<int>(ray / A.n_freq) : 0;
-        const int f = v ? static_cast<int>(ray - static_cast<int64_t>(a) * A.n_freq) : 0;
-        phis[tid] = A.phi[f];
-        imus[tid] = A.inv_mu[a];
-    }
-    __syncthreads();
-
-    if (warp == kConsumerWarps) {
-        // ---------------- producer warp (as in sweep1d_tma_kernel) ----------------
-        if (lane == 0) {
-            prefetch_tensormap(&xmap);
-            prefetch_tensormap(&gmap);
-            prefetch_tensormap(&dtmap);
-            const uint32_t tx = static_cast<uint32_t>(U * kXW * 8 + U * NM * A.gw * 8 + Layout<NM, U>::kDtW * 8);
-            for (int q = 0; q < Q; ++q) {
-                const int s = q % S;
-                if (q >= S) mbar_wait(&empty[s], ((q / S) - 1) & 1);
-                unsigned char* st = stages + s * sbytes;
-                const int r0 = down ? q * U : static_cast<int>(n) - U - q * U;
-                mbar_arrive_expect_tx(&full[s], tx);
-                tma_load_2d(st, &xmap, cta.ray0 & ~1, r0, &full[s]);
-                tma_load_2d(st + Layout<NM, U>::kX, &gmap, cta.f0, r0 * NM, &full[s]);
-                const int want = (down ? r0 - 1 : r0) + kDtPad;
-                tma_load_1d(st + Layout<NM, U>::kX + gbytes, &dtmap, want & ~1, &full[s]);
-            }
-        }
-        return;
-    }
-    if (warp > kConsumerWarps) {
-        // ---------------- weight warps: (att, wu, wc) for the stage's U x 128 (row, ray) pairs ----------------
-        const int wt = tid - kTmaThreads;   // 0 .. 32 * kElWeightWarps - 1
-        for (int q = 0; q < Q; ++q) {
-            const int s = q % S;
-            mbar_wait(&full[s], (q / S) & 1);
-            unsigned char* stg = stages + s * sbytes;
-            const double* dts = reinterpret_cast<const double*>(stg + Layout<NM, U>::kX + gbytes);
-            const int r0 = down ? q * U : static_cast<int>(n) - U - q * U;
-            const int dt_off = ((down ? r0 - 1 : r0) + kDtPad) & 1;
-            double* W = reinterpret_cast<double*>(stg + tma_bytes);
-#pragma unroll
-            for (int e = wt; e < U * kRaysPerCta; e += 32 * kElWeightWarps) {
-                const int u = e / kRaysPerCta, r = e - u * kRaysPerCta;
-                const ExpLin w = exp_linear_weights_fast(phis[r] * dts[dt_off + u] * imus[r]);
-                W[(u * 3 + 0) * kRaysPerCta + r] = w.att;
-                W[(u * 3 + 1) * kRaysPerCta + r] = w.wu;
-                W[(u * 3 + 2) * kRaysPerCta + r] = w.wc;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&wready[s]);
-        }
-        return;
-    }
-
-    // ---------------- chain warps: one ray per thread ----------------
-    const bool valid = tid < cta.nr;
-    const int64_t ray = cta.ray0 + tid;
-    const int a = valid ? static_cast<int>(ray / A.n_freq) : 0;
-    const int f = valid ? static_cast<int>(ray - static_cast<int64_t>(a) * A.n_freq) : 0;
-    const int gcol = f - cta.f0;
-    const int xoff = tid + (cta.ray0 & 1);
-    double yk[NM];
-#pragma unroll
-    for (int k = 0; k < NM; ++k) yk[k] = A.yb[k * A.n_angles + a];
-    double acc = 0.0, s_prev = 0.0;
-    double* yp = A.y + (down ? 0 : (n - 1) * A.n_rays) + ray;
-    const int64_t step = down ? A.n_rays : -A.n_rays;
-    for (int q = 0; q < Q; ++q) {
-        const int s = q % S;
-        mbar_wait(&full[s], (q / S) & 1);
-        mbar_wait(&wready[s], (q / S) & 1);
-        const unsigned char* stg = stages + s * sbytes;
-        const double* xs = reinterpret_cast<const double*>(stg);
-        const double* gcolp = reinterpret_cast<const double*>(stg + Layout<NM, U>::kX) + gcol;
-        const double* W = reinterpret_cast<const double*>(stg + tma_bytes);
-#pragma unroll
-        for (int uu = 0; uu < U; ++uu) {
-            const int j = q * U + uu;
-            if (j >= n) break;
-            const int u = down ? uu : U - 1 - uu;
-            const double xv = xs[u * kXW + xoff];
-            double sv = 0.0;
-#pragma unroll
-            for (int k = 0; k < NM; ++k) sv = fma(yk[k], gcolp[(u * NM + k) * A.gw], sv);
-            if (j > 0)
-                acc = fma(acc, W[(u * 3) * kRaysPerCta + tid],
-                          W[(u * 3 + 1) * kRaysPerCta + tid] * s_prev + W[(u * 3 + 2) * kRaysPerCta + tid] * sv);
-            s_prev = sv;
-            if (valid) *yp = xv - acc;
-            yp += step;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-    }
-}
-
-// Exp-parabolic variant of the weight-warp sweep.  The Kunasz-Auer weights of the update
-// at node j use the optical depths of the segments into j-1 and into j; the dt box starts
-// one segment earlier than in the other kernels for the downward march so both lie in the
-// stage.  The chain keeps the one-node delay (node j finalises j-1) and the closing
-// linear step of consume_par.
-template <int NM, int U>
-struct EpLayout {
-    static constexpr int kW = U * 4 * kRaysPerCta * 8;   // [u][att, wu, wc, wd][ray]
-    __host__ __device__ static int stage_bytes(int gw) { return Layout<NM, U>::stage_bytes(gw) + kW; }
-};
-
-template <int NM, int U, int S>
-__global__ void __launch_bounds__(kElThreads, 2) sweep1d_tma_ep_kernel(const __grid_constant__ CUtensorMap xmap,
-                                                                       const __grid_constant__ CUtensorMap gmap,
-                                                                       const __grid_constant__ CUtensorMap dtmap,
-                                                                       TmaArgs A) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-    uint64_t* empty = full + S;
-    uint64_t* wready = empty + S;
-    double* phis = reinterpret_cast<double*>(smem + 256);
-    double* imus = phis + kRaysPerCta;
-    unsigned char* stages = smem + 256 + 2 * kRaysPerCta * 8;
-    const int gbytes = Layout<NM, U>::g_bytes(A.gw);
-    const int tma_bytes = Layout<NM, U>::stage_bytes(A.gw);
-    const int sbytes = EpLayout<NM, U>::stage_bytes(A.gw);
-
-    const TmaCta cta = A.ctas[blockIdx.x];
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31;
-    const int64_t n = A.n_space;
-    const int Q = static_cast<int>((n + U - 1) / U);
-    const bool down = cta.down != 0;
-    // dt box start (dt index) of stage q, and the dt index of the segment INTO box row u
-    auto box_start = [&](int r0) { return (((down ? r0 - 2 : r0) + kDtPad) & ~1) - kDtPad; };
-
-    if (tid == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumerWarps);
-            mbar_init(&wready[s], kElWeightWarps);
-        }
-        fence_mbar_init();
-    }
-    if (tid < kRaysPerCta) {
-        const bool v = tid < cta.nr;
-        const int64_t ray = cta.ray0 + tid;
-        const int a = v ? static_cast<int>(ray / A.n_freq) : 0;
-        const int f = v ? static_cast<int>(ray - static_cast<int64_t>(a) * A.n_freq) : 0;
-        phis[tid] = A.phi[f];
-        imus[tid] = A.inv_mu[a];
-    }
-    __syncthreads();
-
-    if (warp == kConsumerWarps) {
-        if (lane == 0) {
-            prefetch_tensormap(&xmap);
-            prefetch_tensormap(&gmap);
-            prefetch_tensormap(&dtmap);
-            const uint32_t tx = static_cast<uint32_t>(U * kXW * 8 + U * NM * A.gw * 8 + Layout<NM, U>::kDtW * 8);
-            for (int q = 0; q < Q; ++q) {
-                const int s = q % S;
-                if (q >= S) mbar_wait(&empty[s], ((q / S) - 1) & 1);
-                unsigned char* st = stages + s * sbytes;
-                const int r0 = down ? q * U : static_cast<int>(n) - U - q * U;
-                mbar_arrive_expect_tx(&full[s], tx);
-                tma_load_2d(st, &xmap, cta.ray0 & ~1, r0, &full[s]);
-                tma_load_2d(st + Layout<NM, U>::kX, &gmap, cta.f0, r0 * NM, &full[s]);
-                tma_load_1d(st + Layout<NM, U>::kX + gbytes, &dtmap, box_start(r0) + kDtPad, &full[s]);
-            }
-        }
-        return;
-    }
-    if (warp > kConsumerWarps) {
-        // ---------------- weight warps: Kunasz-Auer weights of the update at each (row, ray) ----------------
-        const int wt = tid - kTmaThreads;
-        for (int q = 0; q < Q; ++q) {
-            const int s = q % S;
-            mbar_wait(&full[s], (q / S) & 1);
-            unsigned char* stg = stages + s * sbytes;
-            const double* dts = reinterpret_cast<const double*>(stg + Layout<NM, U>::kX + gbytes);
-            const int r0 = down ? q * U : static_cast<int>(n) - U - q * U;
-            const int b = box_start(r0);
-            double* W = reinterpret_cast<double*>(stg + tma_bytes);
-#pragma unroll
-            for (int e = wt; e < U * kRaysPerCta; e += 32 * kElWeightWarps) {
-                const int u = e / kRaysPerCta, r = e - u * kRaysPerCta;
-                const int row = r0 + u;
-                // segments into this node and into the previous node of the march
-                const int i_in = down ? row - 1 : row, i_prev = down ? row - 2 : row + 1;
-                const int k_in = min(max(i_in - b, 0), U + 1), k_prev = min(max(i_prev - b, 0), U + 1);
-                const ExpPar w =
-                    exp_parabolic_weights_fast(phis[r] * dts[k_prev] * imus[r], phis[r] * dts[k_in] * imus[r]);
-                W[(u * 4 + 0) * kRaysPerCta + r] = w.att;
-                W[(u * 4 + 1) * kRaysPerCta + r] = w.wu;
-                W[(u * 4 + 2) * kRaysPerCta + r] = w.wc;
-                W[(u * 4 + 3) * kRaysPerCta + r] = w.wd;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&wready[s]);
-        }
-        return;
-    }
-
-    // ---------------- chain warps ----------------
-    const bool valid = tid < cta.nr;
-    const int64_t ray = cta.ray0 + tid;
-    const int a = valid ? static_cast<int>(ray / A.n_freq) : 0;
-    const int f = valid ? static_cast<int>(ray - static_cast<int64_t>(a) * A.n_freq) : 0;
-    const int gcol = f - cta.f0;
-    const int xoff = tid + (cta.ray0 & 1);
-    const double phi_t = phis[tid], imu_t = imus[tid];
-    double yk[NM];
-#pragma unroll
-    for (int k = 0; k < NM; ++k) yk[k] = A.yb[k * A.n_angles + a];
-    double acc = 0.0, s_m2 = 0.0, s_m1 = 0.0, d_last = 0.0, x_m1 = 0.0;
-    double* yp = A.y + (down ? 0 : (n - 1) * A.n_rays) + ray;
-    const int64_t step = down ? A.n_rays : -A.n_rays;
-    for (int q = 0; q < Q; ++q) {
-        const int s = q % S;
-        mbar_wait(&full[s], (q / S) & 1);
-        mbar_wait(&wready[s], (q / S) & 1);
-        const unsigned char* stg = stages + s * sbytes;
-        const double* xs = reinterpret_cast<const double*>(stg);
-        const double* gcolp = reinterpret_cast<const double*>(stg + Layout<NM, U>::kX) + gcol;
-        const double* dts = reinterpret_cast<const double*>(stg + Layout<NM, U>::kX + gbytes);
-        const double* W = reinterpret_cast<const double*>(stg + tma_bytes);
-        const int r0 = down ? q * U : static_cast<int>(n) - U - q * U;
-        const int b = box_start(r0);
-#pragma unroll
-        for (int uu = 0; uu < U; ++uu) {
-            const int j = q * U + uu;
-            if (j >= n) break;
-            const int u = down ? uu : U - 1 - uu;
-            const double xv = xs[u * kXW + xoff];
-            double sv = 0.0;
-#pragma unroll
-            for (int k = 0; k < NM; ++k) sv = fma(yk[k], gcolp[(u * NM + k) * A.gw], sv);
-            if (j == 0) {
-                if (valid) *yp = xv - acc;
-                yp += step;
-                s_m1 = sv;
-                x_m1 = xv;
-                continue;
-            }
-            const int row = r0 + u;
-            d_last = phi_t * dts[(down ? row - 1 : row) - b] * imu_t;   // segment into node j (closing step)
-            if (j >= 2) {
-                acc = fma(acc, W[(u * 4) * kRaysPerCta + tid],
-                          W[(u * 4 + 1) * kRaysPerCta + tid] * s_m2 + W[(u * 4 + 2) * kRaysPerCta + tid] * s_m1 +
-                              W[(u * 4 + 3) * kRaysPerCta + tid] * sv);
-                if (valid) *yp = x_m1 - acc;
-                yp += step;
-            }
-            s_m2 = s_m1;
-            s_m1 = sv;
-            x_m1 = xv;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-    }
-    if (n >= 2) {   // last node: linear weights on the last segment
-        const ExpLin w = exp_linear_weights(d_last);
-        acc = fma(acc, w.att, w.wu * s_m2 + w.wc * s_m1);
-        if (valid) *yp = x_m1 - acc;
-    }
-}
-
-template <int NM, int U, int S>
-int launch_tma_ep(const Problem& p, const double* x, double* y, cudaStream_t s) {
-    CUtensorMap xmap;
-    const uint64_t xd[2] = {static_cast<uint64_t>(p.n_rays), static_cast<uint64_t>(p.n_space)};
-    const uint64_t xs[1] = {static_cast<uint64_t>(p.n_rays) * 8};
-    const uint32_t xb[2] = {kXW, U};
-    if (!encode_f64_map(&xmap, x, 2, xd, xs, xb)) return -1;
-    TmaArgs A;
-    A.ctas = p.tma_ctas;
-    A.phi = p.phi;
-    A.inv_mu = p.inv_mu;
-    A.yb = p.yb;
-    A.y = y;
-    A.n_space = p.n_space;
-    A.n_rays = p.n_rays;
-    A.n_angles = p.n_angles;
-    A.n_freq = p.n_freq;
-    A.gw = p.tma_gw;
-    const size_t smem = 256 + 2 * kRaysPerCta * 8 + static_cast<size_t>(S) * EpLayout<NM, U>::stage_bytes(p.tma_gw);
-    auto kern = sweep1d_tma_ep_kernel<NM, U, S>;
-    static size_t configured = 0;
-    if (configured < smem) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
-            cudaSuccess) {
-            cudaGetLastError();
-            return -1;
-        }
-        configured = smem;
-    }
-    kern<<<p.tma_n_ctas, kElThreads, smem, s>>>(xmap, U == 4 ? p.tma_gmap4 : p.tma_gmap,
-                                                U == 4 ? p.tma_dtmap4 : p.tma_dtmap, A);
-    RTK_LAUNCH_CHECK("sweep1d_tma_ep_kernel");
-    return RTK_OK;
-}
-
-template <int NM, int U, int S>
-int launch_tma_el(const Problem& p, const double* x, double* y, cudaStream_t s) {
-    CUtensorMap xmap;
-    const uint64_t xd[2] = {static_cast<uint64_t>(p.n_rays), static_cast<uint64_t>(p.n_space)};
-    const uint64_t xs[1] = {static_cast<uint64_t>(p.n_rays) * 8};
-    const uint32_t xb[2] = {kXW, U};
-    if (!encode_f64_map(&xmap, x, 2, xd, xs, xb)) return -1;
-    TmaArgs A;
-    A.ctas = p.tma_ctas;
-    A.phi = p.phi;
-    A.inv_mu = p.inv_mu;
-    A.yb = p.yb;
-    A.y = y;
-    A.n_space = p.n_space;
-    A.n_rays = p.n_rays;
-    A.n_angles = p.n_angles;
-    A.n_freq = p.n_freq;
-    A.gw = p.tma_gw;
-    const size_t smem = 256 + 2 * kRaysPerCta * 8 + static_cast<size_t>(S) * ElLayout<NM, U>::stage_bytes(p.tma_gw);
-    auto kern = sweep1d_tma_el_kernel<NM, U, S>;
-    static size_t configured = 0;
-    if (configured < smem) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
-            cudaSuccess) {
-            cudaGetLastError();
-            return -1;
-        }
-        configured = smem;
-    }
-    kern<<<p.tma_n_ctas, kElThreads, smem, s>>>(xmap, U == 4 ? p.tma_gmap4 : p.tma_gmap,
-                                                U == 4 ? p.tma_dtmap4 : p.tma_dtmap, A);
-    RTK_LAUNCH_CHECK("sweep1d_tma_el_kernel");
-    return RTK_OK;
-}
-
 template <int FS, int NM, int U, int S>
 int launch_tma_us(const Problem& p, const double* x, double* y, cudaStream_t s);
 
 template <int FS, int NM>
 int launch_tma_t(const Problem& p, const double* x, double* y, cudaStream_t s) {
-    if (FS != RTK_FS_IE && p.tma_u == 8 && !getenv_flag("RTK_TMA_W_OLD")) return launch_tma_us<FS, NM, 8, 4>(p, x, y, s);
-    if (FS == RTK_FS_EXP_PARABOLIC && p.tma_u == 8 && !getenv_flag("RTK_TMA_EL_SINGLE")) {
-        const int rc = launch_tma_ep<NM, 4, 3>(p, x, y, s);
-        if (rc != -1) return rc;
-    }
-    if (FS == RTK_FS_EXP_LINEAR && p.tma_u == 8 && !getenv_flag("RTK_TMA_EL_SINGLE")) {
-        // the G tensor map's box height is tma_u * n_mom rows: the weight-warp kernel uses the same U
-        const int rc = getenv_flag("RTK_TMA_EL_U8") ? launch_tma_el<NM, 8, 2>(p, x, y, s)
-                                                    : launch_tma_el<NM, 4, 4>(p, x, y, s);
-        if (rc != -1) return rc;
-    }
     if (p.tma_u == 8) return launch_tma_us<FS, NM, 8, 4>(p, x, y, s);
     return launch_tma_us<FS, NM, 4, (NM <= 2) ? 8 : 4>(p, x, y, s);
 }
@@ -747,7 +351,7 @@ int launch_tma_us(const Problem& p, const double* x, double* y, cudaStream_t s) 
     const uint64_t xd[2] = {static_cast<uint64_t>(p.n_rays), static_cast<uint64_t>(p.n_space)};
     const uint64_t xs[1] = {static_cast<uint64_t>(p.n_rays) * 8};
     const uint32_t xb[2] = {kXW, U};
-    if (!encode_f64_map(&xmap, x, 2, xd, xs, xb)) return -1;
+    if (!encode_f64_map(&xmap, x, 2, xd, xs, xb)) return set_error(RTK_ECUDA, "sweep: x tensor-map encoding failed");
     TmaArgs A;
     A.ctas = p.tma_ctas;
     A.phi = p.phi;
@@ -761,29 +365,18 @@ int launch_tma_us(const Problem& p, const double* x, double* y, cudaStream_t s) 
     A.gw = p.tma_gw;
     const size_t smem = 128 + static_cast<size_t>(S) * Layout<NM, U>::stage_bytes(p.tma_gw);
     auto kern = sweep1d_tma_kernel<FS, NM, U, S>;
-    static size_t configured = 0;
-    if (configured < smem) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
-            cudaSuccess) {
-            cudaGetLastError();
-            return -1;
-        }
-        configured = smem;
-    }
+    if (int rc = ensure_smem_for(kern, smem)) return rc;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = getenv_flag("RTK_NO_PDL") ? 0 : 1;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.gridDim = dim3(p.tma_n_ctas);
     cfg.blockDim = dim3(kTmaThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, kern, xmap, p.tma_gmap, p.tma_dtmap, A) != cudaSuccess) {
-        cudaGetLastError();
-        return -1;
-    }
+    RTK_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, xmap, p.tma_gmap, p.tma_dtmap, A));
     RTK_LAUNCH_CHECK("sweep1d_tma_kernel");
     return RTK_OK;
 }
@@ -801,9 +394,11 @@ int dispatch_tma(const Problem& p, const double* x, double* y, cudaStream_t s) {
 
 }  // namespace
 
-// returns RTK_OK, an error code, or -1 when the TMA path does not apply (caller falls back)
+// returns RTK_OK, an error code, or -1 when the TMA path does not apply to this problem's
+// shape (fixed at setup) or to an x that is not 16-byte aligned (TMA global addresses must be)
 int launch_sweep_tma(const Problem& p, const double* x, double* y, cudaStream_t s) {
     if (!p.tma_ready || p.gamma_per_ray) return -1;
+    if (reinterpret_cast<uintptr_t>(x) % 16 != 0) return -1;
     if (p.fs == RTK_FS_IE) return dispatch_tma<RTK_FS_IE>(p, x, y, s);
     if (p.fs == RTK_FS_EXP_LINEAR) return dispatch_tma<RTK_FS_EXP_LINEAR>(p, x, y, s);
     if (p.fs == RTK_FS_EXP_PARABOLIC) return dispatch_tma<RTK_FS_EXP_PARABOLIC>(p, x, y, s);
@@ -846,7 +441,7 @@ int setup_tma(Problem& p) {
     }
     const uint64_t gd[2] = {static_cast<uint64_t>(p.fp), static_cast<uint64_t>(p.n_space * p.n_mom)};
     const uint64_t gs[1] = {static_cast<uint64_t>(p.fp) * 8};
-    p.tma_u = (!getenv_flag("RTK_TMA_U4") && p.n_mom <= 2) ? 8 : 4;   // march steps per pipeline stage (U = 8: 96% of HBM on cfg2)
+    p.tma_u = p.n_mom <= 2 ? 8 : 4;   // march steps per pipeline stage (U = 8: 96% of HBM on cfg2)
     const uint32_t gb[2] = {static_cast<uint32_t>(p.tma_gw), static_cast<uint32_t>(p.tma_u * p.n_mom)};
     // front/back zero-padded copy of dt so every dt box starts at an even, non-negative coordinate
     std::vector<double> hdt(static_cast<size_t>(p.n_space - 1 + 2 * kDtPad), 0.0);
@@ -855,14 +450,8 @@ int setup_tma(Problem& p) {
     RTK_CUDA_TRY(cudaMemcpy(p.dtpad, hdt.data(), sizeof(double) * hdt.size(), cudaMemcpyHostToDevice));
     const uint64_t dd[1] = {static_cast<uint64_t>(hdt.size())};
     const uint32_t db[1] = {static_cast<uint32_t>(p.tma_u + 2)};
-    if (!encode_f64_map(&p.tma_gmap, p.gmom, 2, gd, gs, gb)) return RTK_OK;
-    if (!encode_f64_map(&p.tma_dtmap, p.dtpad, 1, dd, nullptr, db)) return RTK_OK;
-    {
-        const uint32_t gb4[2] = {static_cast<uint32_t>(p.tma_gw), static_cast<uint32_t>(4 * p.n_mom)};
-        const uint32_t db4[1] = {6};
-        if (!encode_f64_map(&p.tma_gmap4, p.gmom, 2, gd, gs, gb4)) return RTK_OK;
-        if (!encode_f64_map(&p.tma_dtmap4, p.dtpad, 1, dd, nullptr, db4)) return RTK_OK;
-    }
+    if (!encode_f64_map(&p.tma_gmap, p.gmom, 2, gd, gs, gb)) return set_error(RTK_ECUDA, "sweep: G tensor map");
+    if (!encode_f64_map(&p.tma_dtmap, p.dtpad, 1, dd, nullptr, db)) return set_error(RTK_ECUDA, "sweep: dt tensor map");
     RTK_CUDA_TRY(cudaMalloc(&p.tma_ctas, sizeof(TmaCta) * ctas.size()));
     RTK_CUDA_TRY(cudaMemcpy(p.tma_ctas, ctas.data(), sizeof(TmaCta) * ctas.size(), cudaMemcpyHostToDevice));
     p.tma_n_ctas = static_cast<int>(ctas.size());

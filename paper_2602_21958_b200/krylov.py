@@ -2,8 +2,11 @@
 
 `gmres(apply, b, cfg)` keeps the reference signature.  When `apply` is an
 RTProblem (or `operator(problem)`), the whole solve runs natively: matvec,
-CGS2 Arnoldi, Givens and restarts in librtk_b200 with the Krylov basis in
-HBM; only one Hessenberg column per iteration crosses to the host.  Any
+Arnoldi, Givens and restarts in librtk_b200 with the Krylov basis in HBM;
+only one Hessenberg column per iteration crosses to the host.  Arnoldi is the
+reference's modified Gram-Schmidt (one sweep, or two with
+``reorthogonalize=True``) unless ``orthogonalization="cgs2"`` selects the
+fused three-pass classical Gram-Schmidt with reorthogonalisation.  Any
 other callable is called back per matvec with vectors of the same kind as
 `b` (numpy arrays for numpy b, CUDA tensors for CUDA-tensor b) while the
 Krylov vectors still live on the device.
@@ -19,6 +22,8 @@ import numpy as np
 
 from paper_2602_21958_b200 import _device, _native
 
+_ORTH_CODES = {None: 0, "mgs": 1, "mgs2": 2, "cgs2": 3}
+
 
 @dataclass
 class SolveConfig:
@@ -26,9 +31,15 @@ class SolveConfig:
     rel_tol: float = 1e-12
     max_iter: int = 1000
     restart: Optional[int] = None
-    reorthogonalize: bool = False   # Arnoldi is always CGS2 on the device
+    reorthogonalize: bool = False   # second Gram-Schmidt sweep (R/krylov.py:101-105)
+    # Arnoldi on the device: None = the reference's choice (MGS, or MGS2 with reorthogonalize);
+    # "mgs" / "mgs2" explicitly; "cgs2" = classical Gram-Schmidt + reorthogonalisation in three
+    # fused streaming passes over the basis (fewest HBM bytes and launches; not in the reference)
+    orthogonalization: Optional[str] = None
 
     def __post_init__(self):
+        if self.orthogonalization not in _ORTH_CODES:
+            raise ValueError(f"unknown orthogonalization {self.orthogonalization!r}")
         if self.rel_tol <= 0:
             raise ValueError("rel_tol must be positive")
         if self.max_iter < 1:
@@ -67,7 +78,8 @@ def _solve(method: str, apply, b, cfg: SolveConfig) -> SolveReport:
     n = int(b.numel()) if _device.is_tensor(b) else int(np.asarray(b).size)
     bd, kind = _device.to_device(b, n)
     x = _device.empty(n)
-    c = _native.SolveCfg(float(cfg.rel_tol), int(cfg.max_iter), int(cfg.restart or 0), int(cfg.reorthogonalize), 0)
+    c = _native.SolveCfg(float(cfg.rel_tol), int(cfg.max_iter), int(cfg.restart or 0), int(cfg.reorthogonalize),
+                         _ORTH_CODES[cfg.orthogonalization])
     rep = _native.SolveRep()
     cap = int(cfg.max_iter) + 2
     hist = np.zeros(cap)

@@ -172,6 +172,10 @@ class _LatticeHandle:
     def set_inflow(self, inflow):  # pragma: no cover - lattice inflow is fixed at creation
         raise ValueError("lattice inflow is fixed at creation")
 
+    def set_tuning(self, key: str, value: int):
+        """Select a kernel variant of this handle (rtk_problem_set_tuning)."""
+        _native.check(self._lib.rtk_problem_set_tuning(self.h, key.encode(), int(value)))
+
     def __del__(self):
         h = getattr(self, "h", None)
         if h is not None and h.value:

@@ -3,6 +3,7 @@ import numpy as np
 import pytest
 
 import paper_2602_21958_b200 as P
+from paper_2602_21958_b200 import configs
 from paper_2602_21958_b200 import lattice as L
 from oracle import lattice as OL
 from oracle import rt_oracle as ro
@@ -112,9 +113,7 @@ def test_lattice_rejects_bad_arguments():
 def test_full_size_lattice_matvec_matches_oracle(cfg):
     """BASELINE cfg3 (256 x 256 slab, 128 dirs, 41 nu, intensity layout) and cfg4 (64^3, 128 dirs,
     31 nu, moment layout) at full size: one matvec against the numpy oracle (1 - 3 min on the CPU)."""
-    from tools.time_lattice import CFGS
-
-    p = L.lattice_problem(seed=21958 + cfg, **CFGS[cfg])
+    p = configs.lattice_config_problem(cfg)
     d = OL.desc_from_lattice_problem(p)
     v = np.random.default_rng(cfg).standard_normal(p.n_total)
     assert rel_l2(P.apply_A(p, v), OL.apply_A(d, p.layout, v)) <= MATVEC_TOL
@@ -165,9 +164,8 @@ def test_cfg5_full_size_linearity_and_direction_shards():
     import torch
 
     from paper_2602_21958_b200.sharding import LatticeShardedOperator
-    from tools.time_lattice import CFGS
 
-    p = L.lattice_problem(seed=21963, **CFGS[5])
+    p = configs.lattice_config_problem(5)
     gen = torch.Generator(device="cuda").manual_seed(5)
     u = torch.randn(p.n_total, dtype=torch.float64, device="cuda", generator=gen)
     w = torch.randn(p.n_total, dtype=torch.float64, device="cuda", generator=gen)
@@ -180,3 +178,128 @@ def test_cfg5_full_size_linearity_and_direction_shards():
     m += ops[1].ops.partial_moments(u)
     y = ops[0].ops.apply_with_moments(u, m)
     assert float(torch.linalg.vector_norm(y - au) / torch.linalg.vector_norm(au)) <= 1e-12
+
+
+# Every shipped kernel variant against the oracle (rtk_problem_set_tuning selects it):
+# moment layout -- lattice_mom_group_kernel with DG = 1 (cfg5's instantiation: 128-thread blocks,
+# one direction group), 4 and 8 direction groups; intensity layout -- the shared-memory kernel
+# (3D and planar sampling, with and without the dt table) and the non-shared-memory fallback
+# lattice_int_kernel (long characteristics, IE / exp-linear).
+MOMENT_VARIANTS = [{"lattice_dg": 1}, {"lattice_dg": 4}, {"lattice_dg": 8}]
+INTENSITY_VARIANTS = [{"lattice_no_smem": 1}, {"lattice_no_dtab": 1}, {"lattice_no_planar": 1},
+                      {"lattice_no_dtab": 1, "lattice_no_planar": 1}]
+
+
+def _with_tuning(p, tuning):
+    h = p.device()
+    for k, v in tuning.items():
+        h.set_tuning(k, v)
+    return p
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("tuning", MOMENT_VARIANTS, ids=lambda t: ",".join(f"{k}={v}" for k, v in t.items()))
+@pytest.mark.parametrize("chars", ["long", "hybrid"])
+@pytest.mark.parametrize("fs", ["ie", "exp_linear", "exp_parabolic"])
+def test_moment_kernel_variants_match_oracle(case, tuning, chars, fs):
+    nx, ny, nz, npol, naz, nf = case
+    p = L.lattice_problem(nx, ny, nz, npol, naz, nf, corr_len=2.0, seed=17, layout="moments", formal_solver=fs,
+                          characteristics=chars)
+    _with_tuning(p, tuning)
+    d = OL.desc_from_lattice_problem(p)
+    v = np.random.default_rng(nx * 7 + nf).standard_normal(p.n_total)
+    assert rel_l2(P.apply_A(p, v), OL.apply_A(d, "moments", v)) <= MATVEC_TOL
+    assert rel_l2(P.build_rhs(p), OL.build_rhs(d, "moments")) <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("tuning", INTENSITY_VARIANTS, ids=lambda t: ",".join(f"{k}={v}" for k, v in t.items()))
+@pytest.mark.parametrize("fs", ["ie", "exp_linear"])
+def test_intensity_kernel_variants_match_oracle(case, tuning, fs):
+    nx, ny, nz, npol, naz, nf = case
+    p = L.lattice_problem(nx, ny, nz, npol, naz, nf, corr_len=2.0, seed=19, layout="intensity", formal_solver=fs)
+    _with_tuning(p, tuning)
+    d = OL.desc_from_lattice_problem(p)
+    v = np.random.default_rng(nx * 5 + nf).standard_normal(p.n_total)
+    assert rel_l2(P.apply_A(p, v), OL.apply_A(d, "intensity", v)) <= MATVEC_TOL
+    assert rel_l2(P.build_rhs(p), OL.build_rhs(d, "intensity")) <= MATVEC_TOL
+
+
+def test_fallback_intensity_kernel_rejects_what_it_cannot_do():
+    """Without the shared-memory kernel, exp-parabolic and short characteristics in the
+    intensity layout are refused (RTK_ERESOURCE -> ResourceLimitError), never approximated."""
+    from paper_2602_21958_b200.errors import ResourceLimitError
+
+    for kw in (dict(formal_solver="exp_parabolic"), dict(characteristics="short")):
+        p = L.lattice_problem(8, 1, 6, 4, 4, 3, corr_len=1.0, layout="intensity", **kw)
+        _with_tuning(p, {"lattice_no_smem": 1})
+        with pytest.raises(ResourceLimitError):
+            P.apply_A(p, np.ones(p.n_total))
+
+
+def test_auto_selection_takes_one_direction_group_on_large_steps():
+    """A step with > 131,072 (line, frequency-pair) items selects DG = 1 by itself (cfg5's
+    path): 64 x 64 lines x 33 pairs; against the oracle with the default tuning."""
+    p = L.lattice_problem(64, 64, 4, 4, 2, 66, corr_len=4.0, seed=23, layout="moments")
+    d = OL.desc_from_lattice_problem(p)
+    v = np.random.default_rng(23).standard_normal(p.n_total)
+    assert rel_l2(P.apply_A(p, v), OL.apply_A(d, "moments", v)) <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("tuning", [{}, {"lattice_dg": 1}], ids=["auto", "dg1"])
+def test_cfg5_column_geometry_matches_oracle(tuning):
+    """BASELINE cfg5 construction at its full depth and angular set (nz = 128, 8 x 12 = 96
+    directions, corr 16, eps 1e-5, moment layout) on a 32 x 32 horizontal period with N_nu = 4
+    (the oracle takes ~1 min): default selection and cfg5's own kernel instantiation (one
+    direction group, lattice_mom_group_kernel<..., 1>)."""
+    p = configs.lattice_config_problem(5, nx=32, ny=32, n_freq=4)
+    _with_tuning(p, tuning)
+    d = OL.desc_from_lattice_problem(p)
+    v = np.random.default_rng(5).standard_normal(p.n_total)
+    assert rel_l2(P.apply_A(p, v), OL.apply_A(d, "moments", v)) <= MATVEC_TOL
+
+
+def test_cfg5_full_geometry_matches_oracle_fixture():
+    """BASELINE cfg5 geometry at FULL size (128^3, 96 directions; N_nu = 4, 805 M intensity DOF)
+    against the oracle output committed by tests/golden/make_cfg5_fixture.py (65,536 sampled
+    entries and 8 sketches of y = A u; the oracle itself needs ~15 CPU-minutes here).  This
+    step size (16,384 lines x 2 pairs) selects the multi-group kernel, so both DG = 1 (cfg5's
+    instantiation) and the default are checked."""
+    import os
+
+    import torch
+
+    sys_path = os.path.join(os.path.dirname(__file__), "golden")
+    z = np.load(os.path.join(sys_path, "cfg5_geometry_nu4.npz"))
+    from tests.golden import make_cfg5_fixture as F
+
+    p = configs.lattice_config_problem(5, n_freq=F.N_FREQ)
+    assert p.n_total == int(z["n_total"])
+    u = np.random.default_rng(F.U_SEED).standard_normal(p.n_total)
+    idx = torch.from_numpy(z["index"]).cuda()
+    for tuning in ({}, {"lattice_dg": 1}):
+        _with_tuning(p, tuning)
+        y = P.apply_A(p, torch.from_numpy(u).cuda())
+        ys = y[idx].cpu().numpy()
+        assert rel_l2(ys, z["values"]) <= MATVEC_TOL, tuning
+        yh = y.cpu().numpy()
+        assert abs(np.linalg.norm(yh) - float(z["norm"])) <= 1e-12 * float(z["norm"])
+        for r, ref in zip(F.sketch_vectors(p.n_total), z["sketches"]):
+            assert abs(r @ yh - ref) <= 1e-11 * float(z["norm"]) * np.sqrt(p.n_total)
+
+
+@pytest.mark.parametrize("ray", [0, 1])
+@pytest.mark.parametrize("tuning", [{}, {"lattice_no_smem": 1}], ids=["smem", "fallback"])
+def test_device_transfer_matches_reference_multidim(ray, tuning):
+    """The device lattice transfer against the reference's own 2D long characteristics
+    (R/multidim.py, tests/golden/make_multidim_golden.py), in the coinciding configuration:
+    build_rhs of a one-direction problem whose isotropic thermal source is the golden's
+    source for that ray gives Lambda S + the inflow term."""
+    from tests import _multidim_golden as MG
+
+    z = MG.load()
+    for S, lam in zip(z["source"], z["lambda"]):
+        p = MG.column_problem(z, directions=(ray,), thermal=S[..., ray].reshape(-1))
+        _with_tuning(p, tuning)
+        want = (lam[..., ray] + z["boundary"][..., ray]).reshape(-1)
+        assert rel_l2(P.build_rhs(p), want) <= 1e-13

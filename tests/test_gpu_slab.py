@@ -35,17 +35,42 @@ def test_rhs_matches_reference_goldens(key):
     np.testing.assert_allclose(P.build_rhs(p), z[f"{key}/rhs"], rtol=1e-12, atol=1e-15)
 
 
-@pytest.mark.parametrize("key", ["mono", "coherent", "crd", "log_legendre", "log_crd", "cfg1_legendre", "cfg1_crd"])
+GOLDEN_GMRES_KEYS = ["mono", "coherent", "crd", "log_legendre", "log_crd", "cfg1_legendre", "cfg1_crd"]
+
+
+@pytest.mark.parametrize("key", GOLDEN_GMRES_KEYS)
 def test_gmres_matches_reference_goldens(key):
+    """The reference's own Arnoldi (MGS, or MGS2 with reorthogonalize, the golden's setting):
+    iteration count within +-1 (north_star), restarted or not, history and solution."""
     p = product_from_golden(key)
     for case in G.gmres_cases(key):
-        cfg = P.SolveConfig(rel_tol=case["rel_tol"], max_iter=case["max_iter"], restart=case["restart"])
+        cfg = P.SolveConfig(rel_tol=case["rel_tol"], max_iter=case["max_iter"], restart=case["restart"],
+                            reorthogonalize=case["reorthogonalize"])
         rep = P.gmres(p, case["b"], cfg)
         assert rep.converged == case["converged"]
-        slack = 1 if case["restart"] is None else 15   # restarted counts: measured noise band
-        assert abs(rep.iterations - case["iterations"]) <= slack, (rep.iterations, case["iterations"])
+        assert abs(rep.iterations - case["iterations"]) <= 1, (case["name"], rep.iterations, case["iterations"])
         k = min(len(rep.residual_history), len(case["history"]), 100)
         np.testing.assert_allclose(rep.residual_history[:k], case["history"][:k], rtol=1e-8, atol=1e-13)
+        assert rel_l2(rep.solution, case["solution"]) <= 1e-7
+
+
+# Measured iteration-count band of the CGS2 Arnoldi against the reference's MGS goldens
+# (restarted cycles amplify last-bit differences in stagnating problems, SURVEY 0.4b):
+# unrestarted +-1; restarted within CGS2_RESTART_BAND (largest difference over these
+# goldens, measured on the B200 by this test's own harness; see DESIGN.md section 6).
+CGS2_RESTART_BAND = 3
+
+
+@pytest.mark.parametrize("key", GOLDEN_GMRES_KEYS)
+def test_cgs2_gmres_against_reference_goldens(key):
+    p = product_from_golden(key)
+    for case in G.gmres_cases(key):
+        cfg = P.SolveConfig(rel_tol=case["rel_tol"], max_iter=case["max_iter"], restart=case["restart"],
+                            orthogonalization="cgs2")
+        rep = P.gmres(p, case["b"], cfg)
+        assert rep.converged == case["converged"]
+        band = 1 if case["restart"] is None else CGS2_RESTART_BAND
+        assert abs(rep.iterations - case["iterations"]) <= band, (case["name"], rep.iterations, case["iterations"])
         assert rel_l2(rep.solution, case["solution"]) <= 1e-7
 
 
@@ -138,32 +163,40 @@ def test_bicgstab_matches_oracle_on_golden_crd():
 
 
 @pytest.mark.parametrize("fs", ["ie", "exp_linear"])
-def test_cp_async_fallback_sweep_matches_tma_sweep(fs, monkeypatch):
-    """The generic (non-TMA) sweep kernel and the TMA kernel agree to rounding."""
+def test_cp_async_fallback_sweep_matches_tma_sweep(fs):
+    """The generic (non-TMA) sweep kernel and the TMA kernel agree to rounding, and both
+    match the oracle."""
     p = configs.slab_problem(1, formal_solver=fs)
     v = np.random.default_rng(9).standard_normal(p.n_total)
     y_tma = P.apply_A(p, v)
-    monkeypatch.setenv("RTK_DISABLE_TMA", "1")
+    p.device().set_tuning("disable_tma", 1)
     y_gen = P.apply_A(p, v)
     assert rel_l2(y_gen, y_tma) <= 1e-14
+    assert rel_l2(y_gen, ro.apply_A(oracle_desc(p), v)) <= MATVEC_TOL
+
+
+def test_unaligned_vector_takes_the_cp_async_sweep():
+    """A device x that is not 16-byte aligned (TMA needs 16) is swept by the cp.async kernel
+    (decided per call, never a silent fallback after a failed launch)."""
+    import torch
+
+    p = configs.slab_problem(1, n_space=40, n_angles=8, n_freq=11)
+    v = np.random.default_rng(2).standard_normal(p.n_total)
+    buf = torch.empty(p.n_total + 1, dtype=torch.float64, device="cuda")
+    buf[1:] = torch.from_numpy(v).cuda()
+    y = P.apply_A(p, buf[1:])
+    assert rel_l2(y.cpu().numpy(), ro.apply_A(oracle_desc(p), v)) <= MATVEC_TOL
 
 
 @pytest.mark.parametrize("fs", ["exp_linear", "exp_parabolic"])
 @pytest.mark.parametrize("shape", [(2000, 64, 512), (37, 8, 256), (6, 4, 128)])
-def test_branch_free_weight_sweep_matches_weight_warp_sweep(fs, shape, monkeypatch):
-    """The default exponential sweep (branch-free weights inside the TMA sweep) and the
-    weight-warp kernels (RTK_TMA_W_OLD=1, two-branch weights) agree to a few ulp per
-    weight (the two-branch closed form loses up to ~40 ulp in w_c just above its 0.05
-    switch, so the bound is 1e-13), and the default path matches the oracle."""
+def test_exponential_sweeps_match_oracle(fs, shape):
+    """The exponential TMA sweeps (branch-free range-reduced weights) against the oracle's
+    three-branch weights, up to the cfg2 full size."""
     ns, na, nf = shape
     p = configs.slab_problem(2, formal_solver=fs, n_space=ns, n_angles=na, n_freq=nf)
     v = np.random.default_rng(ns + 1).standard_normal(p.n_total)
-    y_new = P.apply_A(p, v)
-    monkeypatch.setenv("RTK_TMA_W_OLD", "1")
-    y_old = P.apply_A(p, v)
-    assert rel_l2(y_new, y_old) <= 1e-13
-    if ns < 2000:
-        assert rel_l2(y_new, ro.apply_A(oracle_desc(p), v)) <= MATVEC_TOL
+    assert rel_l2(P.apply_A(p, v), ro.apply_A(oracle_desc(p), v)) <= MATVEC_TOL
 
 
 @pytest.mark.parametrize("shape", [(37, 6, 5), (64, 12, 130), (50, 4, 257), (9, 2, 1)])
@@ -188,25 +221,17 @@ def test_fused_sigma_shapes_match_oracle(shape):
     assert rel_l2(P.apply_A(p, v), ro.apply_A(d, v)) <= MATVEC_TOL
 
 
-@pytest.mark.parametrize("shape", [(101, 20, 256), (2000, 64, 512)])
-def test_fused_sigma_bn256_shape_matches_oracle(shape, monkeypatch):
-    """The opt-in 256-column cluster shape of the fused kernel (RTK_SIGMA_BN256=1)."""
-    monkeypatch.setenv("RTK_SIGMA_BN256", "1")
-    ns, na, nf = shape
-    p = configs.slab_problem(2, n_space=ns, n_angles=na, n_freq=nf)
-    d = oracle_desc(p)
-    v = np.random.default_rng(ns).standard_normal(p.n_total)
-    assert rel_l2(P.apply_A(p, v), ro.apply_A(d, v)) <= MATVEC_TOL
-
-
-def test_fused_sigma_equals_unfused_pair(monkeypatch):
-    """cfg2 full size: the fused kernel and the K2a + K2b pair agree to rounding."""
+def test_fused_sigma_equals_unfused_pair():
+    """cfg2 full size: the fused kernel and the K2a + K2b pair (and the 8-byte moment kernel)
+    agree to rounding."""
     p = configs.slab_problem(2)
     v = np.random.default_rng(5).standard_normal(p.n_total)
     y_fused = P.apply_A(p, v)
-    monkeypatch.setenv("RTK_SIGMA_UNFUSED", "1")
+    p.device().set_tuning("sigma_unfused", 1)
     y_pair = P.apply_A(p, v)
     assert rel_l2(y_fused, y_pair) <= 1e-14
+    p.device().set_tuning("moments_scalar", 1)
+    assert rel_l2(P.apply_A(p, v), y_pair) <= 1e-14
 
 
 @pytest.mark.parametrize("ns", [2, 3, 5, 9])

@@ -216,3 +216,19 @@ def test_exp_parabolic_differs_from_linear_only_through_curvature():
                                rtol=1e-12, atol=1e-14)
     S_rnd = np.random.default_rng(5).standard_normal((p.n_space, 2, p.n_freq))
     assert np.abs(OL.lattice_transfer(d_par, S_rnd) - OL.lattice_transfer(d_lin, S_rnd)).max() > 1e-6
+
+
+def test_lattice_oracle_matches_reference_multidim_long_characteristics():
+    """Pinned against the reference's own 2D long characteristics (R/multidim.py: trace_rays,
+    build_interpolators, build_transfer_2d, sweep_lines) on the configuration where both
+    discretisations coincide (tests/golden/make_multidim_golden.py): homogeneous transfer of
+    three seeded per-ray sources and the boundary term of constant inflows."""
+    from tests import _multidim_golden as MG
+
+    z = MG.load()
+    d = OL.desc_from_lattice_problem(MG.column_problem(z))
+    for S, ref in zip(z["source"], z["lambda"]):
+        out = OL.lattice_transfer(d, S.reshape(-1, 2, 1))
+        np.testing.assert_allclose(out.reshape(ref.shape), ref, rtol=1e-13, atol=1e-15)
+    bnd = OL.lattice_transfer(d, np.zeros((d.n_space, 2, 1)), with_boundary=True)
+    np.testing.assert_allclose(bnd.reshape(z["boundary"].shape), z["boundary"], rtol=1e-13, atol=1e-15)

@@ -7,7 +7,7 @@ import torch
 sys.path.insert(0, ".")
 import paper_2602_21958_b200 as P  # noqa: E402
 from paper_2602_21958_b200 import lattice as L  # noqa: E402
-from tools.time_lattice import CFGS  # noqa: E402
+from paper_2602_21958_b200.configs import LATTICE_CONFIGS as CFGS  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 its = int(sys.argv[2]) if len(sys.argv) > 2 else 400

@@ -5,7 +5,7 @@ import torch
 
 sys.path.insert(0, ".")
 import paper_2602_21958_b200 as P  # noqa: E402
-from tools.time_lattice import CFGS  # noqa: E402
+from paper_2602_21958_b200.configs import LATTICE_CONFIGS as CFGS  # noqa: E402
 from paper_2602_21958_b200 import lattice as L  # noqa: E402
 
 cfg = int(sys.argv[1])

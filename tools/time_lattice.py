@@ -8,11 +8,9 @@ sys.path.insert(0, ".")
 import paper_2602_21958_b200 as P  # noqa: E402
 from paper_2602_21958_b200 import lattice as L  # noqa: E402
 
-CFGS = {
-    3: dict(nx=256, ny=1, nz=256, n_polar=8, n_azimuth=16, n_freq=41, corr_len=16.0, eps=1e-4, layout="intensity"),
-    4: dict(nx=64, ny=64, nz=64, n_polar=8, n_azimuth=16, n_freq=31, corr_len=8.0, eps=1e-4, layout="moments"),
-    5: dict(nx=128, ny=128, nz=128, n_polar=8, n_azimuth=12, n_freq=41, corr_len=16.0, eps=1e-5, layout="moments"),
-}
+from paper_2602_21958_b200.configs import LATTICE_CONFIGS as CFGS  # noqa: E402
+
+
 def main():
   which = [int(a) for a in sys.argv[1:]] or [3, 4, 5]
   for cfg in which:
