@@ -9,9 +9,11 @@ N = 65,536,000 DOF, 524 MB per vector.  A step is one matvec y = A x.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-N > 1 (torchrun): every rank runs an independent replica on its own GPU
-(weak scaling; the matvec shards by direction with one moment all-reduce,
-which this single-GPU tier does not implement -- DESIGN.md "Multi-GPU").
+N > 1: launched under torchrun (one rank per GPU; `--gpus N` without torchrun
+re-launches itself through torch.distributed.run).  Default `--mode sharded`:
+ONE cfg2 matvec per step, its 64 directions split over the ranks, one NCCL
+all-reduce of the 16 MB moment array per matvec (strong scaling, DESIGN.md
+section 10); `--mode replicas`: an independent cfg2 matvec per GPU (weak).
 Timing: CUDA events on the launching stream, barrier + synchronize on both
 sides, max over ranks.  The vector (524 MB) exceeds the 126 MB L2, so no
 explicit flush is needed between steps.
@@ -51,9 +53,11 @@ def parse():
     ap.add_argument("--no-lattice", action="store_true")
     ap.add_argument("--cfg5-gmres", action="store_true",
                     help="also run cfg5 GMRES(20) to 1e-8 (about 1,550 iterations, ~9 minutes)")
-    ap.add_argument("--mode", choices=["replicas", "sharded"], default="replicas",
-                    help="N > 1: independent cfg2 matvecs per GPU (weak scaling, default) or ONE cfg2 matvec "
-                         "sharded by direction with an NCCL all-reduce of the moments (strong scaling)")
+    ap.add_argument("--mode", choices=["replicas", "sharded"], default="sharded",
+                    help="N > 1: ONE cfg2 matvec sharded by direction with an NCCL all-reduce of the moments "
+                         "(strong scaling, default) or independent cfg2 matvecs per GPU (weak scaling)")
+    ap.add_argument("--no-reference-as-shipped", action="store_true",
+                    help="skip timing the installed reference package (baseline/_ref) on cfg2 shapes")
     return ap.parse_args()
 
 
@@ -230,6 +234,100 @@ def cpu_port_timing(problem, target_s=12.0, max_steps=30):
                       f"threads, mean {statistics.mean(times) * 1e3:.1f} ms"}
 
 
+REF_PKG = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _ref_shipped_child():
+    """(child process) The installed, unmodified reference package (baseline/_ref, rtkrylov
+    0.1.0) on cfg2 shapes, timed through its own public API: apply_A with its own dipole
+    kernel LegendreKernel((1, 0, 1/2)) -- the reference's Sigma is frequency-flat; the PRD
+    contraction is not expressible in it -- and apply_transfer alone (its numba
+    sweeps, R/transfer.py:134-141, R/_kernels.py:70-88).  Best of k, the reference's own
+    benchmark pattern (benchmarks/bench_kernels.py:19-25).  Prints one JSON object."""
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/rtk_numba_cache")
+    sys.path.insert(0, REF_PKG)
+    import numpy as np_
+
+    from rtkrylov import _kernels
+    from rtkrylov.grid import Grid
+    from rtkrylov.operator import RTProblem, apply_A
+    from rtkrylov.quadrature import gauss_legendre, trapezoid
+    from rtkrylov.scattering import LegendreKernel, build_scattering
+    from rtkrylov.transfer import apply_transfer, build_transfer
+
+    from paper_2602_21958_b200 import configs
+
+    c = configs.SLAB_CONFIGS[CFG]
+    t = configs.slab_t_nodes(c["n_space"], c["t_range"], c["sigma"], configs.SEED_BASE + CFG)
+    dn = gauss_legendre(c["n_angles"] // 2, -1.0, 0.0)
+    up = gauss_legendre(c["n_angles"] // 2, 0.0, 1.0)
+    fr = trapezoid(c["n_freq"], -c["x_max"], c["x_max"])
+
+    def gauss(nu):
+        nu = np_.asarray(nu, dtype=float)
+        return np_.exp(-nu * nu) / np_.sqrt(np_.pi)
+
+    grid = Grid(t, np_.concatenate([dn.nodes, up.nodes]), np_.concatenate([dn.weights, up.weights]), fr.nodes,
+                fr.weights, gauss)
+    eps = c["eps"]
+    wsum = float(fr.weights.sum())
+    scat = build_scattering(grid, LegendreKernel((1.0, 0.0, 0.5)),
+                            lambda tt, mu, nu: (1.0 - eps) / (2.0 * wsum) * np_.ones_like(tt + mu + nu))
+    tr = build_transfer(grid, 0.0, 0.0)
+    prob = RTProblem(grid, tr, scat, thermal=np_.full(grid.n_total, eps))
+    v = np_.random.default_rng(7).standard_normal(grid.n_total)
+
+    def best_of(fn, k):
+        best = float("inf")
+        for _ in range(k):
+            t0 = time.perf_counter()
+            fn()
+            best = min(best, time.perf_counter() - t0)
+        return best
+
+    apply_transfer(tr, v)   # numba compile / page-in
+    t_lam = best_of(lambda: apply_transfer(tr, v), 2)
+    apply_A(prob, v)
+    t_a = best_of(lambda: apply_A(prob, v), 2)
+    print(json.dumps({"apply_A_s": t_a, "apply_transfer_s": t_lam, "backend": _kernels.backend(),
+                      "n_dof": int(grid.n_total)}), flush=True)
+
+
+def reference_as_shipped(timeout_s=900):
+    """The installed reference (baseline/_ref) timed as shipped (numba sweeps on one core, numpy
+    BLAS on all cores) and with OPENBLAS_NUM_THREADS=1, each in a fresh process; plus the host's
+    CPU model and core count.  {} entries say why a leg is missing."""
+    import platform
+
+    cpu_model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    cpu_model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    out = {"cpu_model": cpu_model, "nproc": os.cpu_count(), "package": "rtkrylov 0.1.0 (baseline/_ref, unmodified)",
+           "workload": "cfg2 shapes (2000 x 64 x 512 = 65.5 M DOF), the reference's own frequency-flat dipole "
+                       "kernel LegendreKernel((1, 0, 1/2)); best of 2 after a warm-up call"}
+    if not os.path.isdir(os.path.join(REF_PKG, "rtkrylov")):
+        out["unavailable"] = "baseline/_ref not installed (pip install --target baseline/_ref /root/reference)"
+        return out
+    for name, extra in (("as_shipped", {}), ("openblas_1_thread", {"OPENBLAS_NUM_THREADS": "1",
+                                                                   "OMP_NUM_THREADS": "1", "MKL_NUM_THREADS": "1"})):
+        env = dict(os.environ, **extra)
+        try:
+            res = subprocess.run([sys.executable, os.path.abspath(__file__), "--ref-shipped-child"], env=env,
+                                 capture_output=True, text=True, timeout=timeout_s)
+            rec = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
+            rec["matvecs_per_s"] = 1.0 / rec["apply_A_s"]
+            out[name] = rec
+        except Exception as exc:  # pragma: no cover - reported, not fatal
+            out[name] = {"unavailable": f"{type(exc).__name__}: {str(exc)[:200]}"}
+    return out
+
+
 def run_reference(args):
     """--impl reference: the oracle port of the reference CPU path on the host cores (rank 0 only)."""
     world, rank, _ = dist_setup("gloo")
@@ -258,56 +356,125 @@ def run_reference(args):
             "gdof_per_s": value * problem.n_total / 1e9,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                              "sample": f"each step one full cfg2 matvec by oracle/rt_oracle_c.c (C restatement of "
-                                       f"R/operator.py:48-53 + R/_kernels.py:70-88), OpenMP {threads} threads"},
+                                       f"R/operator.py:48-53 + R/_kernels.py:70-88), OpenMP {threads} threads",
+                             "reference_as_shipped": None if args.no_reference_as_shipped
+                             else reference_as_shipped()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+class _PlumbingShardOps:
+    """BENCH_PLUMBING=1 only (tests/test_bench_multirank.py, CPU ranks): stand-ins with the
+    shapes of the two device halves and NO radiative-transfer arithmetic, so the multi-rank
+    bench path (torchrun relaunch, all-reduce, barriers, max over ranks, the JSON line) runs
+    end to end without a GPU.  Its line says so in "data"; it is never a measurement."""
+
+    def __init__(self, local):
+        import torch
+
+        from paper_2602_21958_b200.scattering import separable_form
+
+        g = local.grid
+        self.torch = torch
+        self.n_m = g.n_space * separable_form(local.scattering.kernel, g)[0].shape[0] * g.n_freq
+
+    def partial_moments(self, x):
+        return self.torch.zeros(self.n_m, dtype=self.torch.float64)
+
+    def apply_with_moments(self, x, m):
+        return x.clone()
+
+
 def run_sharded(args):
-    """--mode sharded: one cfg2 matvec per step, directions split over the ranks
-    (paper_2602_21958_b200.sharding), one NCCL all-reduce of the 16 MB moment array per matvec."""
+    """--mode sharded (default for N > 1): ONE cfg2 matvec per step, the 64 directions split
+    over the ranks (paper_2602_21958_b200.sharding), one NCCL all-reduce of the 16 MB moment
+    array per matvec.  `value` = whole-job matvecs/s (strong scaling); e2e adds each rank's
+    H2D of its x slice and D2H of its y slice (pinned host buffers) inside the timed region."""
     import torch
 
-    world, rank, local = dist_setup("nccl")
-    torch.cuda.set_device(local)
+    plumbing = os.environ.get("BENCH_PLUMBING") == "1"
+    world, rank, local = dist_setup("gloo" if plumbing else "nccl")
     from paper_2602_21958_b200 import _native, configs
-    from paper_2602_21958_b200.sharding import ShardedOperator
+    from paper_2602_21958_b200.sharding import NativeShardOps, ShardedOperator
 
-    problem = configs.slab_problem(CFG, formal_solver=args.formal_solver)
-    op = ShardedOperator(problem, rank=rank, world=world)
-    gen = torch.Generator(device="cuda").manual_seed(1234)
-    x = torch.randn(problem.n_total, dtype=torch.float64, device="cuda", generator=gen)
+    if plumbing:
+        problem = configs.slab_problem(CFG, n_space=40, n_angles=8, n_freq=16)
+        op = ShardedOperator(problem, rank=rank, world=world, ops_factory=_PlumbingShardOps)
+        dev = "cpu"
+    else:
+        torch.cuda.set_device(local)
+        problem = configs.slab_problem(CFG, formal_solver=args.formal_solver)
+        op = ShardedOperator(problem, rank=rank, world=world, ops_factory=NativeShardOps)
+        dev = "cuda"
+    gen = torch.Generator(device=dev).manual_seed(1234)
+    x = torch.randn(problem.n_total, dtype=torch.float64, device=dev, generator=gen)
     x_local = op.local_slice(x).contiguous()
     del x
+
+    def sync():
+        if not plumbing:
+            torch.cuda.synchronize()
+
+    def timed(fn, steps):
+        """ms of `steps` calls: CUDA events on the launching stream (wall clock on CPU ranks)."""
+        sync()
+        torch.distributed.barrier()
+        if plumbing:
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                fn()
+            ms = (time.perf_counter() - t0) * 1e3
+        else:
+            stream = torch.cuda.current_stream()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(steps):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+        torch.distributed.barrier()
+        return ms
+
     for _ in range(max(args.warmup, 3)):
         op(x_local)
-    torch.cuda.synchronize()
-    torch.distributed.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
-    launches0 = _native.launch_count()
-    stream = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record(stream)
-    for _ in range(args.steps):
-        op(x_local)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    launches = _native.launch_count() - launches0
-    ms = e0.elapsed_time(e1)
-    torch.distributed.barrier()
-    clk = clocks.stop()
-    ms_max, _ = aggregate(ms, args.steps, world, "cuda")
+    clocks = None if plumbing else ClockSampler(local)
+    if clocks:
+        clocks.start()
+    launches0 = 0 if plumbing else _native.launch_count()
+    ms = timed(lambda: op(x_local), args.steps)
+    launches = 0 if plumbing else _native.launch_count() - launches0
+    clk = clocks.stop() if clocks else {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["cpu plumbing run"]}
+    ms_max, _ = aggregate(ms, args.steps, world, dev)
     value = args.steps / (ms_max / 1e3)   # whole-job matvecs/s: every step is ONE global matvec
+
+    # e2e: host slices in, host slices out (pinned), one sharded matvec per step
+    hx = torch.empty(x_local.numel(), dtype=torch.float64, pin_memory=not plumbing)
+    hx.copy_(x_local.cpu())
+    hy = torch.empty_like(hx)
+
+    def e2e_step():
+        xd = hx.to(dev, non_blocking=True)
+        yd = op(xd)
+        hy.copy_(yd, non_blocking=True)
+        sync()
+
+    ms_e = timed(e2e_step, max(3, min(args.steps, 10)))
+    ms_e_max, _ = aggregate(ms_e, max(3, min(args.steps, 10)), world, dev)
+    e2e = {"value": max(3, min(args.steps, 10)) / (ms_e_max / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": 8 * problem.n_total, "d2h_bytes_per_step": 8 * problem.n_total,
+           "path": "ShardedOperator (rtk_partial_moments + all-reduce + rtk_apply_A_with_moments) with each "
+                   "rank's x slice copied H2D and its y slice D2H every step (bytes summed over ranks)"}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; BASELINE cfg2 shapes)",
-                "config": workload_config({"formal_solver": args.formal_solver,
-                                           "parallelism": f"direction-sharded x{world} (NCCL all-reduce of moments)"}),
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": ("PLUMBING TEST: CPU gloo ranks, stand-in halves with no transfer arithmetic, reduced cfg2 "
+                         "shapes -- not a measurement") if plumbing else "synthetic (seeded; BASELINE cfg2 shapes)",
+                "config": workload_config({"formal_solver": args.formal_solver}),
+                "parallelism": f"direction-sharded x{world} (NCCL all-reduce of moments)",
                 "gdof_per_s": value * problem.n_total / 1e9, "gpu_launches": launches, "clocks": clk,
-                "e2e": None, "mode": "sharded"}
+                "e2e": e2e, "mode": "sharded", "cpu_baseline": None}
         print(json.dumps(line), flush=True)
     torch.distributed.barrier()
     torch.distributed.destroy_process_group()
@@ -381,13 +548,13 @@ def run_b200(args):
     }
     if kms[1] < 0:
         # the unfused pair (K2a moments, K2b DMMA GEMM) on the same input, for the per-kernel roofline
-        os.environ["RTK_SIGMA_UNFUSED"] = "1"
+        h.set_tuning("sigma_unfused", 1)
         kun = np.zeros(3)
         for _ in range(kreps):
             _native.check(lib.rtk_profile_apply_A(h.h, _device.ptr(x), _device.ptr(y), n, sptr, buf))
             kun += np.array(list(buf), dtype=float)
         kun /= kreps
-        del os.environ["RTK_SIGMA_UNFUSED"]
+        h.set_tuning("sigma_unfused", 0)
         kernels["unfused_pair"] = {
             "moments": {"ms": kun[0], "bytes": moments_bytes, "achieved_gbs": moments_bytes / kun[0] / 1e6,
                         "frac_hbm": moments_bytes / kun[0] / 1e6 / hbm},
@@ -501,12 +668,14 @@ def run_b200(args):
             cpu = cpu_port_timing(problem)
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {exc}"}
+        if not args.no_reference_as_shipped:
+            cpu["reference_as_shipped"] = reference_as_shipped()
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; BASELINE cfg2 shapes)",
-                "config": workload_config({"formal_solver": args.formal_solver,
-                                           "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}),
+                "config": workload_config({"formal_solver": args.formal_solver}),
+                "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                 "gdof_per_s": value * n / 1e9, "gpu_launches": launches, "clocks": clk, "roofline": roofline,
                 "kernels": kernels, "e2e": e2e, "cpu_baseline": cpu}
         line.update(extra)
@@ -725,11 +894,31 @@ def lattice_timings(torch):
     return out
 
 
+def relaunch_under_torchrun(args):
+    """`bench.py --gpus N` (N > 1) outside torchrun: run this same command line under
+    torch.distributed.run with N ranks on this node (127.0.0.1 rendezvous) and return its
+    exit code.  BENCH_BACKEND=gloo lets the CPU tests drive the multi-rank path."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
+    if "--ref-shipped-child" in sys.argv:
+        _ref_shipped_child()
+        return
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         run_reference(args)
-    elif args.mode == "sharded" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+    elif args.mode == "sharded" and world > 1:
         run_sharded(args)
     else:
         run_b200(args)

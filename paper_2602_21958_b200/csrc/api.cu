@@ -65,6 +65,10 @@ Problem::~Problem() {
     if (lat_gat_shift) cudaFree(lat_gat_shift);
     if (lat_down_shift) cudaFree(lat_down_shift);
     if (lat_dtab) cudaFree(lat_dtab);
+    if (lat_tile_hdr) cudaFree(lat_tile_hdr);
+    if (lat_tile_sub) cudaFree(lat_tile_sub);
+    if (lat_order) cudaFree(lat_order);
+    if (lat_scratch) cudaFree(lat_scratch);
     double* lat[] = {lat_chi, lat_in_top, lat_in_bot, lat_state[0], lat_state[1], lat_src, lat_zero, lat_splane[0],
                      lat_splane[1], lat_splane[2]};
     for (double* b : lat)
@@ -90,6 +94,8 @@ Tuning tuning_from_env() {
     t.lat_no_planar = getenv_flag("RTK_LATTICE_NO_PLANAR");
     t.moments_scalar = getenv_flag("RTK_MOMENTS_SCALAR");
     t.sigma_unfused = getenv_flag("RTK_SIGMA_UNFUSED");
+    t.lat_no_tile = getenv_flag("RTK_LATTICE_NO_TILE");
+    t.lat_dgz = getenv_int("RTK_LAT_DGZ");
     return t;
 }
 
@@ -105,7 +111,11 @@ int tuning_set(Tuning& t, const char* key, int64_t value) {
     else if (k == "lattice_no_planar") t.lat_no_planar = v;
     else if (k == "moments_scalar") t.moments_scalar = v;
     else if (k == "sigma_unfused") t.sigma_unfused = v;
-    else return 1;
+    else if (k == "lattice_no_tile") t.lat_no_tile = v;
+    else if (k == "lattice_dgz") {
+        if (v < 0 || v > 8) return 1;
+        t.lat_dgz = v;
+    } else return 1;
     return 0;
 }
 

@@ -19,6 +19,7 @@
 //    array.  The source is rebuilt on the fly from the moment unknown u.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -900,14 +901,26 @@ __global__ void __launch_bounds__(DG == 1 ? 128 : 256, DG == 1 ? 5 : 3)
 // o = 0, 1, 2 from step t (down: t + o, up: nz - 1 - t - o) into plane_o, for the offsets in
 // fill_mask (bit o); S = gamma sum_l c_l Y_l(a) u_l (SRC_U) or the isotropic thermal source
 // (SRC_ISO).  Layout plane[a][c][f].  Offset 2 is the exp-parabolic downwind plane.
-template <int SRC, int NM>
+// PM (pair-major, the tiled moment kernel's layout): plane[a][f / 2][c][f % 2], i.e. each
+// frequency pair of a direction is a contiguous [ny][nx] image of double2; threads are
+// (pair, node) with the node fastest so the writes stay coalesced.
+template <int SRC, int NM, bool PM>
 __global__ void __launch_bounds__(256) lattice_splane_kernel(LatArgs A, int t, double* __restrict__ plane0,
                                                               double* __restrict__ plane1,
                                                               double* __restrict__ plane2, int fill_mask, int fp) {
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (tid >= A.nxy * fp) return;
-    const int64_t c = tid / fp;
-    const int fpad = static_cast<int>(tid - c * fp);
+    int64_t c;
+    int fpad;
+    if (PM) {   // tid = (pair, node, e): pair-major, node, then the pair's two frequencies
+        const int64_t pr = tid / (2 * A.nxy);
+        const int64_t rem = tid - pr * 2 * A.nxy;
+        c = rem >> 1;
+        fpad = static_cast<int>(2 * pr + (rem & 1));
+    } else {
+        c = tid / fp;
+        fpad = static_cast<int>(tid - c * fp);
+    }
     const bool fvalid = fpad < A.n_freq;
     const int f = fvalid ? fpad : 0;
     const int64_t plane = A.nxy * fp;
@@ -951,12 +964,341 @@ __global__ void __launch_bounds__(256) lattice_splane_kernel(LatArgs A, int t, d
             } else {
                 v = g[q];
             }
-            planes[q >> 1][a * plane + c * fp + fpad] = fvalid ? v : 0.0;
+            const int64_t idx = PM ? a * plane + ((fpad >> 1) * A.nxy + c) * 2 + (fpad & 1) : a * plane + c * fp + fpad;
+            planes[q >> 1][idx] = fvalid ? v : 0.0;
         }
     }
 }
 
+// ---------------- moment layout, tiled: one CTA per (tile of lines, frequency pair) ----------------
+//
+// lattice_mom_tile_kernel (IE / exp-linear).  Every line of a direction samples the source at
+// the same fractional offset at a given (layer step, sub-node), so for a TX x TY tile of lines
+// the samples of one step lie in one (TX + span_x + 1) x (TY + span_y + 1) window of the two
+// source planes the step crosses (span = the whole-cell shift range of the step, <= |s| + 1).
+// The CTA stages that window of direction a + 1 (both planes, one frequency pair, double2 in
+// the pair-major [dir][pair][node] plane layout) and the direction's sub-node table with
+// cp.async while it marches direction a out of shared memory: a sample is 8 LDS.128 from
+// 32-bit addresses instead of 8 L1/L2 gathers with 64-bit address arithmetic.  The T_RC node
+// gather (once per direction and step) reads the [dir][pair][line] line states from global.
+// Moments accumulate in registers over one hemisphere's directions (fixed order); with DGZ > 1
+// direction groups (gridDim.z) the groups' partial moments go to a scratch array that
+// lattice_mom_reduce_kernel sums in group order (deterministic).
+struct TileHdr {
+    int fx, fy;   // window origin: min over the step's sub-nodes of floor(offset), wrapped mod (nx, ny)
+    int w, h;     // window extent (nodes)
+};
+struct TileSub {
+    int dx, dy;           // sub-node offset within the window (unwrapped)
+    int pad0, pad1;
+    double w00, w10, w01, w11;   // bilinear weights (same arithmetic as stencil_at)
+};
+
+struct TileArgs {
+    const TileHdr* hdr;     // [dir][step]
+    const TileSub* sub;     // indexed like the sub-node Shift table: shift_off + t (n_sub + 1) + m
+    const int* order;       // direction order: this call's down directions, then its up directions
+    int n_order, n_down;    // entries of order; the first n_down are Omega_z < 0
+    int region_cap;         // double2 per staged plane window (max over directions)
+    int sub_cap;            // max n_sub + 1
+    int ntx;                // tiles along x
+    int dgz;                // direction groups (gridDim.z)
+    double* scratch;        // DGZ > 1: [group][hemi][line][NM][fp]
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+
+template <int FS, int NM, int TX, int TY>
+__global__ void __launch_bounds__(TX * TY, 3)
+    lattice_mom_tile_kernel(LatArgs A, TileArgs T, int t, const double2* __restrict__ st_in,
+                            double2* __restrict__ st_out, double* __restrict__ mom, int with_inflow, int fp,
+                            const double2* __restrict__ plane_cur, const double2* __restrict__ plane_next) {
+    constexpr int NT = TX * TY;
+    const int hp = fp >> 1;
+    const int g = blockIdx.y;                    // frequency pair
+    const int tile = blockIdx.x;
+    const int ty0 = (tile / T.ntx) * TY, tx0 = (tile - (tile / T.ntx) * T.ntx) * TX;
+    const int lx = tx0 + static_cast<int>(threadIdx.x) % TX, ly = ty0 + static_cast<int>(threadIdx.x) / TX;
+    const bool line_ok = lx < A.nx && ly < A.ny;
+    const int c = line_ok ? ly * A.nx + lx : 0;
+    const int llx = static_cast<int>(threadIdx.x) % TX, lly = static_cast<int>(threadIdx.x) / TX;
+    const int64_t plane2 = A.nxy * static_cast<int64_t>(hp);   // double2 per direction plane
+    const int nsteps = A.nz - 1;
+    const bool march = t < nsteps;
+
+    extern __shared__ __align__(16) double2 tsm[];
+    // two stages: [plane a window][plane b window][sub table]
+    const int stage_d2 = 2 * T.region_cap + T.sub_cap * 3;   // TileSub = 48 B = 3 double2
+    auto win_a = [&](int st) { return tsm + st * stage_d2; };
+    auto win_b = [&](int st) { return tsm + st * stage_d2 + T.region_cap; };
+    auto subs = [&](int st) { return reinterpret_cast<const TileSub*>(tsm + st * stage_d2 + 2 * T.region_cap); };
+
+    double phi[2], in_top[2], in_bot[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int f = 2 * g + q;
+        const bool fv = f < A.n_freq;
+        phi[q] = fv ? A.phi[f] : 0.0;
+        in_top[q] = (with_inflow && fv && A.inflow_top) ? A.inflow_top[f] : 0.0;
+        in_bot[q] = (with_inflow && fv && A.inflow_bottom) ? A.inflow_bottom[f] : 0.0;
+    }
+
+    // directions of this CTA: order[i] for i = z, z + dgz, ...
+    const int z = blockIdx.z;
+    auto dir_at = [&](int i) { return T.order[i]; };
+
+    // stage the window of direction order[i] into stage st (cp.async; caller commits)
+    auto stage = [&](int i, int st) {
+        const int a = dir_at(i);
+        const LatDir& D = A.dirs[a];
+        const TileHdr H = T.hdr[static_cast<int64_t>(a) * nsteps + t];
+        int gx0 = tx0 + H.fx;
+        if (gx0 >= A.nx) gx0 -= A.nx;
+        int gy0 = ty0 + H.fy;
+        if (gy0 >= A.ny) gy0 -= A.ny;
+        const double2* pa = plane_cur + a * plane2 + static_cast<int64_t>(g) * A.nxy;
+        const double2* pb = plane_next + a * plane2 + static_cast<int64_t>(g) * A.nxy;
+        double2* wa = win_a(st);
+        double2* wb = win_b(st);
+        const int cx = static_cast<int>(threadIdx.x) & 31, ry0 = static_cast<int>(threadIdx.x) >> 5;
+        for (int ry = ry0; ry < H.h; ry += NT / 32) {
+            int gy = gy0 + ry;
+            while (gy >= A.ny) gy -= A.ny;
+            const int row = gy * A.nx;
+            for (int rx = cx; rx < H.w; rx += 32) {
+                int gx = gx0 + rx;
+                while (gx >= A.nx) gx -= A.nx;
+                cp_async16(wa + ry * H.w + rx, pa + row + gx);
+                cp_async16(wb + ry * H.w + rx, pb + row + gx);
+            }
+        }
+        const int n_sub1 = D.n_sub + 1;
+        const double2* src = reinterpret_cast<const double2*>(T.sub + D.shift_off + static_cast<int64_t>(t) * n_sub1);
+        double2* dst = reinterpret_cast<double2*>(const_cast<TileSub*>(subs(st)));
+        for (int e = threadIdx.x; e < 3 * n_sub1; e += NT) cp_async16(dst + e, src + e);
+    };
+
+    const int n_mine = T.n_order > z ? (T.n_order - z + T.dgz - 1) / T.dgz : 0;
+    if (march && n_mine > 0) stage(z, 0);
+    asm volatile("cp.async.commit_group;\n" ::);
+
+    double mo[NM][2];
+#pragma unroll
+    for (int l = 0; l < NM; ++l) mo[l][0] = mo[l][1] = 0.0;
+    int hemi = 0;   // hemisphere of the accumulated moments (0: down, layer t; 1: up, layer nz-1-t)
+
+    auto flush = [&](int hm) {
+        // moments of one hemisphere's directions (of this group) for this step's layer
+        const int k = hm == 0 ? t : A.nz - 1 - t;
+        if (line_ok) {
+            if (T.dgz > 1) {
+                double* o = T.scratch + ((static_cast<int64_t>(z) * 2 + hm) * A.nxy + c) * NM * fp + 2 * g;
+#pragma unroll
+                for (int l = 0; l < NM; ++l)
+                    *reinterpret_cast<double2*>(o + static_cast<int64_t>(l) * fp) = make_double2(mo[l][0], mo[l][1]);
+            } else {
+                // step t is the first visit of layers t and nz-1-t iff t < nz-1-t; the middle layer
+                // (odd nz) gets both parts from this thread, up added to down
+                const bool first = (hm == 0) ? (t <= A.nz - 1 - t) : (t < A.nz - 1 - t);
+                double* o = mom + (static_cast<int64_t>(k) * A.nxy + c) * NM * fp + 2 * g;
+#pragma unroll
+                for (int l = 0; l < NM; ++l) {
+                    double2* op = reinterpret_cast<double2*>(o + static_cast<int64_t>(l) * fp);
+                    double2 v = make_double2(mo[l][0], mo[l][1]);
+                    if (!first) {
+                        const double2 old = *op;
+                        v.x += old.x;
+                        v.y += old.y;
+                    }
+                    if (2 * g + 1 >= A.n_freq) v.y = 0.0;   // pad column of an odd N_nu stays zero
+                    *op = v;
+                }
+            }
+        }
+#pragma unroll
+        for (int l = 0; l < NM; ++l) mo[l][0] = mo[l][1] = 0.0;
+    };
+
+    for (int it = 0; it < n_mine; ++it) {
+        const int i = z + it * T.dgz;
+        const int a = dir_at(i);
+        const int hm = i < T.n_down ? 0 : 1;
+        if (hm != hemi) {
+            flush(hemi);
+            hemi = hm;
+        }
+        const int st = it & 1;
+        // prefetch the next direction's window into the other stage, then wait for this one
+        if (march && it + 1 < n_mine) stage(z + (it + 1) * T.dgz, st ^ 1);
+        asm volatile("cp.async.commit_group;\n" ::);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        __syncthreads();
+
+        const LatDir& D = A.dirs[a];
+        const double2* lin = st_in + a * plane2 + static_cast<int64_t>(g) * A.nxy;
+        if (line_ok) {
+            // T_RC: node c of layer k from the four lines around it (line values after t steps)
+            double v0, v1;
+            if (t == 0) {
+                v0 = hm == 0 ? in_top[0] : in_bot[0];
+                v1 = hm == 0 ? in_top[1] : in_bot[1];
+            } else {
+                const Stencil sg = stencil_at(lx, ly, A.gat_shift[a * A.nz + t], A.nx, A.ny);
+                const double2 s00 = lin[sg.c00], s10 = lin[sg.c10], s01 = lin[sg.c01], s11 = lin[sg.c11];
+                v0 = sg.w00 * s00.x + sg.w10 * s10.x + sg.w01 * s01.x + sg.w11 * s11.x;
+                v1 = sg.w00 * s00.y + sg.w10 * s10.y + sg.w01 * s01.y + sg.w11 * s11.y;
+            }
+#pragma unroll
+            for (int l = 0; l < NM; ++l) {
+                mo[l][0] = fma(D.wy[l], v0, mo[l][0]);
+                mo[l][1] = fma(D.wy[l], v1, mo[l][1]);
+            }
+            if (march) {
+                double acc0, acc1;
+                if (t == 0) {
+                    acc0 = hm == 0 ? in_top[0] : in_bot[0];
+                    acc1 = hm == 0 ? in_top[1] : in_bot[1];
+                } else if (D.sc) {
+                    // short characteristics: restart at the upwind point of node c
+                    const Stencil rs = stencil_at(lx, ly, restart_shift(D), A.nx, A.ny);
+                    const double2 s00 = lin[rs.c00], s10 = lin[rs.c10], s01 = lin[rs.c01], s11 = lin[rs.c11];
+                    acc0 = rs.w00 * s00.x + rs.w10 * s10.x + rs.w01 * s01.x + rs.w11 * s11.x;
+                    acc1 = rs.w00 * s00.y + rs.w10 * s10.y + rs.w01 * s01.y + rs.w11 * s11.y;
+                } else {
+                    const double2 s2 = lin[c];
+                    acc0 = s2.x;
+                    acc1 = s2.y;
+                }
+                const TileHdr H = T.hdr[static_cast<int64_t>(a) * nsteps + t];
+                const double2* wa = win_a(st);
+                const double2* wb = win_b(st);
+                const TileSub* sb = subs(st);
+                const double* dtl = A.dtab + D.dtab_off + static_cast<int64_t>(t) * D.n_sub * A.nxy + c;
+                const int n_sub = D.n_sub;
+                const double inv_n = 1.0 / n_sub;
+                double ps0 = 0.0, ps1 = 0.0;
+                for (int m = (FS == RTK_FS_IE ? 1 : 0); m <= n_sub; ++m) {
+                    const TileSub S = sb[m];
+                    const int o = (lly + S.dy) * H.w + llx + S.dx;
+                    const double2 a00 = wa[o], a10 = wa[o + 1], a01 = wa[o + H.w], a11 = wa[o + H.w + 1];
+                    const double2 b00 = wb[o], b10 = wb[o + 1], b01 = wb[o + H.w], b11 = wb[o + H.w + 1];
+                    const double wz = m * inv_n;
+                    const double s0 = (1 - wz) * (S.w00 * a00.x + S.w10 * a10.x + S.w01 * a01.x + S.w11 * a11.x) +
+                                      wz * (S.w00 * b00.x + S.w10 * b10.x + S.w01 * b01.x + S.w11 * b11.x);
+                    const double s1 = (1 - wz) * (S.w00 * a00.y + S.w10 * a10.y + S.w01 * a01.y + S.w11 * a11.y) +
+                                      wz * (S.w00 * b00.y + S.w10 * b10.y + S.w01 * b01.y + S.w11 * b11.y);
+                    if (m > 0) {
+                        const double dt = __ldg(dtl + static_cast<int64_t>(m - 1) * A.nxy);
+                        const double d0 = phi[0] * dt, d1 = phi[1] * dt;
+                        if (FS == RTK_FS_IE) {
+                            const double r0 = rcp_nr(1.0 + d0), r1 = rcp_nr(1.0 + d1);
+                            acc0 = fma(acc0, r0, (d0 * s0) * r0);
+                            acc1 = fma(acc1, r1, (d1 * s1) * r1);
+                        } else {
+                            const ExpLin w0 = exp_linear_weights(d0), w1 = exp_linear_weights(d1);
+                            acc0 = fma(acc0, w0.att, w0.wu * ps0 + w0.wc * s0);
+                            acc1 = fma(acc1, w1.att, w1.wu * ps1 + w1.wc * s1);
+                        }
+                    }
+                    ps0 = s0;
+                    ps1 = s1;
+                }
+                st_out[a * plane2 + static_cast<int64_t>(g) * A.nxy + c] = make_double2(acc0, acc1);
+            }
+        }
+        __syncthreads();   // stage st is refilled by the next iteration's prefetch
+    }
+    flush(hemi);
+    if (hemi == 0) flush(1);   // no up direction in this CTA: its (zero) part is still written
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// DGZ > 1: mom of the step's two layers = sum over the direction groups in group order
+template <int NM>
+__global__ void lattice_mom_reduce_kernel(const double* __restrict__ scratch, double* __restrict__ mom, int t, int nz,
+                                          int64_t nxy, int fp, int dgz, int n_freq) {
+    const int64_t per = nxy * NM * fp;
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= per) return;
+    const int f = static_cast<int>(e % fp);
+    for (int hm = 0; hm < 2; ++hm) {
+        const int k = hm == 0 ? t : nz - 1 - t;
+        const bool first = (hm == 0) ? (t <= nz - 1 - t) : (t < nz - 1 - t);
+        double sum = 0.0;
+        for (int zz = 0; zz < dgz; ++zz) sum += scratch[(static_cast<int64_t>(zz) * 2 + hm) * per + e];
+        if (f >= n_freq) sum = 0.0;
+        double* o = mom + static_cast<int64_t>(k) * per + e;
+        *o = first ? sum : *o + sum;
+    }
+}
+
 }  // namespace
+
+// ---------------------------------------------------------------------------
+// Window and sub-node tables of the tiled moment kernel, per (direction, layer step): the
+// same offsets and floor/fraction arithmetic as the Shift tables (shift_of), kept unwrapped
+// so a tile's samples index one window.
+static int setup_tile_tables(Problem& p, const rtk_lattice_desc* d, const std::vector<LatDir>& dirs) {
+    p.lat_tile_tx = d->ny > 1 ? 16 : 128;
+    p.lat_tile_ty = d->ny > 1 ? 16 : 1;
+    const int nsteps = d->nz - 1;
+    std::vector<TileHdr> hdr(static_cast<size_t>(d->n_dirs) * std::max(1, nsteps));
+    size_t n_sub_total = 0;
+    for (const auto& D : dirs) n_sub_total = std::max<size_t>(n_sub_total, D.shift_off + static_cast<size_t>(nsteps) * (D.n_sub + 1));
+    std::vector<TileSub> sub(std::max<size_t>(1, n_sub_total));
+    p.lat_region_cap = 0;
+    p.lat_sub_cap = 0;
+    p.h_lat_down.assign(d->n_dirs, 0);
+    for (int a = 0; a < d->n_dirs; ++a) {
+        const LatDir& D = dirs[a];
+        p.h_lat_down[a] = D.down;
+        p.lat_sub_cap = std::max(p.lat_sub_cap, D.n_sub + 1);
+        for (int t = 0; t < nsteps; ++t) {
+            int fxmin = 0, fxmax = 0, fymin = 0, fymax = 0;
+            std::vector<double> fxs(D.n_sub + 1), fys(D.n_sub + 1), oxs(D.n_sub + 1), oys(D.n_sub + 1);
+            for (int m = 0; m <= D.n_sub; ++m) {
+                const double tt = D.sc ? static_cast<double>(m) / D.n_sub - 1.0 : t + static_cast<double>(m) / D.n_sub;
+                oxs[m] = tt * D.sx;
+                oys[m] = tt * D.sy;
+                fxs[m] = std::floor(oxs[m]);
+                fys[m] = std::floor(oys[m]);
+                const int fx = static_cast<int>(fxs[m]), fy = static_cast<int>(fys[m]);
+                if (m == 0 || fx < fxmin) fxmin = fx;
+                if (m == 0 || fx > fxmax) fxmax = fx;
+                if (m == 0 || fy < fymin) fymin = fy;
+                if (m == 0 || fy > fymax) fymax = fy;
+            }
+            TileHdr& H = hdr[static_cast<size_t>(a) * nsteps + t];
+            H.fx = ((fxmin % d->nx) + d->nx) % d->nx;
+            H.fy = ((fymin % d->ny) + d->ny) % d->ny;
+            H.w = p.lat_tile_tx + (fxmax - fxmin) + 1;
+            H.h = p.lat_tile_ty + (fymax - fymin) + 1;
+            p.lat_region_cap = std::max(p.lat_region_cap, H.w * H.h);
+            for (int m = 0; m <= D.n_sub; ++m) {
+                TileSub& S = sub[D.shift_off + static_cast<size_t>(t) * (D.n_sub + 1) + m];
+                S.dx = static_cast<int>(fxs[m]) - fxmin;
+                S.dy = static_cast<int>(fys[m]) - fymin;
+                S.pad0 = S.pad1 = 0;
+                const double ax = oxs[m] - fxs[m], ay = oys[m] - fys[m];
+                S.w00 = (1 - ax) * (1 - ay);
+                S.w10 = ax * (1 - ay);
+                S.w01 = (1 - ax) * ay;
+                S.w11 = ax * ay;
+            }
+        }
+    }
+    RTK_CUDA_TRY(cudaMalloc(&p.lat_tile_hdr, sizeof(TileHdr) * hdr.size()));
+    RTK_CUDA_TRY(cudaMemcpy(p.lat_tile_hdr, hdr.data(), sizeof(TileHdr) * hdr.size(), cudaMemcpyHostToDevice));
+    RTK_CUDA_TRY(cudaMalloc(&p.lat_tile_sub, sizeof(TileSub) * sub.size()));
+    RTK_CUDA_TRY(cudaMemcpy(p.lat_tile_sub, sub.data(), sizeof(TileSub) * sub.size(), cudaMemcpyHostToDevice));
+    RTK_CUDA_TRY(cudaMalloc(&p.lat_order, sizeof(int) * d->n_dirs));
+    p.lat_region_cap = (p.lat_region_cap + 1) / 2 * 2;   // keep the stages 32-byte aligned
+    return RTK_OK;
+}
 
 // ---------------------------------------------------------------------------
 int setup_lattice(Problem& p, const rtk_lattice_desc* d) {
@@ -1046,6 +1388,9 @@ int setup_lattice(Problem& p, const rtk_lattice_desc* d) {
                                            p.lat_dtab, d->n_dirs, d->nx, d->ny, d->nz);
         RTK_LAUNCH_CHECK("lattice_dtab_kernel");
         RTK_CUDA_TRY(cudaDeviceSynchronize());
+    }
+    if (d->layout == RTK_LAYOUT_MOMENTS) {
+        if (int rc = setup_tile_tables(p, d, dirs)) return rc;
     }
     return RTK_OK;
 }
@@ -1156,7 +1501,7 @@ static int launch_mom_steps_dg(const Problem& p, const LatArgs& A, bool with_inf
         if (t < A.nz - 1) {
             // step 0 fills every plane of the ring; later steps only the newest one
             const int mask = PAR ? (t == 0 ? 7 : 4) : (t == 0 ? 3 : 2);
-            lattice_splane_kernel<SRC, NM><<<pblocks, 256, 0, s>>>(A, t, cur, nxt, nn, mask, p.fp);
+            lattice_splane_kernel<SRC, NM, false><<<pblocks, 256, 0, s>>>(A, t, cur, nxt, nn, mask, p.fp);
             RTK_LAUNCH_CHECK("lattice_splane_kernel");
         }
         kern<<<sblocks, mb, mom_smem, s>>>(A, t, a, b, mom, with_inflow ? 1 : 0, p.fp, cur, nxt,
@@ -1169,8 +1514,102 @@ static int launch_mom_steps_dg(const Problem& p, const LatArgs& A, bool with_inf
     return RTK_OK;
 }
 
+// Tiled path (IE / exp-linear): per layer step the pair-major source planes, the tiled
+// moment kernel over (tiles x frequency pairs x direction groups) and, with several
+// direction groups, the ordered reduction of their partial moments.  -1: not applicable.
+template <int FS, int SRC, int NM, int TX, int TY>
+static int launch_mom_tiles_t(const Problem& p, const LatArgs& A, bool with_inflow, double* mom, cudaStream_t s) {
+    const int hp = p.fp / 2;
+    const int ntx = (A.nx + TX - 1) / TX, nty = (A.ny + TY - 1) / TY;
+    const int ntiles = ntx * nty;
+    // direction order of this call's range: down directions, then up
+    if (p.lat_order_a0 != A.a0 || p.lat_order_a1 != A.a1) {
+        p.h_lat_order.clear();
+        for (int pass = 0; pass < 2; ++pass)
+            for (int a = A.a0; a < A.a1; ++a)
+                if ((p.h_lat_down[a] != 0) == (pass == 0)) p.h_lat_order.push_back(a);
+        int nd = 0;
+        for (int a = A.a0; a < A.a1; ++a) nd += p.h_lat_down[a] ? 1 : 0;
+        p.lat_order_down = nd;
+        if (!p.h_lat_order.empty())
+            RTK_CUDA_TRY(cudaMemcpyAsync(p.lat_order, p.h_lat_order.data(), sizeof(int) * p.h_lat_order.size(),
+                                         cudaMemcpyHostToDevice, s));
+        p.lat_order_a0 = A.a0;
+        p.lat_order_a1 = A.a1;
+    }
+    const int n_order = static_cast<int>(p.h_lat_order.size());
+    // direction groups: enough CTAs for ~6 per SM (148 SMs), at most 8 and one per direction
+    int dgz = p.tune.lat_dgz;
+    if (dgz <= 0) {
+        const int64_t ctas = static_cast<int64_t>(ntiles) * hp;
+        dgz = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, (148 * 6 + ctas - 1) / ctas)));
+    }
+    dgz = std::max(1, std::min(dgz, std::max(1, n_order)));
+    const size_t stage_d2 = 2 * static_cast<size_t>(p.lat_region_cap) + 3 * static_cast<size_t>(p.lat_sub_cap);
+    const size_t smem = 2 * stage_d2 * sizeof(double2);
+    if (smem > 110 * 1024) return -1;   // very grazing directions on large tiles: per-item kernel
+    TileArgs T;
+    T.hdr = reinterpret_cast<const TileHdr*>(p.lat_tile_hdr);
+    T.sub = reinterpret_cast<const TileSub*>(p.lat_tile_sub);
+    T.order = p.lat_order;
+    T.n_order = n_order;
+    T.n_down = p.lat_order_down;
+    T.region_cap = p.lat_region_cap;
+    T.sub_cap = p.lat_sub_cap;
+    T.ntx = ntx;
+    T.dgz = dgz;
+    T.scratch = nullptr;
+    if (dgz > 1) {
+        const size_t need = static_cast<size_t>(dgz) * 2 * A.nxy * NM * p.fp;
+        if (p.lat_scratch_count < need) {
+            if (p.lat_scratch) cudaFreeAsync(p.lat_scratch, s);
+            p.lat_scratch = nullptr;
+            p.lat_scratch_count = 0;
+            RTK_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p.lat_scratch), sizeof(double) * need, s));
+            p.lat_scratch_count = need;
+        }
+        T.scratch = p.lat_scratch;
+    }
+    auto kern = lattice_mom_tile_kernel<FS, NM, TX, TY>;
+    if (int rc = ensure_smem_for(kern, smem)) return rc;
+    const unsigned pblocks = static_cast<unsigned>((A.nxy * p.fp + 255) / 256);
+    double2* a = reinterpret_cast<double2*>(p.lat_state[0]);
+    double2* b = reinterpret_cast<double2*>(p.lat_state[1]);
+    const dim3 grid(static_cast<unsigned>(ntiles), static_cast<unsigned>(hp), static_cast<unsigned>(dgz));
+    for (int t = 0; t < A.nz; ++t) {
+        double* cur = p.lat_splane[t % 2];
+        double* nxt = p.lat_splane[(t + 1) % 2];
+        if (t < A.nz - 1) {
+            lattice_splane_kernel<SRC, NM, true><<<pblocks, 256, 0, s>>>(A, t, cur, nxt, nullptr, t == 0 ? 3 : 2, p.fp);
+            RTK_LAUNCH_CHECK("lattice_splane_kernel");
+        }
+        kern<<<grid, TX * TY, smem, s>>>(A, T, t, a, b, mom, with_inflow ? 1 : 0, p.fp,
+                                         reinterpret_cast<const double2*>(cur), reinterpret_cast<const double2*>(nxt));
+        RTK_LAUNCH_CHECK("lattice_mom_tile_kernel");
+        if (dgz > 1) {
+            const int64_t per = A.nxy * NM * p.fp;
+            lattice_mom_reduce_kernel<NM><<<static_cast<unsigned>((per + 255) / 256), 256, 0, s>>>(
+                p.lat_scratch, mom, t, A.nz, A.nxy, p.fp, dgz, A.n_freq);
+            RTK_LAUNCH_CHECK("lattice_mom_reduce_kernel");
+        }
+        std::swap(a, b);
+    }
+    return RTK_OK;
+}
+
+template <int FS, int SRC, int NM>
+static int launch_mom_tiles(const Problem& p, const LatArgs& A, bool with_inflow, double* mom, cudaStream_t s) {
+    if (FS == RTK_FS_EXP_PARABOLIC || p.tune.lat_no_tile || !p.lat_tile_hdr || (p.fp & 1)) return -1;
+    if (p.lat_tile_ty == 1) return launch_mom_tiles_t<FS, SRC, NM, 128, 1>(p, A, with_inflow, mom, s);
+    return launch_mom_tiles_t<FS, SRC, NM, 16, 16>(p, A, with_inflow, mom, s);
+}
+
 template <int FS, int SRC, int NM>
 static int launch_mom_steps(const Problem& p, const LatArgs& A, bool with_inflow, double* mom, cudaStream_t s) {
+    {
+        const int rc = launch_mom_tiles<FS, SRC, NM>(p, A, with_inflow, mom, s);
+        if (rc != -1) return rc;
+    }
     // direction groups only where a step has too few items to fill the SMs: measured cfg4
     // (65,536 items) 45.0 -> 41.3 ms with DG = 8; cfg5 (344,064 items) is slower with it
     const int64_t items = A.nxy * ((p.fp + 1) / 2);

@@ -82,6 +82,9 @@ struct Tuning {
     int lat_no_planar = 0;    // "lattice_no_planar" RTK_LATTICE_NO_PLANAR: 2D slabs through the 3D sampling path
     int moments_scalar = 0;   // "moments_scalar"   RTK_MOMENTS_SCALAR: 8-byte moment kernel instead of the pair kernel
     int sigma_unfused = 0;    // "sigma_unfused"    RTK_SIGMA_UNFUSED: K2a + K2b instead of the fused Sigma kernel
+    int lat_no_tile = 0;      // "lattice_no_tile"  RTK_LATTICE_NO_TILE: moment layout through the per-item gather
+                              //                    kernel (lattice_mom_group_kernel) instead of the tiled one
+    int lat_dgz = 0;          // "lattice_dgz"      RTK_LAT_DGZ: direction groups of the tiled kernel (0 auto, 1..8)
 };
 Tuning tuning_from_env();
 // 0 ok, 1 unknown key
@@ -153,6 +156,18 @@ struct Problem {
     int lat_max_sub = 0;                         // largest sub-segment count over the directions
     bool lat_any_sc = false;   // some direction uses short characteristics
     int lat_total_sub = 0;                       // sum over directions of (n_sub + 1)
+    // tiled moment kernel (lattice.cu lattice_mom_tile_kernel)
+    void* lat_tile_hdr = nullptr;                // TileHdr [dir][step]
+    void* lat_tile_sub = nullptr;                // TileSub, indexed like lat_sub_shift
+    int lat_tile_tx = 0, lat_tile_ty = 0;        // lines per tile
+    int lat_region_cap = 0, lat_sub_cap = 0;     // staged window (double2) / sub-node table capacity
+    std::vector<int> h_lat_down;                 // per direction: Omega_z < 0
+    // launch-time workspace of the (logically const) operator application
+    int* lat_order = nullptr;                    // device direction order of the current range
+    mutable std::vector<int> h_lat_order;
+    mutable int lat_order_a0 = -1, lat_order_a1 = -1, lat_order_down = 0;
+    mutable double* lat_scratch = nullptr;       // per-group partial moments (direction groups > 1)
+    mutable size_t lat_scratch_count = 0;
     CUtensorMap tma_gmap, tma_dtmap;
     ~Problem();
 };

@@ -51,3 +51,10 @@ def gmres_cases(key):
                         rel_tol=float(tol), max_iter=int(max_iter),
                         restart=None if restart < 0 else int(restart), reorthogonalize=bool(reorth)))
     return out
+
+
+def gmres_band(key, name):
+    """Iteration counts of the unmodified reference on 16 ulp-perturbed right-hand sides
+    (tests/golden/make_gmres_bands.py) for a restarted golden case."""
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ref_gmres_bands.npz"))
+    return z[f"{key}/{name}/iterations"]

@@ -181,11 +181,14 @@ def test_cfg5_full_size_linearity_and_direction_shards():
 
 
 # Every shipped kernel variant against the oracle (rtk_problem_set_tuning selects it):
-# moment layout -- lattice_mom_group_kernel with DG = 1 (cfg5's instantiation: 128-thread blocks,
-# one direction group), 4 and 8 direction groups; intensity layout -- the shared-memory kernel
-# (3D and planar sampling, with and without the dt table) and the non-shared-memory fallback
-# lattice_int_kernel (long characteristics, IE / exp-linear).
-MOMENT_VARIANTS = [{"lattice_dg": 1}, {"lattice_dg": 4}, {"lattice_dg": 8}]
+# moment layout -- the tiled kernel lattice_mom_tile_kernel (default for IE / exp-linear) with
+# 1, 3 and 8 direction groups, and the per-item gather kernel lattice_mom_group_kernel (the
+# exp-parabolic path, and IE / exp-linear with lattice_no_tile) with DG = 1, 4 and 8 direction
+# groups; intensity layout -- the shared-memory kernel (3D and planar sampling, with and
+# without the dt table) and the non-shared-memory fallback lattice_int_kernel.
+MOMENT_VARIANTS = [{}, {"lattice_dgz": 1}, {"lattice_dgz": 3}, {"lattice_dgz": 8},
+                   {"lattice_no_tile": 1, "lattice_dg": 1}, {"lattice_no_tile": 1, "lattice_dg": 4},
+                   {"lattice_no_tile": 1, "lattice_dg": 8}]
 INTENSITY_VARIANTS = [{"lattice_no_smem": 1}, {"lattice_no_dtab": 1}, {"lattice_no_planar": 1},
                       {"lattice_no_dtab": 1, "lattice_no_planar": 1}]
 
@@ -241,17 +244,18 @@ def test_auto_selection_takes_one_direction_group_on_large_steps():
     """A step with > 131,072 (line, frequency-pair) items selects DG = 1 by itself (cfg5's
     path): 64 x 64 lines x 33 pairs; against the oracle with the default tuning."""
     p = L.lattice_problem(64, 64, 4, 4, 2, 66, corr_len=4.0, seed=23, layout="moments")
+    _with_tuning(p, {"lattice_no_tile": 1})
     d = OL.desc_from_lattice_problem(p)
     v = np.random.default_rng(23).standard_normal(p.n_total)
     assert rel_l2(P.apply_A(p, v), OL.apply_A(d, "moments", v)) <= MATVEC_TOL
 
 
-@pytest.mark.parametrize("tuning", [{}, {"lattice_dg": 1}], ids=["auto", "dg1"])
+@pytest.mark.parametrize("tuning", [{}, {"lattice_no_tile": 1, "lattice_dg": 1}], ids=["tiled", "group_dg1"])
 def test_cfg5_column_geometry_matches_oracle(tuning):
     """BASELINE cfg5 construction at its full depth and angular set (nz = 128, 8 x 12 = 96
     directions, corr 16, eps 1e-5, moment layout) on a 32 x 32 horizontal period with N_nu = 4
     (the oracle takes ~1 min): default selection and cfg5's own kernel instantiation (one
-    direction group, lattice_mom_group_kernel<..., 1>)."""
+    direction group, lattice_mom_group_kernel<..., 1>) and the tiled kernel."""
     p = configs.lattice_config_problem(5, nx=32, ny=32, n_freq=4)
     _with_tuning(p, tuning)
     d = OL.desc_from_lattice_problem(p)
@@ -277,7 +281,7 @@ def test_cfg5_full_geometry_matches_oracle_fixture():
     assert p.n_total == int(z["n_total"])
     u = np.random.default_rng(F.U_SEED).standard_normal(p.n_total)
     idx = torch.from_numpy(z["index"]).cuda()
-    for tuning in ({}, {"lattice_dg": 1}):
+    for tuning in ({}, {"lattice_no_tile": 1, "lattice_dg": 1}):
         _with_tuning(p, tuning)
         y = P.apply_A(p, torch.from_numpy(u).cuda())
         ys = y[idx].cpu().numpy()

