@@ -708,16 +708,20 @@ def gmres_timings(torch):
     p = configs.slab_problem(1)
     b = P.build_rhs(p, device=True)
     out = {"cpu": cpu_gmres_cfg1(p, b.cpu().numpy())}
-    for name, restart in (("cfg1_gmres30", 30), ("cfg1_gmres_full", None)):
-        cfg = P.SolveConfig(rel_tol=1e-8, max_iter=6000, restart=restart)
-        P.gmres(p, b, P.SolveConfig(rel_tol=1e-8, max_iter=5, restart=restart))   # warm-up
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        rep = P.gmres(p, b, cfg)
-        torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        out[name] = {"iterations": rep.iterations, "converged": rep.converged, "time_s": el,
-                     "true_residual": rep.true_residual, "matvecs": rep.matvecs}
+    # the fused CGS2 Arnoldi (north star) and the reference's own MGS (SolveConfig default)
+    for orth in ("cgs2", None):
+        tag = "" if orth == "cgs2" else "_mgs"
+        for name, restart in (("cfg1_gmres30", 30), ("cfg1_gmres_full", None)):
+            cfg = P.SolveConfig(rel_tol=1e-8, max_iter=6000, restart=restart, orthogonalization=orth)
+            P.gmres(p, b, P.SolveConfig(rel_tol=1e-8, max_iter=5, restart=restart, orthogonalization=orth))
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rep = P.gmres(p, b, cfg)
+            torch.cuda.synchronize()
+            el = time.perf_counter() - t0
+            out[name + tag] = {"iterations": rep.iterations, "converged": rep.converged, "time_s": el,
+                               "true_residual": rep.true_residual, "matvecs": rep.matvecs,
+                               "orthogonalization": orth or "mgs (reference default)"}
     return out
 
 
@@ -734,10 +738,11 @@ def gmres_cfg2_moments(torch):
     for name, restart, its in (("gmres30_3000", 30, 3000), ("gmres_unrestarted", None, 4000)):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        rep = P.gmres(p, b, P.SolveConfig(rel_tol=1e-8, max_iter=its, restart=restart))
+        rep = P.gmres(p, b, P.SolveConfig(rel_tol=1e-8, max_iter=its, restart=restart, orthogonalization="cgs2"))
         torch.cuda.synchronize()
         out[name] = {"iterations": rep.iterations, "converged": rep.converged, "time_s": time.perf_counter() - t0,
-                     "true_residual": rep.true_residual, "matvecs": rep.matvecs, "unknowns": p.n_total}
+                     "true_residual": rep.true_residual, "matvecs": rep.matvecs, "unknowns": p.n_total,
+                     "orthogonalization": "cgs2"}
     return out
 
 
@@ -747,8 +752,8 @@ def krylov_cfg2(torch, problem, matvec_ms, hbm):
 
     n = problem.n_total
     b = torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator(device="cuda").manual_seed(5))
-    cfg = P.SolveConfig(rel_tol=1e-30, max_iter=30, restart=30)
-    P.gmres(problem, b, P.SolveConfig(rel_tol=1e-30, max_iter=30, restart=30))   # warm the memory pool
+    cfg = P.SolveConfig(rel_tol=1e-30, max_iter=30, restart=30, orthogonalization="cgs2")
+    P.gmres(problem, b, cfg)   # warm the memory pool
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     rep = P.gmres(problem, b, cfg)
@@ -804,31 +809,27 @@ def formal_solver_timings(torch, lib, hbm):
 
 def lattice_gmres_timings(torch, cfg5=False):
     """GMRES time-to-1e-8 on the multi-D configurations that reach it within a bench run:
-    cfg4 (moment layout) unrestarted, cfg3 (intensity layout, 2.75 GB vectors) GMRES(40).
-    cfg5 GMRES(20) needs ~10^3 iterations (minutes); see DESIGN.md section 11."""
-    import time
-
+    cfg4 (moment layout) unrestarted; cfg3 in BOTH layouts -- intensity (2.75 GB vectors)
+    GMRES(40), moment layout (129 MB vectors) unrestarted.  cfg5 GMRES(20) (BASELINE's
+    restart) with --cfg5-gmres.  Arnoldi: the fused CGS2."""
     import paper_2602_21958_b200 as P
-    from paper_2602_21958_b200 import lattice as L
+    from paper_2602_21958_b200 import configs
 
-    runs = {4: (dict(nx=64, ny=64, nz=64, n_polar=8, n_azimuth=16, n_freq=31, corr_len=8.0, eps=1e-4,
-                     layout="moments"), None, 600),
-            3: (dict(nx=256, ny=1, nz=256, n_polar=8, n_azimuth=16, n_freq=41, corr_len=16.0, eps=1e-4,
-                     layout="intensity"), 40, 1200)}
+    runs = [(4, "moments", None, 600), (3, "intensity", 40, 1200), (3, "moments", None, 1500)]
     if cfg5:
-        runs[5] = (dict(nx=128, ny=128, nz=128, n_polar=8, n_azimuth=12, n_freq=41, corr_len=16.0, eps=1e-5,
-                        layout="moments"), 20, 2500)
+        runs.append((5, "moments", 20, 2500))
     out = {}
-    for cfg, (kw, restart, its) in runs.items():
-        p = L.lattice_problem(seed=21958 + cfg, **kw)
+    for cfg, layout, restart, its in runs:
+        p = configs.lattice_config_problem(cfg, layout=layout)
         b = P.build_rhs(p, device=True)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        rep = P.gmres(p, b, P.SolveConfig(rel_tol=1e-8, max_iter=its, restart=restart))
+        rep = P.gmres(p, b, P.SolveConfig(rel_tol=1e-8, max_iter=its, restart=restart, orthogonalization="cgs2"))
         torch.cuda.synchronize()
-        out[f"cfg{cfg}"] = {"restart": restart, "iterations": rep.iterations, "converged": bool(rep.converged),
-                            "time_s": time.perf_counter() - t0, "true_residual": float(rep.true_residual),
-                            "unknowns": p.n_total, "layout": kw["layout"]}
+        key = f"cfg{cfg}" if layout == configs.LATTICE_CONFIGS[cfg]["layout"] else f"cfg{cfg}_{layout}"
+        out[key] = {"restart": restart, "iterations": rep.iterations, "converged": bool(rep.converged),
+                    "time_s": time.perf_counter() - t0, "true_residual": float(rep.true_residual),
+                    "unknowns": p.n_total, "layout": layout, "orthogonalization": "cgs2"}
         del p, b, rep
         torch.cuda.empty_cache()
     return out
@@ -839,12 +840,9 @@ def lattice_timings(torch):
     import paper_2602_21958_b200 as P
     from paper_2602_21958_b200 import lattice as L
 
-    cfgs = {3: dict(nx=256, ny=1, nz=256, n_polar=8, n_azimuth=16, n_freq=41, corr_len=16.0, eps=1e-4,
-                    layout="intensity"),
-            4: dict(nx=64, ny=64, nz=64, n_polar=8, n_azimuth=16, n_freq=31, corr_len=8.0, eps=1e-4,
-                    layout="moments"),
-            5: dict(nx=128, ny=128, nz=128, n_polar=8, n_azimuth=12, n_freq=41, corr_len=16.0, eps=1e-5,
-                    layout="moments")}
+    from paper_2602_21958_b200 import configs
+
+    cfgs = {cfg: dict(configs.LATTICE_CONFIGS[cfg]) for cfg in (3, 4, 5)}
     out = {}
 
     def time_matvec(p):
@@ -863,6 +861,11 @@ def lattice_timings(torch):
     for cfg, kw in cfgs.items():
         p = L.lattice_problem(seed=21958 + cfg, **kw)
         ms = time_matvec(p)
+        if cfg == 3:   # cfg3 also in the moment layout (u = 129 MB instead of I = 2.75 GB)
+            pm = L.lattice_problem(seed=21958 + cfg, **dict(kw, layout="moments"))
+            ms_m = time_matvec(pm)
+            del pm
+            torch.cuda.empty_cache()
         dof = p.n_space * p.n_dirs * p.n_freq
         n_total = p.n_total
         del p
@@ -875,6 +878,8 @@ def lattice_timings(torch):
         out[f"cfg{cfg}"] = {"layout": kw["layout"], "unknowns": n_total, "dof": dof, "ms_per_matvec": ms,
                             "matvecs_per_s": 1e3 / ms, "gdof_per_s": dof / ms / 1e6,
                             "hybrid_characteristics": {"ms_per_matvec": ms_h, "gdof_per_s": dof / ms_h / 1e6}}
+        if cfg == 3:
+            out["cfg3"]["moment_layout"] = {"ms_per_matvec": ms_m, "gdof_per_s": dof / ms_m / 1e6}
         if cfg in (3, 4):   # the exponential integrators (cfg5 skipped to keep the default run short)
             fsd = {}
             for fs in ("exp_linear", "exp_parabolic"):

@@ -185,6 +185,12 @@ int rtk_lattice_partial_moments(rtk_problem* p, const double* u_dev, double* m_d
                                 int32_t a1, void* stream);
 int rtk_lattice_apply_with_moments(rtk_problem* p, const double* u_dev, const double* m_dev, int64_t n_m,
                                    double* y_dev, int64_t n, void* stream);
+/* Space-sharded finish of the same operator (Krylov vectors sharded by space): for the node
+ * block [node0, node1) (n_b = (node1 - node0) * n_moments * n_freq values, the block's slices
+ * of u, of the fully summed moments m, and of y), y_b = u_b - R_w m_b.  With the partial
+ * moments of all ranks reduce-scattered by space, the blocks of all ranks form apply_A. */
+int rtk_lattice_apply_with_moments_nodes(rtk_problem* p, const double* u_dev, const double* m_dev, int64_t node0,
+                                         int64_t node1, double* y_dev, void* stream);
 /* s = Sigma x -- apply_scattering, R/scattering.py:126-148. */
 int rtk_apply_sigma(rtk_problem* p, const double* x_dev, double* s_dev, int64_t n, void* stream);
 /* y = Lambda s (homogeneous part) -- apply_transfer, R/transfer.py:134-141. */

@@ -91,6 +91,7 @@ SIGNATURES = [
     ("rtk_apply_A_with_moments", ctypes.c_int, [_P, _P, _P, _I64, _P, _I64, _P]),
     ("rtk_lattice_partial_moments", ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _P]),
     ("rtk_lattice_apply_with_moments", ctypes.c_int, [_P, _P, _P, _I64, _P, _I64, _P]),
+    ("rtk_lattice_apply_with_moments_nodes", ctypes.c_int, [_P, _P, _P, _I64, _I64, _P, _P]),
     ("rtk_apply_sigma", ctypes.c_int, [_P, _P, _P, _I64, _P]),
     ("rtk_apply_lambda", ctypes.c_int, [_P, _P, _P, _I64, _P]),
     ("rtk_boundary", ctypes.c_int, [_P, _P, _I64, _P]),

@@ -667,6 +667,21 @@ int rtk_lattice_apply_with_moments(rtk_problem* p, const double* u, const double
     return rtk::launch_redistribute_ex(q, q.mom, y, q.n_freq, rtk::EPI_SUB, u, q.n_freq, s);
 }
 
+int rtk_lattice_apply_with_moments_nodes(rtk_problem* p, const double* u, const double* m, int64_t node0,
+                                         int64_t node1, double* y, void* stream) {
+    int rc = check_lattice_shard(p, p ? p->impl.n_total : 0);
+    if (rc) return rc;
+    Problem& q = p->impl;
+    if (node0 < 0 || node1 > q.n_space || node0 >= node1)
+        return set_error(RTK_EINVAL, "node range must satisfy 0 <= node0 < node1 <= n_space");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t nodes = node1 - node0;
+    RTK_CUDA_TRY(cudaMemcpy2DAsync(q.mom, sizeof(double) * q.fp, m, sizeof(double) * q.n_freq,
+                                   sizeof(double) * q.n_freq, nodes * q.n_mom, cudaMemcpyDeviceToDevice, s));
+    return rtk::launch_redistribute_ex(q, q.mom, y, q.n_freq, rtk::EPI_SUB, u, q.n_freq, s, nodes,
+                                       q.gamma + node0 * q.n_freq);
+}
+
 int rtk_partial_moments(rtk_problem* p, const double* x, double* m, int64_t n_m, void* stream) {
     int rc = check_shard(p, n_m);
     if (rc) return rc;

@@ -158,6 +158,11 @@ __device__ __forceinline__ double advance_line(const LatDir& D, const Shift* __r
     return acc;
 }
 
+// Shared-memory planes of the intensity kernel are pair-major: frequency q of node c sits at
+// pidx(c, q) = [q / 2][c][q % 2], so a warp's double2 loads of consecutive nodes are
+// contiguous (bank-conflict-free LDS.128; node-major [c][kFC] put lanes 32 B apart).
+__device__ __forceinline__ int pidx(int c, int q, int nxy) { return (q >> 1) * 2 * nxy + 2 * c + (q & 1); }
+
 // Shared-memory variant of advance_line for kFC frequencies at once: the geometry
 // (shift, stencil, trilinear opacity, dt) is computed once per line and sub-node and
 // reused for the kFC frequencies of the chunk.  Planes: chi [nxy], S [nxy][kFC].
@@ -195,23 +200,24 @@ __device__ __forceinline__ void advance_line_smem4(const LatDir& D, const Shift*
             c_m = (1 - wz) * ca + wz * cb;
             dt = D.sub_len * (prev_c + c_m) * 0.5;
         }
-        const double2* a00 = reinterpret_cast<const double2*>(Sa + st.c00 * kFC);
-        const double2* a10 = reinterpret_cast<const double2*>(Sa + st.c10 * kFC);
-        const double2* a01 = reinterpret_cast<const double2*>(Sa + st.c01 * kFC);
-        const double2* a11 = reinterpret_cast<const double2*>(Sa + st.c11 * kFC);
-        const double2* b00 = reinterpret_cast<const double2*>(Sb + st.c00 * kFC);
-        const double2* b10 = reinterpret_cast<const double2*>(Sb + st.c10 * kFC);
-        const double2* b01 = reinterpret_cast<const double2*>(Sb + st.c01 * kFC);
-        const double2* b11 = reinterpret_cast<const double2*>(Sb + st.c11 * kFC);
+        const double2* a00 = reinterpret_cast<const double2*>(Sa) + st.c00;
+        const double2* a10 = reinterpret_cast<const double2*>(Sa) + st.c10;
+        const double2* a01 = reinterpret_cast<const double2*>(Sa) + st.c01;
+        const double2* a11 = reinterpret_cast<const double2*>(Sa) + st.c11;
+        const double2* b00 = reinterpret_cast<const double2*>(Sb) + st.c00;
+        const double2* b10 = reinterpret_cast<const double2*>(Sb) + st.c10;
+        const double2* b01 = reinterpret_cast<const double2*>(Sb) + st.c01;
+        const double2* b11 = reinterpret_cast<const double2*>(Sb) + st.c11;
 #pragma unroll
         for (int h = 0; h < kFC / 2; ++h) {
-            const double2 p00 = a00[h], p10 = a10[h], q00 = b00[h], q10 = b10[h];
+            const int hh = h * nxy;
+            const double2 p00 = a00[hh], p10 = a10[hh], q00 = b00[hh], q10 = b10[hh];
             double s2[2];
             if (PLANAR) {
                 s2[0] = (1 - wz) * (st.w00 * p00.x + st.w10 * p10.x) + wz * (st.w00 * q00.x + st.w10 * q10.x);
                 s2[1] = (1 - wz) * (st.w00 * p00.y + st.w10 * p10.y) + wz * (st.w00 * q00.y + st.w10 * q10.y);
             } else {
-                const double2 p01 = a01[h], p11 = a11[h], q01 = b01[h], q11 = b11[h];
+                const double2 p01 = a01[hh], p11 = a11[hh], q01 = b01[hh], q11 = b11[hh];
                 s2[0] = (1 - wz) * (st.w00 * p00.x + st.w10 * p10.x + st.w01 * p01.x + st.w11 * p11.x) +
                         wz * (st.w00 * q00.x + st.w10 * q10.x + st.w01 * q01.x + st.w11 * q11.x);
                 s2[1] = (1 - wz) * (st.w00 * p00.y + st.w10 * p10.y + st.w01 * p01.y + st.w11 * p11.y) +
@@ -252,7 +258,7 @@ struct ParSample {
 template <bool PLANAR>
 __device__ __forceinline__ void sample_planes(ParSample<PLANAR>& o, const Stencil& st, double wz,
                                               const double* chi_a, const double* chi_b, const double* Sa,
-                                              const double* Sb) {
+                                              const double* Sb, int nxy) {
     const double ca = PLANAR ? st.w00 * chi_a[st.c00] + st.w10 * chi_a[st.c10]
                              : st.w00 * chi_a[st.c00] + st.w10 * chi_a[st.c10] + st.w01 * chi_a[st.c01] +
                                    st.w11 * chi_a[st.c11];
@@ -262,12 +268,12 @@ __device__ __forceinline__ void sample_planes(ParSample<PLANAR>& o, const Stenci
     o.c = (1 - wz) * ca + wz * cb;
 #pragma unroll
     for (int q = 0; q < kFC; ++q) {
-        const double pa = PLANAR ? st.w00 * Sa[st.c00 * kFC + q] + st.w10 * Sa[st.c10 * kFC + q]
-                                 : st.w00 * Sa[st.c00 * kFC + q] + st.w10 * Sa[st.c10 * kFC + q] +
-                                       st.w01 * Sa[st.c01 * kFC + q] + st.w11 * Sa[st.c11 * kFC + q];
-        const double pb = PLANAR ? st.w00 * Sb[st.c00 * kFC + q] + st.w10 * Sb[st.c10 * kFC + q]
-                                 : st.w00 * Sb[st.c00 * kFC + q] + st.w10 * Sb[st.c10 * kFC + q] +
-                                       st.w01 * Sb[st.c01 * kFC + q] + st.w11 * Sb[st.c11 * kFC + q];
+        const double pa = PLANAR ? st.w00 * Sa[pidx(st.c00, q, nxy)] + st.w10 * Sa[pidx(st.c10, q, nxy)]
+                                 : st.w00 * Sa[pidx(st.c00, q, nxy)] + st.w10 * Sa[pidx(st.c10, q, nxy)] +
+                                       st.w01 * Sa[pidx(st.c01, q, nxy)] + st.w11 * Sa[pidx(st.c11, q, nxy)];
+        const double pb = PLANAR ? st.w00 * Sb[pidx(st.c00, q, nxy)] + st.w10 * Sb[pidx(st.c10, q, nxy)]
+                                 : st.w00 * Sb[pidx(st.c00, q, nxy)] + st.w10 * Sb[pidx(st.c10, q, nxy)] +
+                                       st.w01 * Sb[pidx(st.c01, q, nxy)] + st.w11 * Sb[pidx(st.c11, q, nxy)];
         o.s[q] = (1 - wz) * pa + wz * pb;
     }
 }
@@ -277,17 +283,17 @@ __device__ __forceinline__ void advance_line_smem4_par(const LatDir& D, const Sh
                                                        double (&acc)[kFC], int lx, int ly, int nx, int ny,
                                                        const double* chi_a, const double* chi_b,
                                                        const double* chi_c, const double* Sa, const double* Sb,
-                                                       const double* Sc, const double (&phi)[kFC]) {
+                                                       const double* Sc, const double (&phi)[kFC], int nxy) {
     ParSample<PLANAR> prev, cur, nxt;
-    sample_planes<PLANAR>(prev, stencil_at(lx, ly, sub[0], nx, ny), 0.0, chi_a, chi_b, Sa, Sb);
-    sample_planes<PLANAR>(cur, stencil_at(lx, ly, sub[1], nx, ny), 1.0 / D.n_sub, chi_a, chi_b, Sa, Sb);
+    sample_planes<PLANAR>(prev, stencil_at(lx, ly, sub[0], nx, ny), 0.0, chi_a, chi_b, Sa, Sb, nxy);
+    sample_planes<PLANAR>(cur, stencil_at(lx, ly, sub[1], nx, ny), 1.0 / D.n_sub, chi_a, chi_b, Sa, Sb, nxy);
     for (int m = 1; m <= D.n_sub; ++m) {
         const bool down = m < D.n_sub || Sc != nullptr;
         if (m < D.n_sub)
             sample_planes<PLANAR>(nxt, stencil_at(lx, ly, sub[m + 1], nx, ny), static_cast<double>(m + 1) / D.n_sub,
-                                  chi_a, chi_b, Sa, Sb);
+                                  chi_a, chi_b, Sa, Sb, nxy);
         else if (Sc != nullptr)
-            sample_planes<PLANAR>(nxt, stencil_at(lx, ly, dsh, nx, ny), 1.0 / D.n_sub, chi_b, chi_c, Sb, Sc);
+            sample_planes<PLANAR>(nxt, stencil_at(lx, ly, dsh, nx, ny), 1.0 / D.n_sub, chi_b, chi_c, Sb, Sc, nxy);
         const double dtu = D.sub_len * (prev.c + cur.c) * 0.5;
         const double dtd = D.sub_len * (cur.c + nxt.c) * 0.5;
 #pragma unroll
@@ -351,10 +357,10 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
         for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) {
             const int c = e / kFC, q = e - c * kFC;
             if (q < nq) {
-                if (SRC == LSRC_VEC) cp_async8(sp + e, A.src + ((base + c) * A.n_dirs + a) * A.n_freq + f0 + q);
-                else cp_async8(sp + e, A.src + (base + c) * A.n_freq + f0 + q);
+                if (SRC == LSRC_VEC) cp_async8(sp + pidx(c, q, nxy), A.src + ((base + c) * A.n_dirs + a) * A.n_freq + f0 + q);
+                else cp_async8(sp + pidx(c, q, nxy), A.src + (base + c) * A.n_freq + f0 + q);
             } else {
-                sp[e] = 0.0;
+                sp[pidx(c, q, nxy)] = 0.0;
             }
         }
         if (!DT)
@@ -366,11 +372,11 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
         double* xp = xplane + r * nxy * kFC;
         for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) {
             const int c = e / kFC, q = e - c * kFC;
-            if (q < nq) cp_async8(xp + e, A.x + ((base + c) * A.n_dirs + a) * A.n_freq + f0 + q);
+            if (q < nq) cp_async8(xp + pidx(c, q, nxy), A.x + ((base + c) * A.n_dirs + a) * A.n_freq + f0 + q);
         }
     };
     auto commit = []() { asm volatile("cp.async.commit_group;\n" ::); };
-    for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) lines[e] = inflow[e % kFC];
+    for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) lines[pidx(e / kFC, e % kFC, nxy)] = inflow[e % kFC];
     // prologue: group 0 = planes(t=0) + x(t=0); group 1 = planes(t=1) + x(t=1)
     issue_planes(layer_of(0), 0);
     issue_x(layer_of(0), 0);
@@ -399,11 +405,11 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
             const int c = e / kFC, q = e - c * kFC;
             const int j = c / A.nx, i = c - j * A.nx;
             const Stencil st = stencil_at(i, j, gsh, A.nx, A.ny);
-            const double v = st.w00 * lines[st.c00 * kFC + q] + st.w10 * lines[st.c10 * kFC + q] +
-                             st.w01 * lines[st.c01 * kFC + q] + st.w11 * lines[st.c11 * kFC + q];
+            const double v = st.w00 * lines[pidx(st.c00, q, nxy)] + st.w10 * lines[pidx(st.c10, q, nxy)] +
+                             st.w01 * lines[pidx(st.c01, q, nxy)] + st.w11 * lines[pidx(st.c11, q, nxy)];
             if (q < nq) {
                 const int64_t idx = ((static_cast<int64_t>(k) * A.nxy + c) * A.n_dirs + a) * A.n_freq + f0 + q;
-                A.y[idx] = XM ? xp[e] - v : v;
+                A.y[idx] = XM ? xp[pidx(c, q, nxy)] - v : v;
             }
         }
         if (t == A.nz - 1) break;
@@ -415,8 +421,8 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
                 const int c = e / kFC, q = e - c * kFC;
                 const int j = c / A.nx, i = c - j * A.nx;
                 const Stencil st = stencil_at(i, j, rsh, A.nx, A.ny);
-                seeds[e] = st.w00 * lines[st.c00 * kFC + q] + st.w10 * lines[st.c10 * kFC + q] +
-                           st.w01 * lines[st.c01 * kFC + q] + st.w11 * lines[st.c11 * kFC + q];
+                seeds[pidx(c, q, nxy)] = st.w00 * lines[pidx(st.c00, q, nxy)] + st.w10 * lines[pidx(st.c10, q, nxy)] +
+                                         st.w01 * lines[pidx(st.c01, q, nxy)] + st.w11 * lines[pidx(st.c11, q, nxy)];
             }
         }
         __syncthreads();   // the gather read `lines` before the march overwrites them; shifts staged
@@ -433,15 +439,15 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
             const int ly = c / A.nx, lx = c - ly * A.nx;
             double acc[kFC];
 #pragma unroll
-            for (int q = 0; q < kFC; ++q) acc[q] = start[c * kFC + q];
+            for (int q = 0; q < kFC; ++q) acc[q] = start[pidx(c, q, nxy)];
             if (PAR)
-                advance_line_smem4_par<PLANAR>(D, shs, dsh, acc, lx, ly, A.nx, A.ny, ca, cb, cc, Sa, Sb, Sc, phi);
+                advance_line_smem4_par<PLANAR>(D, shs, dsh, acc, lx, ly, A.nx, A.ny, ca, cb, cc, Sa, Sb, Sc, phi, nxy);
             else
             advance_line_smem4<FS, DT, PLANAR>(D, shs, acc, lx, ly, t, A.nx, A.ny, ca, cb, Sa, Sb, phi,
                                        DT ? A.dtab + D.dtab_off + static_cast<int64_t>(t) * D.n_sub * A.nxy + c : nullptr,
                                        nxy);
 #pragma unroll
-            for (int q = 0; q < kFC; ++q) lines[c * kFC + q] = acc[q];
+            for (int q = 0; q < kFC; ++q) lines[pidx(c, q, nxy)] = acc[q];
         }
     }
 }
@@ -925,6 +931,7 @@ __global__ void __launch_bounds__(256) lattice_splane_kernel(LatArgs A, int t, d
     const int f = fvalid ? fpad : 0;
     const int64_t plane = A.nxy * fp;
     double* planes[3] = {plane0, plane1, plane2};
+
     // q = 2 o + (0: down, 1: up)
     double uval[6][NM], g[6];
     bool use[6];
@@ -1012,8 +1019,21 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
                  : "memory");
 }
 
+// per-direction metadata of one launch (one layer step), staged in shared memory once so the
+// per-direction control flow never waits on a global load
+struct TileDir {
+    int n_sub, sc, shift_off, down;
+    long long dtab;          // this step's first dt-table entry of the direction
+    TileHdr hdr;             // this step's window
+    Shift gat;               // this step's T_RC gather shift
+    double wy[RTK_MAX_MOMENTS];
+};
+
+#ifndef RTK_TILE_MINB
+#define RTK_TILE_MINB 2
+#endif
 template <int FS, int NM, int TX, int TY>
-__global__ void __launch_bounds__(TX * TY, 3)
+__global__ void __launch_bounds__(TX * TY, TX * TY >= 256 ? RTK_TILE_MINB : 2 * RTK_TILE_MINB)
     lattice_mom_tile_kernel(LatArgs A, TileArgs T, int t, const double2* __restrict__ st_in,
                             double2* __restrict__ st_out, double* __restrict__ mom, int with_inflow, int fp,
                             const double2* __restrict__ plane_cur, const double2* __restrict__ plane_next) {
@@ -1021,21 +1041,39 @@ __global__ void __launch_bounds__(TX * TY, 3)
     const int hp = fp >> 1;
     const int g = blockIdx.y;                    // frequency pair
     const int tile = blockIdx.x;
-    const int ty0 = (tile / T.ntx) * TY, tx0 = (tile - (tile / T.ntx) * T.ntx) * TX;
-    const int lx = tx0 + static_cast<int>(threadIdx.x) % TX, ly = ty0 + static_cast<int>(threadIdx.x) / TX;
+    const int tyi = tile / T.ntx;
+    const int ty0 = tyi * TY, tx0 = (tile - tyi * T.ntx) * TX;
+    const int llx = static_cast<int>(threadIdx.x) % TX, lly = static_cast<int>(threadIdx.x) / TX;
+    const int lx = tx0 + llx, ly = ty0 + lly;
     const bool line_ok = lx < A.nx && ly < A.ny;
     const int c = line_ok ? ly * A.nx + lx : 0;
-    const int llx = static_cast<int>(threadIdx.x) % TX, lly = static_cast<int>(threadIdx.x) / TX;
     const int64_t plane2 = A.nxy * static_cast<int64_t>(hp);   // double2 per direction plane
     const int nsteps = A.nz - 1;
     const bool march = t < nsteps;
+    const int z = blockIdx.z;
+    const int n_mine = T.n_order > z ? (T.n_order - z + T.dgz - 1) / T.dgz : 0;
 
     extern __shared__ __align__(16) double2 tsm[];
-    // two stages: [plane a window][plane b window][sub table]
+    // [TileDir x n_mine][stage 0: window a, window b, sub table][stage 1: ...]
+    TileDir* tdir = reinterpret_cast<TileDir*>(tsm);
+    double2* stages = tsm + (n_mine * sizeof(TileDir) + 15) / 16;
     const int stage_d2 = 2 * T.region_cap + T.sub_cap * 3;   // TileSub = 48 B = 3 double2
-    auto win_a = [&](int st) { return tsm + st * stage_d2; };
-    auto win_b = [&](int st) { return tsm + st * stage_d2 + T.region_cap; };
-    auto subs = [&](int st) { return reinterpret_cast<const TileSub*>(tsm + st * stage_d2 + 2 * T.region_cap); };
+    for (int e = threadIdx.x; e < n_mine; e += NT) {
+        const int a = T.order[z + e * T.dgz];
+        const LatDir& D = A.dirs[a];
+        TileDir td;
+        td.n_sub = D.n_sub;
+        td.sc = D.sc;
+        td.shift_off = D.shift_off;
+        td.down = D.down;
+        td.dtab = D.dtab_off + static_cast<long long>(t) * D.n_sub * A.nxy;
+        td.hdr = march ? T.hdr[static_cast<int64_t>(a) * nsteps + t] : TileHdr{0, 0, 0, 0};
+        td.gat = A.gat_shift[a * A.nz + t];
+#pragma unroll
+        for (int l = 0; l < RTK_MAX_MOMENTS; ++l) td.wy[l] = D.wy[l];
+        tdir[e] = td;
+    }
+    __syncthreads();
 
     double phi[2], in_top[2], in_bot[2];
 #pragma unroll
@@ -1047,44 +1085,67 @@ __global__ void __launch_bounds__(TX * TY, 3)
         in_bot[q] = (with_inflow && fv && A.inflow_bottom) ? A.inflow_bottom[f] : 0.0;
     }
 
-    // directions of this CTA: order[i] for i = z, z + dgz, ...
-    const int z = blockIdx.z;
-    auto dir_at = [&](int i) { return T.order[i]; };
-
-    // stage the window of direction order[i] into stage st (cp.async; caller commits)
-    auto stage = [&](int i, int st) {
-        const int a = dir_at(i);
-        const LatDir& D = A.dirs[a];
-        const TileHdr H = T.hdr[static_cast<int64_t>(a) * nsteps + t];
-        int gx0 = tx0 + H.fx;
+    // stage the window of this CTA's it-th direction into stage st (cp.async; caller commits):
+    // a warp per window row, lanes along the row; the wrap is a conditional subtraction (a
+    // window narrower than the lattice) or a modulo (tiny periodic lattices)
+    auto stage = [&](int it, int st) {
+        const int a = T.order[z + it * T.dgz];
+        const TileDir& D = tdir[it];
+        int gx0 = tx0 + D.hdr.fx;
         if (gx0 >= A.nx) gx0 -= A.nx;
-        int gy0 = ty0 + H.fy;
+        int gy0 = ty0 + D.hdr.fy;
         if (gy0 >= A.ny) gy0 -= A.ny;
         const double2* pa = plane_cur + a * plane2 + static_cast<int64_t>(g) * A.nxy;
         const double2* pb = plane_next + a * plane2 + static_cast<int64_t>(g) * A.nxy;
-        double2* wa = win_a(st);
-        double2* wb = win_b(st);
-        const int cx = static_cast<int>(threadIdx.x) & 31, ry0 = static_cast<int>(threadIdx.x) >> 5;
-        for (int ry = ry0; ry < H.h; ry += NT / 32) {
+        double2* wa = stages + st * stage_d2;
+        double2* wb = wa + T.region_cap;
+        const int w = D.hdr.w, h = D.hdr.h;
+        const bool small = w <= A.nx && h <= A.ny;
+        const int cx = static_cast<int>(threadIdx.x) & 31;
+        for (int ry = static_cast<int>(threadIdx.x) >> 5; ry < h; ry += NT / 32) {
             int gy = gy0 + ry;
-            while (gy >= A.ny) gy -= A.ny;
-            const int row = gy * A.nx;
-            for (int rx = cx; rx < H.w; rx += 32) {
+            gy = small ? (gy >= A.ny ? gy - A.ny : gy) : gy % A.ny;
+            const double2* ra = pa + gy * A.nx;
+            const double2* rb = pb + gy * A.nx;
+            for (int rx = cx; rx < w; rx += 32) {
                 int gx = gx0 + rx;
-                while (gx >= A.nx) gx -= A.nx;
-                cp_async16(wa + ry * H.w + rx, pa + row + gx);
-                cp_async16(wb + ry * H.w + rx, pb + row + gx);
+                gx = small ? (gx >= A.nx ? gx - A.nx : gx) : gx % A.nx;
+                cp_async16(wa + ry * w + rx, ra + gx);
+                cp_async16(wb + ry * w + rx, rb + gx);
             }
         }
         const int n_sub1 = D.n_sub + 1;
         const double2* src = reinterpret_cast<const double2*>(T.sub + D.shift_off + static_cast<int64_t>(t) * n_sub1);
-        double2* dst = reinterpret_cast<double2*>(const_cast<TileSub*>(subs(st)));
+        double2* dst = wa + 2 * T.region_cap;
         for (int e = threadIdx.x; e < 3 * n_sub1; e += NT) cp_async16(dst + e, src + e);
     };
 
-    const int n_mine = T.n_order > z ? (T.n_order - z + T.dgz - 1) / T.dgz : 0;
-    if (march && n_mine > 0) stage(z, 0);
+    // global operands of a direction, loaded one direction ahead into registers: the T_RC
+    // gather corners of node c, the line's own state (or the SC restart corners) and its first dt
+    struct Pre {
+        double2 g00, g10, g01, g11;   // gather corners (t > 0)
+        double2 s00;                  // own state (LC; SC restarts are gathered in place)
+        double dt0;                   // first sub-segment's dt
+    };
+    auto prefetch = [&](int it, Pre& P) {
+        if (!line_ok || t == 0) return;
+        const int a = T.order[z + it * T.dgz];
+        const TileDir& D = tdir[it];
+        const double2* lin = st_in + a * plane2 + static_cast<int64_t>(g) * A.nxy;
+        const Stencil sg = stencil_at(lx, ly, D.gat, A.nx, A.ny);
+        P.g00 = lin[sg.c00];
+        P.g10 = lin[sg.c10];
+        P.g01 = lin[sg.c01];
+        P.g11 = lin[sg.c11];
+        if (!march) return;
+        if (!D.sc) P.s00 = lin[c];
+        P.dt0 = __ldg(A.dtab + D.dtab + c);
+    };
+
+    if (march && n_mine > 0) stage(0, 0);
     asm volatile("cp.async.commit_group;\n" ::);
+    Pre cur;
+    if (n_mine > 0) prefetch(0, cur);
 
     double mo[NM][2];
 #pragma unroll
@@ -1092,7 +1153,6 @@ __global__ void __launch_bounds__(TX * TY, 3)
     int hemi = 0;   // hemisphere of the accumulated moments (0: down, layer t; 1: up, layer nz-1-t)
 
     auto flush = [&](int hm) {
-        // moments of one hemisphere's directions (of this group) for this step's layer
         const int k = hm == 0 ? t : A.nz - 1 - t;
         if (line_ok) {
             if (T.dgz > 1) {
@@ -1125,7 +1185,7 @@ __global__ void __launch_bounds__(TX * TY, 3)
 
     for (int it = 0; it < n_mine; ++it) {
         const int i = z + it * T.dgz;
-        const int a = dir_at(i);
+        const int a = T.order[i];
         const int hm = i < T.n_down ? 0 : 1;
         if (hm != hemi) {
             flush(hemi);
@@ -1133,24 +1193,23 @@ __global__ void __launch_bounds__(TX * TY, 3)
         }
         const int st = it & 1;
         // prefetch the next direction's window into the other stage, then wait for this one
-        if (march && it + 1 < n_mine) stage(z + (it + 1) * T.dgz, st ^ 1);
+        if (march && it + 1 < n_mine) stage(it + 1, st ^ 1);
         asm volatile("cp.async.commit_group;\n" ::);
+        Pre nxt;
+        if (it + 1 < n_mine) prefetch(it + 1, nxt);   // global loads in flight across this direction
         asm volatile("cp.async.wait_group 1;\n" ::: "memory");
         __syncthreads();
 
-        const LatDir& D = A.dirs[a];
-        const double2* lin = st_in + a * plane2 + static_cast<int64_t>(g) * A.nxy;
+        const TileDir& D = tdir[it];
         if (line_ok) {
-            // T_RC: node c of layer k from the four lines around it (line values after t steps)
             double v0, v1;
             if (t == 0) {
                 v0 = hm == 0 ? in_top[0] : in_bot[0];
                 v1 = hm == 0 ? in_top[1] : in_bot[1];
             } else {
-                const Stencil sg = stencil_at(lx, ly, A.gat_shift[a * A.nz + t], A.nx, A.ny);
-                const double2 s00 = lin[sg.c00], s10 = lin[sg.c10], s01 = lin[sg.c01], s11 = lin[sg.c11];
-                v0 = sg.w00 * s00.x + sg.w10 * s10.x + sg.w01 * s01.x + sg.w11 * s11.x;
-                v1 = sg.w00 * s00.y + sg.w10 * s10.y + sg.w01 * s01.y + sg.w11 * s11.y;
+                const Stencil sg = stencil_at(lx, ly, D.gat, A.nx, A.ny);
+                v0 = sg.w00 * cur.g00.x + sg.w10 * cur.g10.x + sg.w01 * cur.g01.x + sg.w11 * cur.g11.x;
+                v1 = sg.w00 * cur.g00.y + sg.w10 * cur.g10.y + sg.w01 * cur.g01.y + sg.w11 * cur.g11.y;
             }
 #pragma unroll
             for (int l = 0; l < NM; ++l) {
@@ -1164,35 +1223,37 @@ __global__ void __launch_bounds__(TX * TY, 3)
                     acc1 = hm == 0 ? in_top[1] : in_bot[1];
                 } else if (D.sc) {
                     // short characteristics: restart at the upwind point of node c
-                    const Stencil rs = stencil_at(lx, ly, restart_shift(D), A.nx, A.ny);
-                    const double2 s00 = lin[rs.c00], s10 = lin[rs.c10], s01 = lin[rs.c01], s11 = lin[rs.c11];
-                    acc0 = rs.w00 * s00.x + rs.w10 * s10.x + rs.w01 * s01.x + rs.w11 * s11.x;
-                    acc1 = rs.w00 * s00.y + rs.w10 * s10.y + rs.w01 * s01.y + rs.w11 * s11.y;
+                    const double2* lin = st_in + a * plane2 + static_cast<int64_t>(g) * A.nxy;
+                    const Stencil rs = stencil_at(lx, ly, restart_shift(A.dirs[a]), A.nx, A.ny);
+                    const double2 r00 = lin[rs.c00], r10 = lin[rs.c10], r01 = lin[rs.c01], r11 = lin[rs.c11];
+                    acc0 = rs.w00 * r00.x + rs.w10 * r10.x + rs.w01 * r01.x + rs.w11 * r11.x;
+                    acc1 = rs.w00 * r00.y + rs.w10 * r10.y + rs.w01 * r01.y + rs.w11 * r11.y;
                 } else {
-                    const double2 s2 = lin[c];
-                    acc0 = s2.x;
-                    acc1 = s2.y;
+                    acc0 = cur.s00.x;
+                    acc1 = cur.s00.y;
                 }
-                const TileHdr H = T.hdr[static_cast<int64_t>(a) * nsteps + t];
-                const double2* wa = win_a(st);
-                const double2* wb = win_b(st);
-                const TileSub* sb = subs(st);
-                const double* dtl = A.dtab + D.dtab_off + static_cast<int64_t>(t) * D.n_sub * A.nxy + c;
+                const int w = D.hdr.w;
+                const double2* wa = stages + st * stage_d2;
+                const double2* wb = wa + T.region_cap;
+                const TileSub* sb = reinterpret_cast<const TileSub*>(wa + 2 * T.region_cap);
+                const double* dtl = A.dtab + D.dtab + c;
                 const int n_sub = D.n_sub;
                 const double inv_n = 1.0 / n_sub;
                 double ps0 = 0.0, ps1 = 0.0;
+                double dt_next = t == 0 ? __ldg(dtl) : cur.dt0;
                 for (int m = (FS == RTK_FS_IE ? 1 : 0); m <= n_sub; ++m) {
                     const TileSub S = sb[m];
-                    const int o = (lly + S.dy) * H.w + llx + S.dx;
-                    const double2 a00 = wa[o], a10 = wa[o + 1], a01 = wa[o + H.w], a11 = wa[o + H.w + 1];
-                    const double2 b00 = wb[o], b10 = wb[o + 1], b01 = wb[o + H.w], b11 = wb[o + H.w + 1];
+                    const int o = (lly + S.dy) * w + llx + S.dx;
+                    const double2 a00 = wa[o], a10 = wa[o + 1], a01 = wa[o + w], a11 = wa[o + w + 1];
+                    const double2 b00 = wb[o], b10 = wb[o + 1], b01 = wb[o + w], b11 = wb[o + w + 1];
                     const double wz = m * inv_n;
                     const double s0 = (1 - wz) * (S.w00 * a00.x + S.w10 * a10.x + S.w01 * a01.x + S.w11 * a11.x) +
                                       wz * (S.w00 * b00.x + S.w10 * b10.x + S.w01 * b01.x + S.w11 * b11.x);
                     const double s1 = (1 - wz) * (S.w00 * a00.y + S.w10 * a10.y + S.w01 * a01.y + S.w11 * a11.y) +
                                       wz * (S.w00 * b00.y + S.w10 * b10.y + S.w01 * b01.y + S.w11 * b11.y);
                     if (m > 0) {
-                        const double dt = __ldg(dtl + static_cast<int64_t>(m - 1) * A.nxy);
+                        const double dt = dt_next;
+                        if (m < n_sub) dt_next = __ldg(dtl + static_cast<int64_t>(m) * A.nxy);   // one ahead
                         const double d0 = phi[0] * dt, d1 = phi[1] * dt;
                         if (FS == RTK_FS_IE) {
                             const double r0 = rcp_nr(1.0 + d0), r1 = rcp_nr(1.0 + d1);
@@ -1210,6 +1271,7 @@ __global__ void __launch_bounds__(TX * TY, 3)
                 st_out[a * plane2 + static_cast<int64_t>(g) * A.nxy + c] = make_double2(acc0, acc1);
             }
         }
+        cur = nxt;
         __syncthreads();   // stage st is refilled by the next iteration's prefetch
     }
     flush(hemi);
@@ -1297,6 +1359,7 @@ static int setup_tile_tables(Problem& p, const rtk_lattice_desc* d, const std::v
     RTK_CUDA_TRY(cudaMemcpy(p.lat_tile_sub, sub.data(), sizeof(TileSub) * sub.size(), cudaMemcpyHostToDevice));
     RTK_CUDA_TRY(cudaMalloc(&p.lat_order, sizeof(int) * d->n_dirs));
     p.lat_region_cap = (p.lat_region_cap + 1) / 2 * 2;   // keep the stages 32-byte aligned
+
     return RTK_OK;
 }
 
@@ -1546,7 +1609,8 @@ static int launch_mom_tiles_t(const Problem& p, const LatArgs& A, bool with_infl
     }
     dgz = std::max(1, std::min(dgz, std::max(1, n_order)));
     const size_t stage_d2 = 2 * static_cast<size_t>(p.lat_region_cap) + 3 * static_cast<size_t>(p.lat_sub_cap);
-    const size_t smem = 2 * stage_d2 * sizeof(double2);
+    const int per_cta = (n_order + dgz - 1) / dgz;
+    const size_t smem = 2 * stage_d2 * sizeof(double2) + (per_cta * sizeof(TileDir) + 15) / 16 * 16;
     if (smem > 110 * 1024) return -1;   // very grazing directions on large tiles: per-item kernel
     TileArgs T;
     T.hdr = reinterpret_cast<const TileHdr*>(p.lat_tile_hdr);

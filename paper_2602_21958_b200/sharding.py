@@ -205,6 +205,117 @@ class LatticeShardedOperator:
         return self.ops.apply_with_moments(u, m)
 
 
+# ---------------------------------------------------------------------------
+# Lattice problems, moment layout, Krylov vectors sharded by SPACE
+#
+# Rank r owns a contiguous block of layers of u (its Krylov vectors are that block only) and
+# a cost-balanced block of directions.  One matvec:
+#   all-gather u (every rank needs the source on all layers its directions cross),
+#   transfer of the rank's directions -> partial moments on ALL of space,
+#   reduce-scatter by space -> the summed moments of the rank's layers,
+#   y_b = u_b - R_w m_b on the rank's layers (rtk_lattice_apply_with_moments_nodes).
+# The collective volume equals the all-reduce of the replicated variant (an all-reduce is a
+# reduce-scatter plus an all-gather), but the Krylov basis, the CGS2 passes and the
+# redistribution GEMM are divided by the world size instead of replicated (cfg5: 21 basis
+# vectors x 4.1 GB on every GPU replicated, 4.1 / W GB each sharded).
+
+
+def layer_blocks(nz: int, world: int):
+    """Contiguous layer ranges [(k0, k1)], sizes differing by at most one."""
+    if world > nz:
+        raise ValueError(f"cannot shard {nz} layers over {world} ranks")
+    return [((nz * r) // world, (nz * (r + 1)) // world) for r in range(world)]
+
+
+class NativeLatticeSpaceOps(NativeLatticeShardOps):
+    """Device halves of the space-sharded lattice matvec."""
+
+    def apply_with_moments_nodes(self, u_b, m_b, node0: int, node1: int):
+        h = self.problem.device()
+        y = _device.empty(u_b.numel())
+        _native.check(_native.lib().rtk_lattice_apply_with_moments_nodes(
+            h.h, _device.ptr(u_b), _device.ptr(m_b), node0, node1, _device.ptr(y), _device.stream_ptr()))
+        return y
+
+
+def _dist_all_gather(t, group=None):
+    import torch
+    import torch.distributed as dist
+
+    out = torch.empty(t.numel() * dist.get_world_size(group), dtype=t.dtype, device=t.device)
+    dist.all_gather_into_tensor(out, t, group=group)
+    return out
+
+
+def _dist_reduce_scatter(t, group=None):
+    import torch
+    import torch.distributed as dist
+
+    out = torch.empty(t.numel() // dist.get_world_size(group), dtype=t.dtype, device=t.device)
+    dist.reduce_scatter_tensor(out, t, op=dist.ReduceOp.SUM, group=group)
+    return out
+
+
+class LatticeSpaceShardedOperator:
+    """y_b = (u - R_w M Lambda S(u))_b on this rank's layer block b (see above).  Vectors are
+    local blocks; uneven blocks are padded to the largest for the collectives."""
+
+    def __init__(self, problem, rank: int = None, world: int = None, group=None,
+                 ops_factory=NativeLatticeSpaceOps, all_reduce=None, all_gather=None, reduce_scatter=None):
+        if getattr(problem, "layout", None) != "moments":
+            raise ValueError("lattice sharding needs the moment layout")
+        if rank is None or world is None:
+            import torch.distributed as dist
+
+            rank = dist.get_rank(group) if rank is None else rank
+            world = dist.get_world_size(group) if world is None else world
+        self.problem = problem
+        self.rank, self.world = rank, world
+        self.a0, self.a1 = direction_blocks(lattice_direction_cost(problem), world)[rank]
+        self.layers = layer_blocks(problem.nz, world)
+        nxy = problem.nx * problem.ny
+        self.per_node = problem.n_mom * problem.n_freq
+        self.nodes = [(k0 * nxy, k1 * nxy) for k0, k1 in self.layers]
+        self.node0, self.node1 = self.nodes[rank]
+        self.pad = max(n1 - n0 for n0, n1 in self.nodes) * self.per_node
+        self.ops = ops_factory(problem, self.a0, self.a1)
+        self._all_reduce = all_reduce or (lambda t: _dist_all_reduce(t, group))
+        self._all_gather = all_gather or (lambda t: _dist_all_gather(t, group))
+        self._reduce_scatter = reduce_scatter or (lambda t: _dist_reduce_scatter(t, group))
+
+    def local_slice(self, u):
+        return u[self.node0 * self.per_node:self.node1 * self.per_node]
+
+    def _padded(self, v, lo, hi):
+        import torch
+
+        out = torch.zeros(self.pad, dtype=v.dtype, device=v.device)
+        out[:(hi - lo) * self.per_node] = v
+        return out
+
+    def gather(self, u_b):
+        """The full vector from the blocks of all ranks."""
+        g = self._all_gather(self._padded(u_b, self.node0, self.node1))
+        import torch
+
+        return torch.cat([g[r * self.pad:r * self.pad + (n1 - n0) * self.per_node]
+                          for r, (n0, n1) in enumerate(self.nodes)])
+
+    def scatter_sum(self, m):
+        """Sum over ranks of m, this rank's block (reduce-scatter by space)."""
+        import torch
+
+        blocks = [self._padded(m[n0 * self.per_node:n1 * self.per_node], n0, n1) for n0, n1 in self.nodes]
+        part = self._reduce_scatter(torch.cat(blocks))
+        return part[:(self.node1 - self.node0) * self.per_node]
+
+    def __call__(self, u_b):
+        u = self.gather(u_b)
+        m = self.ops.partial_moments(u)
+        m_b = self.scatter_sum(m)
+        return self.ops.apply_with_moments_nodes(u_b, m_b.contiguous(), self.node0, self.node1)
+
+
 def sharded_gmres(op: ShardedOperator, b_local, rel_tol: float = 1e-12, max_iter: int = 1000, restart: int = None):
     """GMRES on direction-sharded vectors (R/krylov.py:56-158 control flow: x0 = 0, Givens least
     squares, restart, breakdown below 1e-14 ||b||, 10 rel_tol true-residual guard).  Every rank

@@ -132,3 +132,69 @@ def test_direction_cost_uses_the_oracle_geometry():
         d = OL.desc_from_lattice_problem(p)
         n_sub = np.array([OL.direction_geometry(d, a)[3] for a in range(p.n_dirs)])
         np.testing.assert_array_equal(lattice_direction_cost(p), n_sub + 1)
+
+
+class OracleLatticeSpaceOps(OracleLatticeShardOps):
+    def apply_with_moments_nodes(self, u_b, m_b, node0, node1):
+        import torch
+
+        d = self.d
+        nodes = node1 - node0
+        Rm = self.OL.redistribute(d, np.asarray(m_b, dtype=float).reshape(nodes, d.n_mom, d.n_freq))
+        return torch.from_numpy(np.asarray(u_b, dtype=float) - Rm.reshape(-1))
+
+
+def _space_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    from oracle import lattice as OL
+    from paper_2602_21958_b200.sharding import LatticeSpaceShardedOperator, sharded_gmres
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    p = _problem()
+    op = LatticeSpaceShardedOperator(p, ops_factory=OracleLatticeSpaceOps)
+    u = torch.from_numpy(np.random.default_rng(3).standard_normal(p.n_total))
+    y_b = op(op.local_slice(u))
+    d = OL.desc_from_lattice_problem(p)
+    b = torch.from_numpy(OL.build_rhs(d, "moments"))
+    x_b, its, conv, hist, tr = sharded_gmres(op, op.local_slice(b).clone(), rel_tol=1e-9, max_iter=300)
+    q.put((rank, (op.node0, op.node1), y_b.numpy().tolist(), its, x_b.numpy().tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world", [2, 3])
+def test_space_sharded_ranks_reproduce_the_operator_and_gmres(world):
+    """Krylov vectors sharded by layers (all-gather u, direction-block transfer, reduce-scatter of
+    the moments by space, finish on the rank's layers): the blocks of all ranks form apply_A, and
+    sharded_gmres on the blocks takes the single-process GMRES path (3 ranks: uneven blocks)."""
+    from oracle import lattice as OL
+    from oracle import rt_oracle as ro
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30100 + world * 37 + os.getpid() % 800
+    procs = [ctx.Process(target=_space_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = sorted(q.get(timeout=280) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=30)
+    assert all(pr.exitcode == 0 for pr in procs)
+    p = _problem()
+    d = OL.desc_from_lattice_problem(p)
+    u = np.random.default_rng(3).standard_normal(p.n_total)
+    ref = OL.apply_A_moments(d, u)
+    y = np.concatenate([np.asarray(o[2]) for o in out])
+    assert [o[1] for o in out][0][0] == 0 and out[-1][1][1] == p.n_space
+    assert np.linalg.norm(y - ref) <= 1e-13 * np.linalg.norm(ref)
+    b = OL.build_rhs(d, "moments")
+    single = ro.gmres(lambda v: OL.apply_A_moments(d, v), b, rel_tol=1e-9, max_iter=300)
+    assert len({o[3] for o in out}) == 1 and abs(out[0][3] - single.iterations) <= 1
+    x = np.concatenate([np.asarray(o[4]) for o in out])
+    sol = np.asarray(single.solution)
+    assert np.linalg.norm(x - sol) <= 1e-7 * np.linalg.norm(sol)
