@@ -57,6 +57,7 @@ Problem::~Problem() {
     }
     if (tma_ctas) cudaFree(tma_ctas);
     if (dtpad) cudaFree(dtpad);
+    if (par_tab) cudaFree(par_tab);
     if (lat_dirs) cudaFree(lat_dirs);
     if (mom_ctas) cudaFree(mom_ctas);
     if (mom_partial) cudaFree(mom_partial);

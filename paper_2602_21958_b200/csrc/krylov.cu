@@ -310,8 +310,32 @@ __global__ void scale_kernel(const double* __restrict__ x, double* __restrict__ 
     const double s = norm2 ? sqrt(*norm2) : a;
     const double r = s != 0.0 ? 1.0 / s : 0.0;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride)
-        y[e] = s != 0.0 ? x[e] / s : x[e] * r;
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    // 16-byte accesses, four in flight per thread (one 8-byte load per iteration left the
+    // kernel latency-bound at 4.3 TB/s in ncu); the division keeps numpy's v = w / h bits
+    const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
+    const int64_t n2 = vec ? n / 2 : 0;
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    double2* y2 = reinterpret_cast<double2*>(y);
+    int64_t e = tid;
+    for (; e + 3 * stride < n2; e += 4 * stride) {
+        double2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldcs(x2 + e + u * stride);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            v[u].x = s != 0.0 ? v[u].x / s : v[u].x * r;
+            v[u].y = s != 0.0 ? v[u].y / s : v[u].y * r;
+            y2[e + u * stride] = v[u];
+        }
+    }
+    for (; e < n2; e += stride) {
+        double2 v = x2[e];
+        v.x = s != 0.0 ? v.x / s : v.x * r;
+        v.y = s != 0.0 ? v.y / s : v.y * r;
+        y2[e] = v;
+    }
+    for (int64_t k = 2 * n2 + tid; k < n; k += stride) y[k] = s != 0.0 ? x[k] / s : x[k] * r;
 }
 
 // out = base + sum_k y_k V_k  (the reference's _combine, R/krylov.py:173-177, added to x)

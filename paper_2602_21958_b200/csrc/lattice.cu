@@ -322,7 +322,8 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
 }
 
 template <int FS, int SRC, int OUT, bool DT, bool PLANAR>
-__global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A, int with_inflow, int max_sub) {
+__global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A, int with_inflow, int max_sub,
+                                                                       int fchunk_slack) {
     extern __shared__ __align__(16) double sm[];
     const int nxy = static_cast<int>(A.nxy);
     constexpr bool XM = (OUT == OUT_X_MINUS);
@@ -334,16 +335,23 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
     double* xplane = cplane + RING * nxy;       // [2][nxy][kFC]   (XM only)
     double* seeds = xplane + 2 * nxy * kFC;     // [nxy][kFC] SC restart values
     Shift* shs = reinterpret_cast<Shift*>(seeds + nxy * kFC);   // [max_sub + 1] shifts of the step
-    const int nfc = (A.n_freq + kFC - 1) / kFC;
+    // Frequency chunks are cut at 32-byte sectors of the [node][direction][frequency] vectors:
+    // with (n_dirs n_freq) % 4 == 0 the row of (node, direction a) starts (a n_freq) % 4
+    // doubles past a sector boundary for every node, so the chunks of direction a start at
+    // f0 = 4 j - (a n_freq) % 4 (the first and last ones partial) and each chunk's 4 doubles
+    // are exactly one sector of src, x and y (an odd N_nu otherwise makes 3 of 4 directions
+    // straddle two sectors per chunk: measured 1.85x the algorithmic DRAM traffic at cfg3).
+    const int nfc = (A.n_freq + fchunk_slack + kFC - 1) / kFC;
     const int a = blockIdx.x / nfc;
-    const int f0 = (blockIdx.x % nfc) * kFC;
-    const int nq = min(kFC, A.n_freq - f0);     // valid frequencies of this chunk
+    const int f0 = (blockIdx.x % nfc) * kFC - (fchunk_slack ? (a * A.n_freq) % kFC : 0);
+    const int qlo = max(0, -f0), qhi = min(kFC, A.n_freq - f0);   // valid frequencies: f0 + [qlo, qhi)
+    if (qhi <= qlo) return;
     const LatDir D = A.dirs[a];
     double phi[kFC], inflow[kFC];
 #pragma unroll
     for (int q = 0; q < kFC; ++q) {
         const int f = f0 + q;
-        const bool fv = f < A.n_freq;
+        const bool fv = f >= 0 && f < A.n_freq;
         phi[q] = fv ? A.phi[f] : 0.0;
         const double* in = D.down ? A.inflow_top : A.inflow_bottom;
         inflow[q] = (with_inflow && fv && in) ? in[f] : 0.0;
@@ -356,7 +364,7 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
         double* cp = cplane + r * nxy;
         for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) {
             const int c = e / kFC, q = e - c * kFC;
-            if (q < nq) {
+            if (q >= qlo && q < qhi) {
                 if (SRC == LSRC_VEC) cp_async8(sp + pidx(c, q, nxy), A.src + ((base + c) * A.n_dirs + a) * A.n_freq + f0 + q);
                 else cp_async8(sp + pidx(c, q, nxy), A.src + (base + c) * A.n_freq + f0 + q);
             } else {
@@ -372,7 +380,7 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
         double* xp = xplane + r * nxy * kFC;
         for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) {
             const int c = e / kFC, q = e - c * kFC;
-            if (q < nq) cp_async8(xp + pidx(c, q, nxy), A.x + ((base + c) * A.n_dirs + a) * A.n_freq + f0 + q);
+            if (q >= qlo && q < qhi) cp_async8(xp + pidx(c, q, nxy), A.x + ((base + c) * A.n_dirs + a) * A.n_freq + f0 + q);
         }
     };
     auto commit = []() { asm volatile("cp.async.commit_group;\n" ::); };
@@ -388,6 +396,17 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
     commit();
     if (PAR && A.nz > 2) issue_planes(layer_of(2), 2);
     if (PAR) commit();
+    static_assert(kIntThreads % kFC == 0, "a thread keeps its frequency across gather iterations");
+    const int gj0 = (static_cast<int>(threadIdx.x) / kFC) / A.nx, gi0 = static_cast<int>(threadIdx.x) / kFC - gj0 * A.nx;
+    int gnbx, gnby;
+    double gnax, gnay;
+    {
+        const Shift g0 = A.gat_shift[a * A.nz];
+        gnbx = g0.bx;
+        gnby = g0.by;
+        gnax = g0.ax;
+        gnay = g0.ay;
+    }
     for (int t = 0; t < A.nz; ++t) {
         const int k = layer_of(t);
         // groups committed so far: t + 2 (steps 0..t+1); step t needs groups 0..t+1 (planes t and
@@ -398,16 +417,42 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
         if (t + RING - 1 < A.nz) issue_planes(layer_of(t + RING - 1), (t + RING - 1) % RING);
         if (t + 1 < A.nz && t > 0) issue_x(layer_of(t + 1), (t + 1) & 1);
         commit();
-        // T_RC gather: one thread per (node, frequency) for coalesced y writes
-        const Shift gsh = A.gat_shift[a * A.nz + t];
+        // next step's sub-segment paths of this thread's lines into L1 (the march reads them one
+        // sub-node ahead only, which left their L2 latency exposed)
+        if (DT && t + 2 < A.nz) {
+            const double* dn = A.dtab + D.dtab_off + static_cast<int64_t>(t + 1) * D.n_sub * A.nxy;
+            for (int c = threadIdx.x; c < nxy; c += blockDim.x)
+                for (int m = 0; m < D.n_sub; ++m)
+                    asm volatile("prefetch.global.L1 [%0];\n" ::"l"(dn + static_cast<int64_t>(m) * A.nxy + c));
+        }
+        // T_RC gather: one thread per (node, frequency) for coalesced y writes; the node's (i, j)
+        // advance incrementally (blockDim.x / kFC nodes per iteration) instead of by division
+        Shift gsh;
+        gsh.bx = gnbx;
+        gsh.by = gnby;
+        gsh.ax = gnax;
+        gsh.ay = gnay;
+        if (t + 1 < A.nz) {
+            const Shift* gn = A.gat_shift + a * A.nz + t + 1;
+            gnbx = gn->bx;
+            gnby = gn->by;
+            gnax = gn->ax;
+            gnay = gn->ay;
+        }
         const double* xp = xplane + (t & 1) * nxy * kFC;
+        int gi = gi0, gj = gj0;
         for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) {
             const int c = e / kFC, q = e - c * kFC;
-            const int j = c / A.nx, i = c - j * A.nx;
+            const int j = gj, i = gi;
+            gi += kIntThreads / kFC;
+            while (gi >= A.nx) {
+                gi -= A.nx;
+                ++gj;
+            }
             const Stencil st = stencil_at(i, j, gsh, A.nx, A.ny);
             const double v = st.w00 * lines[pidx(st.c00, q, nxy)] + st.w10 * lines[pidx(st.c10, q, nxy)] +
                              st.w01 * lines[pidx(st.c01, q, nxy)] + st.w11 * lines[pidx(st.c11, q, nxy)];
-            if (q < nq) {
+            if (q >= qlo && q < qhi) {
                 const int64_t idx = ((static_cast<int64_t>(k) * A.nxy + c) * A.n_dirs + a) * A.n_freq + f0 + q;
                 A.y[idx] = XM ? xp[pidx(c, q, nxy)] - v : v;
             }
@@ -977,6 +1022,78 @@ __global__ void __launch_bounds__(256) lattice_splane_kernel(LatArgs A, int t, d
     }
 }
 
+// Pair-major source planes for the tiled moment kernel: thread = (frequency pair, node), node
+// fastest, so each direction's plane is written with one coalesced 16-byte store per thread
+// (the generic kernel above: 8-byte stores and ~60 instructions per value).  The per-direction
+// coefficients c_l Y_l(a) and the hemisphere flags sit in shared memory; the node's moments
+// (both frequencies of the pair) are loaded once per hemisphere and reused by its directions.
+// Same arithmetic as lattice_splane_kernel (v = (sum_l cy_l u_l) gamma in l order).
+template <int SRC, int NM>
+__global__ void __launch_bounds__(256) lattice_splane_pm_kernel(LatArgs A, int t, double2* __restrict__ plane0,
+                                                                 double2* __restrict__ plane1,
+                                                                 double2* __restrict__ plane2, int fill_mask, int fp) {
+    extern __shared__ __align__(16) double spm[];
+    const int nd = A.a1 - A.a0;
+    double* cys = spm;                                         // [nd][NM]
+    int* downs = reinterpret_cast<int*>(cys + nd * NM);        // [nd]
+    for (int e = threadIdx.x; e < nd * NM; e += blockDim.x) cys[e] = A.dirs[A.a0 + e / NM].cy[e % NM];
+    for (int e = threadIdx.x; e < nd; e += blockDim.x) downs[e] = A.dirs[A.a0 + e].down;
+    __syncthreads();
+    const int hp = fp >> 1;
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (tid >= A.nxy * hp) return;
+    const int pr = static_cast<int>(tid / A.nxy);
+    const int64_t c = tid - pr * A.nxy;
+    const int f0 = 2 * pr, f1 = 2 * pr + 1;
+    const bool v0 = f0 < A.n_freq, v1 = f1 < A.n_freq;
+    const int64_t plane = A.nxy * hp;   // double2 per direction
+    double2* planes[3] = {plane0, plane1, plane2};
+    for (int o = 0; o < 3; ++o) {
+        if (!((fill_mask >> o) & 1)) continue;
+        double2* out = planes[o] + pr * A.nxy + c;
+        for (int hm = 0; hm < 2; ++hm) {
+            const int layer = hm ? A.nz - 1 - t - o : t + o;
+            if (layer < 0 || layer >= A.nz) continue;
+            const int64_t sidx = static_cast<int64_t>(layer) * A.nxy + c;
+            double u0[NM], u1[NM], g0, g1;
+            if (SRC == LSRC_U) {
+#pragma unroll
+                for (int l = 0; l < NM; ++l) {
+                    const double* up = A.src + (sidx * NM + l) * A.n_freq;
+                    u0[l] = v0 ? __ldg(up + f0) : 0.0;
+                    u1[l] = v1 ? __ldg(up + f1) : 0.0;
+                }
+                g0 = v0 ? __ldg(A.gamma + sidx * A.n_freq + f0) : 0.0;
+                g1 = v1 ? __ldg(A.gamma + sidx * A.n_freq + f1) : 0.0;
+            } else {
+                g0 = v0 ? __ldg(A.src + sidx * A.n_freq + f0) : 0.0;
+                g1 = v1 ? __ldg(A.src + sidx * A.n_freq + f1) : 0.0;
+            }
+#pragma unroll 4
+            for (int i = 0; i < nd; ++i) {
+                if ((downs[i] != 0) != (hm == 0)) continue;
+                double s0, s1;
+                if (SRC == LSRC_U) {
+                    const double* cy = cys + i * NM;
+                    s0 = 0.0;
+                    s1 = 0.0;
+#pragma unroll
+                    for (int l = 0; l < NM; ++l) {
+                        s0 = fma(cy[l], u0[l], s0);
+                        s1 = fma(cy[l], u1[l], s1);
+                    }
+                    s0 *= g0;
+                    s1 *= g1;
+                } else {
+                    s0 = g0;
+                    s1 = g1;
+                }
+                out[(A.a0 + i) * plane] = make_double2(v0 ? s0 : 0.0, v1 ? s1 : 0.0);
+            }
+        }
+    }
+}
+
 // ---------------- moment layout, tiled: one CTA per (tile of lines, frequency pair) ----------------
 //
 // lattice_mom_tile_kernel (IE / exp-linear).  Every line of a direction samples the source at
@@ -997,9 +1114,14 @@ struct TileHdr {
 };
 struct TileSub {
     int dx, dy;           // sub-node offset within the window (unwrapped)
-    int pad0, pad1;
-    double w00, w10, w01, w11;   // bilinear weights (same arithmetic as stencil_at)
+    // trilinear weights of the eight corners: plane a (the step's start layer) carries
+    // (1 - wz) w_xy, plane b wz w_xy, with w_xy the bilinear weights of stencil_at and
+    // wz = m / n_sub (folded on the host: 8 FMAs per sample and frequency instead of 11)
+    double a00, a10, a01, a11, b00, b10, b01, b11;
+    double pad;
 };
+static_assert(sizeof(TileSub) == 80, "TileSub is staged as five 16-byte words");
+constexpr int kTileSubW = sizeof(TileSub) / 16;
 
 struct TileArgs {
     const TileHdr* hdr;     // [dir][step]
@@ -1057,7 +1179,7 @@ __global__ void __launch_bounds__(TX * TY, TX * TY >= 256 ? RTK_TILE_MINB : 2 * 
     // [TileDir x n_mine][stage 0: window a, window b, sub table][stage 1: ...]
     TileDir* tdir = reinterpret_cast<TileDir*>(tsm);
     double2* stages = tsm + (n_mine * sizeof(TileDir) + 15) / 16;
-    const int stage_d2 = 2 * T.region_cap + T.sub_cap * 3;   // TileSub = 48 B = 3 double2
+    const int stage_d2 = 2 * T.region_cap + T.sub_cap * kTileSubW;
     for (int e = threadIdx.x; e < n_mine; e += NT) {
         const int a = T.order[z + e * T.dgz];
         const LatDir& D = A.dirs[a];
@@ -1117,7 +1239,7 @@ __global__ void __launch_bounds__(TX * TY, TX * TY >= 256 ? RTK_TILE_MINB : 2 * 
         const int n_sub1 = D.n_sub + 1;
         const double2* src = reinterpret_cast<const double2*>(T.sub + D.shift_off + static_cast<int64_t>(t) * n_sub1);
         double2* dst = wa + 2 * T.region_cap;
-        for (int e = threadIdx.x; e < 3 * n_sub1; e += NT) cp_async16(dst + e, src + e);
+        for (int e = threadIdx.x; e < kTileSubW * n_sub1; e += NT) cp_async16(dst + e, src + e);
     };
 
     // global operands of a direction, loaded one direction ahead into registers: the T_RC
@@ -1139,7 +1261,12 @@ __global__ void __launch_bounds__(TX * TY, TX * TY >= 256 ? RTK_TILE_MINB : 2 * 
         P.g11 = lin[sg.c11];
         if (!march) return;
         if (!D.sc) P.s00 = lin[c];
-        P.dt0 = __ldg(A.dtab + D.dtab + c);
+        const double* dtl = A.dtab + D.dtab + c;
+        P.dt0 = __ldg(dtl);
+        // the direction's remaining sub-segment paths into L1 (the march reads one per sub-node;
+        // loaded only one sub-node ahead they were the kernel's largest stall: 24% of samples)
+        for (int m = 1; m < D.n_sub; ++m)
+            asm volatile("prefetch.global.L1 [%0];\n" ::"l"(dtl + static_cast<int64_t>(m) * A.nxy));
     };
 
     if (march && n_mine > 0) stage(0, 0);
@@ -1207,9 +1334,11 @@ __global__ void __launch_bounds__(TX * TY, TX * TY >= 256 ? RTK_TILE_MINB : 2 * 
                 v0 = hm == 0 ? in_top[0] : in_bot[0];
                 v1 = hm == 0 ? in_top[1] : in_bot[1];
             } else {
-                const Stencil sg = stencil_at(lx, ly, D.gat, A.nx, A.ny);
-                v0 = sg.w00 * cur.g00.x + sg.w10 * cur.g10.x + sg.w01 * cur.g01.x + sg.w11 * cur.g11.x;
-                v1 = sg.w00 * cur.g00.y + sg.w10 * cur.g10.y + sg.w01 * cur.g01.y + sg.w11 * cur.g11.y;
+                // T_RC weights (the corner values were loaded one direction ahead by prefetch)
+                const double gax = D.gat.ax, gay = D.gat.ay;
+                const double w00 = (1 - gax) * (1 - gay), w10 = gax * (1 - gay), w01 = (1 - gax) * gay, w11 = gax * gay;
+                v0 = w00 * cur.g00.x + w10 * cur.g10.x + w01 * cur.g01.x + w11 * cur.g11.x;
+                v1 = w00 * cur.g00.y + w10 * cur.g10.y + w01 * cur.g01.y + w11 * cur.g11.y;
             }
 #pragma unroll
             for (int l = 0; l < NM; ++l) {
@@ -1238,7 +1367,6 @@ __global__ void __launch_bounds__(TX * TY, TX * TY >= 256 ? RTK_TILE_MINB : 2 * 
                 const TileSub* sb = reinterpret_cast<const TileSub*>(wa + 2 * T.region_cap);
                 const double* dtl = A.dtab + D.dtab + c;
                 const int n_sub = D.n_sub;
-                const double inv_n = 1.0 / n_sub;
                 double ps0 = 0.0, ps1 = 0.0;
                 double dt_next = t == 0 ? __ldg(dtl) : cur.dt0;
                 for (int m = (FS == RTK_FS_IE ? 1 : 0); m <= n_sub; ++m) {
@@ -1246,11 +1374,10 @@ __global__ void __launch_bounds__(TX * TY, TX * TY >= 256 ? RTK_TILE_MINB : 2 * 
                     const int o = (lly + S.dy) * w + llx + S.dx;
                     const double2 a00 = wa[o], a10 = wa[o + 1], a01 = wa[o + w], a11 = wa[o + w + 1];
                     const double2 b00 = wb[o], b10 = wb[o + 1], b01 = wb[o + w], b11 = wb[o + w + 1];
-                    const double wz = m * inv_n;
-                    const double s0 = (1 - wz) * (S.w00 * a00.x + S.w10 * a10.x + S.w01 * a01.x + S.w11 * a11.x) +
-                                      wz * (S.w00 * b00.x + S.w10 * b10.x + S.w01 * b01.x + S.w11 * b11.x);
-                    const double s1 = (1 - wz) * (S.w00 * a00.y + S.w10 * a10.y + S.w01 * a01.y + S.w11 * a11.y) +
-                                      wz * (S.w00 * b00.y + S.w10 * b10.y + S.w01 * b01.y + S.w11 * b11.y);
+                    const double s0 = (S.a00 * a00.x + S.a10 * a10.x + S.a01 * a01.x + S.a11 * a11.x) +
+                                      (S.b00 * b00.x + S.b10 * b10.x + S.b01 * b01.x + S.b11 * b11.x);
+                    const double s1 = (S.a00 * a00.y + S.a10 * a10.y + S.a01 * a01.y + S.a11 * a11.y) +
+                                      (S.b00 * b00.y + S.b10 * b10.y + S.b01 * b01.y + S.b11 * b11.y);
                     if (m > 0) {
                         const double dt = dt_next;
                         if (m < n_sub) dt_next = __ldg(dtl + static_cast<int64_t>(m) * A.nxy);   // one ahead
@@ -1344,12 +1471,18 @@ static int setup_tile_tables(Problem& p, const rtk_lattice_desc* d, const std::v
                 TileSub& S = sub[D.shift_off + static_cast<size_t>(t) * (D.n_sub + 1) + m];
                 S.dx = static_cast<int>(fxs[m]) - fxmin;
                 S.dy = static_cast<int>(fys[m]) - fymin;
-                S.pad0 = S.pad1 = 0;
+                S.pad = 0.0;
                 const double ax = oxs[m] - fxs[m], ay = oys[m] - fys[m];
-                S.w00 = (1 - ax) * (1 - ay);
-                S.w10 = ax * (1 - ay);
-                S.w01 = (1 - ax) * ay;
-                S.w11 = ax * ay;
+                const double w00 = (1 - ax) * (1 - ay), w10 = ax * (1 - ay), w01 = (1 - ax) * ay, w11 = ax * ay;
+                const double wz = m * (1.0 / D.n_sub);
+                S.a00 = (1 - wz) * w00;
+                S.a10 = (1 - wz) * w10;
+                S.a01 = (1 - wz) * w01;
+                S.a11 = (1 - wz) * w11;
+                S.b00 = wz * w00;
+                S.b10 = wz * w10;
+                S.b01 = wz * w01;
+                S.b11 = wz * w11;
             }
         }
     }
@@ -1503,8 +1636,15 @@ static int launch_int(const Problem& p, const LatArgs& A, int with_inflow, cudaS
                        : (planar ? lattice_int_smem_kernel<FS, SRC, OUT, false, true>
                                  : lattice_int_smem_kernel<FS, SRC, OUT, false, false>);
         if (int rc = ensure_smem_for(kern, smem_planes)) return rc;
-        const int nfc = (A.n_freq + kFC - 1) / kFC;
-        kern<<<A.n_dirs * nfc, kIntThreads, smem_planes, s>>>(A, with_inflow, p.lat_max_sub);
+        // sector-aligned frequency chunks (see the kernel) when every (node, direction) row
+        // has the same offset within a 32-byte sector
+        const bool aligned_rows = (static_cast<int64_t>(A.n_dirs) * A.n_freq) % kFC == 0 && A.n_freq % kFC != 0 &&
+                                  (SRC != LSRC_VEC || reinterpret_cast<uintptr_t>(A.src) % 32 == 0) &&
+                                  (A.y == nullptr || reinterpret_cast<uintptr_t>(A.y) % 32 == 0) &&
+                                  (A.x == nullptr || reinterpret_cast<uintptr_t>(A.x) % 32 == 0);
+        const int slack = aligned_rows ? kFC - 1 : 0;
+        const int nfc = (A.n_freq + slack + kFC - 1) / kFC;
+        kern<<<A.n_dirs * nfc, kIntThreads, smem_planes, s>>>(A, with_inflow, p.lat_max_sub, slack);
         RTK_LAUNCH_CHECK("lattice_int_smem_kernel");
         return RTK_OK;
     }
@@ -1608,7 +1748,7 @@ static int launch_mom_tiles_t(const Problem& p, const LatArgs& A, bool with_infl
         dgz = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, (148 * 6 + ctas - 1) / ctas)));
     }
     dgz = std::max(1, std::min(dgz, std::max(1, n_order)));
-    const size_t stage_d2 = 2 * static_cast<size_t>(p.lat_region_cap) + 3 * static_cast<size_t>(p.lat_sub_cap);
+    const size_t stage_d2 = 2 * static_cast<size_t>(p.lat_region_cap) + kTileSubW * static_cast<size_t>(p.lat_sub_cap);
     const int per_cta = (n_order + dgz - 1) / dgz;
     const size_t smem = 2 * stage_d2 * sizeof(double2) + (per_cta * sizeof(TileDir) + 15) / 16 * 16;
     if (smem > 110 * 1024) return -1;   // very grazing directions on large tiles: per-item kernel
@@ -1636,7 +1776,8 @@ static int launch_mom_tiles_t(const Problem& p, const LatArgs& A, bool with_infl
     }
     auto kern = lattice_mom_tile_kernel<FS, NM, TX, TY>;
     if (int rc = ensure_smem_for(kern, smem)) return rc;
-    const unsigned pblocks = static_cast<unsigned>((A.nxy * p.fp + 255) / 256);
+    const unsigned pmblocks = static_cast<unsigned>((A.nxy * hp + 255) / 256);
+    const size_t pm_smem = static_cast<size_t>(A.a1 - A.a0) * (NM * sizeof(double) + sizeof(int));
     double2* a = reinterpret_cast<double2*>(p.lat_state[0]);
     double2* b = reinterpret_cast<double2*>(p.lat_state[1]);
     const dim3 grid(static_cast<unsigned>(ntiles), static_cast<unsigned>(hp), static_cast<unsigned>(dgz));
@@ -1644,8 +1785,9 @@ static int launch_mom_tiles_t(const Problem& p, const LatArgs& A, bool with_infl
         double* cur = p.lat_splane[t % 2];
         double* nxt = p.lat_splane[(t + 1) % 2];
         if (t < A.nz - 1) {
-            lattice_splane_kernel<SRC, NM, true><<<pblocks, 256, 0, s>>>(A, t, cur, nxt, nullptr, t == 0 ? 3 : 2, p.fp);
-            RTK_LAUNCH_CHECK("lattice_splane_kernel");
+            lattice_splane_pm_kernel<SRC, NM><<<pmblocks, 256, pm_smem, s>>>(
+                A, t, reinterpret_cast<double2*>(cur), reinterpret_cast<double2*>(nxt), nullptr, t == 0 ? 3 : 2, p.fp);
+            RTK_LAUNCH_CHECK("lattice_splane_pm_kernel");
         }
         kern<<<grid, TX * TY, smem, s>>>(A, T, t, a, b, mom, with_inflow ? 1 : 0, p.fp,
                                          reinterpret_cast<const double2*>(cur), reinterpret_cast<const double2*>(nxt));

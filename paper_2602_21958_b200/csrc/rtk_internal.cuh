@@ -135,6 +135,7 @@ struct Problem {
     int tma_n_ctas = 0, tma_gw = 0, tma_u = 4;
     TmaCta* tma_ctas = nullptr;
     double* dtpad = nullptr;
+    double* par_tab = nullptr;                   // exp-parabolic Lagrange denominators (4 padded tables, sweep_tma.cu)
     // lattice (multi-D) state
     int lat_nx = 0, lat_ny = 0, lat_nz = 0;
     LatDir* lat_dirs = nullptr;
@@ -169,6 +170,7 @@ struct Problem {
     mutable double* lat_scratch = nullptr;       // per-group partial moments (direction groups > 1)
     mutable size_t lat_scratch_count = 0;
     CUtensorMap tma_gmap, tma_dtmap;
+    CUtensorMap tma_qmap[4];                     // par_tab: [down: qc, qd | up: qc, qd]
     ~Problem();
 };
 

@@ -108,7 +108,8 @@ struct Layout {
     __host__ __device__ static int g_bytes(int gw) { return round128(U * NM * gw * 8); }
     static constexpr int kDtW = U + 2;
     static constexpr int kDt = round128(kDtW * 8);
-    __host__ __device__ static int stage_bytes(int gw) { return kX + g_bytes(gw) + kDt; }
+    // the exp-parabolic stage carries two more dt-shaped rows (qc, qd of the hemisphere)
+    __host__ __device__ static int stage_bytes(int gw, bool par = false) { return kX + g_bytes(gw) + (par ? 3 : 1) * kDt; }
 };
 
 struct SweepState {
@@ -119,7 +120,7 @@ struct SweepState {
 template <int NM>
 struct ConsumerCtx {
     int xoff, gcol, gw;
-    double phi_f, inv_mu;
+    double phi_f, inv_mu, rc2;   // rc2 = 1 / (phi_f inv_mu)^2 (exp-parabolic tables)
     bool valid;
     double yk[NM];
 };
@@ -177,17 +178,20 @@ struct ParState {
 
 template <int NM, int U, bool DOWN, bool CHECK>
 __device__ __forceinline__ void consume_par(const ConsumerCtx<NM>& c, ParState& st, const double* __restrict__ xs,
-                                            const double* __restrict__ gs, const double* __restrict__ dts, int q,
+                                            const double* __restrict__ gs, const double* __restrict__ dts,
+                                            const double* __restrict__ qcs, const double* __restrict__ qds, int q,
                                             int64_t n, int64_t step) {
     const double* gcol = gs + c.gcol;
     // optical depths of the segments into each step's node, then the stage's weights
-    // (update at step uu uses the segments into nodes j-1 and j)
+    // (update at step uu uses the segments into nodes j-1 and j; qcs / qds hold the Lagrange
+    // denominators of that segment pair at the position of the segment into node j)
     double din[U], w0[U], w1[U], w2[U], w3[U];
 #pragma unroll
     for (int uu = 0; uu < U; ++uu) din[uu] = c.phi_f * dts[DOWN ? uu : U - 1 - uu] * c.inv_mu;
 #pragma unroll
     for (int uu = 0; uu < U; ++uu) {
-        const ExpPar w = exp_parabolic_weights_bf(uu == 0 ? st.d_m2 : din[uu - 1], din[uu]);
+        const int u = DOWN ? uu : U - 1 - uu;
+        const ExpPar w = exp_parabolic_weights_tab(uu == 0 ? st.d_m2 : din[uu - 1], din[uu], c.rc2, qcs[u], qds[u]);
         w0[uu] = w.att;
         w1[uu] = w.wu;
         w2[uu] = w.wc;
@@ -225,13 +229,18 @@ template <int FS, int NM, int U, int S>
 __global__ void __launch_bounds__(kTmaThreads) sweep1d_tma_kernel(const __grid_constant__ CUtensorMap xmap,
                                                                   const __grid_constant__ CUtensorMap gmap,
                                                                   const __grid_constant__ CUtensorMap dtmap,
+                                                                  const __grid_constant__ CUtensorMap qcmap_dn,
+                                                                  const __grid_constant__ CUtensorMap qdmap_dn,
+                                                                  const __grid_constant__ CUtensorMap qcmap_up,
+                                                                  const __grid_constant__ CUtensorMap qdmap_up,
                                                                   TmaArgs A) {
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + S;
     unsigned char* stages = smem + 128;
     const int gbytes = Layout<NM, U>::g_bytes(A.gw);
-    const int sbytes = Layout<NM, U>::stage_bytes(A.gw);
+    constexpr bool PAR = FS == RTK_FS_EXP_PARABOLIC;
+    const int sbytes = Layout<NM, U>::stage_bytes(A.gw, PAR);
 
     const TmaCta cta = A.ctas[blockIdx.x];
     const int tid = threadIdx.x;
@@ -258,7 +267,12 @@ __global__ void __launch_bounds__(kTmaThreads) sweep1d_tma_kernel(const __grid_c
             prefetch_tensormap(&xmap);
             prefetch_tensormap(&gmap);
             prefetch_tensormap(&dtmap);
-            const uint32_t tx = static_cast<uint32_t>(U * kXW * 8 + U * NM * A.gw * 8 + Layout<NM, U>::kDtW * 8);
+            const uint32_t tx = static_cast<uint32_t>(U * kXW * 8 + U * NM * A.gw * 8 +
+                                                      (PAR ? 3 : 1) * Layout<NM, U>::kDtW * 8);
+            if (PAR) {
+                prefetch_tensormap(down ? &qcmap_dn : &qcmap_up);
+                prefetch_tensormap(down ? &qdmap_dn : &qdmap_up);
+            }
             for (int q = 0; q < Q; ++q) {
                 const int s = q % S;
                 if (q >= S) mbar_wait(&empty[s], ((q / S) - 1) & 1);
@@ -270,6 +284,11 @@ __global__ void __launch_bounds__(kTmaThreads) sweep1d_tma_kernel(const __grid_c
                 // dt_pad[kDtPad + i] = dt[i]; down rows need dt[r0 - 1 + u], up rows dt[r0 + u]
                 const int want = (down ? r0 - 1 : r0) + kDtPad;
                 tma_load_1d(st + Layout<NM, U>::kX + gbytes, &dtmap, want & ~1, &full[s]);
+                if (PAR) {   // same box as dt: entry i of the tables belongs to segment i
+                    unsigned char* qb = st + Layout<NM, U>::kX + gbytes + Layout<NM, U>::kDt;
+                    tma_load_1d(qb, down ? &qcmap_dn : &qcmap_up, want & ~1, &full[s]);
+                    tma_load_1d(qb + Layout<NM, U>::kDt, down ? &qdmap_dn : &qdmap_up, want & ~1, &full[s]);
+                }
             }
         }
         return;
@@ -296,6 +315,7 @@ __global__ void __launch_bounds__(kTmaThreads) sweep1d_tma_kernel(const __grid_c
     c2.gw = A.gw;
     c2.phi_f = phi_f;
     c2.inv_mu = inv_mu;
+    c2.rc2 = 1.0 / ((phi_f * inv_mu) * (phi_f * inv_mu));
     c2.valid = valid;
 #pragma unroll
     for (int k = 0; k < NM; ++k) c2.yk[k] = yk[k];
@@ -312,12 +332,14 @@ __global__ void __launch_bounds__(kTmaThreads) sweep1d_tma_kernel(const __grid_c
         const int dt_off = ((down ? r0 - 1 : r0) + kDtPad) & 1;
         const bool edge = (q == 0) || (q == Q - 1);
         if (FS == RTK_FS_EXP_PARABOLIC) {
+            const double* qcs = dts + Layout<NM, U>::kDt / 8 + dt_off;
+            const double* qds = qcs + Layout<NM, U>::kDt / 8;
             if (down) {
-                if (edge) consume_par<NM, U, true, true>(c2, ps, xs, gs, dts + dt_off, q, n, step);
-                else consume_par<NM, U, true, false>(c2, ps, xs, gs, dts + dt_off, q, n, step);
+                if (edge) consume_par<NM, U, true, true>(c2, ps, xs, gs, dts + dt_off, qcs, qds, q, n, step);
+                else consume_par<NM, U, true, false>(c2, ps, xs, gs, dts + dt_off, qcs, qds, q, n, step);
             } else {
-                if (edge) consume_par<NM, U, false, true>(c2, ps, xs, gs, dts + dt_off, q, n, step);
-                else consume_par<NM, U, false, false>(c2, ps, xs, gs, dts + dt_off, q, n, step);
+                if (edge) consume_par<NM, U, false, true>(c2, ps, xs, gs, dts + dt_off, qcs, qds, q, n, step);
+                else consume_par<NM, U, false, false>(c2, ps, xs, gs, dts + dt_off, qcs, qds, q, n, step);
             }
         } else if (down) {
             if (edge) consume<FS, NM, U, true, true>(c2, st, xs, gs, dts + dt_off, q, n, step);
@@ -363,7 +385,7 @@ int launch_tma_us(const Problem& p, const double* x, double* y, cudaStream_t s) 
     A.n_angles = p.n_angles;
     A.n_freq = p.n_freq;
     A.gw = p.tma_gw;
-    const size_t smem = 128 + static_cast<size_t>(S) * Layout<NM, U>::stage_bytes(p.tma_gw);
+    const size_t smem = 128 + static_cast<size_t>(S) * Layout<NM, U>::stage_bytes(p.tma_gw, FS == RTK_FS_EXP_PARABOLIC);
     auto kern = sweep1d_tma_kernel<FS, NM, U, S>;
     if (int rc = ensure_smem_for(kern, smem)) return rc;
     cudaLaunchConfig_t cfg = {};
@@ -376,7 +398,8 @@ int launch_tma_us(const Problem& p, const double* x, double* y, cudaStream_t s) 
     cfg.stream = s;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    RTK_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, xmap, p.tma_gmap, p.tma_dtmap, A));
+    RTK_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, xmap, p.tma_gmap, p.tma_dtmap, p.tma_qmap[0], p.tma_qmap[1],
+                                    p.tma_qmap[2], p.tma_qmap[3], A));
     RTK_LAUNCH_CHECK("sweep1d_tma_kernel");
     return RTK_OK;
 }
@@ -452,6 +475,35 @@ int setup_tma(Problem& p) {
     const uint32_t db[1] = {static_cast<uint32_t>(p.tma_u + 2)};
     if (!encode_f64_map(&p.tma_gmap, p.gmom, 2, gd, gs, gb)) return set_error(RTK_ECUDA, "sweep: G tensor map");
     if (!encode_f64_map(&p.tma_dtmap, p.dtpad, 1, dd, nullptr, db)) return set_error(RTK_ECUDA, "sweep: dt tensor map");
+    {
+        // Exp-parabolic Lagrange denominators, indexed like dtpad (entry kDtPad + i = segment i,
+        // between nodes i and i + 1).  The update that finalises a node uses the segment pair
+        // around it; the table entry sits at the pair's LATER segment in march order:
+        //   down, entry i: (u, d) = (dt[i-1], dt[i]);   up, entry i: (u, d) = (dt[i+1], dt[i]);
+        //   qc = 1 / (u d),  qd = 1 / (d (u + d)).  Pairs reaching outside the slab are never
+        // used by the kernel (first update skipped, last node linear); they hold 0.
+        const int64_t nseg = p.n_space - 1;
+        const size_t len = hdt.size();
+        std::vector<double> tab(4 * len, 0.0);
+        auto dtv = [&](int64_t i) { return hdt[kDtPad + i]; };
+        for (int64_t i = 0; i < nseg; ++i) {
+            if (i >= 1) {
+                const double u = dtv(i - 1), d = dtv(i);
+                tab[0 * len + kDtPad + i] = 1.0 / (u * d);
+                tab[1 * len + kDtPad + i] = 1.0 / (d * (u + d));
+            }
+            if (i + 1 < nseg) {
+                const double u = dtv(i + 1), d = dtv(i);
+                tab[2 * len + kDtPad + i] = 1.0 / (u * d);
+                tab[3 * len + kDtPad + i] = 1.0 / (d * (u + d));
+            }
+        }
+        RTK_CUDA_TRY(cudaMalloc(&p.par_tab, sizeof(double) * tab.size()));
+        RTK_CUDA_TRY(cudaMemcpy(p.par_tab, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice));
+        for (int k = 0; k < 4; ++k)
+            if (!encode_f64_map(&p.tma_qmap[k], p.par_tab + k * len, 1, dd, nullptr, db))
+                return set_error(RTK_ECUDA, "sweep: exp-parabolic table tensor map");
+    }
     RTK_CUDA_TRY(cudaMalloc(&p.tma_ctas, sizeof(TmaCta) * ctas.size()));
     RTK_CUDA_TRY(cudaMemcpy(p.tma_ctas, ctas.data(), sizeof(TmaCta) * ctas.size(), cudaMemcpyHostToDevice));
     p.tma_n_ctas = static_cast<int>(ctas.size());
