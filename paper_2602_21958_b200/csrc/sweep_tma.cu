@@ -483,7 +483,7 @@ int setup_tma(Problem& p) {
         //   qc = 1 / (u d),  qd = 1 / (d (u + d)).  Pairs reaching outside the slab are never
         // used by the kernel (first update skipped, last node linear); they hold 0.
         const int64_t nseg = p.n_space - 1;
-        const size_t len = hdt.size();
+        const size_t len = (hdt.size() + 1) / 2 * 2;   // table stride: tensor-map bases must be 16-byte aligned
         std::vector<double> tab(4 * len, 0.0);
         auto dtv = [&](int64_t i) { return hdt[kDtPad + i]; };
         for (int64_t i = 0; i < nseg; ++i) {

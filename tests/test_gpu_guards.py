@@ -62,7 +62,8 @@ def _oracle_apply(p, v):
         return OL.apply_A(OL.desc_from_lattice_problem(p), p.layout, v)
     from oracle import rt_oracle as ro
 
-    return ro.apply_A(ro.desc_from_problem(p), v)
+    d = ro.desc_from_problem(p)
+    return ro.apply_A_moments(d, v) if p.layout == "moments" else ro.apply_A(d, v)
 
 
 def _guarded_apply(p, x):
@@ -110,6 +111,6 @@ def test_gmres_runs_are_bitwise_reproducible(orth, restart):
     cfg = P.SolveConfig(rel_tol=1e-8, max_iter=80, restart=restart, orthogonalization=orth)
     r1 = P.gmres(p, b, cfg)
     r2 = P.gmres(p, b, cfg)
-    assert r1.converged and r1.iterations == r2.iterations
+    assert r1.iterations == r2.iterations and r1.converged == r2.converged   # GMRES(7) may stop at max_iter
     assert np.array_equal(np.asarray(r1.residual_history), np.asarray(r2.residual_history))
     assert np.array_equal(np.asarray(r1.solution).view(np.int64), np.asarray(r2.solution).view(np.int64))
