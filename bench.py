@@ -73,14 +73,24 @@ def dist_setup(backend):
     return world, rank, local
 
 
-def ncu_raw(path):
-    """The `raw:` metrics line of a committed ncu summary (profiles/), as a dict, or {}."""
+def profile_path(name):
+    """profiles/r02_<name> when this round captured it, else round 1's file."""
+    for rnd in ("r02", "r01"):
+        path = os.path.join(ROOT, "profiles", f"{rnd}_{name}")
+        if os.path.exists(path):
+            return path
+    return os.path.join(ROOT, "profiles", f"r02_{name}")
+
+
+def ncu_raw(path, kernel=None):
+    """The `raw:` metrics line of a committed ncu summary (profiles/) -- the first one, or the
+    one labelled with `kernel` -- as a dict, or {}."""
     try:
         with open(path) as fh:
             for line in fh:
-                if "raw:" in line:
+                if "raw:" in line and (kernel is None or kernel in line):
                     out = {}
-                    for part in line.split("raw:")[1].split(","):
+                    for part in line.split("raw:")[1].split("]", 1)[-1].split(","):
                         if "=" in part:
                             k, v = part.strip().split("=", 1)
                             out[k] = v
@@ -109,26 +119,30 @@ def ncu_dmma_pipes(path=os.path.join(ROOT, "profiles", "r01_ncu_dmma_pipes.txt")
     return out
 
 
-def ncu_traffic(path=os.path.join(ROOT, "profiles", "r01_ncu_sweep_tma_v3.txt")):
+def sweep_traffic_source():
+    """(path, kernel label) of the committed `ncu --set full` capture of the IE sweep."""
+    r02 = os.path.join(ROOT, "profiles", "r02_ncu_cfg2_kernels.txt")
+    if os.path.exists(r02) and ncu_raw(r02, "sweep1d_tma"):
+        return r02, "sweep1d_tma"
+    return os.path.join(ROOT, "profiles", "r01_ncu_sweep_tma_v3.txt"), None
+
+
+def ncu_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum of the sweep kernel from the committed
     `ncu --set full` capture (profiles/), bytes per launch, or None."""
+    path, kernel = sweep_traffic_source()
+    vals = ncu_raw(path, kernel)
+
+    def to_bytes(v):
+        for unit, mul in (("Gbyte", 1e9), ("Mbyte", 1e6), ("Kbyte", 1e3), ("byte", 1.0)):
+            if v.endswith(unit):
+                return float(v[: -len(unit)]) * mul
+        return float(v)
+
     try:
-        with open(path) as fh:
-            for line in fh:
-                if "dram__bytes_read.sum=" in line:
-                    vals = {}
-                    for part in line.split("raw:")[1].split(","):
-                        k, v = part.strip().split("=")
-                        vals[k] = v
-                    def to_bytes(v):
-                        for unit, mul in (("Gbyte", 1e9), ("Mbyte", 1e6), ("Kbyte", 1e3), ("byte", 1.0)):
-                            if v.endswith(unit):
-                                return float(v[: -len(unit)]) * mul
-                        return float(v)
-                    return to_bytes(vals["dram__bytes_read.sum"]) + to_bytes(vals["dram__bytes_write.sum"])
-    except (OSError, KeyError, ValueError):
+        return to_bytes(vals["dram__bytes_read.sum"]) + to_bytes(vals["dram__bytes_write.sum"])
+    except (KeyError, ValueError):
         return None
-    return None
 
 
 def measured_peaks():
@@ -583,7 +597,8 @@ def run_b200(args):
     roofline = {"bound": "hbm", "kernel": "sweep1d_tma_kernel (K1: fused source expansion + IE sweep + y = x - acc)",
                 "achieved": sweep_bytes / kms[2] / 1e6, "peak": hbm, "unit": "GB/s",
                 "frac": sweep_bytes / kms[2] / 1e6 / hbm, "traffic": ncu_traffic(), "peak_source": peak_src,
-                "traffic_source": "profiles/r01_ncu_sweep_tma_v3.txt (ncu --set full, dram read+write per launch)",
+                "traffic_source": os.path.relpath(sweep_traffic_source()[0], ROOT) +
+                                  " (ncu --set full, dram read+write per launch)",
                 "algorithmic_bytes_per_launch": sweep_bytes,
                 "matvec_algorithmic_bytes": matvec_bytes,
                 "matvec_frac_hbm": matvec_bytes / (ms_per_step / 1e3) / 1e9 / hbm}
@@ -891,11 +906,12 @@ def lattice_timings(torch):
             out[f"cfg{cfg}"]["formal_solvers"] = fsd
         # the multi-D sweeps are bound by the FP64 pipe / latency, not HBM -- report the
         # transfer kernel's FP64-pipe utilisation from the committed ncu capture of this config
-        raw = ncu_raw(os.path.join(ROOT, "profiles", f"r01_ncu_lattice_cfg{cfg}.txt"))
+        src = profile_path(f"ncu_lattice_cfg{cfg}.txt")
+        raw = ncu_raw(src)
         key = "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"
         if key in raw:
             out[f"cfg{cfg}"]["transfer_kernel_fp64_pipe_frac"] = float(raw[key].rstrip("%")) / 100
-            out[f"cfg{cfg}"]["fp64_source"] = f"profiles/r01_ncu_lattice_cfg{cfg}.txt (ncu --set full, one launch)"
+            out[f"cfg{cfg}"]["fp64_source"] = f"{os.path.relpath(src, ROOT)} (ncu --set full, one launch)"
     return out
 
 

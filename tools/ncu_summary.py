@@ -33,8 +33,10 @@ def main(path, out=None):
                                                        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
                                                        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
                                                        "smsp__inst_executed.sum", "gpu__time_duration.sum")]
+        kn = h.index("Kernel Name") if "Kernel Name" in h else None
         for r in rr[2:]:
-            lines.append("  raw: " + ", ".join(f"{h[i]}={r[i]}{rr[1][i]}" for i in want))
+            label = f"[{r[kn].split('(')[0].split('::')[-1][:60]}] " if kn is not None else ""
+            lines.append(f"  raw: {label}" + ", ".join(f"{h[i]}={r[i]}{rr[1][i]}" for i in want))
     text = "\n".join(lines)
     if out:
         open(out, "w").write(f"# ncu --set full summary of {path}\n" + text + "\n")

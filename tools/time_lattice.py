@@ -18,6 +18,8 @@ def main():
     import os
     if os.environ.get("FS"):
         kw["formal_solver"] = os.environ["FS"]
+    if os.environ.get("LAYOUT"):
+        kw["layout"] = os.environ["LAYOUT"]
     if os.environ.get("CHARS"):
         kw["characteristics"] = os.environ["CHARS"]
     t0 = time.time()
