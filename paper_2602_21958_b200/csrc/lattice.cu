@@ -1154,6 +1154,10 @@ struct TileDir {
 #ifndef RTK_TILE_MINB
 #define RTK_TILE_MINB 2
 #endif
+#ifndef RTK_TILE_TX3
+#define RTK_TILE_TX3 16   // tile of lines on 3D lattices (2D slabs: 128 x 1)
+#define RTK_TILE_TY3 16
+#endif
 template <int FS, int NM, int TX, int TY>
 __global__ void __launch_bounds__(TX * TY, TX * TY >= 256 ? RTK_TILE_MINB : 2 * RTK_TILE_MINB)
     lattice_mom_tile_kernel(LatArgs A, TileArgs T, int t, const double2* __restrict__ st_in,
@@ -1432,8 +1436,8 @@ __global__ void lattice_mom_reduce_kernel(const double* __restrict__ scratch, do
 // same offsets and floor/fraction arithmetic as the Shift tables (shift_of), kept unwrapped
 // so a tile's samples index one window.
 static int setup_tile_tables(Problem& p, const rtk_lattice_desc* d, const std::vector<LatDir>& dirs) {
-    p.lat_tile_tx = d->ny > 1 ? 16 : 128;
-    p.lat_tile_ty = d->ny > 1 ? 16 : 1;
+    p.lat_tile_tx = d->ny > 1 ? RTK_TILE_TX3 : 128;
+    p.lat_tile_ty = d->ny > 1 ? RTK_TILE_TY3 : 1;
     const int nsteps = d->nz - 1;
     std::vector<TileHdr> hdr(static_cast<size_t>(d->n_dirs) * std::max(1, nsteps));
     size_t n_sub_total = 0;
@@ -1808,7 +1812,7 @@ template <int FS, int SRC, int NM>
 static int launch_mom_tiles(const Problem& p, const LatArgs& A, bool with_inflow, double* mom, cudaStream_t s) {
     if (FS == RTK_FS_EXP_PARABOLIC || p.tune.lat_no_tile || !p.lat_tile_hdr || (p.fp & 1)) return -1;
     if (p.lat_tile_ty == 1) return launch_mom_tiles_t<FS, SRC, NM, 128, 1>(p, A, with_inflow, mom, s);
-    return launch_mom_tiles_t<FS, SRC, NM, 16, 16>(p, A, with_inflow, mom, s);
+    return launch_mom_tiles_t<FS, SRC, NM, RTK_TILE_TX3, RTK_TILE_TY3>(p, A, with_inflow, mom, s);
 }
 
 template <int FS, int SRC, int NM>
