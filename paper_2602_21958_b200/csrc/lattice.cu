@@ -1745,12 +1745,13 @@ static int launch_mom_tiles_t(const Problem& p, const LatArgs& A, bool with_infl
         p.lat_order_a1 = A.a1;
     }
     const int n_order = static_cast<int>(p.h_lat_order.size());
-    // direction groups: enough CTAs for ~6 per SM (148 SMs), at most 16 and one per direction
-    // (2D slabs have few tiles: cfg3 in the moment layout is 2 tiles x 21 pairs)
+    // direction groups: enough CTAs for ~6 per SM (148 SMs), at most 8 and one per direction
+    // (16 groups measured no faster on cfg3's 2 tiles x 21 pairs: 22.7 vs 22.2 ms -- a layer step
+    // there is bound by the per-direction latency chain, not by occupancy)
     int dgz = p.tune.lat_dgz;
     if (dgz <= 0) {
         const int64_t ctas = static_cast<int64_t>(ntiles) * hp;
-        dgz = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, (148 * 6 + ctas - 1) / ctas)));
+        dgz = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, (148 * 6 + ctas - 1) / ctas)));
     }
     dgz = std::max(1, std::min(dgz, std::max(1, n_order)));
     const size_t stage_d2 = 2 * static_cast<size_t>(p.lat_region_cap) + kTileSubW * static_cast<size_t>(p.lat_sub_cap);
