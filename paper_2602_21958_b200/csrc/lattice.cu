@@ -170,8 +170,34 @@ __device__ __forceinline__ int pidx(int c, int q, int nxy) { return (q >> 1) * 2
 // step, line), stride nxy; prefetched one sub-node ahead) instead of the opacity planes.
 // PLANAR (ny = 1, the 2D slab): sy = 0, so the stencil's second row has weight exactly 0
 // and only two corners per layer are read (half the shared-memory traffic; same result).
+// Sub-node table of one (direction, layer step), built once per CTA and step from the Shift
+// table: integer shift plus the trilinear corner weights with wz = m / n_sub folded in
+// (plane a: (1 - wz) w_xy, plane b: wz w_xy), so a thread spends no division, no weight
+// products and 4 (planar) or 8 FMAs per sample and frequency.
+struct SubW {
+    int bx, by;
+    double a00, a10, a01, a11, b00, b10, b01, b11;
+};
+__device__ __forceinline__ SubW subw_of(const Shift& sh, int m, int n_sub) {
+    const double wz = static_cast<double>(m) / n_sub;
+    const double w00 = (1 - sh.ax) * (1 - sh.ay), w10 = sh.ax * (1 - sh.ay), w01 = (1 - sh.ax) * sh.ay,
+                 w11 = sh.ax * sh.ay;
+    SubW w;
+    w.bx = sh.bx;
+    w.by = sh.by;
+    w.a00 = (1 - wz) * w00;
+    w.a10 = (1 - wz) * w10;
+    w.a01 = (1 - wz) * w01;
+    w.a11 = (1 - wz) * w11;
+    w.b00 = wz * w00;
+    w.b10 = wz * w10;
+    w.b01 = wz * w01;
+    w.b11 = wz * w11;
+    return w;
+}
+
 template <int FS, bool DT, bool PLANAR>
-__device__ __forceinline__ void advance_line_smem4(const LatDir& D, const Shift* __restrict__ sub,
+__device__ __forceinline__ void advance_line_smem4(const LatDir& D, const SubW* __restrict__ sub,
                                                    double (&acc)[kFC], int lx, int ly, int t, int nx, int ny,
                                                    const double* chi_a, const double* chi_b,
                                                    const double* Sa, const double* Sb, const double (&phi)[kFC],
@@ -180,10 +206,26 @@ __device__ __forceinline__ void advance_line_smem4(const LatDir& D, const Shift*
 #pragma unroll
     for (int q = 0; q < kFC; ++q) prev_s[q] = 0.0;
     double dt_next = DT ? __ldg(dtl) : 0.0;
-    for (int m = 0; m <= D.n_sub; ++m) {
-        const double wz = static_cast<double>(m) / D.n_sub;
-        const Shift sh = sub[m];   // warp-uniform, precomputed at setup (same arithmetic as shift_of)
-        const Stencil st = stencil_at(lx, ly, sh, nx, ny);
+    // IE with tabulated dt needs no sample at the step's first point (its source enters only
+    // the exponential solvers' upwind term, its opacity only the on-the-fly dt)
+    for (int m = (FS == RTK_FS_IE && DT) ? 1 : 0; m <= D.n_sub; ++m) {
+        const SubW W = sub[m];   // warp-uniform
+        int i0 = lx + W.bx;
+        if (i0 >= nx) i0 -= nx;
+        const int i1 = (i0 + 1 == nx) ? 0 : i0 + 1;
+        int c00, c10, c01 = 0, c11 = 0;
+        if (PLANAR) {
+            c00 = i0;
+            c10 = i1;
+        } else {
+            int j0 = ly + W.by;
+            if (j0 >= ny) j0 -= ny;
+            const int j1 = (j0 + 1 == ny) ? 0 : j0 + 1;
+            c00 = j0 * nx + i0;
+            c10 = j0 * nx + i1;
+            c01 = j1 * nx + i0;
+            c11 = j1 * nx + i1;
+        }
         double dt = 0.0, c_m = 0.0;
         if (DT) {
             if (m > 0) {
@@ -191,37 +233,27 @@ __device__ __forceinline__ void advance_line_smem4(const LatDir& D, const Shift*
                 if (m < D.n_sub) dt_next = __ldg(dtl + static_cast<int64_t>(m) * nxy);
             }
         } else {
-            const double ca = PLANAR ? st.w00 * chi_a[st.c00] + st.w10 * chi_a[st.c10]
-                                     : st.w00 * chi_a[st.c00] + st.w10 * chi_a[st.c10] + st.w01 * chi_a[st.c01] +
-                                           st.w11 * chi_a[st.c11];
-            const double cb = PLANAR ? st.w00 * chi_b[st.c00] + st.w10 * chi_b[st.c10]
-                                     : st.w00 * chi_b[st.c00] + st.w10 * chi_b[st.c10] + st.w01 * chi_b[st.c01] +
-                                           st.w11 * chi_b[st.c11];
-            c_m = (1 - wz) * ca + wz * cb;
+            c_m = PLANAR ? (W.a00 * chi_a[c00] + W.a10 * chi_a[c10]) + (W.b00 * chi_b[c00] + W.b10 * chi_b[c10])
+                         : (W.a00 * chi_a[c00] + W.a10 * chi_a[c10] + W.a01 * chi_a[c01] + W.a11 * chi_a[c11]) +
+                               (W.b00 * chi_b[c00] + W.b10 * chi_b[c10] + W.b01 * chi_b[c01] + W.b11 * chi_b[c11]);
             dt = D.sub_len * (prev_c + c_m) * 0.5;
         }
-        const double2* a00 = reinterpret_cast<const double2*>(Sa) + st.c00;
-        const double2* a10 = reinterpret_cast<const double2*>(Sa) + st.c10;
-        const double2* a01 = reinterpret_cast<const double2*>(Sa) + st.c01;
-        const double2* a11 = reinterpret_cast<const double2*>(Sa) + st.c11;
-        const double2* b00 = reinterpret_cast<const double2*>(Sb) + st.c00;
-        const double2* b10 = reinterpret_cast<const double2*>(Sb) + st.c10;
-        const double2* b01 = reinterpret_cast<const double2*>(Sb) + st.c01;
-        const double2* b11 = reinterpret_cast<const double2*>(Sb) + st.c11;
+        const double2* pa = reinterpret_cast<const double2*>(Sa);
+        const double2* pb = reinterpret_cast<const double2*>(Sb);
 #pragma unroll
         for (int h = 0; h < kFC / 2; ++h) {
             const int hh = h * nxy;
-            const double2 p00 = a00[hh], p10 = a10[hh], q00 = b00[hh], q10 = b10[hh];
+            const double2 p00 = pa[hh + c00], p10 = pa[hh + c10], q00 = pb[hh + c00], q10 = pb[hh + c10];
             double s2[2];
             if (PLANAR) {
-                s2[0] = (1 - wz) * (st.w00 * p00.x + st.w10 * p10.x) + wz * (st.w00 * q00.x + st.w10 * q10.x);
-                s2[1] = (1 - wz) * (st.w00 * p00.y + st.w10 * p10.y) + wz * (st.w00 * q00.y + st.w10 * q10.y);
+                s2[0] = (W.a00 * p00.x + W.a10 * p10.x) + (W.b00 * q00.x + W.b10 * q10.x);
+                s2[1] = (W.a00 * p00.y + W.a10 * p10.y) + (W.b00 * q00.y + W.b10 * q10.y);
             } else {
-                const double2 p01 = a01[hh], p11 = a11[hh], q01 = b01[hh], q11 = b11[hh];
-                s2[0] = (1 - wz) * (st.w00 * p00.x + st.w10 * p10.x + st.w01 * p01.x + st.w11 * p11.x) +
-                        wz * (st.w00 * q00.x + st.w10 * q10.x + st.w01 * q01.x + st.w11 * q11.x);
-                s2[1] = (1 - wz) * (st.w00 * p00.y + st.w10 * p10.y + st.w01 * p01.y + st.w11 * p11.y) +
-                        wz * (st.w00 * q00.y + st.w10 * q10.y + st.w01 * q01.y + st.w11 * q11.y);
+                const double2 p01 = pa[hh + c01], p11 = pa[hh + c11], q01 = pb[hh + c01], q11 = pb[hh + c11];
+                s2[0] = (W.a00 * p00.x + W.a10 * p10.x + W.a01 * p01.x + W.a11 * p11.x) +
+                        (W.b00 * q00.x + W.b10 * q10.x + W.b01 * q01.x + W.b11 * q11.x);
+                s2[1] = (W.a00 * p00.y + W.a10 * p10.y + W.a01 * p01.y + W.a11 * p11.y) +
+                        (W.b00 * q00.y + W.b10 * q10.y + W.b01 * q01.y + W.b11 * q11.y);
             }
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
@@ -316,6 +348,11 @@ __device__ __forceinline__ void advance_line_smem4_par(const LatDir& D, const Sh
 // The source / opacity planes the lines cross and the x plane of the y = x - v gather
 // are staged in shared memory by cp.async two layer steps ahead (rings of 3 and 2),
 // so the global-memory latency of the plane loads overlaps the line march.
+__device__ __forceinline__ void cp_async16_d(double* dst, const double* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
                  "l"(src));
@@ -323,7 +360,7 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
 
 template <int FS, int SRC, int OUT, bool DT, bool PLANAR>
 __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A, int with_inflow, int max_sub,
-                                                                       int fchunk_slack) {
+                                                                       int fchunk_slack, int vec16) {
     extern __shared__ __align__(16) double sm[];
     const int nxy = static_cast<int>(A.nxy);
     constexpr bool XM = (OUT == OUT_X_MINUS);
@@ -332,9 +369,10 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
     constexpr int RING = PAR ? 4 : 3;           // source / opacity plane ring (PAR reads layer t + 2)
     double* splane = lines + nxy * kFC;         // [RING][nxy][kFC]
     double* cplane = splane + RING * nxy * kFC; // [RING][nxy]      (opacity; unused with DT)
-    double* xplane = cplane + RING * nxy;       // [2][nxy][kFC]   (XM only)
+    double* xplane = cplane + ((RING * nxy + 1) & ~1);   // [2][nxy][kFC]   (XM only; 16-byte aligned for double2)
     double* seeds = xplane + 2 * nxy * kFC;     // [nxy][kFC] SC restart values
-    Shift* shs = reinterpret_cast<Shift*>(seeds + nxy * kFC);   // [max_sub + 1] shifts of the step
+    Shift* shs = reinterpret_cast<Shift*>(seeds + nxy * kFC);   // [max_sub + 1] shifts of the step (exp-parabolic)
+    SubW* sws = reinterpret_cast<SubW*>(shs + max_sub + 1);     // [max_sub + 1] folded sub-node table of the step
     // Frequency chunks are cut at 32-byte sectors of the [node][direction][frequency] vectors:
     // with (n_dirs n_freq) % 4 == 0 the row of (node, direction a) starts (a n_freq) % 4
     // doubles past a sector boundary for every node, so the chunks of direction a start at
@@ -362,13 +400,21 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
         const int64_t base = static_cast<int64_t>(k) * A.nxy;
         double* sp = splane + r * nxy * kFC;
         double* cp = cplane + r * nxy;
-        for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) {
-            const int c = e / kFC, q = e - c * kFC;
-            if (q >= qlo && q < qhi) {
-                if (SRC == LSRC_VEC) cp_async8(sp + pidx(c, q, nxy), A.src + ((base + c) * A.n_dirs + a) * A.n_freq + f0 + q);
-                else cp_async8(sp + pidx(c, q, nxy), A.src + (base + c) * A.n_freq + f0 + q);
+        // one (node, frequency pair) per iteration: a 16-byte copy when the pair is whole and
+        // the chunks are sector-aligned (vec16), else per element
+        for (int e = threadIdx.x; e < nxy * (kFC / 2); e += blockDim.x) {
+            const int c = e / (kFC / 2), q = 2 * (e - c * (kFC / 2));
+            const bool v0 = q >= qlo && q < qhi, v1 = q + 1 >= qlo && q + 1 < qhi;
+            double* d = sp + pidx(c, q, nxy);
+            const double* gsrc = SRC == LSRC_VEC ? A.src + ((base + c) * A.n_dirs + a) * A.n_freq + f0 + q
+                                                 : A.src + (base + c) * A.n_freq + f0 + q;
+            if (SRC == LSRC_VEC && vec16 && v0 && v1) {
+                cp_async16_d(d, gsrc);
             } else {
-                sp[pidx(c, q, nxy)] = 0.0;
+                if (v0) cp_async8(d, gsrc);
+                else d[0] = 0.0;
+                if (v1) cp_async8(d + 1, gsrc + 1);
+                else d[1] = 0.0;
             }
         }
         if (!DT)
@@ -378,9 +424,17 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
         if (!XM) return;
         const int64_t base = static_cast<int64_t>(k) * A.nxy;
         double* xp = xplane + r * nxy * kFC;
-        for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) {
-            const int c = e / kFC, q = e - c * kFC;
-            if (q >= qlo && q < qhi) cp_async8(xp + pidx(c, q, nxy), A.x + ((base + c) * A.n_dirs + a) * A.n_freq + f0 + q);
+        for (int e = threadIdx.x; e < nxy * (kFC / 2); e += blockDim.x) {
+            const int c = e / (kFC / 2), q = 2 * (e - c * (kFC / 2));
+            const bool v0 = q >= qlo && q < qhi, v1 = q + 1 >= qlo && q + 1 < qhi;
+            double* d = xp + pidx(c, q, nxy);
+            const double* gsrc = A.x + ((base + c) * A.n_dirs + a) * A.n_freq + f0 + q;
+            if (vec16 && v0 && v1) {
+                cp_async16_d(d, gsrc);
+            } else {
+                if (v0) cp_async8(d, gsrc);
+                if (v1) cp_async8(d + 1, gsrc + 1);
+            }
         }
     };
     auto commit = []() { asm volatile("cp.async.commit_group;\n" ::); };
@@ -396,8 +450,9 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
     commit();
     if (PAR && A.nz > 2) issue_planes(layer_of(2), 2);
     if (PAR) commit();
-    static_assert(kIntThreads % kFC == 0, "a thread keeps its frequency across gather iterations");
-    const int gj0 = (static_cast<int>(threadIdx.x) / kFC) / A.nx, gi0 = static_cast<int>(threadIdx.x) / kFC - gj0 * A.nx;
+    static_assert(kIntThreads % (kFC / 2) == 0, "a thread keeps its frequency pair across gather iterations");
+    const int gj0 = (static_cast<int>(threadIdx.x) / (kFC / 2)) / A.nx,
+              gi0 = static_cast<int>(threadIdx.x) / (kFC / 2) - gj0 * A.nx;
     int gnbx, gnby;
     double gnax, gnay;
     {
@@ -441,24 +496,40 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
         }
         const double* xp = xplane + (t & 1) * nxy * kFC;
         int gi = gi0, gj = gj0;
-        for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) {
-            const int c = e / kFC, q = e - c * kFC;
+        for (int e = threadIdx.x; e < nxy * (kFC / 2); e += blockDim.x) {
+            const int c = e / (kFC / 2), q = 2 * (e - c * (kFC / 2));   // frequency pair (q, q + 1) of node c
             const int j = gj, i = gi;
-            gi += kIntThreads / kFC;
+            gi += kIntThreads / (kFC / 2);
             while (gi >= A.nx) {
                 gi -= A.nx;
                 ++gj;
             }
             const Stencil st = stencil_at(i, j, gsh, A.nx, A.ny);
-            const double v = st.w00 * lines[pidx(st.c00, q, nxy)] + st.w10 * lines[pidx(st.c10, q, nxy)] +
-                             st.w01 * lines[pidx(st.c01, q, nxy)] + st.w11 * lines[pidx(st.c11, q, nxy)];
-            if (q >= qlo && q < qhi) {
-                const int64_t idx = ((static_cast<int64_t>(k) * A.nxy + c) * A.n_dirs + a) * A.n_freq + f0 + q;
-                A.y[idx] = XM ? xp[pidx(c, q, nxy)] - v : v;
+            const double2* lp = reinterpret_cast<const double2*>(lines) + (q >> 1) * nxy;   // pair-major planes
+            const double2 l00 = lp[st.c00], l10 = lp[st.c10], l01 = lp[st.c01], l11 = lp[st.c11];
+            double2 v;
+            v.x = st.w00 * l00.x + st.w10 * l10.x + st.w01 * l01.x + st.w11 * l11.x;
+            v.y = st.w00 * l00.y + st.w10 * l10.y + st.w01 * l01.y + st.w11 * l11.y;
+            if (XM) {
+                const double2 xv = reinterpret_cast<const double2*>(xp)[(q >> 1) * nxy + c];
+                v.x = xv.x - v.x;
+                v.y = xv.y - v.y;
+            }
+            const bool v0 = q >= qlo && q < qhi, v1 = q + 1 >= qlo && q + 1 < qhi;
+            double* yo = A.y + ((static_cast<int64_t>(k) * A.nxy + c) * A.n_dirs + a) * A.n_freq + f0 + q;
+            if (vec16 && v0 && v1) {
+                *reinterpret_cast<double2*>(yo) = v;
+            } else {
+                if (v0) yo[0] = v.x;
+                if (v1) yo[1] = v.y;
             }
         }
         if (t == A.nz - 1) break;
-        for (int m = threadIdx.x; m <= D.n_sub; m += blockDim.x) shs[m] = A.sub_shift[D.shift_off + t * (D.n_sub + 1) + m];
+        for (int m = threadIdx.x; m <= D.n_sub; m += blockDim.x) {
+            const Shift sh = A.sub_shift[D.shift_off + t * (D.n_sub + 1) + m];
+            if (PAR) shs[m] = sh;
+            else sws[m] = subw_of(sh, m, D.n_sub);
+        }
         if (D.sc) {
             // short characteristics: every line restarts at its node's upwind point on this layer
             const Shift rsh = restart_shift(D);
@@ -488,7 +559,7 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
             if (PAR)
                 advance_line_smem4_par<PLANAR>(D, shs, dsh, acc, lx, ly, A.nx, A.ny, ca, cb, cc, Sa, Sb, Sc, phi, nxy);
             else
-            advance_line_smem4<FS, DT, PLANAR>(D, shs, acc, lx, ly, t, A.nx, A.ny, ca, cb, Sa, Sb, phi,
+            advance_line_smem4<FS, DT, PLANAR>(D, sws, acc, lx, ly, t, A.nx, A.ny, ca, cb, Sa, Sb, phi,
                                        DT ? A.dtab + D.dtab_off + static_cast<int64_t>(t) * D.n_sub * A.nxy + c : nullptr,
                                        nxy);
 #pragma unroll
@@ -1626,8 +1697,8 @@ static LatArgs lat_args(const Problem& p, const double* src, const double* x, do
 template <int FS, int SRC, int OUT>
 static int launch_int(const Problem& p, const LatArgs& A, int with_inflow, cudaStream_t s) {
     constexpr int ring = FS == RTK_FS_EXP_PARABOLIC ? 4 : 3;
-    const size_t smem_planes = sizeof(double) * A.nxy * (kFC + ring * kFC + ring + 2 * kFC + kFC) +
-                               sizeof(Shift) * (p.lat_max_sub + 1);
+    const size_t smem_planes = sizeof(double) * (A.nxy * (kFC + ring * kFC + ring + 2 * kFC + kFC) + 1) +
+                               (sizeof(Shift) + sizeof(SubW)) * (p.lat_max_sub + 1);
     if (FS == RTK_FS_EXP_PARABOLIC && (smem_planes > 160 * 1024 || p.tune.lat_no_smem))
         return set_error(RTK_ERESOURCE, "exp-parabolic in the intensity layout needs the shared-memory kernel "
                                         "(small layers); use the moment layout");
@@ -1648,7 +1719,13 @@ static int launch_int(const Problem& p, const LatArgs& A, int with_inflow, cudaS
                                   (A.x == nullptr || reinterpret_cast<uintptr_t>(A.x) % 32 == 0);
         const int slack = aligned_rows ? kFC - 1 : 0;
         const int nfc = (A.n_freq + slack + kFC - 1) / kFC;
-        kern<<<A.n_dirs * nfc, kIntThreads, smem_planes, s>>>(A, with_inflow, p.lat_max_sub, slack);
+        // whole frequency pairs move as 16-byte words when they are 16-byte aligned in src, x
+        // and y: always with sector-aligned chunks, else with an even N_nu and aligned bases
+        const bool ptr16 = (SRC != LSRC_VEC || reinterpret_cast<uintptr_t>(A.src) % 16 == 0) &&
+                           (A.y == nullptr || reinterpret_cast<uintptr_t>(A.y) % 16 == 0) &&
+                           (A.x == nullptr || reinterpret_cast<uintptr_t>(A.x) % 16 == 0);
+        const int vec16 = (aligned_rows || (A.n_freq % 2 == 0 && ptr16)) ? 1 : 0;
+        kern<<<A.n_dirs * nfc, kIntThreads, smem_planes, s>>>(A, with_inflow, p.lat_max_sub, slack, vec16);
         RTK_LAUNCH_CHECK("lattice_int_smem_kernel");
         return RTK_OK;
     }
