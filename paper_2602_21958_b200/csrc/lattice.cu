@@ -31,6 +31,9 @@ namespace {
 
 constexpr int kFC = 4;            // frequencies per CTA in the intensity kernel
 constexpr int kIntThreads = 256;
+#ifndef RTK_INT_MINB
+#define RTK_INT_MINB 2   // CTAs per SM the shared-memory intensity kernel is compiled for
+#endif
 
 __device__ __forceinline__ double rcp_nr(double x) {
     double r;
@@ -359,20 +362,20 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
 }
 
 template <int FS, int SRC, int OUT, bool DT, bool PLANAR>
-__global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A, int with_inflow, int max_sub,
+__global__ void __launch_bounds__(kIntThreads, RTK_INT_MINB) lattice_int_smem_kernel(LatArgs A, int with_inflow, int max_sub,
                                                                        int fchunk_slack, int vec16) {
     extern __shared__ __align__(16) double sm[];
     const int nxy = static_cast<int>(A.nxy);
     constexpr bool XM = (OUT == OUT_X_MINUS);
-    double* lines = sm;                         // [nxy][kFC]
+    double* lines0 = sm;                        // [2][nxy][kFC] line values: step t reads buffer t % 2, writes the other
     constexpr bool PAR = FS == RTK_FS_EXP_PARABOLIC;
     constexpr int RING = PAR ? 4 : 3;           // source / opacity plane ring (PAR reads layer t + 2)
-    double* splane = lines + nxy * kFC;         // [RING][nxy][kFC]
+    double* splane = lines0 + 2 * nxy * kFC;    // [RING][nxy][kFC]
     double* cplane = splane + RING * nxy * kFC; // [RING][nxy]      (opacity; unused with DT)
     double* xplane = cplane + ((RING * nxy + 1) & ~1);   // [2][nxy][kFC]   (XM only; 16-byte aligned for double2)
     double* seeds = xplane + 2 * nxy * kFC;     // [nxy][kFC] SC restart values
-    Shift* shs = reinterpret_cast<Shift*>(seeds + nxy * kFC);   // [max_sub + 1] shifts of the step (exp-parabolic)
-    SubW* sws = reinterpret_cast<SubW*>(shs + max_sub + 1);     // [max_sub + 1] folded sub-node table of the step
+    Shift* shs0 = reinterpret_cast<Shift*>(seeds + nxy * kFC);  // [2][max_sub + 1] shifts of a step (exp-parabolic)
+    SubW* sws0 = reinterpret_cast<SubW*>(shs0 + 2 * (max_sub + 1));   // [2][max_sub + 1] folded sub-node tables
     // Frequency chunks are cut at 32-byte sectors of the [node][direction][frequency] vectors:
     // with (n_dirs n_freq) % 4 == 0 the row of (node, direction a) starts (a n_freq) % 4
     // doubles past a sector boundary for every node, so the chunks of direction a start at
@@ -438,7 +441,18 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
         }
     };
     auto commit = []() { asm volatile("cp.async.commit_group;\n" ::); };
-    for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) lines[pidx(e / kFC, e % kFC, nxy)] = inflow[e % kFC];
+    for (int e = threadIdx.x; e < nxy * kFC; e += blockDim.x) lines0[pidx(e / kFC, e % kFC, nxy)] = inflow[e % kFC];
+    // sub-node table of step t into buffer t % 2 (staged one step ahead; the step's top barrier
+    // orders it before its readers)
+    auto stage_sub = [&](int t) {
+        if (t >= A.nz - 1) return;
+        for (int m = threadIdx.x; m <= D.n_sub; m += blockDim.x) {
+            const Shift sh = A.sub_shift[D.shift_off + t * (D.n_sub + 1) + m];
+            if (PAR) shs0[(t & 1) * (max_sub + 1) + m] = sh;
+            else sws0[(t & 1) * (max_sub + 1) + m] = subw_of(sh, m, D.n_sub);
+        }
+    };
+    stage_sub(0);
     // prologue: group 0 = planes(t=0) + x(t=0); group 1 = planes(t=1) + x(t=1)
     issue_planes(layer_of(0), 0);
     issue_x(layer_of(0), 0);
@@ -472,6 +486,11 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
         if (t + RING - 1 < A.nz) issue_planes(layer_of(t + RING - 1), (t + RING - 1) % RING);
         if (t + 1 < A.nz && t > 0) issue_x(layer_of(t + 1), (t + 1) & 1);
         commit();
+        stage_sub(t + 1);
+        double* lines = lines0 + (t & 1) * nxy * kFC;          // written by the previous step's march
+        double* lines_out = lines0 + ((t + 1) & 1) * nxy * kFC;
+        const Shift* shs = shs0 + (t & 1) * (max_sub + 1);
+        const SubW* sws = sws0 + (t & 1) * (max_sub + 1);
         // next step's sub-segment paths of this thread's lines into L1 (the march reads them one
         // sub-node ahead only, which left their L2 latency exposed)
         if (DT && t + 2 < A.nz) {
@@ -525,11 +544,6 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
             }
         }
         if (t == A.nz - 1) break;
-        for (int m = threadIdx.x; m <= D.n_sub; m += blockDim.x) {
-            const Shift sh = A.sub_shift[D.shift_off + t * (D.n_sub + 1) + m];
-            if (PAR) shs[m] = sh;
-            else sws[m] = subw_of(sh, m, D.n_sub);
-        }
         if (D.sc) {
             // short characteristics: every line restarts at its node's upwind point on this layer
             const Shift rsh = restart_shift(D);
@@ -541,7 +555,9 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
                                          st.w01 * lines[pidx(st.c01, q, nxy)] + st.w11 * lines[pidx(st.c11, q, nxy)];
             }
         }
-        __syncthreads();   // the gather read `lines` before the march overwrites them; shifts staged
+        // The march writes the OTHER line buffer, so the gather above needs no barrier before it
+        // (one barrier per layer step); only the SC restart values cross threads here.
+        if (D.sc) __syncthreads();
         const double* start = D.sc ? seeds : lines;
         const double* Sa = splane + (t % RING) * nxy * kFC;
         const double* Sb = splane + ((t + 1) % RING) * nxy * kFC;
@@ -563,7 +579,7 @@ __global__ void __launch_bounds__(kIntThreads) lattice_int_smem_kernel(LatArgs A
                                        DT ? A.dtab + D.dtab_off + static_cast<int64_t>(t) * D.n_sub * A.nxy + c : nullptr,
                                        nxy);
 #pragma unroll
-            for (int q = 0; q < kFC; ++q) lines[pidx(c, q, nxy)] = acc[q];
+            for (int q = 0; q < kFC; ++q) lines_out[pidx(c, q, nxy)] = acc[q];
         }
     }
 }
@@ -1203,6 +1219,7 @@ struct TileArgs {
     int sub_cap;            // max n_sub + 1
     int ntx;                // tiles along x
     int dgz;                // direction groups (gridDim.z)
+    int n_stages;           // window stages in shared memory (3 when they fit, else 2)
     double* scratch;        // DGZ > 1: [group][hemi][line][NM][fp]
 };
 
@@ -1393,9 +1410,12 @@ __global__ void __launch_bounds__(TX * TY, TX * TY >= 256 ? RTK_TILE_MINB : 2 * 
             flush(hemi);
             hemi = hm;
         }
-        const int st = it & 1;
-        // prefetch the next direction's window into the other stage, then wait for this one
-        if (march && it + 1 < n_mine) stage(it + 1, st ^ 1);
+        // prefetch the next direction's window into the next stage, then wait for this one.  With
+        // three stages the refilled stage was last read two iterations ago, and every thread has
+        // passed the barrier below since, so one barrier per direction suffices; with two stages
+        // (windows too large for three) a second barrier ends the iteration.
+        const int st = it % T.n_stages;
+        if (march && it + 1 < n_mine) stage(it + 1, (it + 1) % T.n_stages);
         asm volatile("cp.async.commit_group;\n" ::);
         Pre nxt;
         if (it + 1 < n_mine) prefetch(it + 1, nxt);   // global loads in flight across this direction
@@ -1474,7 +1494,7 @@ __global__ void __launch_bounds__(TX * TY, TX * TY >= 256 ? RTK_TILE_MINB : 2 * 
             }
         }
         cur = nxt;
-        __syncthreads();   // stage st is refilled by the next iteration's prefetch
+        if (T.n_stages == 2) __syncthreads();   // stage st is refilled by the next iteration's prefetch
     }
     flush(hemi);
     if (hemi == 0) flush(1);   // no up direction in this CTA: its (zero) part is still written
@@ -1697,8 +1717,9 @@ static LatArgs lat_args(const Problem& p, const double* src, const double* x, do
 template <int FS, int SRC, int OUT>
 static int launch_int(const Problem& p, const LatArgs& A, int with_inflow, cudaStream_t s) {
     constexpr int ring = FS == RTK_FS_EXP_PARABOLIC ? 4 : 3;
-    const size_t smem_planes = sizeof(double) * (A.nxy * (kFC + ring * kFC + ring + 2 * kFC + kFC) + 1) +
-                               (sizeof(Shift) + sizeof(SubW)) * (p.lat_max_sub + 1);
+    // [2] line buffers, source ring, opacity ring, [2] x planes, SC seeds, [2] sub-node tables
+    const size_t smem_planes = sizeof(double) * (A.nxy * (2 * kFC + ring * kFC + ring + 2 * kFC + kFC) + 1) +
+                               2 * (sizeof(Shift) + sizeof(SubW)) * (p.lat_max_sub + 1);
     if (FS == RTK_FS_EXP_PARABOLIC && (smem_planes > 160 * 1024 || p.tune.lat_no_smem))
         return set_error(RTK_ERESOURCE, "exp-parabolic in the intensity layout needs the shared-memory kernel "
                                         "(small layers); use the moment layout");
@@ -1833,7 +1854,13 @@ static int launch_mom_tiles_t(const Problem& p, const LatArgs& A, bool with_infl
     dgz = std::max(1, std::min(dgz, std::max(1, n_order)));
     const size_t stage_d2 = 2 * static_cast<size_t>(p.lat_region_cap) + kTileSubW * static_cast<size_t>(p.lat_sub_cap);
     const int per_cta = (n_order + dgz - 1) / dgz;
-    const size_t smem = 2 * stage_d2 * sizeof(double2) + (per_cta * sizeof(TileDir) + 15) / 16 * 16;
+    const size_t dir_bytes = (per_cta * sizeof(TileDir) + 15) / 16 * 16;
+    int n_stages = 3;
+    size_t smem = n_stages * stage_d2 * sizeof(double2) + dir_bytes;
+    if (smem > 110 * 1024) {   // keep two CTAs per SM
+        n_stages = 2;
+        smem = n_stages * stage_d2 * sizeof(double2) + dir_bytes;
+    }
     if (smem > 110 * 1024) return -1;   // very grazing directions on large tiles: per-item kernel
     TileArgs T;
     T.hdr = reinterpret_cast<const TileHdr*>(p.lat_tile_hdr);
@@ -1845,6 +1872,7 @@ static int launch_mom_tiles_t(const Problem& p, const LatArgs& A, bool with_infl
     T.sub_cap = p.lat_sub_cap;
     T.ntx = ntx;
     T.dgz = dgz;
+    T.n_stages = n_stages;
     T.scratch = nullptr;
     if (dgz > 1) {
         const size_t need = static_cast<size_t>(dgz) * 2 * A.nxy * NM * p.fp;

@@ -6,7 +6,7 @@ for v in "$@"; do
   echo "== variant $v"
   rm -f build/rtk/lattice.o
   make -C paper_2602_21958_b200/csrc -j8 NVCC="/usr/local/cuda/bin/nvcc $v" > /tmp/build_variant.log 2>&1 || { tail -5 /tmp/build_variant.log; continue; }
-  grep -A2 "lattice_mom_tile_kernelILi0ELi6ELi16ELi16E" build/rtk/lattice.o.ptxas.log | grep -E "spill|registers"
-  python tools/time_lattice.py 4 5 2>&1 | tail -2
+  grep -A2 "${KPAT:-lattice_mom_tile_kernelILi0ELi6ELi16ELi16E}" build/rtk/lattice.o.ptxas.log | grep -E "spill|registers"
+  python tools/time_lattice.py ${CFGS:-4 5} 2>&1 | tail -${NTAIL:-2}
 done
 cp /tmp/librtk_keep.so paper_2602_21958_b200/librtk_b200.so
