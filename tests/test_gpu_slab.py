@@ -79,7 +79,7 @@ def test_cfg1_dipole_prd_matvec_matches_oracle(fs):
     assert rel_l2(P.build_rhs(p), ro.build_rhs(d)) <= MATVEC_TOL
 
 
-@pytest.mark.parametrize("fs", ["ie", "exp_linear"])
+@pytest.mark.parametrize("fs", ["ie", "exp_linear", "exp_parabolic"])
 def test_cfg2_full_size_matvec_matches_oracle(fs):
     p = configs.slab_problem(2, formal_solver=fs)
     d = oracle_desc(p)
