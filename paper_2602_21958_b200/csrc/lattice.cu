@@ -1247,11 +1247,19 @@ struct TileDir {
 #define RTK_TILE_TY3 16
 #endif
 template <int FS, int NM, int TX, int TY>
-__global__ void __launch_bounds__(TX * TY, TX * TY >= 256 ? RTK_TILE_MINB : 2 * RTK_TILE_MINB)
+__global__ void __launch_bounds__(TX * TY, FS == RTK_FS_EXP_PARABOLIC
+                                               ? 1
+                                               : (TX * TY >= 256 ? RTK_TILE_MINB : 2 * RTK_TILE_MINB))
     lattice_mom_tile_kernel(LatArgs A, TileArgs T, int t, const double2* __restrict__ st_in,
                             double2* __restrict__ st_out, double* __restrict__ mom, int with_inflow, int fp,
-                            const double2* __restrict__ plane_cur, const double2* __restrict__ plane_next) {
+                            const double2* __restrict__ plane_cur, const double2* __restrict__ plane_next,
+                            const double2* __restrict__ plane_nn) {
     constexpr int NT = TX * TY;
+    // Exp-parabolic (long characteristics): a third window (layer t + 2) for the downwind sample
+    // one sub-segment beyond the crossing, whose table entry n_sub + 1 carries the weights of
+    // planes b / c; plane_nn == nullptr on the line's last step (linear weights there).
+    constexpr bool PAR = FS == RTK_FS_EXP_PARABOLIC;
+    constexpr int NW = PAR ? 3 : 2;   // staged windows per direction
     const int hp = fp >> 1;
     const int g = blockIdx.y;                    // frequency pair
     const int tile = blockIdx.x;
@@ -1271,7 +1279,7 @@ __global__ void __launch_bounds__(TX * TY, TX * TY >= 256 ? RTK_TILE_MINB : 2 * 
     // [TileDir x n_mine][stage 0: window a, window b, sub table][stage 1: ...]
     TileDir* tdir = reinterpret_cast<TileDir*>(tsm);
     double2* stages = tsm + (n_mine * sizeof(TileDir) + 15) / 16;
-    const int stage_d2 = 2 * T.region_cap + T.sub_cap * kTileSubW;
+    const int stage_d2 = NW * T.region_cap + T.sub_cap * kTileSubW;
     for (int e = threadIdx.x; e < n_mine; e += NT) {
         const int a = T.order[z + e * T.dgz];
         const LatDir& D = A.dirs[a];
@@ -1311,8 +1319,10 @@ __global__ void __launch_bounds__(TX * TY, TX * TY >= 256 ? RTK_TILE_MINB : 2 * 
         if (gy0 >= A.ny) gy0 -= A.ny;
         const double2* pa = plane_cur + a * plane2 + static_cast<int64_t>(g) * A.nxy;
         const double2* pb = plane_next + a * plane2 + static_cast<int64_t>(g) * A.nxy;
+        const double2* pc = (PAR && plane_nn) ? plane_nn + a * plane2 + static_cast<int64_t>(g) * A.nxy : nullptr;
         double2* wa = stages + st * stage_d2;
         double2* wb = wa + T.region_cap;
+        double2* wc = wb + T.region_cap;   // PAR only
         const int w = D.hdr.w, h = D.hdr.h;
         const bool small = w <= A.nx && h <= A.ny;
         const int cx = static_cast<int>(threadIdx.x) & 31;
@@ -1326,12 +1336,17 @@ __global__ void __launch_bounds__(TX * TY, TX * TY >= 256 ? RTK_TILE_MINB : 2 * 
                 gx = small ? (gx >= A.nx ? gx - A.nx : gx) : gx % A.nx;
                 cp_async16(wa + ry * w + rx, ra + gx);
                 cp_async16(wb + ry * w + rx, rb + gx);
+                if (PAR && pc) cp_async16(wc + ry * w + rx, pc + gy * A.nx + gx);
             }
         }
-        const int n_sub1 = D.n_sub + 1;
-        const double2* src = reinterpret_cast<const double2*>(T.sub + D.shift_off + static_cast<int64_t>(t) * n_sub1);
-        double2* dst = wa + 2 * T.region_cap;
-        for (int e = threadIdx.x; e < kTileSubW * n_sub1; e += NT) cp_async16(dst + e, src + e);
+        // sub-node table of (direction, step): n_sub + 2 entries (the last one is the exp-parabolic
+        // downwind sample), stored after the direction's preceding (n_sub + 2)-entry steps
+        const int n_sub2 = D.n_sub + 2;
+        const double2* src = reinterpret_cast<const double2*>(
+            T.sub + D.shift_off + static_cast<int64_t>(a) * nsteps + static_cast<int64_t>(t) * n_sub2);
+        double2* dst = wa + NW * T.region_cap;
+        const int n_copy = PAR ? n_sub2 : n_sub2 - 1;
+        for (int e = threadIdx.x; e < kTileSubW * n_copy; e += NT) cp_async16(dst + e, src + e);
     };
 
     // global operands of a direction, loaded one direction ahead into registers: the T_RC
@@ -1459,11 +1474,60 @@ __global__ void __launch_bounds__(TX * TY, TX * TY >= 256 ? RTK_TILE_MINB : 2 * 
                 const int w = D.hdr.w;
                 const double2* wa = stages + st * stage_d2;
                 const double2* wb = wa + T.region_cap;
-                const TileSub* sb = reinterpret_cast<const TileSub*>(wa + 2 * T.region_cap);
+                const TileSub* sb = reinterpret_cast<const TileSub*>(wa + NW * T.region_cap);
                 const double* dtl = A.dtab + D.dtab + c;
                 const int n_sub = D.n_sub;
                 double ps0 = 0.0, ps1 = 0.0;
                 double dt_next = t == 0 ? __ldg(dtl) : cur.dt0;
+                if (PAR) {
+                    // Kunasz-Auer along the line (advance_lineF_par / oracle/lattice.py): point m is
+                    // updated from the samples at m - 1, m and the downwind m + 1; the downwind of
+                    // the step's last point lies one sub-segment beyond the crossing (windows b / c,
+                    // table entry n_sub + 1; its dt is the line's first entry of step t + 1, which
+                    // follows this step's last), or the linear weights apply on the last step.
+                    const double2* wc = wb + T.region_cap;
+                    auto samp = [&](int m, const double2* pa_, const double2* pb_, double& o0, double& o1) {
+                        const TileSub S = sb[m];
+                        const int o = (lly + S.dy) * w + llx + S.dx;
+                        const double2 a00 = pa_[o], a10 = pa_[o + 1], a01 = pa_[o + w], a11 = pa_[o + w + 1];
+                        const double2 b00 = pb_[o], b10 = pb_[o + 1], b01 = pb_[o + w], b11 = pb_[o + w + 1];
+                        o0 = (S.a00 * a00.x + S.a10 * a10.x + S.a01 * a01.x + S.a11 * a11.x) +
+                             (S.b00 * b00.x + S.b10 * b10.x + S.b01 * b01.x + S.b11 * b11.x);
+                        o1 = (S.a00 * a00.y + S.a10 * a10.y + S.a01 * a01.y + S.a11 * a11.y) +
+                             (S.b00 * b00.y + S.b10 * b10.y + S.b01 * b01.y + S.b11 * b11.y);
+                    };
+                    const bool has_c = plane_nn != nullptr;
+                    double sp0, sp1, sc0, sc1, sn0 = 0.0, sn1 = 0.0;
+                    samp(0, wa, wb, sp0, sp1);
+                    samp(1, wa, wb, sc0, sc1);
+                    double dtu = dt_next;
+                    for (int m = 1; m <= n_sub; ++m) {
+                        const bool down = m < n_sub || has_c;
+                        double dtd = 0.0;
+                        if (m < n_sub) {
+                            samp(m + 1, wa, wb, sn0, sn1);
+                            dtd = __ldg(dtl + static_cast<int64_t>(m) * A.nxy);
+                        } else if (has_c) {
+                            samp(n_sub + 1, wb, wc, sn0, sn1);
+                            dtd = __ldg(dtl + static_cast<int64_t>(n_sub) * A.nxy);
+                        }
+                        if (down) {
+                            const ExpPar w0 = exp_parabolic_weights_bf(phi[0] * dtu, phi[0] * dtd);
+                            const ExpPar w1 = exp_parabolic_weights_bf(phi[1] * dtu, phi[1] * dtd);
+                            acc0 = fma(acc0, w0.att, w0.wu * sp0 + w0.wc * sc0 + w0.wd * sn0);
+                            acc1 = fma(acc1, w1.att, w1.wu * sp1 + w1.wc * sc1 + w1.wd * sn1);
+                        } else {
+                            const ExpLin w0 = exp_linear_weights_bf(phi[0] * dtu), w1 = exp_linear_weights_bf(phi[1] * dtu);
+                            acc0 = fma(acc0, w0.att, w0.wu * sp0 + w0.wc * sc0);
+                            acc1 = fma(acc1, w1.att, w1.wu * sp1 + w1.wc * sc1);
+                        }
+                        sp0 = sc0;
+                        sp1 = sc1;
+                        sc0 = sn0;
+                        sc1 = sn1;
+                        dtu = dtd;
+                    }
+                } else
                 for (int m = (FS == RTK_FS_IE ? 1 : 0); m <= n_sub; ++m) {
                     const TileSub S = sb[m];
                     const int o = (lly + S.dy) * w + llx + S.dx;
@@ -1532,20 +1596,32 @@ static int setup_tile_tables(Problem& p, const rtk_lattice_desc* d, const std::v
     const int nsteps = d->nz - 1;
     std::vector<TileHdr> hdr(static_cast<size_t>(d->n_dirs) * std::max(1, nsteps));
     size_t n_sub_total = 0;
-    for (const auto& D : dirs) n_sub_total = std::max<size_t>(n_sub_total, D.shift_off + static_cast<size_t>(nsteps) * (D.n_sub + 1));
+    // n_sub + 2 entries per (direction, step): sub-nodes 0..n_sub, then the exp-parabolic downwind
+    // sample; direction a's block starts at shift_off + a nsteps (one extra entry per earlier step)
+    for (int a = 0; a < d->n_dirs; ++a)
+        n_sub_total = std::max<size_t>(n_sub_total, dirs[a].shift_off + static_cast<size_t>(a) * nsteps +
+                                                        static_cast<size_t>(nsteps) * (dirs[a].n_sub + 2));
     std::vector<TileSub> sub(std::max<size_t>(1, n_sub_total));
+    const bool par = d->formal_solver == RTK_FS_EXP_PARABOLIC;
     p.lat_region_cap = 0;
     p.lat_sub_cap = 0;
     p.h_lat_down.assign(d->n_dirs, 0);
     for (int a = 0; a < d->n_dirs; ++a) {
         const LatDir& D = dirs[a];
         p.h_lat_down[a] = D.down;
-        p.lat_sub_cap = std::max(p.lat_sub_cap, D.n_sub + 1);
+        p.lat_sub_cap = std::max(p.lat_sub_cap, D.n_sub + 2);
         for (int t = 0; t < nsteps; ++t) {
             int fxmin = 0, fxmax = 0, fymin = 0, fymax = 0;
-            std::vector<double> fxs(D.n_sub + 1), fys(D.n_sub + 1), oxs(D.n_sub + 1), oys(D.n_sub + 1);
-            for (int m = 0; m <= D.n_sub; ++m) {
-                const double tt = D.sc ? static_cast<double>(m) / D.n_sub - 1.0 : t + static_cast<double>(m) / D.n_sub;
+            // entry n_sub + 1: the downwind point of the step's last sub-node (exp-parabolic, LC:
+            // the line at t + 1 + 1 / n_sub, as the Shift table's down_shift); it widens the
+            // window only for exp-parabolic problems
+            const int n_ent = D.n_sub + 2;
+            std::vector<double> fxs(n_ent), fys(n_ent), oxs(n_ent), oys(n_ent);
+            for (int m = 0; m < n_ent; ++m) {
+                if (m == D.n_sub + 1 && !par) break;
+                const double tt = m == D.n_sub + 1
+                                      ? (D.sc ? 1.0 / D.n_sub : t + 1.0 + 1.0 / D.n_sub)
+                                      : (D.sc ? static_cast<double>(m) / D.n_sub - 1.0 : t + static_cast<double>(m) / D.n_sub);
                 oxs[m] = tt * D.sx;
                 oys[m] = tt * D.sy;
                 fxs[m] = std::floor(oxs[m]);
@@ -1562,14 +1638,19 @@ static int setup_tile_tables(Problem& p, const rtk_lattice_desc* d, const std::v
             H.w = p.lat_tile_tx + (fxmax - fxmin) + 1;
             H.h = p.lat_tile_ty + (fymax - fymin) + 1;
             p.lat_region_cap = std::max(p.lat_region_cap, H.w * H.h);
-            for (int m = 0; m <= D.n_sub; ++m) {
-                TileSub& S = sub[D.shift_off + static_cast<size_t>(t) * (D.n_sub + 1) + m];
+            for (int m = 0; m < n_ent; ++m) {
+                TileSub& S = sub[D.shift_off + static_cast<size_t>(a) * nsteps + static_cast<size_t>(t) * n_ent + m];
+                if (m == D.n_sub + 1 && !par) {
+                    S = TileSub{};
+                    break;
+                }
                 S.dx = static_cast<int>(fxs[m]) - fxmin;
                 S.dy = static_cast<int>(fys[m]) - fymin;
                 S.pad = 0.0;
                 const double ax = oxs[m] - fxs[m], ay = oys[m] - fys[m];
                 const double w00 = (1 - ax) * (1 - ay), w10 = ax * (1 - ay), w01 = (1 - ax) * ay, w11 = ax * ay;
-                const double wz = m * (1.0 / D.n_sub);
+                // the downwind sample interpolates between layers t + 1 and t + 2 at wz = 1 / n_sub
+                const double wz = m == D.n_sub + 1 ? 1.0 / D.n_sub : m * (1.0 / D.n_sub);
                 S.a00 = (1 - wz) * w00;
                 S.a10 = (1 - wz) * w10;
                 S.a01 = (1 - wz) * w01;
@@ -1852,16 +1933,21 @@ static int launch_mom_tiles_t(const Problem& p, const LatArgs& A, bool with_infl
         dgz = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, (148 * 6 + ctas - 1) / ctas)));
     }
     dgz = std::max(1, std::min(dgz, std::max(1, n_order)));
-    const size_t stage_d2 = 2 * static_cast<size_t>(p.lat_region_cap) + kTileSubW * static_cast<size_t>(p.lat_sub_cap);
+    constexpr bool PAR = FS == RTK_FS_EXP_PARABOLIC;
+    const size_t stage_d2 = (PAR ? 3 : 2) * static_cast<size_t>(p.lat_region_cap) +
+                            kTileSubW * static_cast<size_t>(p.lat_sub_cap);
     const int per_cta = (n_order + dgz - 1) / dgz;
     const size_t dir_bytes = (per_cta * sizeof(TileDir) + 15) / 16 * 16;
+    // IE / exp-linear: two CTAs per SM (110 KB each); exp-parabolic: one CTA per SM (its register
+    // count allows no more), so its three windows may take up to 200 KB
+    const size_t smem_cap = (PAR ? 200 : 110) * 1024;
     int n_stages = 3;
     size_t smem = n_stages * stage_d2 * sizeof(double2) + dir_bytes;
-    if (smem > 110 * 1024) {   // keep two CTAs per SM
+    if (smem > smem_cap) {
         n_stages = 2;
         smem = n_stages * stage_d2 * sizeof(double2) + dir_bytes;
     }
-    if (smem > 110 * 1024) return -1;   // very grazing directions on large tiles: per-item kernel
+    if (smem > smem_cap) return -1;   // very grazing directions on large tiles: per-item kernel
     TileArgs T;
     T.hdr = reinterpret_cast<const TileHdr*>(p.lat_tile_hdr);
     T.sub = reinterpret_cast<const TileSub*>(p.lat_tile_sub);
@@ -1892,16 +1978,22 @@ static int launch_mom_tiles_t(const Problem& p, const LatArgs& A, bool with_infl
     double2* a = reinterpret_cast<double2*>(p.lat_state[0]);
     double2* b = reinterpret_cast<double2*>(p.lat_state[1]);
     const dim3 grid(static_cast<unsigned>(ntiles), static_cast<unsigned>(hp), static_cast<unsigned>(dgz));
+    constexpr int ring = PAR ? 3 : 2;   // source planes: current, next (and the one after, exp-parabolic)
     for (int t = 0; t < A.nz; ++t) {
-        double* cur = p.lat_splane[t % 2];
-        double* nxt = p.lat_splane[(t + 1) % 2];
+        double* cur = p.lat_splane[t % ring];
+        double* nxt = p.lat_splane[(t + 1) % ring];
+        double* nn = PAR ? p.lat_splane[(t + 2) % ring] : nullptr;
         if (t < A.nz - 1) {
+            // step 0 fills every plane of the ring; later steps only the newest one
+            const int mask = PAR ? (t == 0 ? 7 : 4) : (t == 0 ? 3 : 2);
             lattice_splane_pm_kernel<SRC, NM><<<pmblocks, 256, pm_smem, s>>>(
-                A, t, reinterpret_cast<double2*>(cur), reinterpret_cast<double2*>(nxt), nullptr, t == 0 ? 3 : 2, p.fp);
+                A, t, reinterpret_cast<double2*>(cur), reinterpret_cast<double2*>(nxt), reinterpret_cast<double2*>(nn),
+                mask, p.fp);
             RTK_LAUNCH_CHECK("lattice_splane_pm_kernel");
         }
         kern<<<grid, TX * TY, smem, s>>>(A, T, t, a, b, mom, with_inflow ? 1 : 0, p.fp,
-                                         reinterpret_cast<const double2*>(cur), reinterpret_cast<const double2*>(nxt));
+                                         reinterpret_cast<const double2*>(cur), reinterpret_cast<const double2*>(nxt),
+                                         PAR && t + 2 < A.nz ? reinterpret_cast<const double2*>(nn) : nullptr);
         RTK_LAUNCH_CHECK("lattice_mom_tile_kernel");
         if (dgz > 1) {
             const int64_t per = A.nxy * NM * p.fp;
@@ -1916,7 +2008,10 @@ static int launch_mom_tiles_t(const Problem& p, const LatArgs& A, bool with_infl
 
 template <int FS, int SRC, int NM>
 static int launch_mom_tiles(const Problem& p, const LatArgs& A, bool with_inflow, double* mom, cudaStream_t s) {
-    if (FS == RTK_FS_EXP_PARABOLIC || p.tune.lat_no_tile || !p.lat_tile_hdr || (p.fp & 1)) return -1;
+    if (p.tune.lat_no_tile || !p.lat_tile_hdr || (p.fp & 1)) return -1;
+    // exp-parabolic: long characteristics only (the short-characteristics downwind segment needs
+    // the opacity planes, which the tiled kernel does not stage)
+    if (FS == RTK_FS_EXP_PARABOLIC && (p.lat_any_sc || !p.lat_splane[2])) return -1;
     if (p.lat_tile_ty == 1) return launch_mom_tiles_t<FS, SRC, NM, 128, 1>(p, A, with_inflow, mom, s);
     return launch_mom_tiles_t<FS, SRC, NM, RTK_TILE_TX3, RTK_TILE_TY3>(p, A, with_inflow, mom, s);
 }
