@@ -6,17 +6,21 @@
 // sampling of opacity and source, the IE / exp-linear recursion
 // (R/_kernels.py:90-99), and bilinear T_RC back to the nodes of each layer.
 //
-// Two kernels:
-//  * lattice_int_kernel  (intensity layout, cfg3): one CTA per (direction,
-//    4-frequency chunk) marches ALL lines of that direction through ALL layers
-//    in one launch; line values are exchanged through shared memory for the
-//    T_RC gather (two barriers per layer).  Output y = x - I (or I).
-//  * lattice_mom_step_kernel (moment layout, cfg4/5): layer-synchronous, one
-//    launch per layer step; one thread per (line, frequency) loops over every
-//    direction, advancing the line and gathering the node value of the layer,
-//    and accumulates the angular moments in registers (deterministic order,
-//    no atomics).  Line states live in a double-buffered [dir][line][freq]
-//    array.  The source is rebuilt on the fly from the moment unknown u.
+// Kernels:
+//  * lattice_int_smem_kernel (intensity layout, cfg3): one CTA per (direction, sector-aligned
+//    4-frequency chunk) marches ALL lines of that direction through ALL layers in one launch;
+//    source / x planes staged by cp.async rings, line values double-buffered in shared memory
+//    for the T_RC gather (one barrier per layer step).  Output y = x - I (or I).
+//    lattice_int_kernel is its fallback for layers too large for shared memory.
+//  * lattice_mom_tile_kernel (moment layout, cfg4/5; IE, exp-linear, exp-parabolic LC):
+//    layer-synchronous, one launch per layer step; a CTA owns a tile of lines and a frequency
+//    pair and loops over the directions, sampling the source from shared-memory windows of the
+//    pair-major planes written by lattice_splane_pm_kernel; angular moments accumulate in
+//    registers in a fixed order (no atomics); line states live in a double-buffered
+//    [dir][pair][line] array.  The source is rebuilt from the moment unknown u per layer.
+//  * lattice_mom_group_kernel (+ lattice_splane_kernel): the per-item moment kernel, one thread
+//    per (line, frequency pair[, direction group]) reading through L1/L2 -- exp-parabolic with
+//    short characteristics, odd padded N_nu, oversized windows, and the parity-test variants.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1038,27 +1042,16 @@ __global__ void __launch_bounds__(DG == 1 ? 128 : 256, DG == 1 ? 5 : 3)
 // Source planes: for every direction a, S_a on the layers its march visits at offsets
 // o = 0, 1, 2 from step t (down: t + o, up: nz - 1 - t - o) into plane_o, for the offsets in
 // fill_mask (bit o); S = gamma sum_l c_l Y_l(a) u_l (SRC_U) or the isotropic thermal source
-// (SRC_ISO).  Layout plane[a][c][f].  Offset 2 is the exp-parabolic downwind plane.
-// PM (pair-major, the tiled moment kernel's layout): plane[a][f / 2][c][f % 2], i.e. each
-// frequency pair of a direction is a contiguous [ny][nx] image of double2; threads are
-// (pair, node) with the node fastest so the writes stay coalesced.
-template <int SRC, int NM, bool PM>
+// (SRC_ISO).  Layout plane[a][c][f] (the per-item kernels; the tiled kernel's pair-major planes
+// come from lattice_splane_pm_kernel below).  Offset 2 is the exp-parabolic downwind plane.
+template <int SRC, int NM>
 __global__ void __launch_bounds__(256) lattice_splane_kernel(LatArgs A, int t, double* __restrict__ plane0,
                                                               double* __restrict__ plane1,
                                                               double* __restrict__ plane2, int fill_mask, int fp) {
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (tid >= A.nxy * fp) return;
-    int64_t c;
-    int fpad;
-    if (PM) {   // tid = (pair, node, e): pair-major, node, then the pair's two frequencies
-        const int64_t pr = tid / (2 * A.nxy);
-        const int64_t rem = tid - pr * 2 * A.nxy;
-        c = rem >> 1;
-        fpad = static_cast<int>(2 * pr + (rem & 1));
-    } else {
-        c = tid / fp;
-        fpad = static_cast<int>(tid - c * fp);
-    }
+    const int64_t c = tid / fp;
+    const int fpad = static_cast<int>(tid - c * fp);
     const bool fvalid = fpad < A.n_freq;
     const int f = fvalid ? fpad : 0;
     const int64_t plane = A.nxy * fp;
@@ -1103,7 +1096,7 @@ __global__ void __launch_bounds__(256) lattice_splane_kernel(LatArgs A, int t, d
             } else {
                 v = g[q];
             }
-            const int64_t idx = PM ? a * plane + ((fpad >> 1) * A.nxy + c) * 2 + (fpad & 1) : a * plane + c * fp + fpad;
+            const int64_t idx = a * plane + c * fp + fpad;
             planes[q >> 1][idx] = fvalid ? v : 0.0;
         }
     }
@@ -1887,7 +1880,7 @@ static int launch_mom_steps_dg(const Problem& p, const LatArgs& A, bool with_inf
         if (t < A.nz - 1) {
             // step 0 fills every plane of the ring; later steps only the newest one
             const int mask = PAR ? (t == 0 ? 7 : 4) : (t == 0 ? 3 : 2);
-            lattice_splane_kernel<SRC, NM, false><<<pblocks, 256, 0, s>>>(A, t, cur, nxt, nn, mask, p.fp);
+            lattice_splane_kernel<SRC, NM><<<pblocks, 256, 0, s>>>(A, t, cur, nxt, nn, mask, p.fp);
             RTK_LAUNCH_CHECK("lattice_splane_kernel");
         }
         kern<<<sblocks, mb, mom_smem, s>>>(A, t, a, b, mom, with_inflow ? 1 : 0, p.fp, cur, nxt,
