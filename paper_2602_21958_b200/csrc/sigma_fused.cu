@@ -126,7 +126,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int n_chunks = (n_angles + AC - 1) / AC;
     const int n_apad = n_chunks * AC;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    double* Bs = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte alignment (swizzled TMA boxes) as an OFFSET on the shared array, so the compiler
+    // keeps the shared address space and emits LDS / STS (rounding the pointer through an integer
+    // made every fragment and x load a generic LD.E on the long scoreboard)
+    double* Bs = reinterpret_cast<double*>(smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u));
     double* Xs = Bs + BS * C::b_elems;                  // [XS][SP][AC][KS]    (TMA boxes, slot pitch XBOX)
     double* As = Xs + XS * XBOX;                        // [AS][CN][ROWS][PA]  (slice r from CTA r)
     double* wys = As + AS * C::a_elems;                 // [NM][n_apad] (zero padded)
