@@ -50,6 +50,7 @@ constexpr int RED0 = 32 * MMA_WARPS;   // first reducer thread
 constexpr int XPROD = 32 * (MMA_WARPS + RED_WARPS);
 constexpr int BPROD = XPROD + 1;
 constexpr int MAX_ANGLES = 256;
+constexpr unsigned kMmaNapNs = 200;    // see the MMA loop
 constexpr size_t kSmemLimit = 232448;
 
 // Variant: CN CTAs per cluster, MT m8 tiles of GEMM rows (2 SP <= 8 MT), NT n8 tiles per
@@ -304,6 +305,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int i = 0; i < MT; ++i)
 #pragma unroll
                     for (int jn = 0; jn < NT; ++jn) mma(acc[i][jn], af[i], bf[jn]);
+                // FP64-pipe fairness: DMMA and the reducers' DFMA share one pipe per SM sub-partition,
+                // and two MMA warps issuing back-to-back DMMAs (16 cycles each) starve the reducer
+                // warps, so the next A slice is produced only while the MMA warps wait for it (ncu:
+                // reducers stalled on `math`, MMA warps 38% on a_full).  A 200 ns nap after every
+                // 32 DMMAs of a warp hands the pipe to the reducers: 140.0 -> 131.0 us at cfg2
+                // (measured: 20-300 ns and adaptive naps within 1%, every 16 DMMAs or 600 ns slower).
+                if ((kk + 4) % 8 == 0) __nanosleep(kMmaNapNs);
             }
             __syncwarp();
             if (lane == 0) {
