@@ -100,8 +100,10 @@ def ncu_raw(path, kernel=None):
     return {}
 
 
-def ncu_dmma_pipes(path=os.path.join(ROOT, "profiles", "r01_ncu_dmma_pipes.txt")):
-    """{kernel: DMMA sub-pipe active fraction} from the committed ncu capture, or {}."""
+def ncu_dmma_pipes(path=None):
+    """{kernel: DMMA sub-pipe active fraction} from the committed ncu capture
+    (profiles/r02_ncu_dmma_pipes.txt by tools/ncu_dmma_pipes.sh, else round 1's), or {}."""
+    path = path or profile_path("ncu_dmma_pipes.txt")
     out, name = {}, None
     try:
         with open(path) as fh:
